@@ -1,0 +1,1505 @@
+// Host side of libjtb200.so: plan (tree structure), state (HBM arenas), the
+// wave scheduler that turns Hugin collect/distribute into passes, the pass
+// compiler (block split, stride tables, chunking), and the C ABI.
+//
+// Reference correspondence (paths relative to the reference repo):
+//   jt_plan_create        JunctionTree (pkg/src/jtprop/compiler.py:40-80)
+//   jt_state_*            PropagationState / from_potentials (propagate.py:172-240)
+//   jt_apply_evidence     apply_evidence (propagate.py:243-260)
+//   jt_message            message_passing → _pass_block (propagate.py:56-76, 263-274)
+//   jt_propagate          belief_propagation = collect_evidence + distribute_evidence
+//                         per component (propagate.py:296-360)
+//   jt_query              query_marginal / posterior_marginals (propagate.py:363-390)
+//   jt_plan_mapping_table build_mapping_table (compiler.py:285-304)
+//   jt_run_message_mu     SequentialEngine.run_message (propagate.py:79-94)
+#include "jt_b200.h"
+#include "jt_internal.h"
+
+#include <algorithm>
+#include <array>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+using namespace jt;
+
+#define CK(x)                                  \
+  do {                                         \
+    cudaError_t e__ = (x);                     \
+    if (e__ != cudaSuccess) {                  \
+      last_cuda_error() = e__;                 \
+      return e__ == cudaErrorMemoryAllocation ? JT_ERR_OOM : JT_ERR_CUDA; \
+    }                                          \
+  } while (0)
+
+static cudaError_t& last_cuda_error() {
+  static thread_local cudaError_t e = cudaSuccess;
+  return e;
+}
+
+// ---------------------------------------------------------------- plan ----
+struct jt_plan {
+  int n_vars = 0;
+  std::vector<int> cards;
+  int n_cliques = 0;
+  std::vector<std::vector<int>> cvars;
+  int n_seps = 0;
+  std::vector<std::array<int, 2>> sedge;
+  std::vector<std::vector<int>> svars;
+  std::vector<int> roots;
+  std::vector<std::vector<std::pair<int, int>>> nbrs;  // (clique, sep) ascending clique id
+  std::vector<int64_t> csize, ssize;
+  std::vector<int> comp;  // component index (position in roots) per clique
+  int dtype = JT_F32;
+  int device = 0;
+};
+
+static int64_t prod_cards(const jt_plan* p, const std::vector<int>& vars) {
+  int64_t n = 1;
+  for (int v : vars) n *= p->cards[v];
+  return n;
+}
+
+extern "C" int jt_plan_create(int n_vars, const int32_t* cards, int n_cliques, const int32_t* clique_off,
+                              const int32_t* clique_vars, int n_seps, const int32_t* sep_edge,
+                              const int32_t* sep_off, const int32_t* sep_vars, int n_roots,
+                              const int32_t* roots, int dtype, int device, jt_plan** out) {
+  if (!out || n_vars < 0 || n_cliques <= 0 || n_seps < 0 || n_roots <= 0) return JT_ERR_BAD_ARG;
+  if (dtype != JT_F32 && dtype != JT_F64) return JT_ERR_BAD_ARG;
+  auto p = std::make_unique<jt_plan>();
+  p->n_vars = n_vars;
+  p->cards.assign(cards, cards + n_vars);
+  for (int c : p->cards)
+    if (c < 1) return JT_ERR_BAD_ARG;
+  p->n_cliques = n_cliques;
+  p->cvars.resize(n_cliques);
+  for (int c = 0; c < n_cliques; ++c) {
+    for (int i = clique_off[c]; i < clique_off[c + 1]; ++i) {
+      const int v = clique_vars[i];
+      if (v < 0 || v >= n_vars) return JT_ERR_BAD_ARG;
+      if (!p->cvars[c].empty() && v <= p->cvars[c].back()) return JT_ERR_BAD_ARG;
+      p->cvars[c].push_back(v);
+    }
+  }
+  p->n_seps = n_seps;
+  p->sedge.resize(n_seps);
+  p->svars.resize(n_seps);
+  p->nbrs.resize(n_cliques);
+  for (int s = 0; s < n_seps; ++s) {
+    const int a = sep_edge[2 * s], b = sep_edge[2 * s + 1];
+    if (a < 0 || b < 0 || a >= n_cliques || b >= n_cliques || a == b) return JT_ERR_BAD_ARG;
+    p->sedge[s] = {a, b};
+    for (int i = sep_off[s]; i < sep_off[s + 1]; ++i) {
+      const int v = sep_vars[i];
+      if (v < 0 || v >= n_vars) return JT_ERR_BAD_ARG;
+      if (!p->svars[s].empty() && v <= p->svars[s].back()) return JT_ERR_BAD_ARG;
+      for (int c : {a, b})
+        if (!std::binary_search(p->cvars[c].begin(), p->cvars[c].end(), v)) return JT_ERR_BAD_ARG;
+      p->svars[s].push_back(v);
+    }
+    p->nbrs[a].push_back({b, s});
+    p->nbrs[b].push_back({a, s});
+  }
+  for (auto& l : p->nbrs) std::sort(l.begin(), l.end());
+  p->roots.assign(roots, roots + n_roots);
+  p->comp.assign(n_cliques, -1);
+  for (int r = 0; r < n_roots; ++r) {
+    const int root = p->roots[r];
+    if (root < 0 || root >= n_cliques || p->comp[root] != -1) return JT_ERR_BAD_ARG;
+    std::vector<int> stack{root};
+    p->comp[root] = r;
+    while (!stack.empty()) {
+      const int c = stack.back();
+      stack.pop_back();
+      for (auto& nb : p->nbrs[c]) {
+        if (p->comp[nb.first] == -1) {
+          p->comp[nb.first] = r;
+          stack.push_back(nb.first);
+        } else if (p->comp[nb.first] != r) {
+          return JT_ERR_BAD_ARG;
+        }
+      }
+    }
+  }
+  for (int c = 0; c < n_cliques; ++c)
+    if (p->comp[c] == -1) return JT_ERR_BAD_ARG;  // a component without a root
+  if (n_seps != n_cliques - n_roots) return JT_ERR_BAD_ARG;  // forest check (compiler.py:402)
+  for (int c = 0; c < n_cliques; ++c) p->csize.push_back(prod_cards(p.get(), p->cvars[c]));
+  for (int s = 0; s < n_seps; ++s) p->ssize.push_back(prod_cards(p.get(), p->svars[s]));
+  p->dtype = dtype;
+  p->device = device;
+  *out = p.release();
+  return JT_OK;
+}
+
+extern "C" void jt_plan_destroy(jt_plan* plan) { delete plan; }
+
+// --------------------------------------------------------- tensors / specs --
+struct Tensor {
+  int arena = A_AUX;  // where it lives
+  int64_t off = 0;
+  std::vector<int> vars;  // ascending
+  bool batch = false;     // trailing batch dim
+};
+
+struct PassSpec {
+  int clique = 0;
+  int src_arena = A_CLIQUE;
+  bool write = false;
+  std::vector<Tensor> factors;
+  int out_kind = OUT_NONE;
+  Tensor out;
+  int64_t ratio_off = -1;
+};
+
+struct WaveRt {
+  int vec = 1;
+  int grid = 0;
+  int n_items = 0;
+  int64_t pass_base = 0, item_base = 0;
+};
+
+struct Program {
+  std::vector<WaveRt> waves;
+  DevPass* d_passes = nullptr;
+  Item* d_items = nullptr;
+  int64_t* d_blk = nullptr;
+  int32_t* d_bins = nullptr;
+  double* d_part = nullptr;
+  int* d_cnt = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  cudaStream_t gstream = nullptr;
+  int runs = 0;
+  ~Program() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    cudaFree(d_passes);
+    cudaFree(d_items);
+    cudaFree(d_blk);
+    cudaFree(d_bins);
+    cudaFree(d_part);
+    cudaFree(d_cnt);
+  }
+};
+
+// ------------------------------------------------------------------ state --
+struct jt_state {
+  const jt_plan* plan = nullptr;
+  int B = 1;
+  int mode = JT_MATERIALIZED;
+  int esz = 4;
+  int num_sms = 148;
+  void* d_clique = nullptr;
+  void* d_base = nullptr;
+  void* d_aux = nullptr;
+  double* d_qout = nullptr;
+  double* d_post = nullptr;
+  int64_t post_cap = 0;
+  double* d_stage = nullptr;
+  int64_t stage_cap = 0;
+  int* d_err = nullptr;
+  std::map<std::string, std::pair<int64_t*, int>> qmeta;  // per var list: device metadata, total cols
+  cudaStream_t stream = nullptr;
+  std::vector<int64_t> coff, boff, sep_off, ratC_off, ratD_off, ev_off, q_off;
+  int64_t msg_ratio_off = 0;
+  int64_t n_clique = 0, n_base = 0, n_aux = 0, n_qout = 0;
+  std::vector<std::vector<float>> ev_host;  // per var mask [card*B] (shared mode bookkeeping)
+  std::vector<int> ev_clique;               // per var: clique holding its active factor, -1 none
+  std::map<std::string, std::unique_ptr<Program>> programs;
+  int64_t launches = 0;
+  int64_t device_bytes = 0;
+  ~jt_state() {
+    programs.clear();
+    cudaFree(d_clique);
+    cudaFree(d_base);
+    cudaFree(d_aux);
+    cudaFree(d_qout);
+    cudaFree(d_post);
+    cudaFree(d_stage);
+    cudaFree(d_err);
+    for (auto& kv : qmeta) cudaFree(kv.second.first);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+static int64_t align4(int64_t x) { return (x + 3) & ~int64_t(3); }
+
+struct DevGuard {
+  int prev = 0;
+  explicit DevGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DevGuard() {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != prev) cudaSetDevice(prev);
+  }
+};
+
+extern "C" int jt_state_create(const jt_plan* plan, int batch, int mode, jt_state** out) {
+  if (!plan || !out || batch < 1 || (mode != JT_MATERIALIZED && mode != JT_SHARED_BASE))
+    return JT_ERR_BAD_ARG;
+  DevGuard g(plan->device);
+  auto st = std::make_unique<jt_state>();
+  st->plan = plan;
+  st->B = batch;
+  st->mode = mode;
+  st->esz = plan->dtype == JT_F32 ? 4 : 8;
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, plan->device));
+  st->num_sms = prop.multiProcessorCount;
+  const int64_t B = batch;
+  // clique arena (materialized) / base arena (shared)
+  int64_t off = 0;
+  for (int c = 0; c < plan->n_cliques; ++c) {
+    st->coff.push_back(off);
+    off = align4(off + plan->csize[c] * (mode == JT_MATERIALIZED ? B : 1));
+  }
+  if (mode == JT_MATERIALIZED) st->n_clique = off;
+  // base replica (one copy of every table, no batch dim): the shared-base
+  // engine reads it directly; materialized states reset from it (jt_state_reset)
+  int64_t boff = 0;
+  for (int c = 0; c < plan->n_cliques; ++c) {
+    st->boff.push_back(boff);
+    boff = align4(boff + plan->csize[c]);
+  }
+  st->n_base = boff;
+  // aux arena: seps | ratioC | ratioD | msg ratio | evidence vectors
+  off = 0;
+  auto take = [&](int64_t n) {
+    const int64_t o = off;
+    off = align4(off + n);
+    return o;
+  };
+  int64_t max_s = 1;
+  for (int s = 0; s < plan->n_seps; ++s) st->sep_off.push_back(take(plan->ssize[s] * B));
+  for (int s = 0; s < plan->n_seps; ++s) st->ratC_off.push_back(take(plan->ssize[s] * B));
+  for (int s = 0; s < plan->n_seps; ++s) st->ratD_off.push_back(take(plan->ssize[s] * B));
+  for (int s = 0; s < plan->n_seps; ++s) max_s = std::max(max_s, plan->ssize[s]);
+  st->msg_ratio_off = take(max_s * B);
+  for (int v = 0; v < plan->n_vars; ++v) st->ev_off.push_back(take((int64_t)plan->cards[v] * B));
+  st->n_aux = off;
+  int64_t qo = 0;
+  for (int v = 0; v < plan->n_vars; ++v) {
+    st->q_off.push_back(qo);
+    qo += (int64_t)plan->cards[v] * B;
+  }
+  st->n_qout = std::max<int64_t>(qo, 1);
+  st->ev_clique.assign(plan->n_vars, -1);
+  st->ev_host.resize(plan->n_vars);
+
+  const size_t es = st->esz;
+  if (st->n_clique) CK(cudaMalloc(&st->d_clique, st->n_clique * es));
+  if (st->n_base) CK(cudaMalloc(&st->d_base, st->n_base * es));
+  CK(cudaMalloc(&st->d_aux, std::max<int64_t>(st->n_aux, 4) * es));
+  CK(cudaMalloc(&st->d_qout, st->n_qout * sizeof(double)));
+  CK(cudaMalloc(&st->d_err, sizeof(int)));
+  CK(cudaMemset(st->d_err, 0, sizeof(int)));
+  CK(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
+  st->device_bytes = (st->n_clique + st->n_base + st->n_aux) * es + st->n_qout * 8;
+  // initial contents: cliques 1 (initialize's np.ones, propagate.py:209), seps 1 (236)
+  if (st->n_clique) CK(launch_fill(plan->dtype, st->d_clique, st->n_clique, 1.0, st->stream));
+  CK(launch_fill(plan->dtype, st->d_base, st->n_base, 1.0, st->stream));
+  CK(launch_fill(plan->dtype, st->d_aux, st->n_aux, 1.0, st->stream));
+  CK(cudaStreamSynchronize(st->stream));
+  *out = st.release();
+  return JT_OK;
+}
+
+extern "C" void jt_state_destroy(jt_state* st) {
+  if (!st) return;
+  DevGuard g(st->plan->device);
+  delete st;
+}
+
+extern "C" int64_t jt_state_device_bytes(const jt_state* st) { return st ? st->device_bytes : 0; }
+extern "C" int64_t jt_state_launch_count(const jt_state* st) { return st ? st->launches : 0; }
+
+static cudaStream_t pick_stream(jt_state* st, void* s) {
+  return s ? reinterpret_cast<cudaStream_t>(s) : st->stream;
+}
+
+static int ensure_stage(jt_state* st, int64_t n) {
+  if (n <= st->stage_cap) return JT_OK;
+  cudaFree(st->d_stage);
+  st->d_stage = nullptr;
+  st->stage_cap = 0;
+  CK(cudaMalloc(&st->d_stage, std::max<int64_t>(n, 1) * sizeof(double)));
+  st->stage_cap = n;
+  return JT_OK;
+}
+
+// ------------------------------------------------------- pass compiler ----
+struct Dim {
+  int64_t card;
+  int64_t src, dst, out;
+  int64_t fac[MAXF];
+};
+
+static int64_t tensor_stride(const jt_plan* p, const Tensor& t, int var, int64_t B) {
+  // var < 0 denotes the batch dim
+  if (var < 0) return t.batch ? 1 : 0;
+  auto it = std::find(t.vars.begin(), t.vars.end(), var);
+  if (it == t.vars.end()) return 0;
+  int64_t s = t.batch ? B : 1;
+  for (auto j = it + 1; j != t.vars.end(); ++j) s *= p->cards[*j];
+  return s;
+}
+
+struct BuiltPass {
+  DevPass d;
+  std::vector<int64_t> blk;
+  std::vector<int32_t> bins;
+  int64_t n_part = 0;
+  int64_t n_cnt = 0;
+  std::vector<Item> items;
+};
+
+static std::vector<Dim> pass_dims(const jt_state* st, const PassSpec& ps) {
+  const jt_plan* p = st->plan;
+  const int64_t B = st->B;
+  const auto& cv = p->cvars[ps.clique];
+  std::vector<int> vars(cv.begin(), cv.end());
+  if (B > 1) vars.push_back(-1);
+  Tensor src;
+  src.vars = cv;
+  src.batch = (B > 1) && ps.src_arena == A_CLIQUE;
+  Tensor dst;
+  dst.vars = cv;
+  dst.batch = B > 1;
+  std::vector<Dim> dims;
+  for (int v : vars) {
+    Dim d{};
+    d.card = v < 0 ? B : p->cards[v];
+    d.src = tensor_stride(p, src, v, B);
+    d.dst = ps.write ? tensor_stride(p, dst, v, B) : 0;
+    d.out = ps.out_kind != OUT_NONE ? tensor_stride(p, ps.out, v, B) : 0;
+    for (size_t f = 0; f < ps.factors.size(); ++f) d.fac[f] = tensor_stride(p, ps.factors[f], v, B);
+    dims.push_back(d);
+  }
+  if (dims.empty()) {  // empty clique scope: a single entry
+    Dim d{};
+    d.card = 1;
+    dims.push_back(d);
+  }
+  return dims;
+}
+
+static int pass_max_vec(const jt_state* st, const PassSpec& ps) {
+  auto dims = pass_dims(st, ps);
+  const int64_t c = dims.back().card;
+  const int maxv = st->esz == 4 ? 4 : 2;
+  for (int v = maxv; v > 1; v >>= 1)
+    if (c % v == 0) return v;
+  return 1;
+}
+
+static bool mergeable(const Dim& a, const Dim& b, int nf) {
+  auto ok = [](int64_t sa, int64_t sb, int64_t cb) { return (sa == 0 && sb == 0) || (sb != 0 && sa == sb * cb); };
+  if (!ok(a.src, b.src, b.card) || !ok(a.dst, b.dst, b.card) || !ok(a.out, b.out, b.card)) return false;
+  for (int f = 0; f < nf; ++f)
+    if (!ok(a.fac[f], b.fac[f], b.card)) return false;
+  return true;
+}
+
+static std::vector<Dim> merge_dims(const std::vector<Dim>& in, int nf) {
+  std::vector<Dim> out;
+  for (const Dim& d : in) {
+    if (!out.empty() && mergeable(out.back(), d, nf)) {
+      Dim m = d;  // strides of the inner dim, card multiplied
+      m.card = out.back().card * d.card;
+      out.back() = m;
+    } else {
+      out.push_back(d);
+    }
+  }
+  return out;
+}
+
+static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pass_idx, BuiltPass& bp) {
+  const int nf = (int)ps.factors.size();
+  if (nf > MAXF) return JT_ERR_UNSUPPORTED;
+  std::vector<Dim> dims = pass_dims(st, ps);
+  const int nd = (int)dims.size();
+  const int TH = NT * KV * vec;
+  const bool has_out = ps.out_kind != OUT_NONE;
+  int64_t total = 1;
+  for (auto& d : dims) total *= d.card;
+
+  struct Cand {
+    int k;
+    int64_t T, n_in, n_out, r_out;
+    int BPI;
+    int64_t n_chunks, bpc;
+    double cost;
+    std::vector<Dim> inner;
+  };
+  Cand best{};
+  best.cost = 1e300;
+  bool found = false;
+  int64_t T = 1;
+  for (int k = nd - 1; k >= 0; --k) {
+    T *= dims[k].card;
+    if (T > TH) break;
+    if (T % vec) continue;
+    std::vector<Dim> inner(dims.begin() + k, dims.end());
+    std::vector<Dim> im = merge_dims(inner, nf);
+    if ((int)im.size() > MAXDI) continue;
+    Cand c;
+    c.k = k;
+    c.T = T;
+    c.inner = im;
+    c.n_in = 1;
+    for (auto& d : inner)
+      if (has_out && d.out) c.n_in *= d.card;
+    c.n_out = 1;
+    c.r_out = 1;
+    for (int i = 0; i < k; ++i) {
+      if (has_out && dims[i].out) c.n_out *= dims[i].card;
+      else c.r_out *= dims[i].card;
+    }
+    c.BPI = (int)std::max<int64_t>(1, std::min<int64_t>(TH / T, c.r_out));
+    // chunking: ~1184 items for big passes, >= 2 iterations per item otherwise
+    const int64_t per_item = std::max<int64_t>(2 * TH, total / (int64_t)(st->num_sms * 8));
+    const int64_t desired = std::max<int64_t>(1, (total + per_item - 1) / per_item);
+    const int64_t max_chunks = (c.r_out + c.BPI - 1) / c.BPI;
+    int64_t nch = has_out ? (desired + c.n_out - 1) / c.n_out : desired;
+    nch = std::max<int64_t>(1, std::min(nch, max_chunks));
+    int64_t bpc = (c.r_out + nch - 1) / nch;
+    bpc = (bpc + c.BPI - 1) / c.BPI * c.BPI;
+    c.bpc = bpc;
+    c.n_chunks = (c.r_out + bpc - 1) / bpc;
+    const double esz = st->esz;
+    double bytes = (double)total * esz * ((ps.src_arena == A_CLIQUE ? 1.0 : 0.05) + (ps.write ? 1.0 : 0.0));
+    double part = (has_out && c.n_chunks > 1) ? (double)c.n_out * c.n_chunks * c.n_in * 16.0 : 0.0;
+    double items = (double)c.n_out * c.n_chunks;
+    double pen = 0.0;
+    if (T * esz < 128) pen = bytes * (128.0 / (T * esz) - 1.0) * 0.5;
+    c.cost = bytes + part + items * 4096.0 + pen + (double)c.n_out * c.r_out * 16.0;
+    if (!found || c.cost < best.cost * 0.999) {
+      best = c;
+      found = true;
+    }
+  }
+  if (!found) return JT_ERR_UNSUPPORTED;
+
+  DevPass& d = bp.d;
+  std::memset(&d, 0, sizeof(d));
+  const jt_plan* p = st->plan;
+  d.src_arena = ps.src_arena;
+  d.src_off = ps.src_arena == A_CLIQUE ? st->coff[ps.clique] : st->boff[ps.clique];
+  d.dst_off = ps.write ? st->coff[ps.clique] : -1;
+  d.nf = nf;
+  d.fac_vec = 0;
+  for (int f = 0; f < nf; ++f) {
+    d.fac_off[f] = ps.factors[f].off;
+    if (dims.back().fac[f] == 1) d.fac_vec |= 1u << f;
+  }
+  d.src_vec = dims.back().src == 1 ? 1 : 0;
+  d.out_kind = ps.out_kind;
+  d.out_off = has_out ? ps.out.off : 0;
+  d.ratio_off = ps.ratio_off;
+  d.T = (int)best.T;
+  d.BPI = best.BPI;
+  d.n_in = (int)best.n_in;
+  d.n_chunks = (int)best.n_chunks;
+  d.n_blocks_per_jout = best.r_out;
+  d.blocks_per_chunk = best.bpc;
+  d.blk_stride = 2 + nf;
+  d.ndi = (int)best.inner.size();
+  for (int i = 0; i < d.ndi; ++i) {
+    const Dim& x = best.inner[i];
+    d.icard[i] = (int)x.card;
+    d.isrc[i] = (int)x.src;
+    d.idst[i] = (int)x.dst;
+    d.iout[i] = (int)x.out;
+    for (int f = 0; f < nf; ++f) d.ifac[f][i] = (int)x.fac[f];
+  }
+  (void)p;
+  // block table: j_out-major over the separator dims outside the block, then
+  // the remaining outer dims
+  std::vector<int> so, ro;
+  for (int i = 0; i < best.k; ++i) ((has_out && dims[i].out) ? so : ro).push_back(i);
+  const int64_t nblk = best.n_out * best.r_out;
+  bp.blk.assign(nblk * (2 + nf), 0);
+  std::vector<int64_t> dig_s(so.size(), 0), dig_r(ro.size(), 0);
+  int64_t bi = 0;
+  for (int64_t jo = 0; jo < best.n_out; ++jo) {
+    int64_t s_src = 0, s_dst = 0, s_fac[MAXF] = {0};
+    {
+      int64_t x = jo;
+      for (int t = (int)so.size() - 1; t >= 0; --t) {
+        const Dim& dd = dims[so[t]];
+        const int64_t dg = x % dd.card;
+        x /= dd.card;
+        s_src += dg * dd.src;
+        s_dst += dg * dd.dst;
+        for (int f = 0; f < nf; ++f) s_fac[f] += dg * dd.fac[f];
+      }
+    }
+    std::fill(dig_r.begin(), dig_r.end(), 0);
+    int64_t r_src = 0, r_dst = 0, r_fac[MAXF] = {0};
+    for (int64_t po = 0; po < best.r_out; ++po) {
+      int64_t* e = &bp.blk[bi * (2 + nf)];
+      e[0] = s_src + r_src;
+      e[1] = s_dst + r_dst;
+      for (int f = 0; f < nf; ++f) e[2 + f] = s_fac[f] + r_fac[f];
+      ++bi;
+      // odometer increment over the rest-outer dims (last fastest)
+      for (int t = (int)ro.size() - 1; t >= 0; --t) {
+        const Dim& dd = dims[ro[t]];
+        dig_r[t]++;
+        r_src += dd.src;
+        r_dst += dd.dst;
+        for (int f = 0; f < nf; ++f) r_fac[f] += dd.fac[f];
+        if (dig_r[t] < dd.card) break;
+        r_src -= dd.src * dd.card;
+        r_dst -= dd.dst * dd.card;
+        for (int f = 0; f < nf; ++f) r_fac[f] -= dd.fac[f] * dd.card;
+        dig_r[t] = 0;
+      }
+    }
+  }
+  // bin tables: position(b, p) = binbase[b] + binrest[p] over the inner block
+  if (has_out && d.n_in > 1) {
+    std::vector<int64_t> pstride(d.ndi, 1);
+    for (int i = d.ndi - 2; i >= 0; --i) pstride[i] = pstride[i + 1] * d.icard[i + 1];
+    std::vector<int64_t> bb{0}, br{0};
+    for (int i = 0; i < d.ndi; ++i) {
+      auto& tgt = d.iout[i] ? bb : br;
+      std::vector<int64_t> nx;
+      nx.reserve(tgt.size() * d.icard[i]);
+      for (int64_t o : tgt)
+        for (int c = 0; c < d.icard[i]; ++c) nx.push_back(o + c * pstride[i]);
+      tgt.swap(nx);
+    }
+    for (auto x : bb) bp.bins.push_back((int32_t)x);
+    for (auto x : br) bp.bins.push_back((int32_t)x);
+  }
+  if (has_out && d.n_chunks > 1) {
+    bp.n_part = best.n_out * best.n_chunks * best.n_in;
+    bp.n_cnt = best.n_out;
+  }
+  for (int64_t jo = 0; jo < best.n_out; ++jo)
+    for (int64_t ch = 0; ch < best.n_chunks; ++ch) bp.items.push_back(Item{pass_idx, (int)ch, jo});
+  return JT_OK;
+}
+
+static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>& waves,
+                         std::unique_ptr<Program>& out) {
+  auto prog = std::make_unique<Program>();
+  std::vector<DevPass> passes;
+  std::vector<Item> items;
+  std::vector<int64_t> blk;
+  std::vector<int32_t> bins;
+  int64_t n_part = 0, n_cnt = 0;
+  for (auto& w : waves) {
+    if (w.empty()) continue;
+    int vec = st->esz == 4 ? 4 : 2;
+    for (auto& ps : w) vec = std::min(vec, pass_max_vec(st, ps));
+    WaveRt rt;
+    rt.vec = vec;
+    rt.pass_base = (int64_t)passes.size();
+    rt.item_base = (int64_t)items.size();
+    for (auto& ps : w) {
+      BuiltPass bp;
+      const int local = (int)(passes.size() - rt.pass_base);
+      int rc = compile_pass(st, ps, vec, local, bp);
+      if (rc != JT_OK) return rc;
+      bp.d.blk_off = (int64_t)blk.size();
+      bp.d.bin_off = (int64_t)bins.size();
+      bp.d.part_off = n_part;
+      bp.d.cnt_off = n_cnt;
+      blk.insert(blk.end(), bp.blk.begin(), bp.blk.end());
+      bins.insert(bins.end(), bp.bins.begin(), bp.bins.end());
+      n_part += bp.n_part;
+      n_cnt += bp.n_cnt;
+      passes.push_back(bp.d);
+      items.insert(items.end(), bp.items.begin(), bp.items.end());
+    }
+    rt.n_items = (int)(items.size() - rt.item_base);
+    const int occ = wave_max_ctas_per_sm(st->plan->dtype, vec);
+    rt.grid = (int)std::min<int64_t>(rt.n_items, (int64_t)occ * st->num_sms);
+    prog->waves.push_back(rt);
+  }
+  auto up = [&](auto** dptr, const auto& vec) -> int {
+    using E = typename std::decay_t<decltype(vec)>::value_type;
+    const size_t n = std::max<size_t>(vec.size(), 1);
+    CK(cudaMalloc((void**)dptr, n * sizeof(E)));
+    if (!vec.empty()) CK(cudaMemcpy(*dptr, vec.data(), vec.size() * sizeof(E), cudaMemcpyHostToDevice));
+    return JT_OK;
+  };
+  int rc;
+  if ((rc = up(&prog->d_passes, passes))) return rc;
+  if ((rc = up(&prog->d_items, items))) return rc;
+  if ((rc = up(&prog->d_blk, blk))) return rc;
+  if ((rc = up(&prog->d_bins, bins))) return rc;
+  CK(cudaMalloc(&prog->d_part, std::max<int64_t>(n_part, 1) * sizeof(double)));
+  CK(cudaMalloc(&prog->d_cnt, std::max<int64_t>(n_cnt, 1) * sizeof(int)));
+  CK(cudaMemset(prog->d_cnt, 0, std::max<int64_t>(n_cnt, 1) * sizeof(int)));
+  out = std::move(prog);
+  return JT_OK;
+}
+
+static int launch_program_waves(jt_state* st, Program* pr, cudaStream_t s) {
+  for (auto& w : pr->waves) {
+    WaveArgs a;
+    a.clique = st->d_clique;
+    a.base = st->d_base;
+    a.aux = st->d_aux;
+    a.qout = st->d_qout;
+    a.partials = pr->d_part;
+    a.counters = pr->d_cnt;
+    a.err = st->d_err;
+    a.blk = pr->d_blk;
+    a.bins = pr->d_bins;
+    a.passes = pr->d_passes + w.pass_base;
+    a.items = pr->d_items + w.item_base;
+    a.n_items = w.n_items;
+    CK(launch_wave(st->plan->dtype, w.vec, a, w.grid, s));
+    st->launches++;
+  }
+  return JT_OK;
+}
+
+// First run launches directly; from the second run on the wave sequence is
+// replayed as a CUDA graph on that stream (launch-bound small trees).
+static int run_program(jt_state* st, Program* pr, cudaStream_t s) {
+  pr->runs++;
+  if (pr->waves.size() <= 1 || pr->runs < 2) return launch_program_waves(st, pr, s);
+  if (pr->gexec && pr->gstream == s) {
+    CK(cudaGraphLaunch(pr->gexec, s));
+    st->launches += (int64_t)pr->waves.size();
+    return JT_OK;
+  }
+  cudaStreamCaptureStatus cs;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone || s == nullptr)
+    return launch_program_waves(st, pr, s);
+  cudaGraph_t graph;
+  CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  const int64_t before = st->launches;
+  int rc = launch_program_waves(st, pr, s);
+  cudaError_t ec = cudaStreamEndCapture(s, &graph);
+  st->launches = before;
+  if (rc != JT_OK) return rc;
+  CK(ec);
+  if (pr->gexec) cudaGraphExecDestroy(pr->gexec);
+  pr->gexec = nullptr;
+  CK(cudaGraphInstantiate(&pr->gexec, graph, 0));
+  cudaGraphDestroy(graph);
+  pr->gstream = s;
+  CK(cudaGraphLaunch(pr->gexec, s));
+  st->launches += (int64_t)pr->waves.size();
+  return JT_OK;
+}
+
+// ------------------------------------------------------------ scheduler ----
+static Tensor sep_tensor(const jt_state* st, int s, int64_t off) {
+  Tensor t;
+  t.arena = A_AUX;
+  t.off = off;
+  t.vars = st->plan->svars[s];
+  t.batch = st->B > 1;
+  return t;
+}
+
+static Tensor ev_tensor(const jt_state* st, int v) {
+  Tensor t;
+  t.arena = A_AUX;
+  t.off = st->ev_off[v];
+  t.vars = {v};
+  t.batch = st->B > 1;
+  return t;
+}
+
+static Tensor var_out_tensor(const jt_state* st, int v) {
+  Tensor t;
+  t.arena = -1;
+  t.off = st->q_off[v];
+  t.vars = {v};
+  t.batch = st->B > 1;
+  return t;
+}
+
+struct Orient {
+  std::vector<int> parent, psep, depth, height;
+  std::vector<std::vector<std::pair<int, int>>> children;  // (child, sep) ascending
+  int max_depth = 0, max_height = 0;
+};
+
+static Orient orient(const jt_plan* p, const std::vector<int>& roots) {
+  Orient o;
+  const int n = p->n_cliques;
+  o.parent.assign(n, -1);
+  o.psep.assign(n, -1);
+  o.depth.assign(n, 0);
+  o.height.assign(n, 0);
+  o.children.resize(n);
+  std::vector<int> order;
+  for (int r : roots) {
+    std::vector<int> stack{r};
+    o.parent[r] = -1;
+    std::vector<char> seen(n, 0);
+    seen[r] = 1;
+    while (!stack.empty()) {
+      const int c = stack.back();
+      stack.pop_back();
+      order.push_back(c);
+      for (auto& nb : p->nbrs[c]) {
+        if (nb.first == o.parent[c] && nb.second == o.psep[c]) continue;
+        if (seen[nb.first]) continue;
+        seen[nb.first] = 1;
+        o.parent[nb.first] = c;
+        o.psep[nb.first] = nb.second;
+        o.depth[nb.first] = o.depth[c] + 1;
+        o.children[c].push_back(nb);
+        stack.push_back(nb.first);
+      }
+    }
+  }
+  for (auto it = order.rbegin(); it != order.rend(); ++it) {
+    const int c = *it;
+    if (o.parent[c] >= 0) o.height[o.parent[c]] = std::max(o.height[o.parent[c]], o.height[c] + 1);
+  }
+  for (int c = 0; c < n; ++c) {
+    o.max_depth = std::max(o.max_depth, o.depth[c]);
+    o.max_height = std::max(o.max_height, o.height[c]);
+    std::sort(o.children[c].begin(), o.children[c].end());
+  }
+  return o;
+}
+
+// Hugin collect+distribute as waves of passes.  Lazy scheme: a clique is read
+// (not written) in collect, with its children's collect ratios multiplied in
+// on the fly; its final table = original × Π children ratios × parent ratio is
+// written once in distribute.  Cliques with more factors than a pass carries
+// absorb their children's ratios eagerly (in-place) during collect instead.
+static int build_propagate(jt_state* st, const std::vector<int>& roots, const std::vector<int>& qvars,
+                           std::vector<std::vector<PassSpec>>& waves) {
+  const jt_plan* p = st->plan;
+  const bool shared = st->mode == JT_SHARED_BASE;
+  const int src_arena = shared ? A_BASE : A_CLIQUE;
+  Orient o = orient(p, roots);
+  const int n = p->n_cliques;
+  std::vector<std::vector<int>> evs(n);  // active evidence vars per clique (shared mode)
+  if (shared)
+    for (int v = 0; v < p->n_vars; ++v)
+      if (st->ev_clique[v] >= 0) evs[st->ev_clique[v]].push_back(v);
+  std::vector<char> eager(n, 0);
+  for (int c = 0; c < n; ++c) {
+    const int nfac = (int)o.children[c].size() + (o.parent[c] >= 0 ? 1 : 0) + (int)evs[c].size();
+    if (nfac > MAXF) {
+      if (shared) return JT_ERR_UNSUPPORTED;
+      eager[c] = 1;
+    }
+  }
+  auto child_ratios = [&](int c) {
+    std::vector<Tensor> f;
+    for (auto& ch : o.children[c]) f.push_back(sep_tensor(st, ch.second, st->ratC_off[ch.second]));
+    return f;
+  };
+  auto ev_factors = [&](int c) {
+    std::vector<Tensor> f;
+    for (int v : evs[c]) f.push_back(ev_tensor(st, v));
+    return f;
+  };
+  // ---- collect: by height, leaves first ----
+  for (int h = 0; h <= o.max_height; ++h) {
+    std::vector<std::vector<PassSpec>> pre;  // absorb sub-waves for eager cliques
+    std::vector<PassSpec> main;
+    for (int c = 0; c < n; ++c) {
+      if (o.height[c] != h) continue;
+      const bool is_root = o.parent[c] < 0;
+      if (is_root && !eager[c]) continue;
+      std::vector<Tensor> cf = child_ratios(c);
+      std::vector<Tensor> ef = ev_factors(c);
+      if (eager[c]) {
+        // absorb children ratios MAXF at a time, in place
+        size_t i = 0;
+        int sub = 0;
+        const size_t last_chunk = is_root ? cf.size() : (cf.size() > 0 ? cf.size() - ((cf.size() - 1) % MAXF + 1) : 0);
+        while (i < last_chunk) {
+          PassSpec ps;
+          ps.clique = c;
+          ps.src_arena = A_CLIQUE;
+          ps.write = true;
+          for (size_t k = i; k < std::min(last_chunk, i + MAXF); ++k) ps.factors.push_back(cf[k]);
+          i += ps.factors.size();
+          if ((int)pre.size() <= sub) pre.resize(sub + 1);
+          pre[sub++].push_back(ps);
+        }
+        if (!is_root) {
+          PassSpec ps;
+          ps.clique = c;
+          ps.src_arena = A_CLIQUE;
+          ps.write = true;
+          for (size_t k = i; k < cf.size(); ++k) ps.factors.push_back(cf[k]);
+          ps.out_kind = OUT_SEP;
+          ps.out = sep_tensor(st, o.psep[c], st->sep_off[o.psep[c]]);
+          ps.ratio_off = st->ratC_off[o.psep[c]];
+          main.push_back(ps);
+        }
+      } else {
+        PassSpec ps;
+        ps.clique = c;
+        ps.src_arena = src_arena;
+        ps.factors = cf;
+        ps.factors.insert(ps.factors.end(), ef.begin(), ef.end());
+        ps.out_kind = OUT_SEP;
+        ps.out = sep_tensor(st, o.psep[c], st->sep_off[o.psep[c]]);
+        ps.ratio_off = st->ratC_off[o.psep[c]];
+        main.push_back(ps);
+      }
+    }
+    for (auto& w : pre) waves.push_back(w);
+    // roots absorb after their children's ratios exist: eager roots are at max height;
+    // their absorb passes were queued in `pre` of their own height, which runs after
+    // all lower heights — correct since every child has a lower height.
+    waves.push_back(main);
+  }
+  // query assignment (fused queries, shared mode)
+  std::vector<std::vector<int>> qby(n);
+  for (int v : qvars) {
+    int best = -1;
+    for (int c = 0; c < n; ++c)
+      if (std::binary_search(p->cvars[c].begin(), p->cvars[c].end(), v))
+        if (best < 0 || p->csize[c] < p->csize[best]) best = c;
+    if (best < 0) return JT_ERR_BAD_ARG;
+    qby[best].push_back(v);
+  }
+  // ---- distribute: by depth, root first ----
+  std::vector<std::vector<PassSpec>> dw(o.max_depth + 3);
+  for (int c = 0; c < n; ++c) {
+    const int d = o.depth[c];
+    std::vector<Tensor> fac;
+    if (!eager[c]) fac = child_ratios(c);
+    if (o.parent[c] >= 0) fac.push_back(sep_tensor(st, o.psep[c], st->ratD_off[o.psep[c]]));
+    std::vector<Tensor> ef = ev_factors(c);
+    fac.insert(fac.end(), ef.begin(), ef.end());
+    const auto& ch = o.children[c];
+    for (size_t i = 0; i < ch.size(); ++i) {
+      PassSpec ps;
+      ps.clique = c;
+      ps.src_arena = eager[c] ? A_CLIQUE : src_arena;
+      ps.factors = fac;
+      ps.write = !shared && ch.size() == 1;
+      ps.out_kind = OUT_SEP;
+      ps.out = sep_tensor(st, ch[i].second, st->sep_off[ch[i].second]);
+      ps.ratio_off = st->ratD_off[ch[i].second];
+      dw[d].push_back(ps);
+    }
+    if (!shared && ch.size() != 1 && !fac.empty()) {
+      PassSpec ps;
+      ps.clique = c;
+      ps.src_arena = A_CLIQUE;
+      ps.factors = fac;
+      ps.write = true;
+      dw[ch.empty() ? d : d + 1].push_back(ps);
+    }
+    for (int v : qby[c]) {
+      PassSpec ps;
+      ps.clique = c;
+      ps.src_arena = shared ? A_BASE : A_CLIQUE;
+      ps.factors = shared ? fac : std::vector<Tensor>{};
+      ps.out_kind = OUT_RAW;
+      ps.out = var_out_tensor(st, v);
+      // materialized: queries read the final table, after its writer
+      dw[shared ? d : d + 2].push_back(ps);
+    }
+  }
+  for (auto& w : dw) waves.push_back(w);
+  return JT_OK;
+}
+
+static std::string key_of(const char* tag, const std::vector<int>& a, const std::vector<int>& b = {}) {
+  std::string k(tag);
+  for (int x : a) k += "," + std::to_string(x);
+  k += "|";
+  for (int x : b) k += "," + std::to_string(x);
+  return k;
+}
+
+static std::vector<int> active_ev(const jt_state* st) {
+  std::vector<int> k;
+  if (st->mode == JT_SHARED_BASE)
+    for (int v = 0; v < st->plan->n_vars; ++v)
+      if (st->ev_clique[v] >= 0) {
+        k.push_back(v);
+        k.push_back(st->ev_clique[v]);
+      }
+  return k;
+}
+
+static int get_program(jt_state* st, const std::string& key,
+                       const std::vector<std::vector<PassSpec>>& waves, Program** out) {
+  auto it = st->programs.find(key);
+  if (it == st->programs.end()) {
+    std::unique_ptr<Program> pr;
+    int rc = build_program(st, waves, pr);
+    if (rc != JT_OK) return rc;
+    it = st->programs.emplace(key, std::move(pr)).first;
+  }
+  *out = it->second.get();
+  return JT_OK;
+}
+
+// ------------------------------------------------------------------ C ABI --
+extern "C" int jt_state_load(jt_state* st, int case_idx, const double* clique_concat, const double* sep_concat) {
+  if (!st || case_idx < -1 || case_idx >= st->B) return JT_ERR_BAD_ARG;
+  const jt_plan* p = st->plan;
+  DevGuard g(p->device);
+  const bool shared = st->mode == JT_SHARED_BASE;
+  if (shared && case_idx != -1 && clique_concat) return JT_ERR_UNSUPPORTED;
+  int64_t tot_c = std::accumulate(p->csize.begin(), p->csize.end(), int64_t(0));
+  int64_t tot_s = std::accumulate(p->ssize.begin(), p->ssize.end(), int64_t(0));
+  int rc = ensure_stage(st, std::max(tot_c, tot_s));
+  if (rc) return rc;
+  cudaStream_t s = st->stream;
+  const int64_t B = st->B;
+  if (clique_concat) {
+    CK(cudaMemcpyAsync(st->d_stage, clique_concat, tot_c * 8, cudaMemcpyHostToDevice, s));
+    int64_t o = 0;
+    for (int c = 0; c < p->n_cliques; ++c) {
+      const int64_t nc = p->csize[c];
+      if (case_idx < 0) {
+        char* dst = (char*)st->d_base + st->boff[c] * st->esz;
+        CK(launch_convert_d2t(p->dtype, st->d_stage + o, dst, nc, 1, 1, s));
+      }
+      if (!shared) {
+        char* dst = (char*)st->d_clique + (st->coff[c] + (case_idx < 0 ? 0 : case_idx)) * st->esz;
+        CK(launch_convert_d2t(p->dtype, st->d_stage + o, dst, nc, B, case_idx < 0 ? B : 1, s));
+      }
+      o += nc;
+    }
+    CK(cudaStreamSynchronize(s));
+  }
+  if (sep_concat) {
+    CK(cudaMemcpyAsync(st->d_stage, sep_concat, tot_s * 8, cudaMemcpyHostToDevice, s));
+  }
+  int64_t o = 0;
+  for (int sp = 0; sp < p->n_seps; ++sp) {
+    const int64_t ns = p->ssize[sp];
+    char* dst = (char*)st->d_aux + (st->sep_off[sp] + (case_idx < 0 ? 0 : case_idx)) * st->esz;
+    if (sep_concat) {
+      CK(launch_convert_d2t(p->dtype, st->d_stage + o, dst, ns, B, case_idx < 0 ? B : 1, s));
+    } else if (case_idx < 0) {
+      CK(launch_fill(p->dtype, dst, ns * B, 1.0, s));
+    }
+    o += ns;
+  }
+  CK(cudaStreamSynchronize(s));
+  return JT_OK;
+}
+
+extern "C" int jt_state_store(jt_state* st, int case_idx, double* clique_concat, double* sep_concat) {
+  if (!st || case_idx < 0 || case_idx >= st->B) return JT_ERR_BAD_ARG;
+  const jt_plan* p = st->plan;
+  DevGuard g(p->device);
+  if (st->mode == JT_SHARED_BASE && clique_concat) return JT_ERR_UNSUPPORTED;
+  int64_t tot_c = std::accumulate(p->csize.begin(), p->csize.end(), int64_t(0));
+  int64_t tot_s = std::accumulate(p->ssize.begin(), p->ssize.end(), int64_t(0));
+  int rc = ensure_stage(st, std::max(tot_c, tot_s));
+  if (rc) return rc;
+  cudaStream_t s = st->stream;
+  const int64_t B = st->B;
+  if (clique_concat) {
+    int64_t o = 0;
+    for (int c = 0; c < p->n_cliques; ++c) {
+      const char* src = (const char*)st->d_clique + (st->coff[c] + case_idx) * st->esz;
+      CK(launch_convert_t2d(p->dtype, src, B, st->d_stage + o, p->csize[c], s));
+      o += p->csize[c];
+    }
+    CK(cudaMemcpyAsync(clique_concat, st->d_stage, tot_c * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  if (sep_concat) {
+    int64_t o = 0;
+    for (int sp = 0; sp < p->n_seps; ++sp) {
+      const char* src = (const char*)st->d_aux + (st->sep_off[sp] + case_idx) * st->esz;
+      CK(launch_convert_t2d(p->dtype, src, B, st->d_stage + o, p->ssize[sp], s));
+      o += p->ssize[sp];
+    }
+    CK(cudaMemcpyAsync(sep_concat, st->d_stage, tot_s * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  return JT_OK;
+}
+
+extern "C" int jt_clear_evidence(jt_state* st) {
+  if (!st) return JT_ERR_BAD_ARG;
+  for (int v = 0; v < st->plan->n_vars; ++v) {
+    st->ev_clique[v] = -1;
+    st->ev_host[v].clear();
+  }
+  return JT_OK;
+}
+
+extern "C" int jt_state_reset(jt_state* st, void* stream) {
+  if (!st) return JT_ERR_BAD_ARG;
+  const jt_plan* p = st->plan;
+  DevGuard g(p->device);
+  cudaStream_t s = pick_stream(st, stream);
+  jt_clear_evidence(st);
+  if (p->n_seps) {
+    const int64_t n = st->ratC_off[0];  // separator tables lead the aux arena
+    CK(launch_fill(p->dtype, st->d_aux, n, 1.0, s));
+    st->launches++;
+  }
+  if (st->mode == JT_SHARED_BASE) return JT_OK;
+  Program* pr;
+  auto it = st->programs.find("reset");
+  if (it != st->programs.end()) {
+    pr = it->second.get();
+  } else {
+    std::vector<std::vector<PassSpec>> waves(1);
+    for (int c = 0; c < p->n_cliques; ++c) {
+      PassSpec ps;
+      ps.clique = c;
+      ps.src_arena = A_BASE;
+      ps.write = true;
+      waves[0].push_back(ps);
+    }
+    int rc = get_program(st, "reset", waves, &pr);
+    if (rc) return rc;
+  }
+  return run_program(st, pr, s);
+}
+
+extern "C" int jt_apply_evidence(jt_state* st, int n, const int32_t* case_idx, const int32_t* var,
+                                 const int32_t* clique, const int32_t* value, void* stream) {
+  if (!st || n < 0) return JT_ERR_BAD_ARG;
+  if (n == 0) return JT_OK;
+  const jt_plan* p = st->plan;
+  DevGuard g(p->device);
+  const int64_t B = st->B;
+  // per var: mask [card][B]; unobserved lanes stay 1
+  std::map<int, std::vector<float>> masks;
+  std::map<int, int> owner;
+  for (int i = 0; i < n; ++i) {
+    const int v = var[i], c = clique[i], b = case_idx ? case_idx[i] : -1;
+    if (v < 0 || v >= p->n_vars || c < 0 || c >= p->n_cliques || b < -1 || b >= B) return JT_ERR_BAD_ARG;
+    if (!std::binary_search(p->cvars[c].begin(), p->cvars[c].end(), v)) return JT_ERR_BAD_ARG;
+    if (value[i] < 0 || value[i] >= p->cards[v]) return JT_ERR_BAD_ARG;
+    auto it = owner.find(v);
+    if (it != owner.end() && it->second != c) return JT_ERR_BAD_ARG;
+    owner[v] = c;
+    auto& m = masks[v];
+    if (m.empty()) m.assign((size_t)p->cards[v] * B, 1.0f);
+    for (int64_t l = (b < 0 ? 0 : b); l < (b < 0 ? B : b + 1); ++l)
+      for (int d = 0; d < p->cards[v]; ++d)
+        if (d != value[i]) m[(size_t)d * B + l] = 0.0f;
+  }
+  cudaStream_t s = pick_stream(st, stream);
+  std::vector<double> hbuf;
+  if (st->mode == JT_SHARED_BASE) {
+    // accumulate into the persistent factor (repeated observations multiply)
+    for (auto& kv : masks) {
+      const int v = kv.first;
+      if (st->ev_clique[v] >= 0 && st->ev_clique[v] != owner[v]) return JT_ERR_UNSUPPORTED;
+      auto& h = st->ev_host[v];
+      if (h.empty()) h.assign(kv.second.size(), 1.0f);
+      for (size_t i = 0; i < h.size(); ++i) h[i] *= kv.second[i];
+      st->ev_clique[v] = owner[v];
+    }
+  }
+  // upload masks (f64 staging → storage type)
+  int64_t tot = 0;
+  for (auto& kv : masks) tot += (int64_t)kv.second.size();
+  int rc = ensure_stage(st, tot);
+  if (rc) return rc;
+  hbuf.reserve(tot);
+  for (auto& kv : masks) {
+    const auto& src = st->mode == JT_SHARED_BASE ? st->ev_host[kv.first] : kv.second;
+    for (float x : src) hbuf.push_back(x);
+  }
+  CK(cudaMemcpyAsync(st->d_stage, hbuf.data(), tot * 8, cudaMemcpyHostToDevice, s));
+  int64_t o = 0;
+  for (auto& kv : masks) {
+    char* dst = (char*)st->d_aux + st->ev_off[kv.first] * st->esz;
+    CK(launch_convert_d2t(p->dtype, st->d_stage + o, dst, (int64_t)kv.second.size(), 1, 1, s));
+    o += (int64_t)kv.second.size();
+  }
+  if (st->mode == JT_SHARED_BASE) {
+    CK(cudaStreamSynchronize(s));  // hbuf lifetime
+    return JT_OK;
+  }
+  // materialized: multiply the masks into the owning cliques now
+  std::map<int, std::vector<int>> by_clique;
+  for (auto& kv : owner) by_clique[kv.second].push_back(kv.first);
+  std::vector<std::vector<PassSpec>> waves;
+  std::vector<int> kk;
+  for (auto& kv : by_clique) {
+    kk.push_back(kv.first);
+    for (size_t i = 0; i < kv.second.size(); i += MAXF) {
+      PassSpec ps;
+      ps.clique = kv.first;
+      ps.src_arena = A_CLIQUE;
+      ps.write = true;
+      for (size_t k = i; k < std::min(kv.second.size(), i + MAXF); ++k) {
+        ps.factors.push_back(ev_tensor(st, kv.second[k]));
+        kk.push_back(kv.second[k]);
+      }
+      const size_t wi = i / MAXF;
+      if (waves.size() <= wi) waves.resize(wi + 1);
+      waves[wi].push_back(ps);
+    }
+    kk.push_back(-1);
+  }
+  Program* pr;
+  rc = get_program(st, key_of("ev", kk), waves, &pr);
+  if (rc) return rc;
+  rc = run_program(st, pr, s);
+  CK(cudaStreamSynchronize(s));  // hbuf lifetime
+  return rc;
+}
+
+extern "C" int jt_message(jt_state* st, int src, int tgt, int sep, void* stream) {
+  if (!st) return JT_ERR_BAD_ARG;
+  const jt_plan* p = st->plan;
+  if (src < 0 || tgt < 0 || sep < 0 || src >= p->n_cliques || tgt >= p->n_cliques || sep >= p->n_seps)
+    return JT_ERR_BAD_ARG;
+  const auto& e = p->sedge[sep];
+  if (!((e[0] == src && e[1] == tgt) || (e[0] == tgt && e[1] == src))) return JT_ERR_BAD_ARG;
+  if (st->mode != JT_MATERIALIZED) return JT_ERR_UNSUPPORTED;
+  DevGuard g(p->device);
+  Program* pr;
+  auto it = st->programs.find(key_of("msg", {src, tgt, sep}));
+  if (it != st->programs.end()) {
+    pr = it->second.get();
+  } else {
+    std::vector<std::vector<PassSpec>> waves(2);
+    PassSpec m;
+    m.clique = src;
+    m.out_kind = OUT_SEP;
+    m.out = sep_tensor(st, sep, st->sep_off[sep]);
+    m.ratio_off = st->msg_ratio_off;
+    waves[0].push_back(m);
+    PassSpec sc;
+    sc.clique = tgt;
+    sc.write = true;
+    sc.factors.push_back(sep_tensor(st, sep, st->msg_ratio_off));
+    waves[1].push_back(sc);
+    int rc = get_program(st, key_of("msg", {src, tgt, sep}), waves, &pr);
+    if (rc) return rc;
+  }
+  return run_program(st, pr, pick_stream(st, stream));
+}
+
+static int resolve_roots(const jt_state* st, const int32_t* roots_or_null, std::vector<int>& roots) {
+  const jt_plan* p = st->plan;
+  roots = p->roots;
+  if (roots_or_null) {
+    for (size_t i = 0; i < roots.size(); ++i) {
+      const int r = roots_or_null[i];
+      if (r < 0 || r >= p->n_cliques || p->comp[r] != (int)i) return JT_ERR_BAD_ARG;
+      roots[i] = r;
+    }
+  }
+  return JT_OK;
+}
+
+extern "C" int jt_propagate(jt_state* st, const int32_t* roots_or_null, void* stream) {
+  if (!st) return JT_ERR_BAD_ARG;
+  DevGuard g(st->plan->device);
+  std::vector<int> roots;
+  int rc = resolve_roots(st, roots_or_null, roots);
+  if (rc) return rc;
+  const std::string key = key_of("bp", roots, active_ev(st));
+  Program* pr;
+  auto it = st->programs.find(key);
+  if (it != st->programs.end()) {
+    pr = it->second.get();
+  } else {
+    std::vector<std::vector<PassSpec>> waves;
+    rc = build_propagate(st, roots, {}, waves);
+    if (rc) return rc;
+    rc = get_program(st, key, waves, &pr);
+    if (rc) return rc;
+  }
+  return run_program(st, pr, pick_stream(st, stream));
+}
+
+static int smallest_holder(const jt_plan* p, int v) {
+  int best = -1;
+  for (int c = 0; c < p->n_cliques; ++c)
+    if (std::binary_search(p->cvars[c].begin(), p->cvars[c].end(), v))
+      if (best < 0 || p->csize[c] < p->csize[best]) best = c;
+  return best;
+}
+
+// raw marginals are already in qout; normalize into out_device [B][Σcard].
+// Per-variable-list metadata is uploaded once and cached, so this is async.
+static int finish_query(jt_state* st, int n, const int32_t* var, int normalize, double* out_device,
+                        cudaStream_t s, int* total_cols_out) {
+  const jt_plan* p = st->plan;
+  std::vector<int> vs(var, var + n);
+  const std::string key = key_of("qm", vs);
+  auto it = st->qmeta.find(key);
+  if (it == st->qmeta.end()) {
+    std::vector<int64_t> meta(3 * (size_t)n + 4);
+    int64_t* qo = meta.data();
+    int32_t* qc = reinterpret_cast<int32_t*>(meta.data() + n);
+    int32_t* qcol = qc + n;
+    int cols = 0;
+    for (int i = 0; i < n; ++i) {
+      qo[i] = st->q_off[var[i]];
+      qc[i] = p->cards[var[i]];
+      qcol[i] = cols;
+      cols += p->cards[var[i]];
+    }
+    int64_t* d = nullptr;
+    CK(cudaMalloc(&d, meta.size() * sizeof(int64_t)));
+    CK(cudaMemcpy(d, meta.data(), meta.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    it = st->qmeta.emplace(key, std::make_pair(d, cols)).first;
+  }
+  const int64_t* dqo = it->second.first;
+  const int32_t* dqc = reinterpret_cast<const int32_t*>(dqo + n);
+  const int32_t* dqcol = dqc + n;
+  const int cols = it->second.second;
+  CK(launch_normalize(st->d_qout, dqo, dqc, dqcol, n, st->B, cols, normalize, out_device, st->d_err, s));
+  st->launches++;
+  if (total_cols_out) *total_cols_out = cols;
+  return JT_OK;
+}
+
+static int query_program(jt_state* st, int n, const int32_t* var, const int32_t* clique, cudaStream_t s) {
+  const jt_plan* p = st->plan;
+  std::vector<int> vs, cs;
+  for (int i = 0; i < n; ++i) {
+    const int v = var[i];
+    if (v < 0 || v >= p->n_vars) return JT_ERR_BAD_ARG;
+    int c = clique ? clique[i] : -1;
+    if (c < 0) c = smallest_holder(p, v);
+    if (c < 0) return JT_ERR_BAD_ARG;
+    if (!std::binary_search(p->cvars[c].begin(), p->cvars[c].end(), v)) return JT_ERR_BAD_ARG;
+    vs.push_back(v);
+    cs.push_back(c);
+  }
+  std::vector<int> kk = vs;
+  kk.insert(kk.end(), cs.begin(), cs.end());
+  const bool shared = st->mode == JT_SHARED_BASE;
+  std::string key = key_of("q", kk, active_ev(st));
+  Program* pr;
+  auto it = st->programs.find(key);
+  if (it != st->programs.end()) {
+    pr = it->second.get();
+  } else {
+    std::vector<std::vector<PassSpec>> waves(1);
+    Orient o;
+    if (shared) o = orient(p, p->roots);
+    for (int i = 0; i < n; ++i) {
+      PassSpec ps;
+      ps.clique = cs[i];
+      ps.src_arena = shared ? A_BASE : A_CLIQUE;
+      ps.out_kind = OUT_RAW;
+      ps.out = var_out_tensor(st, vs[i]);
+      if (shared) {
+        // final table of the clique = base × evidence × Π neighbour ratios
+        const int c = cs[i];
+        for (auto& ch : o.children[c]) ps.factors.push_back(sep_tensor(st, ch.second, st->ratC_off[ch.second]));
+        if (o.parent[c] >= 0) ps.factors.push_back(sep_tensor(st, o.psep[c], st->ratD_off[o.psep[c]]));
+        for (int v = 0; v < p->n_vars; ++v)
+          if (st->ev_clique[v] == c) ps.factors.push_back(ev_tensor(st, v));
+      }
+      waves[0].push_back(ps);
+    }
+    int rc = get_program(st, key, waves, &pr);
+    if (rc) return rc;
+  }
+  return run_program(st, pr, s);
+}
+
+extern "C" int jt_query_device(jt_state* st, int n, const int32_t* var, const int32_t* clique, int normalize,
+                               double* out_device, void* stream) {
+  if (!st || n < 0 || !out_device) return JT_ERR_BAD_ARG;
+  if (n == 0) return JT_OK;
+  DevGuard g(st->plan->device);
+  cudaStream_t s = pick_stream(st, stream);
+  int rc = query_program(st, n, var, clique, s);
+  if (rc) return rc;
+  return finish_query(st, n, var, normalize, out_device, s, nullptr);
+}
+
+extern "C" int jt_query(jt_state* st, int n, const int32_t* var, const int32_t* clique, int normalize,
+                        double* out_host, void* stream) {
+  if (!st || n < 0 || !out_host) return JT_ERR_BAD_ARG;
+  if (n == 0) return JT_OK;
+  DevGuard g(st->plan->device);
+  const jt_plan* p = st->plan;
+  int64_t cols = 0;
+  for (int i = 0; i < n; ++i) {
+    if (var[i] < 0 || var[i] >= p->n_vars) return JT_ERR_BAD_ARG;
+    cols += p->cards[var[i]];
+  }
+  const int64_t need = cols * st->B;
+  if (need > st->post_cap) {
+    cudaFree(st->d_post);
+    st->d_post = nullptr;
+    CK(cudaMalloc(&st->d_post, need * sizeof(double)));
+    st->post_cap = need;
+  }
+  cudaStream_t s = pick_stream(st, stream);
+  int rc = jt_query_device(st, n, var, clique, normalize, st->d_post, s);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(out_host, st->d_post, need * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return JT_OK;
+}
+
+extern "C" int jt_propagate_query(jt_state* st, int n, const int32_t* var, int normalize, double* out_device,
+                                  void* stream) {
+  if (!st || n < 0 || (n > 0 && !out_device)) return JT_ERR_BAD_ARG;
+  const jt_plan* p = st->plan;
+  DevGuard g(p->device);
+  std::vector<int> vs;
+  for (int i = 0; i < n; ++i) {
+    if (var[i] < 0 || var[i] >= p->n_vars) return JT_ERR_BAD_ARG;
+    vs.push_back(var[i]);
+  }
+  if (st->mode != JT_SHARED_BASE) {
+    int rc = jt_propagate(st, nullptr, stream);
+    if (rc) return rc;
+    return n ? jt_query_device(st, n, var, nullptr, normalize, out_device, stream) : JT_OK;
+  }
+  const std::string key = key_of("bpq", vs, active_ev(st));
+  Program* pr;
+  auto it = st->programs.find(key);
+  if (it != st->programs.end()) {
+    pr = it->second.get();
+  } else {
+    std::vector<std::vector<PassSpec>> waves;
+    int rc = build_propagate(st, p->roots, vs, waves);
+    if (rc) return rc;
+    rc = get_program(st, key, waves, &pr);
+    if (rc) return rc;
+  }
+  cudaStream_t s = pick_stream(st, stream);
+  int rc = run_program(st, pr, s);
+  if (rc) return rc;
+  return n ? finish_query(st, n, var, normalize, out_device, s, nullptr) : JT_OK;
+}
+
+extern "C" int jt_sync_error(jt_state* st) {
+  if (!st) return JT_ERR_BAD_ARG;
+  DevGuard g(st->plan->device);
+  CK(cudaDeviceSynchronize());
+  int h = 0;
+  CK(cudaMemcpy(&h, st->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemset(st->d_err, 0, sizeof(int)));
+  if (h & EB_INCONSISTENT) return JT_ERR_INCONSISTENT_DIVISION;
+  if (h & EB_ZERO_MASS) return JT_ERR_ZERO_MASS;
+  return JT_OK;
+}
+
+extern "C" const char* jt_error_string(int code) {
+  switch (code) {
+    case JT_OK: return "ok";
+    case JT_ERR_BAD_ARG: return "bad argument";
+    case JT_ERR_INCONSISTENT_DIVISION: return "separator entry is zero but its fresh marginal is not";
+    case JT_ERR_ZERO_MASS: return "cannot normalize a zero-mass table";
+    case JT_ERR_CUDA: return cudaGetErrorString(last_cuda_error());
+    case JT_ERR_OOM: return "device out of memory";
+    case JT_ERR_UNSUPPORTED: return "unsupported configuration";
+    default: return "unknown error";
+  }
+}
+
+extern "C" int jt_plan_mapping_table(const jt_plan* p, int clique, int sep, int64_t* out_host) {
+  if (!p || !out_host || clique < 0 || clique >= p->n_cliques || sep < 0 || sep >= p->n_seps) return JT_ERR_BAD_ARG;
+  const auto& cv = p->cvars[clique];
+  const auto& sv = p->svars[sep];
+  for (int v : sv)
+    if (!std::binary_search(cv.begin(), cv.end(), v)) return JT_ERR_BAD_ARG;
+  DevGuard g(p->device);
+  std::vector<int64_t> stride(cv.size(), 1);
+  for (int i = (int)cv.size() - 2; i >= 0; --i) stride[i] = stride[i + 1] * p->cards[cv[i + 1]];
+  std::vector<int64_t> sc, ss, rc_, rs;
+  for (int v : sv) {  // separator order (compiler.py:294-299)
+    const int pos = (int)(std::find(cv.begin(), cv.end(), v) - cv.begin());
+    sc.push_back(p->cards[v]);
+    ss.push_back(stride[pos]);
+  }
+  for (size_t i = 0; i < cv.size(); ++i)  // remaining positions ascending (288-292)
+    if (!std::binary_search(sv.begin(), sv.end(), cv[i])) {
+      rc_.push_back(p->cards[cv[i]]);
+      rs.push_back(stride[i]);
+    }
+  const int64_t n_sep = p->ssize[sep], n_rest = p->csize[clique] / std::max<int64_t>(1, p->ssize[sep]);
+  int64_t* d = nullptr;
+  CK(cudaMalloc(&d, std::max<int64_t>(1, n_sep * n_rest) * sizeof(int64_t)));
+  cudaError_t e = launch_mapping_table(d, n_sep, n_rest, (int)sc.size(), sc.data(), ss.data(), (int)rc_.size(),
+                                       rc_.data(), rs.data(), nullptr);
+  if (e == cudaSuccess) e = cudaMemcpy(out_host, d, n_sep * n_rest * sizeof(int64_t), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) {
+    last_cuda_error() = e;
+    return JT_ERR_CUDA;
+  }
+  return JT_OK;
+}
+
+// engine protocol: one message on host arrays through device buffers
+struct MuScratch {
+  int device = -1;
+  void* buf = nullptr;
+  size_t cap = 0;
+  int* err = nullptr;
+  cudaStream_t s = nullptr;
+};
+
+extern "C" int jt_run_message_mu(const double* phi_src, int64_t n_src, double* phi_tgt, int64_t n_tgt, double* phi_sep,
+                                 int64_t n_sep, const void* mu_src, int64_t row_src, const void* mu_tgt,
+                                 int64_t row_tgt, int mu_is_int64, int device) {
+  if (!phi_src || !phi_tgt || !phi_sep || !mu_src || !mu_tgt || n_sep < 0 || row_src < 0 || row_tgt < 0)
+    return JT_ERR_BAD_ARG;
+  if (n_sep * row_src != n_src || n_sep * row_tgt != n_tgt) return JT_ERR_BAD_ARG;
+  static std::mutex mtx;
+  static std::map<int, MuScratch> scratch;
+  std::lock_guard<std::mutex> lock(mtx);
+  DevGuard g(device);
+  MuScratch& m = scratch[device];
+  const size_t isz = mu_is_int64 ? 8 : 4;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t need = al(n_src * 8) + al(n_tgt * 8) + al(n_sep * 8) * 2 + al(n_src * isz) + al(n_tgt * isz) + 256;
+  if (!m.s) {
+    CK(cudaStreamCreateWithFlags(&m.s, cudaStreamNonBlocking));
+    CK(cudaMalloc(&m.err, sizeof(int)));
+  }
+  if (need > m.cap) {
+    cudaFree(m.buf);
+    m.buf = nullptr;
+    m.cap = 0;
+    CK(cudaMalloc(&m.buf, need));
+    m.cap = need;
+  }
+  char* b = (char*)m.buf;
+  double* d_src = (double*)b; b += al(n_src * 8);
+  double* d_tgt = (double*)b; b += al(n_tgt * 8);
+  double* d_sep = (double*)b; b += al(n_sep * 8);
+  double* d_ratio = (double*)b; b += al(n_sep * 8);
+  void* d_mus = b; b += al(n_src * isz);
+  void* d_mut = b;
+  cudaStream_t s = m.s;
+  CK(cudaMemsetAsync(m.err, 0, sizeof(int), s));
+  CK(cudaMemcpyAsync(d_src, phi_src, n_src * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_sep, phi_sep, n_sep * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_mus, mu_src, n_src * isz, cudaMemcpyHostToDevice, s));
+  CK(launch_mu_message(d_src, nullptr, d_sep, d_ratio, d_mus, row_src, nullptr, row_tgt, n_sep, mu_is_int64, m.err, 0, s));
+  int herr = 0;
+  CK(cudaMemcpyAsync(&herr, m.err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (herr & EB_INCONSISTENT) return JT_ERR_INCONSISTENT_DIVISION;  // nothing written back
+  CK(cudaMemcpyAsync(d_tgt, phi_tgt, n_tgt * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_mut, mu_tgt, n_tgt * isz, cudaMemcpyHostToDevice, s));
+  CK(launch_mu_message(nullptr, d_tgt, d_sep, d_ratio, nullptr, row_src, d_mut, row_tgt, n_sep, mu_is_int64, m.err, 1, s));
+  CK(cudaMemcpyAsync(phi_tgt, d_tgt, n_tgt * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(phi_sep, d_sep, n_sep * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return JT_OK;
+}
+
+extern "C" const char* jt_version(void) { return "libjtb200 0.1 sm_100a"; }

@@ -1,0 +1,92 @@
+// Internal types shared by the host planner (jt_plan.cpp) and the kernels
+// (jt_kernels.cu).  See DESIGN.md §3 for the pass/wave model.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace jt {
+
+constexpr int NT = 256;     // threads per CTA of the wave kernel
+constexpr int KV = 4;       // vectors owned per thread per iteration
+constexpr int MAXF = 8;     // factors (ratio / evidence tensors) multiplied in per pass
+constexpr int MAXDI = 8;    // merged inner dimensions per pass
+
+enum ArenaId : int { A_CLIQUE = 0, A_BASE = 1, A_AUX = 2 };
+enum OutKind : int { OUT_NONE = 0, OUT_SEP = 1, OUT_RAW = 2 };
+enum ErrBits : int { EB_INCONSISTENT = 1, EB_ZERO_MASS = 2 };
+
+// One pass = one sweep over one clique table: read (src), multiply the
+// factors in, optionally write (dst), optionally reduce onto one output
+// tensor.  The clique is seen as [outer blocks] x [inner block of T positions].
+struct DevPass {
+  int64_t src_off;          // element offset of the clique in the src arena
+  int64_t dst_off;          // element offset in the clique arena, -1: no write
+  int64_t fac_off[MAXF];    // element offsets of the factor tensors (aux arena)
+  int64_t out_off;          // aux (OUT_SEP) or qout (OUT_RAW) offset of the output
+  int64_t ratio_off;        // aux offset of the ratio array written by OUT_SEP
+  int64_t blk_off;          // offset into the block table (int64 entries)
+  int64_t bin_off;          // offset into the bin table (int32: binbase[n_in], binrest[T/n_in])
+  int64_t part_off;         // offset into the partials arena (doubles)
+  int64_t cnt_off;          // offset into the counters arena (ints)
+  int64_t n_blocks_per_jout;// rest-outer blocks per output group (r_out)
+  int64_t blocks_per_chunk; // multiple of BPI
+  int src_arena;            // A_CLIQUE or A_BASE
+  int src_vec;              // 1: innermost stride 1 (vector load), 0: broadcast
+  int nf;
+  uint32_t fac_vec;         // bit f set: factor f has the innermost dim (vector), else broadcast
+  int out_kind;
+  int n_in;                 // output bins per block
+  int n_chunks;
+  int T;                    // positions per block (multiple of VEC)
+  int BPI;                  // blocks per CTA iteration
+  int blk_stride;           // 2 + nf
+  int ndi;                  // merged inner dims
+  int icard[MAXDI];         // innermost last
+  int isrc[MAXDI];
+  int idst[MAXDI];
+  int iout[MAXDI];
+  int ifac[MAXF][MAXDI];
+};
+
+struct Item {               // one CTA work unit
+  int pass;
+  int chunk;
+  int64_t j_out;
+};
+
+struct WaveArgs {
+  void* clique;             // T*
+  const void* base;         // const T*
+  void* aux;                // T*
+  double* qout;
+  double* partials;
+  int* counters;
+  int* err;
+  const int64_t* blk;
+  const int32_t* bins;
+  const DevPass* passes;
+  const Item* items;
+  int n_items;
+};
+
+// launchers (jt_kernels.cu)
+cudaError_t launch_wave(int dtype, int vec, const WaveArgs& a, int grid, cudaStream_t s);
+int wave_max_ctas_per_sm(int dtype, int vec);
+cudaError_t launch_normalize(const double* qout, const int64_t* q_off, const int32_t* q_card,
+                             const int32_t* q_col, int nq, int B, int total_cols,
+                             int normalize, double* post, int* err, cudaStream_t s);
+cudaError_t launch_convert_d2t(int dtype, const double* src, void* dst, int64_t n,
+                               int64_t dst_stride, int64_t bcount, cudaStream_t s);
+cudaError_t launch_convert_t2d(int dtype, const void* src, int64_t src_stride,
+                               double* dst, int64_t n, cudaStream_t s);
+cudaError_t launch_fill(int dtype, void* dst, int64_t n, double v, cudaStream_t s);
+cudaError_t launch_mapping_table(int64_t* out, int64_t n_sep, int64_t n_rest,
+                                 int nsd, const int64_t* sep_card, const int64_t* sep_stride,
+                                 int nrd, const int64_t* rest_card, const int64_t* rest_stride,
+                                 cudaStream_t s);
+cudaError_t launch_mu_message(const double* src, double* tgt, double* sep, double* ratio,
+                              const void* mu_src, int64_t row_src, const void* mu_tgt,
+                              int64_t row_tgt, int64_t n_sep, int is64, int* err,
+                              int phase, cudaStream_t s);
+
+}  // namespace jt

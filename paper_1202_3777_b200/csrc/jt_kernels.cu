@@ -1,0 +1,546 @@
+// Device kernels of the B200 junction-tree engine (sm_100a).
+//
+// wave_kernel  — one launch per scheduler wave; every CTA walks a list of work
+//   items, each a contiguous run of blocks of one *pass* (one sweep over one
+//   clique table).  Per element: read the clique (or the shared base replica),
+//   multiply the factor tensors in (separator ratios new/old of Alg. 1 step 2,
+//   evidence masks), optionally write it back, and accumulate it into its
+//   output separator entry (Alg. 1 step 1, Eq. 2).  Index maps are never read:
+//   the separator/ratio indices come from stride arithmetic on the block's
+//   outer offsets (host-precomputed per block) plus per-thread inner offsets.
+//   Reductions are fixed-order (per-thread sequential → smem tree → chunk
+//   order), so results are run-to-run deterministic.  The last CTA of an output
+//   group sums the chunk partials and applies the Hugin update
+//   (ratio = star/old with 0/0 = 0, nonzero/0 flagged; propagate.py:67-76).
+#include "jt_internal.h"
+#include <cfloat>
+
+namespace jt {
+
+template <typename T, int VEC> struct VecT;
+template <> struct VecT<float, 4> { using type = float4; };
+template <> struct VecT<float, 2> { using type = float2; };
+template <> struct VecT<float, 1> { using type = float; };
+template <> struct VecT<double, 2> { using type = double2; };
+template <> struct VecT<double, 1> { using type = double; };
+
+template <typename T, int VEC>
+__device__ __forceinline__ void load_vec(const T* p, T (&v)[VEC]) {
+  using V = typename VecT<T, VEC>::type;
+  V x = *reinterpret_cast<const V*>(p);
+  const T* xs = reinterpret_cast<const T*>(&x);
+#pragma unroll
+  for (int l = 0; l < VEC; ++l) v[l] = xs[l];
+}
+
+template <typename T, int VEC>
+__device__ __forceinline__ void load_vec_ro(const T* p, T (&v)[VEC]) {
+  using V = typename VecT<T, VEC>::type;
+  V x = __ldg(reinterpret_cast<const V*>(p));
+  const T* xs = reinterpret_cast<const T*>(&x);
+#pragma unroll
+  for (int l = 0; l < VEC; ++l) v[l] = xs[l];
+}
+
+template <typename T, int VEC>
+__device__ __forceinline__ void store_vec(T* p, const T (&v)[VEC]) {
+  using V = typename VecT<T, VEC>::type;
+  V x;
+  T* xs = reinterpret_cast<T*>(&x);
+#pragma unroll
+  for (int l = 0; l < VEC; ++l) xs[l] = v[l];
+  *reinterpret_cast<V*>(p) = x;
+}
+
+__device__ __forceinline__ double warp_sum(double s) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
+// out[b] = Σ_{r<R} get(b, r), r ascending per thread-group, groups combined in
+// order: deterministic for a given (n_bins, R).  `out` may alias get's source.
+template <class F>
+__device__ __forceinline__ void reduce_bins(F get, int n_bins, int R, double* out, double* part2) {
+  const int tid = threadIdx.x;
+  if (n_bins >= NT) {
+    constexpr int MAXU = (NT * KV * 4) / NT;
+    double res[MAXU];
+#pragma unroll
+    for (int u = 0; u < MAXU; ++u) {
+      const int b = tid + u * NT;
+      double s = 0.0;
+      if (b < n_bins)
+        for (int r = 0; r < R; ++r) s += get(b, r);
+      res[u] = s;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < MAXU; ++u) {
+      const int b = tid + u * NT;
+      if (b < n_bins) out[b] = res[u];
+    }
+    __syncthreads();
+  } else {
+    int G = NT / n_bins;
+    if (G > R) G = R;
+    if (G < 1) G = 1;
+    double s = 0.0;
+    if (tid < n_bins * G) {
+      const int b = tid / G, g = tid - (tid / G) * G;
+      for (int r = g; r < R; r += G) s += get(b, r);
+      part2[tid] = s;
+    }
+    __syncthreads();
+    if (tid < n_bins) {
+      double t = 0.0;
+      for (int g = 0; g < G; ++g) t += part2[tid * G + g];
+      out[tid] = t;
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void finalize_entry(const DevPass& P, int64_t j, double star, T* aux,
+                                               double* qout, int* err) {
+  if (P.out_kind == OUT_SEP) {
+    const double old = (double)aux[P.out_off + j];
+    if (old == 0.0 && star != 0.0) atomicOr(err, EB_INCONSISTENT);
+    const double r = (old != 0.0) ? star / old : 0.0;
+    aux[P.ratio_off + j] = (T)r;
+    aux[P.out_off + j] = (T)star;
+  } else {
+    qout[P.out_off + j] = star;
+  }
+}
+
+template <typename T, int VEC>
+__global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
+  constexpr int TH = NT * KV * VEC;  // positions per CTA iteration
+  __shared__ DevPass P;
+  __shared__ double part2[NT];
+  __shared__ int s_last;
+  extern __shared__ __align__(16) double dsm[];
+  double* red = dsm;                                              // [TH] block partials
+  uint16_t (*s_qfac)[KV][NT] = reinterpret_cast<uint16_t (*)[KV][NT]>(dsm + TH);  // inner factor offsets
+
+  T* __restrict__ clique = reinterpret_cast<T*>(a.clique);
+  const T* __restrict__ base = reinterpret_cast<const T*>(a.base);
+  T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
+  const int tid = threadIdx.x;
+
+  int cur = -1;
+  int q_slot[KV];
+  bool q_ok[KV];
+  int q_src[KV], q_dst[KV];
+
+  for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
+    const Item item = a.items[it];
+    if (item.pass != cur) {
+      __syncthreads();
+      const int* sw = reinterpret_cast<const int*>(a.passes + item.pass);
+      int* dw = reinterpret_cast<int*>(&P);
+      for (int w = tid; w < (int)(sizeof(DevPass) / 4); w += NT) dw[w] = sw[w];
+      __syncthreads();
+      cur = item.pass;
+      const int TV = P.T / VEC;
+      const int nq = P.BPI * TV;
+#pragma unroll
+      for (int k = 0; k < KV; ++k) {
+        const int q = tid + k * NT;
+        q_ok[k] = q < nq;
+        const int slot = q_ok[k] ? q / TV : 0;
+        const int iv = q_ok[k] ? q - slot * TV : 0;
+        q_slot[k] = slot;
+        int rem = iv * VEC, s = 0, dd = 0;
+        int fo[MAXF];
+#pragma unroll
+        for (int f = 0; f < MAXF; ++f) fo[f] = 0;
+        for (int d = P.ndi - 1; d >= 0; --d) {
+          const int c = P.icard[d];
+          const int dig = rem % c;
+          rem /= c;
+          s += dig * P.isrc[d];
+          dd += dig * P.idst[d];
+#pragma unroll
+          for (int f = 0; f < MAXF; ++f)
+            if (f < P.nf) fo[f] += dig * P.ifac[f][d];
+        }
+        q_src[k] = s;
+        q_dst[k] = dd;
+#pragma unroll
+        for (int f = 0; f < MAXF; ++f) s_qfac[f][k][tid] = (uint16_t)fo[f];
+      }
+    }
+
+    const int64_t jb = item.j_out * P.n_blocks_per_jout;
+    const int64_t b0 = jb + (int64_t)item.chunk * P.blocks_per_chunk;
+    int64_t b1 = b0 + P.blocks_per_chunk;
+    if (b1 > jb + P.n_blocks_per_jout) b1 = jb + P.n_blocks_per_jout;
+    const T* __restrict__ srcA = (P.src_arena == A_BASE ? base : clique) + P.src_off;
+    const bool wr = P.dst_off >= 0;
+    T* __restrict__ dstA = clique + (wr ? P.dst_off : 0);
+    const int64_t* __restrict__ blk = a.blk + P.blk_off;
+    const int bs = P.blk_stride;
+    const int nf = P.nf;
+
+    double acc[KV][VEC];
+#pragma unroll
+    for (int k = 0; k < KV; ++k)
+#pragma unroll
+      for (int l = 0; l < VEC; ++l) acc[k][l] = 0.0;
+
+    for (int64_t bb = b0; bb < b1; bb += P.BPI) {
+      T v[KV][VEC];
+      const int64_t* e[KV];
+      bool ok[KV];
+#pragma unroll
+      for (int k = 0; k < KV; ++k) {
+        const int64_t bi = bb + q_slot[k];
+        ok[k] = q_ok[k] && bi < b1;
+        e[k] = blk + (ok[k] ? bi : b0) * bs;
+        if (ok[k]) {
+          const T* p = srcA + e[k][0] + q_src[k];
+          if (VEC == 1 || P.src_vec) {
+            load_vec<T, VEC>(p, v[k]);
+          } else {
+            const T x = *p;
+#pragma unroll
+            for (int l = 0; l < VEC; ++l) v[k][l] = x;
+          }
+        } else {
+#pragma unroll
+          for (int l = 0; l < VEC; ++l) v[k][l] = (T)0;
+        }
+      }
+#pragma unroll
+      for (int f = 0; f < MAXF; ++f) {
+        if (f < nf) {
+          const T* fb = aux + P.fac_off[f];
+          const bool fv = (P.fac_vec >> f) & 1u;
+#pragma unroll
+          for (int k = 0; k < KV; ++k) {
+            if (ok[k]) {
+              const T* p = fb + e[k][2 + f] + s_qfac[f][k][tid];
+              T g[VEC];
+              if (VEC == 1 || fv) {
+                load_vec_ro<T, VEC>(p, g);
+              } else {
+                const T x = __ldg(p);
+#pragma unroll
+                for (int l = 0; l < VEC; ++l) g[l] = x;
+              }
+#pragma unroll
+              for (int l = 0; l < VEC; ++l) v[k][l] *= g[l];
+            }
+          }
+        }
+      }
+      if (wr) {
+#pragma unroll
+        for (int k = 0; k < KV; ++k)
+          if (ok[k]) store_vec<T, VEC>(dstA + e[k][1] + q_dst[k], v[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < KV; ++k)
+#pragma unroll
+        for (int l = 0; l < VEC; ++l) acc[k][l] += (double)v[k][l];
+    }
+
+    if (P.out_kind == OUT_NONE) continue;
+
+    // ---- block partials -> n_in bins (fixed order) ----
+    const int n_in = P.n_in;
+    if (n_in == 1) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < KV; ++k)
+#pragma unroll
+        for (int l = 0; l < VEC; ++l) s += acc[k][l];
+      s = warp_sum(s);
+      if ((tid & 31) == 0) part2[tid >> 5] = s;
+      __syncthreads();
+      if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < NT / 32; ++w) t += part2[w];
+        red[0] = t;
+      }
+      __syncthreads();
+    } else {
+#pragma unroll
+      for (int k = 0; k < KV; ++k) {
+        if (q_ok[k]) {
+          const int q = tid + k * NT;
+#pragma unroll
+          for (int l = 0; l < VEC; ++l) red[q * VEC + l] = acc[k][l];
+        }
+      }
+      __syncthreads();
+      if (!(P.BPI == 1 && n_in == P.T)) {
+        const int rest = P.T / n_in;
+        const int R = P.BPI * rest;
+        const int32_t* __restrict__ bbase = a.bins + P.bin_off;
+        const int32_t* __restrict__ brest = bbase + n_in;
+        const int T_ = P.T;
+        reduce_bins(
+            [&](int b, int r) {
+              const int slot = r / rest;
+              const int p = r - slot * rest;
+              return red[slot * T_ + bbase[b] + brest[p]];
+            },
+            n_in, R, red, part2);
+      }
+    }
+
+    // ---- output: direct or via chunk partials + last-CTA finalize ----
+    const int64_t j0 = item.j_out * (int64_t)n_in;
+    if (P.n_chunks == 1) {
+      for (int b = tid; b < n_in; b += NT) finalize_entry<T>(P, j0 + b, red[b], aux, a.qout, a.err);
+    } else {
+      double* part = a.partials + P.part_off + (item.j_out * P.n_chunks + item.chunk) * (int64_t)n_in;
+      for (int b = tid; b < n_in; b += NT) part[b] = red[b];
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        const int prev = atomicAdd(&a.counters[P.cnt_off + item.j_out], 1);
+        s_last = (prev == P.n_chunks - 1);
+      }
+      __syncthreads();
+      if (s_last) {
+        __threadfence();
+        const double* pj = a.partials + P.part_off + item.j_out * P.n_chunks * (int64_t)n_in;
+        reduce_bins([&](int b, int r) { return __ldcg(pj + (int64_t)r * n_in + b); }, n_in,
+                    P.n_chunks, red, part2);
+        for (int b = tid; b < n_in; b += NT) finalize_entry<T>(P, j0 + b, red[b], aux, a.qout, a.err);
+        if (tid == 0) a.counters[P.cnt_off + item.j_out] = 0;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int VEC>
+constexpr size_t wave_smem() {
+  return (size_t)NT * KV * VEC * sizeof(double) + (size_t)MAXF * KV * NT * sizeof(uint16_t);
+}
+
+template <typename T, int VEC>
+static cudaError_t launch_t(const WaveArgs& a, int grid, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(wave_kernel<T, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)wave_smem<VEC>());
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  wave_kernel<T, VEC><<<grid, NT, wave_smem<VEC>(), s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wave(int dtype, int vec, const WaveArgs& a, int grid, cudaStream_t s) {
+  if (grid <= 0 || a.n_items <= 0) return cudaSuccess;
+  if (dtype == 0) {
+    if (vec == 4) return launch_t<float, 4>(a, grid, s);
+    if (vec == 2) return launch_t<float, 2>(a, grid, s);
+    return launch_t<float, 1>(a, grid, s);
+  }
+  if (vec == 2) return launch_t<double, 2>(a, grid, s);
+  return launch_t<double, 1>(a, grid, s);
+}
+
+template <typename T, int VEC>
+static int occ_t() {
+  int n = 0;
+  cudaFuncSetAttribute(wave_kernel<T, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wave_smem<VEC>());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, wave_kernel<T, VEC>, NT, wave_smem<VEC>());
+  return n > 0 ? n : 1;
+}
+
+int wave_max_ctas_per_sm(int dtype, int vec) {
+  if (dtype == 0) {
+    if (vec == 4) return occ_t<float, 4>();
+    if (vec == 2) return occ_t<float, 2>();
+    return occ_t<float, 1>();
+  }
+  if (vec == 2) return occ_t<double, 2>();
+  return occ_t<double, 1>();
+}
+
+// ---- posteriors: raw marginals [var][card][B] -> normalized [B][Σcard] ----
+// normalize (potential.py:181-186): total <= 0 raises ZeroMassError; here the
+// case's row is NaN-filled and the zero-mass bit is set.
+__global__ void normalize_kernel(const double* __restrict__ qout, const int64_t* __restrict__ q_off,
+                                 const int32_t* __restrict__ q_card, const int32_t* __restrict__ q_col,
+                                 int nq, int B, int total_cols, int normalize,
+                                 double* __restrict__ post, int* err) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)nq * B) return;
+  const int i = (int)(idx / B);
+  const int b = (int)(idx - (int64_t)i * B);
+  const double* q = qout + q_off[i];
+  const int card = q_card[i];
+  double* o = post + (int64_t)b * total_cols + q_col[i];
+  double s = 0.0;
+  for (int d = 0; d < card; ++d) s += q[(int64_t)d * B + b];
+  if (!normalize) {
+    for (int d = 0; d < card; ++d) o[d] = q[(int64_t)d * B + b];
+    return;
+  }
+  if (!(s > 0.0)) {
+    atomicOr(err, EB_ZERO_MASS);
+    for (int d = 0; d < card; ++d) o[d] = __longlong_as_double(0x7ff8000000000000ULL);
+    return;
+  }
+  for (int d = 0; d < card; ++d) o[d] = q[(int64_t)d * B + b] / s;
+}
+
+cudaError_t launch_normalize(const double* qout, const int64_t* q_off, const int32_t* q_card,
+                             const int32_t* q_col, int nq, int B, int total_cols, int normalize,
+                             double* post, int* err, cudaStream_t s) {
+  const int64_t n = (int64_t)nq * B;
+  if (n == 0) return cudaSuccess;
+  normalize_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(qout, q_off, q_card, q_col, nq, B,
+                                                               total_cols, normalize, post, err);
+  return cudaGetLastError();
+}
+
+// ---- host<->arena conversion (f64 staging <-> storage type, batch lanes) ----
+template <typename T>
+__global__ void d2t_kernel(const double* __restrict__ src, T* __restrict__ dst, int64_t n,
+                           int64_t stride, int64_t bcount) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * bcount) return;
+  const int64_t e = idx / bcount, l = idx - (idx / bcount) * bcount;
+  dst[e * stride + l] = (T)src[e];
+}
+
+template <typename T>
+__global__ void t2d_kernel(const T* __restrict__ src, int64_t stride, double* __restrict__ dst, int64_t n) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx < n) dst[idx] = (double)src[idx * stride];
+}
+
+template <typename T>
+__global__ void fill_kernel(T* dst, int64_t n, double v) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx < n) dst[idx] = (T)v;
+}
+
+cudaError_t launch_convert_d2t(int dtype, const double* src, void* dst, int64_t n, int64_t stride,
+                               int64_t bcount, cudaStream_t s) {
+  const int64_t tot = n * bcount;
+  if (tot == 0) return cudaSuccess;
+  const unsigned g = (unsigned)((tot + 255) / 256);
+  if (dtype == 0) d2t_kernel<float><<<g, 256, 0, s>>>(src, (float*)dst, n, stride, bcount);
+  else d2t_kernel<double><<<g, 256, 0, s>>>(src, (double*)dst, n, stride, bcount);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_convert_t2d(int dtype, const void* src, int64_t stride, double* dst, int64_t n,
+                               cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const unsigned g = (unsigned)((n + 255) / 256);
+  if (dtype == 0) t2d_kernel<float><<<g, 256, 0, s>>>((const float*)src, stride, dst, n);
+  else t2d_kernel<double><<<g, 256, 0, s>>>((const double*)src, stride, dst, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill(int dtype, void* dst, int64_t n, double v, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const unsigned g = (unsigned)((n + 255) / 256);
+  if (dtype == 0) fill_kernel<float><<<g, 256, 0, s>>>((float*)dst, n, v);
+  else fill_kernel<double><<<g, 256, 0, s>>>((double*)dst, n, v);
+  return cudaGetLastError();
+}
+
+// ---- K0: device μ builder, μ[j][p] = row_base(j) + rest(p) (compiler.py:285-304) ----
+struct MuDims {
+  int nsd, nrd;
+  int64_t sc[32], ss[32], rc[32], rs[32];
+};
+
+__global__ void mapping_table_kernel(int64_t* __restrict__ out, int64_t n_sep, int64_t n_rest, MuDims m) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_sep * n_rest) return;
+  int64_t j = idx / n_rest, p = idx - (idx / n_rest) * n_rest;
+  int64_t v = 0;
+  for (int d = m.nsd - 1; d >= 0; --d) {  // separator digits, separator order, last fastest
+    v += (j % m.sc[d]) * m.ss[d];
+    j /= m.sc[d];
+  }
+  for (int d = m.nrd - 1; d >= 0; --d) {  // remaining clique positions, ascending
+    v += (p % m.rc[d]) * m.rs[d];
+    p /= m.rc[d];
+  }
+  out[idx] = v;
+}
+
+cudaError_t launch_mapping_table(int64_t* out, int64_t n_sep, int64_t n_rest, int nsd,
+                                 const int64_t* sep_card, const int64_t* sep_stride, int nrd,
+                                 const int64_t* rest_card, const int64_t* rest_stride, cudaStream_t s) {
+  MuDims m;
+  if (nsd > 32 || nrd > 32) return cudaErrorInvalidValue;
+  m.nsd = nsd;
+  m.nrd = nrd;
+  for (int i = 0; i < nsd; ++i) { m.sc[i] = sep_card[i]; m.ss[i] = sep_stride[i]; }
+  for (int i = 0; i < nrd; ++i) { m.rc[i] = rest_card[i]; m.rs[i] = rest_stride[i]; }
+  const int64_t n = n_sep * n_rest;
+  if (n == 0) return cudaSuccess;
+  mapping_table_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(out, n_sep, n_rest, m);
+  return cudaGetLastError();
+}
+
+// ---- engine-protocol path: Alg. 1 driven by host μ tables (paper §3.2) ----
+// phase 0: one warp per separator entry j: star_j = Σ_p φ_src[μ_src[j][p]]
+//          (lane-strided, fixed shuffle order), error check, ratio, sep_j = star_j.
+// phase 1: one thread per (j, p): φ_tgt[μ_tgt[j][p]] *= ratio_j.
+template <typename I>
+__global__ void mu_marg_kernel(const double* __restrict__ src, double* __restrict__ sep,
+                               double* __restrict__ ratio, const I* __restrict__ mu, int64_t row,
+                               int64_t n_sep, int* err) {
+  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= n_sep) return;
+  double s = 0.0;
+  const I* m = mu + j * row;
+  for (int64_t p = lane; p < row; p += 32) s += src[m[p]];
+  s = warp_sum(s);
+  if (lane == 0) {
+    const double old = sep[j];
+    if (old == 0.0 && s != 0.0) atomicOr(err, EB_INCONSISTENT);
+    ratio[j] = (old != 0.0) ? s / old : 0.0;
+    sep[j] = s;
+  }
+}
+
+template <typename I>
+__global__ void mu_scatter_kernel(double* __restrict__ tgt, const double* __restrict__ ratio,
+                                  const I* __restrict__ mu, int64_t row, int64_t n_sep) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_sep * row) return;
+  const int64_t j = idx / row;
+  tgt[mu[idx]] *= ratio[j];
+}
+
+cudaError_t launch_mu_message(const double* src, double* tgt, double* sep, double* ratio,
+                              const void* mu_src, int64_t row_src, const void* mu_tgt,
+                              int64_t row_tgt, int64_t n_sep, int is64, int* err, int phase,
+                              cudaStream_t s) {
+  if (n_sep == 0) return cudaSuccess;
+  if (phase == 0) {
+    const int64_t threads = n_sep * 32;
+    const unsigned g = (unsigned)((threads + 255) / 256);
+    if (is64) mu_marg_kernel<int64_t><<<g, 256, 0, s>>>(src, sep, ratio, (const int64_t*)mu_src, row_src, n_sep, err);
+    else mu_marg_kernel<int32_t><<<g, 256, 0, s>>>(src, sep, ratio, (const int32_t*)mu_src, row_src, n_sep, err);
+  } else {
+    const int64_t n = n_sep * row_tgt;
+    if (n == 0) return cudaSuccess;
+    const unsigned g = (unsigned)((n + 255) / 256);
+    if (is64) mu_scatter_kernel<int64_t><<<g, 256, 0, s>>>(tgt, ratio, (const int64_t*)mu_tgt, row_tgt, n_sep);
+    else mu_scatter_kernel<int32_t><<<g, 256, 0, s>>>(tgt, ratio, (const int32_t*)mu_tgt, row_tgt, n_sep);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace jt

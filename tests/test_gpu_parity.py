@@ -1,0 +1,290 @@
+"""Parity of the CUDA path against the oracle / reference golden vectors.
+
+Tolerances (BASELINE.json north_star): posteriors within 1e-10 relative in the
+fp64 mode and 1e-5 relative in fp32.  Integer index maps are bit-exact.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_cases, load_corpus, load_golden
+from oracle import jtref
+from paper_1202_3777_b200 import synth
+from paper_1202_3777_b200.tree import build_tree
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f64": 1e-10, "f32": 1e-5}
+
+
+def P():
+    from paper_1202_3777_b200 import propagate
+
+    return propagate
+
+
+def rel_err(got, want):
+    got, want = np.asarray(got, float), np.asarray(want, float)
+    return float(np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-300))) if want.size else 0.0
+
+
+def all_posteriors(st, n):
+    return np.concatenate([P().query_marginal(st, v).values for v in range(n)])
+
+
+def demo(src=None, dtype="f64"):
+    tree = build_tree([(0, 1, 3), (1, 2)], (2, 2, 2, 2))
+    tables = [np.arange(8.0) if src is None else np.asarray(src, float), np.ones(4)]
+    return tree, P().from_potentials(tree, tables, engine=P().CudaEngine(dtype=dtype))
+
+
+class TestMessageKnownAnswers:  # test_propagate.py:53-89 through the device path
+    @pytest.mark.parametrize("dtype", ["f64", "f32"])
+    def test_worked_example(self, dtype):
+        tree, st = demo(dtype=dtype)
+        P().message_passing(st, P().Message(0, 1, 0))
+        assert st.sep_values[0].tolist() == [10.0, 18.0]
+        assert st.clique_values[1].tolist() == [10.0, 10.0, 18.0, 18.0]
+        assert st.clique_values[0].tolist() == list(range(8))
+
+    def test_zero_over_zero(self):
+        tree, st = demo([0, 0, 1, 2, 0, 0, 3, 4])
+        st.sep_values[0][:] = [0.0, 1.0]
+        st.clique_values[1][:] = [5.0, 6.0, 7.0, 8.0]
+        P().message_passing(st, P().Message(0, 1, 0))
+        assert st.clique_values[1].tolist() == [0.0, 0.0, 70.0, 80.0]
+        assert st.sep_values[0].tolist() == [0.0, 10.0]
+
+    def test_nonzero_over_zero_raises(self):
+        from paper_1202_3777_b200.errors import InconsistentDivisionError
+
+        tree, st = demo()
+        st.sep_values[0][:] = [0.0, 1.0]
+        with pytest.raises(InconsistentDivisionError):
+            P().message_passing(st, P().Message(0, 1, 0))
+
+    def test_fixed_point(self):
+        tree, st = demo(np.ones(8))
+        st.sep_values[0][:] = [4.0, 4.0]
+        before = st.clique_values[1].copy()
+        P().message_passing(st, P().Message(0, 1, 0))
+        assert np.array_equal(st.clique_values[1], before)
+
+    def test_mass_conservation(self):
+        rng = np.random.default_rng(0)
+        tree, st = demo(rng.uniform(size=8))
+        P().message_passing(st, P().Message(0, 1, 0))
+        assert st.sep_values[0].sum() == pytest.approx(st.clique_values[0].sum(), rel=1e-12)
+
+
+def test_device_mapping_tables_bit_exact():
+    for name in ("c1", "c3", "c5"):
+        tree, _ = load_golden(name)
+        plan = P().plan_for(tree, "f64")
+        for sep in tree.separators:
+            for cid in sep.edge:
+                c = tree.cliques[cid]
+                want = jtref.build_mapping_table(c.scope.ids, c.scope.cards, sep.scope.ids)
+                got = plan.mapping_table(cid, sep.id)
+                assert got.dtype == want.dtype and np.array_equal(got, want), (name, cid, sep.id)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c4M", "c5", "c4B", "c3"])
+def test_config_posteriors_vs_reference(name, dtype):
+    tree, data = load_golden(name)
+    tables = synth.scaled_potentials(tree, seed=0)
+    cases = golden_cases(data)
+    for ev, want in cases[:3]:
+        st = P().from_potentials(tree, tables, engine=P().CudaEngine(dtype=dtype))
+        if ev:
+            P().apply_evidence(st, ev)
+        P().belief_propagation(st)
+        got = all_posteriors(st, len(tree.cards))
+        assert rel_err(got, want) < TOL[dtype], (name, dtype, ev, rel_err(got, want))
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_final_tables_c1(dtype):
+    tree, data = load_golden("c1")
+    st = P().from_potentials(tree, synth.scaled_potentials(tree, 0), engine=P().CudaEngine(dtype=dtype))
+    P().belief_propagation(st)
+    assert rel_err(np.concatenate(st.clique_values), data["cliques0"]) < TOL[dtype] * 10
+    assert rel_err(np.concatenate(st.sep_values), data["sep0"]) < TOL[dtype] * 10
+
+
+def test_separator_tables_c5_vs_reference():
+    tree, data = load_golden("c5")
+    st = P().from_potentials(tree, synth.scaled_potentials(tree, 0))
+    P().belief_propagation(st)
+    seps = st.sep_values
+    assert rel_err([s.sum() for s in seps], data["sep_sums0"]) < 1e-10
+    assert rel_err([c.sum() for c in st.clique_values], data["clique_sums0"]) < 1e-10
+
+
+def test_corpus_initialized_networks():
+    for name, tree, tables, post, cliques, seps in load_corpus():
+        st = P().from_potentials(tree, tables)
+        P().apply_evidence(st, {0: 0})
+        P().belief_propagation(st)
+        got = all_posteriors(st, len(tree.cards))
+        assert rel_err(got, post) < 1e-10, name
+        assert rel_err(np.concatenate(st.clique_values), cliques) < 1e-9, name
+
+
+def test_per_message_traversal_matches_fused():
+    tree, data = load_golden("c2")
+    tables = synth.scaled_potentials(tree, 0)
+    a = P().from_potentials(tree, tables)
+    for r in tree.roots:
+        P().collect_evidence(a, r)
+        P().distribute_evidence(a, r)
+    b = P().from_potentials(tree, tables)
+    P().belief_propagation(b)
+    assert rel_err(np.concatenate(a.clique_values), np.concatenate(b.clique_values)) < 1e-10
+    assert rel_err(all_posteriors(a, len(tree.cards)), data["post0"]) < 1e-10
+
+
+def test_traversal_spy_sees_reference_order(monkeypatch):  # test_propagate.py:168-200
+    from paper_1202_3777_b200 import propagate as prop
+
+    log = []
+    orig = prop.message_passing
+
+    def spy(state, msg):
+        log.append((msg.source, msg.target))
+        return orig(state, msg)
+
+    monkeypatch.setattr(prop, "message_passing", spy)
+    tree = build_tree([(0, 1), (1, 2, 3), (3, 4)], (2,) * 5)
+    st = prop.from_potentials(tree, [np.ones(4), np.ones(8), np.ones(4)])
+    prop.collect_evidence(st, 1)
+    assert log == [(0, 1), (2, 1)]
+    del log[:]
+    prop.distribute_evidence(st, 1)
+    assert log == [(1, 0), (1, 2)]
+
+
+def test_root_choice_and_second_run():
+    tree, data = load_golden("c1")
+    tables = synth.scaled_potentials(tree, 0)
+    ref = None
+    for root in range(len(tree.cliques)):
+        st = P().from_potentials(tree, tables)
+        P().apply_evidence(st, {5: 1})
+        P().belief_propagation(st, root=root)
+        got = all_posteriors(st, len(tree.cards))
+        ref = got if ref is None else ref
+        assert rel_err(got, ref) < 1e-12
+        P().belief_propagation(st)
+        assert rel_err(all_posteriors(st, len(tree.cards)), ref) < 1e-12
+
+
+def test_incremental_evidence():  # test_propagate.py:289-300
+    tree, _ = load_golden("c1")
+    tables = synth.scaled_potentials(tree, 0)
+    st = P().from_potentials(tree, tables)
+    P().apply_evidence(st, {3: 1})
+    P().belief_propagation(st)
+    P().apply_evidence(st, {9: 0})
+    P().belief_propagation(st)
+    want = jtref.case_posteriors(jtref.from_potentials(tree, tables), {3: 1, 9: 0}, range(len(tree.cards)))
+    assert rel_err(all_posteriors(st, len(tree.cards)), want) < 1e-10
+
+
+def test_unnormalized_mass_and_zero_mass():
+    from paper_1202_3777_b200.errors import ZeroMassError
+
+    tree, data = load_golden("c1")
+    tables = synth.scaled_potentials(tree, 0)
+    st = P().from_potentials(tree, tables)
+    P().apply_evidence(st, {2: 1})
+    P().belief_propagation(st)
+    o = jtref.from_potentials(tree, tables)
+    jtref.apply_evidence(o, {2: 1})
+    jtref.belief_propagation(o)
+    raw = P().query_marginal(st, 0, normalize_result=False).total()
+    assert raw == pytest.approx(jtref.query_marginal(o, 0, False).sum(), rel=1e-12)
+    # impossible evidence: two observations of one variable that disagree
+    st2 = P().from_potentials(tree, tables)
+    P().apply_evidence(st2, {2: 1})
+    P().apply_evidence(st2, {2: 0})
+    P().belief_propagation(st2)
+    with pytest.raises(ZeroMassError):
+        P().query_marginal(st2, 0)
+
+
+def test_unknown_engine_and_variable():
+    from paper_1202_3777_b200.errors import UnknownVariableError
+
+    with pytest.raises(ValueError):
+        P().make_engine("gpu")
+    tree, _ = load_golden("c1")
+    st = P().from_potentials(tree, synth.scaled_potentials(tree, 0))
+    with pytest.raises(UnknownVariableError):
+        P().apply_evidence(st, {999: 0})
+    with pytest.raises(UnknownVariableError):
+        P().belief_propagation(st, root=99)
+
+
+def test_engine_protocol_on_host_arrays():
+    """CudaEngine.run_message speaks the reference engine protocol (propagate.py:84)."""
+    rng = np.random.default_rng(3)
+    eng = P().CudaEngine()
+    for ids, cards, sep in [((0, 1, 3), (2, 2, 2), (1,)), ((0, 1, 2, 3), (3, 4, 2, 5), (0, 2)),
+                            ((4, 7, 9), (5, 3, 4), (7,))]:
+        sc = tuple(cards[ids.index(v)] for v in sep)
+        mu_s = jtref.build_mapping_table(ids, cards, sep)
+        tgt_ids = tuple(sorted(set(sep) | {50}))
+        tgt_cards = tuple(sc[list(sep).index(v)] if v in sep else 3 for v in tgt_ids)
+        mu_t = jtref.build_mapping_table(tgt_ids, tgt_cards, sep)
+        src = rng.uniform(size=mu_s.size)
+        tgt = rng.uniform(size=mu_t.size)
+        sp = rng.uniform(0.5, 1.5, size=mu_s.shape[0])
+        a_t, a_s = tgt.copy(), sp.copy()
+        jtref.pass_block(src, a_t, a_s, mu_s, mu_t, 0, len(a_s))
+        b_t, b_s = tgt.copy(), sp.copy()
+        eng.run_message(src, b_t, b_s, mu_s, mu_t)
+        assert rel_err(b_t, a_t) < 1e-13 and rel_err(b_s, a_s) < 1e-13
+
+
+@pytest.mark.parametrize("mode", ["shared", "materialized"])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_batch_engine_vs_reference(mode, dtype):
+    from paper_1202_3777_b200.batch import BatchPropagator
+
+    for name in ("c1", "c5"):
+        tree, data = load_golden(name)
+        tables = synth.scaled_potentials(tree, 0)
+        cases = golden_cases(data)
+        bp = BatchPropagator(tree, tables, batch=8, dtype=dtype, mode=mode)
+        out = bp.run([ev for ev, _ in cases]).cpu().numpy()
+        bp.sync()
+        for i, (ev, want) in enumerate(cases):
+            assert rel_err(out[i], want) < TOL[dtype], (name, mode, dtype, i)
+
+
+def test_batch_engine_vs_oracle_many_cases():
+    from paper_1202_3777_b200.batch import BatchPropagator
+
+    tree, _ = load_golden("c2")
+    tables = synth.scaled_potentials(tree, 0)
+    cases = synth.evidence_cases(tree, 40, seed=99)
+    template = jtref.from_potentials(tree, tables)
+    want = np.stack([jtref.case_posteriors(template, ev, range(len(tree.cards))) for ev in cases[:6]])
+    for mode in ("shared", "materialized"):
+        bp = BatchPropagator(tree, tables, batch=16, dtype="f64", mode=mode)
+        out = bp.run(cases).cpu().numpy()
+        bp.sync()
+        assert rel_err(out[:6], want) < 1e-10, mode
+
+
+def test_calibration_full_size_c3():
+    """Size-independent property at full size: every separator equals the
+    marginal of both adjacent cliques after BP (check_global_consistency)."""
+    tree, data = load_golden("c3")
+    st = P().from_potentials(tree, synth.scaled_potentials(tree, 0), engine=P().CudaEngine(dtype="f64"))
+    P().belief_propagation(st)
+    P().check_global_consistency(st, rtol=1e-9)
+    got = all_posteriors(st, len(tree.cards))
+    assert rel_err(got, data["post0"]) < 1e-10
