@@ -86,6 +86,11 @@ int jt_state_store(jt_state* st, int case_idx, double* clique_concat, double* se
  * clique = owning clique (tree.cpt_assignment[var]).  case = -1 → every case. */
 int jt_apply_evidence(jt_state* st, int n, const int32_t* case_idx, const int32_t* var,
                       const int32_t* clique, const int32_t* value, void* stream);
+/* Same, with the observations already resident on the device: d_obs holds n
+ * int32 triples (case, var, state); var/clique (host, n_vars entries) list every
+ * variable observed in d_obs with its owning clique.  Asynchronous. */
+int jt_apply_evidence_device(jt_state* st, int n, const int32_t* d_obs, int n_vars,
+                             const int32_t* var, const int32_t* clique, void* stream);
 /* Drop all evidence factors (shared-base mode: back to the bare base replica). */
 int jt_clear_evidence(jt_state* st);
 

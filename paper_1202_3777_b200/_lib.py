@@ -44,6 +44,7 @@ SIGNATURES = {
     "jt_state_load": (C.c_int, [_vp, C.c_int, _f64p, _f64p]),
     "jt_state_store": (C.c_int, [_vp, C.c_int, _f64p, _f64p]),
     "jt_apply_evidence": (C.c_int, [_vp, C.c_int, _i32p, _i32p, _i32p, _i32p, _vp]),
+    "jt_apply_evidence_device": (C.c_int, [_vp, C.c_int, _vp, C.c_int, _i32p, _i32p, _vp]),
     "jt_clear_evidence": (C.c_int, [_vp]),
     "jt_state_reset": (C.c_int, [_vp, _vp]),
     "jt_message": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp]),

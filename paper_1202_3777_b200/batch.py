@@ -31,6 +31,26 @@ from ._lib import JT_MATERIALIZED, JT_SHARED_BASE, check, f64, i32, ptr
 from .propagate import _scope_size, plan_for
 
 MODES = {"shared": JT_SHARED_BASE, "materialized": JT_MATERIALIZED}
+MAX_FACTORS = 8  # jt::MAXF
+
+
+def _owners(tree):
+    owner = dict(getattr(tree, "cpt_assignment", {}) or {})
+    for v in range(len(tree.cards)):
+        if v not in owner:
+            holders = [c for c in tree.cliques if v in c.scope.ids]
+            if holders:
+                owner[v] = min(holders, key=lambda c: (_scope_size(c.scope), c.id)).id
+    return owner
+
+
+def shared_supported(tree) -> bool:
+    """Shared-base passes carry every factor of a clique at once: neighbours'
+    ratios plus one evidence mask per variable the clique owns."""
+    owned = {}
+    for v, c in _owners(tree).items():
+        owned[c] = owned.get(c, 0) + 1
+    return all(len(tree.neighbors[c]) + owned.get(c, 0) <= MAX_FACTORS for c in range(len(tree.cliques)))
 
 
 class BatchPropagator:
@@ -40,13 +60,18 @@ class BatchPropagator:
     (normalized), computed `batch` cases per step.
     """
 
-    def __init__(self, tree, clique_tables, batch, dtype="f32", mode="shared", device=0,
+    def __init__(self, tree, clique_tables, batch, dtype="f32", mode="auto", device=0,
                  query_vars=None):
         _lib.require_device()
         import torch
 
         self.tree = tree
         self.batch = int(batch)
+        if mode == "auto":
+            mode = "shared" if shared_supported(tree) else "materialized"
+        elif mode == "shared" and not shared_supported(tree):
+            raise ValueError(f"shared-base mode needs <= {MAX_FACTORS} factors per clique "
+                             "(children + parent + observed variables); use mode='materialized'")
         self.mode = mode
         self.device = int(device)
         self.plan = plan_for(tree, dtype, device)
@@ -65,13 +90,11 @@ class BatchPropagator:
         self.cards = [int(tree.cards[v]) for v in self.query_vars]
         self.cols = int(sum(self.cards))
         self._qv = i32(self.query_vars)
-        self.owner = dict(getattr(tree, "cpt_assignment", {}) or {})
-        for v in range(len(tree.cards)):
-            if v not in self.owner:
-                holders = [c for c in tree.cliques if v in c.scope.ids]
-                if holders:
-                    self.owner[v] = min(holders, key=lambda c: (_scope_size(c.scope), c.id)).id
+        self.owner = _owners(tree)
         self.torch_device = torch.device("cuda", self.device)
+        # all device work of this propagator is ordered on one non-default torch
+        # stream (graph-capturable); callers' streams join it in run()
+        self.stream = torch.cuda.Stream(device=self.torch_device)
 
     @property
     def device_bytes(self) -> int:
@@ -94,13 +117,45 @@ class BatchPropagator:
 
     def step(self, encoded, out, stream=None):
         """One device step over ≤ batch cases: reset, evidence, propagate and
-        posteriors into `out` (a CUDA double tensor [batch, cols])."""
+        posteriors into `out` (a CUDA double tensor [batch, cols]), enqueued on
+        `stream` (default: this propagator's stream)."""
         cidx, vs, cs, xs = encoded
         L = _lib.lib()
+        if stream is None:
+            stream = C.c_void_p(self.stream.cuda_stream)
         check(L.jt_state_reset(self.handle, stream), "reset")
         if len(vs):
             check(L.jt_apply_evidence(self.handle, len(vs), ptr(cidx, C.c_int32), ptr(vs, C.c_int32),
                                       ptr(cs, C.c_int32), ptr(xs, C.c_int32), stream), "evidence")
+        check(L.jt_propagate_query(self.handle, len(self._qv), ptr(self._qv, C.c_int32), 1,
+                                   C.c_void_p(out.data_ptr()), stream), "propagate")
+
+    def encode_obs(self, cases):
+        """Compact device-evidence encoding: int32 [n_obs, 3] (case, var, state);
+        every variable of the tree is listed as active with its owning clique so
+        the propagation program is the same for every batch."""
+        cidx, vs, _, xs = self.encode(cases)
+        obs = np.stack([cidx, vs, xs], axis=1).astype(np.int32) if len(vs) else np.zeros((0, 3), np.int32)
+        return obs
+
+    def active_vars(self):
+        if not hasattr(self, "_act"):
+            vs = sorted(self.owner)
+            self._act = (i32(vs), i32([self.owner[v] for v in vs]))
+        return self._act
+
+    def step_device(self, obs_dev, out, stream=None):
+        """One step with observations already on the device (int32 [n, 3] CUDA
+        tensor): reset → masks built on device → propagate → posteriors."""
+        L = _lib.lib()
+        if stream is None:
+            stream = C.c_void_p(self.stream.cuda_stream)
+        av, ac = self.active_vars()
+        check(L.jt_state_reset(self.handle, stream), "reset")
+        n = int(obs_dev.shape[0])
+        if n:
+            check(L.jt_apply_evidence_device(self.handle, n, C.c_void_p(obs_dev.data_ptr()), len(av),
+                                             ptr(av, C.c_int32), ptr(ac, C.c_int32), stream), "evidence")
         check(L.jt_propagate_query(self.handle, len(self._qv), ptr(self._qv, C.c_int32), 1,
                                    C.c_void_p(out.data_ptr()), stream), "propagate")
 
@@ -110,11 +165,16 @@ class BatchPropagator:
 
         n = len(cases)
         steps = (n + self.batch - 1) // self.batch
+        caller = torch.cuda.current_stream(self.torch_device)
         if out is None:
             out = torch.empty((steps * self.batch, self.cols), dtype=torch.float64, device=self.torch_device)
+        elif out.shape[0] < steps * self.batch or out.shape[1] != self.cols:
+            raise ValueError(f"out must be at least [{steps * self.batch}, {self.cols}]")
+        self.stream.wait_stream(caller)
         for s in range(steps):
             chunk = cases[s * self.batch:(s + 1) * self.batch]
             self.step(self.encode(chunk), out[s * self.batch:(s + 1) * self.batch], stream)
+        caller.wait_stream(self.stream)
         return out[:n]
 
     def sync(self):

@@ -206,8 +206,11 @@ struct jt_state {
   std::vector<int64_t> coff, boff, sep_off, ratC_off, ratD_off, ev_off, q_off;
   int64_t msg_ratio_off = 0;
   int64_t n_clique = 0, n_base = 0, n_aux = 0, n_qout = 0;
-  std::vector<std::vector<float>> ev_host;  // per var mask [card*B] (shared mode bookkeeping)
   std::vector<int> ev_clique;               // per var: clique holding its active factor, -1 none
+  int64_t* d_evoff = nullptr;               // per var: aux offset of its mask [card][B]
+  int32_t* d_cards = nullptr;               // per var cardinality
+  int32_t* d_obs = nullptr;                 // observation staging (case, var, state) + fill list
+  int64_t obs_cap = 0;
   std::map<std::string, std::unique_ptr<Program>> programs;
   int64_t launches = 0;
   int64_t device_bytes = 0;
@@ -220,6 +223,9 @@ struct jt_state {
     cudaFree(d_post);
     cudaFree(d_stage);
     cudaFree(d_err);
+    cudaFree(d_evoff);
+    cudaFree(d_cards);
+    cudaFree(d_obs);
     for (auto& kv : qmeta) cudaFree(kv.second.first);
     if (stream) cudaStreamDestroy(stream);
   }
@@ -290,7 +296,6 @@ extern "C" int jt_state_create(const jt_plan* plan, int batch, int mode, jt_stat
   }
   st->n_qout = std::max<int64_t>(qo, 1);
   st->ev_clique.assign(plan->n_vars, -1);
-  st->ev_host.resize(plan->n_vars);
 
   const size_t es = st->esz;
   if (st->n_clique) CK(cudaMalloc(&st->d_clique, st->n_clique * es));
@@ -300,6 +305,12 @@ extern "C" int jt_state_create(const jt_plan* plan, int batch, int mode, jt_stat
   CK(cudaMalloc(&st->d_err, sizeof(int)));
   CK(cudaMemset(st->d_err, 0, sizeof(int)));
   CK(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
+  CK(cudaMalloc(&st->d_evoff, std::max(1, plan->n_vars) * sizeof(int64_t)));
+  CK(cudaMalloc(&st->d_cards, std::max(1, plan->n_vars) * sizeof(int32_t)));
+  if (plan->n_vars) {
+    CK(cudaMemcpy(st->d_evoff, st->ev_off.data(), plan->n_vars * sizeof(int64_t), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(st->d_cards, plan->cards.data(), plan->n_vars * sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
   st->device_bytes = (st->n_clique + st->n_base + st->n_aux) * es + st->n_qout * 8;
   // initial contents: cliques 1 (initialize's np.ones, propagate.py:209), seps 1 (236)
   if (st->n_clique) CK(launch_fill(plan->dtype, st->d_clique, st->n_clique, 1.0, st->stream));
@@ -1031,10 +1042,7 @@ extern "C" int jt_state_store(jt_state* st, int case_idx, double* clique_concat,
 
 extern "C" int jt_clear_evidence(jt_state* st) {
   if (!st) return JT_ERR_BAD_ARG;
-  for (int v = 0; v < st->plan->n_vars; ++v) {
-    st->ev_clique[v] = -1;
-    st->ev_host[v].clear();
-  }
+  std::fill(st->ev_clique.begin(), st->ev_clique.end(), -1);
   return JT_OK;
 }
 
@@ -1069,67 +1077,51 @@ extern "C" int jt_state_reset(jt_state* st, void* stream) {
   return run_program(st, pr, s);
 }
 
-extern "C" int jt_apply_evidence(jt_state* st, int n, const int32_t* case_idx, const int32_t* var,
-                                 const int32_t* clique, const int32_t* value, void* stream) {
-  if (!st || n < 0) return JT_ERR_BAD_ARG;
-  if (n == 0) return JT_OK;
+// Observations arrive as (case, var, state) triples (host or device); masks are
+// built on the device.  Shared-base states keep them as persistent factors
+// (observations accumulate until reset, like repeated apply_evidence calls on
+// the reference state); materialized states multiply them into the owning
+// cliques right away (propagate.py:257-258).
+static int evidence_common(jt_state* st, int n, const int32_t* d_obs, const std::vector<int>& vars,
+                           const std::vector<int>& cliques, cudaStream_t s) {
   const jt_plan* p = st->plan;
-  DevGuard g(p->device);
-  const int64_t B = st->B;
-  // per var: mask [card][B]; unobserved lanes stay 1
-  std::map<int, std::vector<float>> masks;
-  std::map<int, int> owner;
-  for (int i = 0; i < n; ++i) {
-    const int v = var[i], c = clique[i], b = case_idx ? case_idx[i] : -1;
-    if (v < 0 || v >= p->n_vars || c < 0 || c >= p->n_cliques || b < -1 || b >= B) return JT_ERR_BAD_ARG;
-    if (!std::binary_search(p->cvars[c].begin(), p->cvars[c].end(), v)) return JT_ERR_BAD_ARG;
-    if (value[i] < 0 || value[i] >= p->cards[v]) return JT_ERR_BAD_ARG;
-    auto it = owner.find(v);
-    if (it != owner.end() && it->second != c) return JT_ERR_BAD_ARG;
-    owner[v] = c;
-    auto& m = masks[v];
-    if (m.empty()) m.assign((size_t)p->cards[v] * B, 1.0f);
-    for (int64_t l = (b < 0 ? 0 : b); l < (b < 0 ? B : b + 1); ++l)
-      for (int d = 0; d < p->cards[v]; ++d)
-        if (d != value[i]) m[(size_t)d * B + l] = 0.0f;
-  }
-  cudaStream_t s = pick_stream(st, stream);
-  std::vector<double> hbuf;
-  if (st->mode == JT_SHARED_BASE) {
-    // accumulate into the persistent factor (repeated observations multiply)
-    for (auto& kv : masks) {
-      const int v = kv.first;
-      if (st->ev_clique[v] >= 0 && st->ev_clique[v] != owner[v]) return JT_ERR_UNSUPPORTED;
-      auto& h = st->ev_host[v];
-      if (h.empty()) h.assign(kv.second.size(), 1.0f);
-      for (size_t i = 0; i < h.size(); ++i) h[i] *= kv.second[i];
-      st->ev_clique[v] = owner[v];
+  const bool shared = st->mode == JT_SHARED_BASE;
+  std::vector<int32_t> fill;
+  for (size_t i = 0; i < vars.size(); ++i) {
+    const int v = vars[i], c = cliques[i];
+    if (shared) {
+      if (st->ev_clique[v] >= 0 && st->ev_clique[v] != c) return JT_ERR_UNSUPPORTED;
+      if (st->ev_clique[v] < 0) fill.push_back(v);
+      st->ev_clique[v] = c;
+    } else {
+      fill.push_back(v);
     }
   }
-  // upload masks (f64 staging → storage type)
-  int64_t tot = 0;
-  for (auto& kv : masks) tot += (int64_t)kv.second.size();
-  int rc = ensure_stage(st, tot);
-  if (rc) return rc;
-  hbuf.reserve(tot);
-  for (auto& kv : masks) {
-    const auto& src = st->mode == JT_SHARED_BASE ? st->ev_host[kv.first] : kv.second;
-    for (float x : src) hbuf.push_back(x);
+  // fill list rides behind the observations in the staging buffer
+  int32_t* d_fill = nullptr;
+  if (!fill.empty()) {
+    const int64_t need = 3 * (int64_t)n + (int64_t)fill.size();
+    if (d_obs != st->d_obs) {  // device observations: stage the fill list alone
+      if ((int64_t)fill.size() > st->obs_cap) {
+        cudaFree(st->d_obs);
+        st->d_obs = nullptr;
+        CK(cudaMalloc(&st->d_obs, fill.size() * sizeof(int32_t)));
+        st->obs_cap = (int64_t)fill.size();
+      }
+      d_fill = st->d_obs;
+    } else {
+      d_fill = st->d_obs + 3 * (int64_t)n;
+      (void)need;
+    }
+    CK(cudaMemcpyAsync(d_fill, fill.data(), fill.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    CK(launch_ev_fill(st->d_aux, p->dtype, d_fill, (int)fill.size(), st->d_evoff, st->d_cards, st->B, s));
+    st->launches++;
   }
-  CK(cudaMemcpyAsync(st->d_stage, hbuf.data(), tot * 8, cudaMemcpyHostToDevice, s));
-  int64_t o = 0;
-  for (auto& kv : masks) {
-    char* dst = (char*)st->d_aux + st->ev_off[kv.first] * st->esz;
-    CK(launch_convert_d2t(p->dtype, st->d_stage + o, dst, (int64_t)kv.second.size(), 1, 1, s));
-    o += (int64_t)kv.second.size();
-  }
-  if (st->mode == JT_SHARED_BASE) {
-    CK(cudaStreamSynchronize(s));  // hbuf lifetime
-    return JT_OK;
-  }
-  // materialized: multiply the masks into the owning cliques now
+  CK(launch_ev_zero(st->d_aux, p->dtype, d_obs, n, st->d_evoff, st->d_cards, st->B, s));
+  st->launches++;
+  if (shared) return JT_OK;
   std::map<int, std::vector<int>> by_clique;
-  for (auto& kv : owner) by_clique[kv.second].push_back(kv.first);
+  for (size_t i = 0; i < vars.size(); ++i) by_clique[cliques[i]].push_back(vars[i]);
   std::vector<std::vector<PassSpec>> waves;
   std::vector<int> kk;
   for (auto& kv : by_clique) {
@@ -1150,11 +1142,69 @@ extern "C" int jt_apply_evidence(jt_state* st, int n, const int32_t* case_idx, c
     kk.push_back(-1);
   }
   Program* pr;
-  rc = get_program(st, key_of("ev", kk), waves, &pr);
+  int rc = get_program(st, key_of("ev", kk), waves, &pr);
   if (rc) return rc;
-  rc = run_program(st, pr, s);
-  CK(cudaStreamSynchronize(s));  // hbuf lifetime
-  return rc;
+  return run_program(st, pr, s);
+}
+
+static int collect_vars(const jt_state* st, int n, const int32_t* var, const int32_t* clique,
+                        std::vector<int>& vars, std::vector<int>& cliques) {
+  const jt_plan* p = st->plan;
+  std::map<int, int> owner;
+  for (int i = 0; i < n; ++i) {
+    const int v = var[i], c = clique[i];
+    if (v < 0 || v >= p->n_vars || c < 0 || c >= p->n_cliques) return JT_ERR_BAD_ARG;
+    if (!std::binary_search(p->cvars[c].begin(), p->cvars[c].end(), v)) return JT_ERR_BAD_ARG;
+    auto it = owner.find(v);
+    if (it != owner.end() && it->second != c) return JT_ERR_BAD_ARG;
+    owner[v] = c;
+  }
+  for (auto& kv : owner) {
+    vars.push_back(kv.first);
+    cliques.push_back(kv.second);
+  }
+  return JT_OK;
+}
+
+extern "C" int jt_apply_evidence(jt_state* st, int n, const int32_t* case_idx, const int32_t* var,
+                                 const int32_t* clique, const int32_t* value, void* stream) {
+  if (!st || n < 0) return JT_ERR_BAD_ARG;
+  if (n == 0) return JT_OK;
+  const jt_plan* p = st->plan;
+  DevGuard g(p->device);
+  std::vector<int> vars, cliques;
+  int rc = collect_vars(st, n, var, clique, vars, cliques);
+  if (rc) return rc;
+  std::vector<int32_t> obs(3 * (size_t)n);
+  for (int i = 0; i < n; ++i) {
+    const int b = case_idx ? case_idx[i] : -1;
+    if (b < -1 || b >= st->B || value[i] < 0 || value[i] >= p->cards[var[i]]) return JT_ERR_BAD_ARG;
+    obs[3 * i] = b;
+    obs[3 * i + 1] = var[i];
+    obs[3 * i + 2] = value[i];
+  }
+  const int64_t need = 3 * (int64_t)n + (int64_t)vars.size();
+  if (need > st->obs_cap) {
+    cudaFree(st->d_obs);
+    st->d_obs = nullptr;
+    CK(cudaMalloc(&st->d_obs, need * sizeof(int32_t)));
+    st->obs_cap = need;
+  }
+  cudaStream_t s = pick_stream(st, stream);
+  // pageable source: the copy is staged before cudaMemcpyAsync returns
+  CK(cudaMemcpyAsync(st->d_obs, obs.data(), obs.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  return evidence_common(st, n, st->d_obs, vars, cliques, s);
+}
+
+extern "C" int jt_apply_evidence_device(jt_state* st, int n, const int32_t* d_obs, int n_vars,
+                                        const int32_t* var, const int32_t* clique, void* stream) {
+  if (!st || n < 0 || n_vars < 0 || (n > 0 && !d_obs)) return JT_ERR_BAD_ARG;
+  if (n == 0) return JT_OK;
+  DevGuard g(st->plan->device);
+  std::vector<int> vars, cliques;
+  int rc = collect_vars(st, n_vars, var, clique, vars, cliques);
+  if (rc) return rc;
+  return evidence_common(st, n, d_obs, vars, cliques, pick_stream(st, stream));
 }
 
 extern "C" int jt_message(jt_state* st, int src, int tgt, int sep, void* stream) {

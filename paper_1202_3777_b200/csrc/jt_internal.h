@@ -80,6 +80,10 @@ cudaError_t launch_convert_d2t(int dtype, const double* src, void* dst, int64_t 
 cudaError_t launch_convert_t2d(int dtype, const void* src, int64_t src_stride,
                                double* dst, int64_t n, cudaStream_t s);
 cudaError_t launch_fill(int dtype, void* dst, int64_t n, double v, cudaStream_t s);
+cudaError_t launch_ev_fill(void* aux, int dtype, const int32_t* vars, int nv, const int64_t* var_off,
+                           const int32_t* cards, int B, cudaStream_t s);
+cudaError_t launch_ev_zero(void* aux, int dtype, const int32_t* obs, int n, const int64_t* var_off,
+                           const int32_t* cards, int B, cudaStream_t s);
 cudaError_t launch_mapping_table(int64_t* out, int64_t n_sep, int64_t n_rest,
                                  int nsd, const int64_t* sep_card, const int64_t* sep_stride,
                                  int nrd, const int64_t* rest_card, const int64_t* rest_stride,

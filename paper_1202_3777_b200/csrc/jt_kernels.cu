@@ -454,6 +454,51 @@ cudaError_t launch_fill(int dtype, void* dst, int64_t n, double v, cudaStream_t 
   return cudaGetLastError();
 }
 
+// ---- evidence masks (apply_evidence, propagate.py:243-260) ----
+// mask_v[d][b] = 1 except d != observed state of case b.  Masks of the listed
+// variables are reset to ones, then every observation zeroes its lane.
+__global__ void ev_fill_kernel(void* aux, int dtype, const int32_t* __restrict__ vars, int nv,
+                               const int64_t* __restrict__ var_off, const int32_t* __restrict__ cards, int B) {
+  const int k = blockIdx.y;
+  if (k >= nv) return;
+  const int v = vars[k];
+  const int64_t len = (int64_t)cards[v] * B, off = var_off[v];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+    if (dtype == 0) ((float*)aux)[off + i] = 1.0f;
+    else ((double*)aux)[off + i] = 1.0;
+  }
+}
+
+__global__ void ev_zero_kernel(void* aux, int dtype, const int32_t* __restrict__ obs, int n,
+                               const int64_t* __restrict__ var_off, const int32_t* __restrict__ cards, int B) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int b = obs[3 * i], v = obs[3 * i + 1], x = obs[3 * i + 2];
+  const int card = cards[v];
+  const int64_t base = var_off[v];
+  const int lo = b < 0 ? 0 : b, hi = b < 0 ? B : b + 1;
+  for (int l = lo; l < hi; ++l)
+    for (int d = 0; d < card; ++d)
+      if (d != x) {
+        if (dtype == 0) ((float*)aux)[base + (int64_t)d * B + l] = 0.0f;
+        else ((double*)aux)[base + (int64_t)d * B + l] = 0.0;
+      }
+}
+
+cudaError_t launch_ev_fill(void* aux, int dtype, const int32_t* vars, int nv, const int64_t* var_off,
+                           const int32_t* cards, int B, cudaStream_t s) {
+  if (nv == 0) return cudaSuccess;
+  ev_fill_kernel<<<dim3(8, nv), 256, 0, s>>>(aux, dtype, vars, nv, var_off, cards, B);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ev_zero(void* aux, int dtype, const int32_t* obs, int n, const int64_t* var_off,
+                           const int32_t* cards, int B, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  ev_zero_kernel<<<(n + 127) / 128, 128, 0, s>>>(aux, dtype, obs, n, var_off, cards, B);
+  return cudaGetLastError();
+}
+
 // ---- K0: device μ builder, μ[j][p] = row_base(j) + rest(p) (compiler.py:285-304) ----
 struct MuDims {
   int nsd, nrd;

@@ -272,7 +272,7 @@ def test_batch_engine_vs_oracle_many_cases():
     cases = synth.evidence_cases(tree, 40, seed=99)
     template = jtref.from_potentials(tree, tables)
     want = np.stack([jtref.case_posteriors(template, ev, range(len(tree.cards))) for ev in cases[:6]])
-    for mode in ("shared", "materialized"):
+    for mode in ("auto", "materialized"):
         bp = BatchPropagator(tree, tables, batch=16, dtype="f64", mode=mode)
         out = bp.run(cases).cpu().numpy()
         bp.sync()
