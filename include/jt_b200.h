@@ -129,6 +129,12 @@ int jt_run_message_mu(const double* phi_src, int64_t n_src, double* phi_tgt, int
                       double* phi_sep, int64_t n_sep, const void* mu_src, int64_t row_src,
                       const void* mu_tgt, int64_t row_tgt, int mu_is_int64, int device);
 
+/* Host-only planner report (no device needed): compiles the propagation
+ * program for (batch, mode) — kind 0: jt_propagate, kind 1: the batch program
+ * with posteriors of every variable — and writes one line per wave and pass. */
+int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind, int num_sms, int occ,
+                  char* buf, int64_t len);
+
 /* Library build/version string. */
 const char* jt_version(void);
 

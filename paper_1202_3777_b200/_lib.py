@@ -57,6 +57,7 @@ SIGNATURES = {
     "jt_state_launch_count": (C.c_int64, [_vp]),
     "jt_run_message_mu": (C.c_int, [_f64p, C.c_int64, _f64p, C.c_int64, _f64p, C.c_int64, _vp, C.c_int64,
                                     _vp, C.c_int64, C.c_int, C.c_int]),
+    "jt_debug_plan": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_int64]),
     "jt_version": (C.c_char_p, []),
 }
 

@@ -246,19 +246,11 @@ struct DevGuard {
   }
 };
 
-extern "C" int jt_state_create(const jt_plan* plan, int batch, int mode, jt_state** out) {
-  if (!plan || !out || batch < 1 || (mode != JT_MATERIALIZED && mode != JT_SHARED_BASE))
-    return JT_ERR_BAD_ARG;
-  DevGuard g(plan->device);
-  auto st = std::make_unique<jt_state>();
-  st->plan = plan;
-  st->B = batch;
-  st->mode = mode;
+static void layout_state(jt_state* st) {
+  const jt_plan* plan = st->plan;
+  const int mode = st->mode;
+  const int64_t B = st->B;
   st->esz = plan->dtype == JT_F32 ? 4 : 8;
-  cudaDeviceProp prop;
-  CK(cudaGetDeviceProperties(&prop, plan->device));
-  st->num_sms = prop.multiProcessorCount;
-  const int64_t B = batch;
   // clique arena (materialized) / base arena (shared)
   int64_t off = 0;
   for (int c = 0; c < plan->n_cliques; ++c) {
@@ -296,7 +288,20 @@ extern "C" int jt_state_create(const jt_plan* plan, int batch, int mode, jt_stat
   }
   st->n_qout = std::max<int64_t>(qo, 1);
   st->ev_clique.assign(plan->n_vars, -1);
+}
 
+extern "C" int jt_state_create(const jt_plan* plan, int batch, int mode, jt_state** out) {
+  if (!plan || !out || batch < 1 || (mode != JT_MATERIALIZED && mode != JT_SHARED_BASE))
+    return JT_ERR_BAD_ARG;
+  DevGuard g(plan->device);
+  auto st = std::make_unique<jt_state>();
+  st->plan = plan;
+  st->B = batch;
+  st->mode = mode;
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, plan->device));
+  st->num_sms = prop.multiProcessorCount;
+  layout_state(st.get());
   const size_t es = st->esz;
   if (st->n_clique) CK(cudaMalloc(&st->d_clique, st->n_clique * es));
   if (st->n_base) CK(cudaMalloc(&st->d_base, st->n_base * es));
@@ -376,6 +381,8 @@ static std::vector<Dim> pass_dims(const jt_state* st, const PassSpec& ps) {
   const auto& cv = p->cvars[ps.clique];
   std::vector<int> vars(cv.begin(), cv.end());
   if (B > 1) vars.push_back(-1);
+  // lanes per block for the thread-owned path: one vector per thread
+  const int64_t L = (int64_t)NT * (st->esz == 4 ? 4 : 2);
   Tensor src;
   src.vars = cv;
   src.batch = (B > 1) && ps.src_arena == A_CLIQUE;
@@ -390,6 +397,18 @@ static std::vector<Dim> pass_dims(const jt_state* st, const PassSpec& ps) {
     d.dst = ps.write ? tensor_stride(p, dst, v, B) : 0;
     d.out = ps.out_kind != OUT_NONE ? tensor_stride(p, ps.out, v, B) : 0;
     for (size_t f = 0; f < ps.factors.size(); ++f) d.fac[f] = tensor_stride(p, ps.factors[f], v, B);
+    if (v < 0 && B > L && B % L == 0) {
+      // split the case dim into (B/L outer, L inner lanes); every stride of the
+      // outer part is the lane stride times L
+      Dim hi = d;
+      hi.card = B / L;
+      hi.src *= L;
+      hi.dst *= L;
+      hi.out *= L;
+      for (size_t f = 0; f < ps.factors.size(); ++f) hi.fac[f] *= L;
+      d.card = L;
+      dims.push_back(hi);
+    }
     dims.push_back(d);
   }
   if (dims.empty()) {  // empty clique scope: a single entry
@@ -443,6 +462,9 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
 
   struct Cand {
     int k;
+    bool own = false;
+    int gpi = 1;
+    int64_t j_per_item = 1;
     int64_t T, n_in, n_out, r_out;
     int BPI;
     int64_t n_chunks, bpc;
@@ -473,24 +495,47 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
       if (has_out && dims[i].out) c.n_out *= dims[i].card;
       else c.r_out *= dims[i].card;
     }
-    c.BPI = (int)std::max<int64_t>(1, std::min<int64_t>(TH / T, c.r_out));
-    // chunking: ~1184 items for big passes, >= 2 iterations per item otherwise
+    c.own = has_out && c.n_in == T && T == (int64_t)NT * vec;
+    c.BPI = c.own ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(TH / T, c.r_out));
+    // several whole output groups per iteration when a group is smaller than an iteration
+    c.gpi = 1;
+    if (!c.own && has_out && c.r_out * T * 2 <= TH && c.n_out > 1) {
+      c.gpi = (int)std::min<int64_t>(TH / (c.r_out * T), c.n_out);
+      if (c.gpi * c.n_in > 4096) c.gpi = (int)std::max<int64_t>(1, 4096 / c.n_in);
+      if (c.gpi > 1) c.BPI = (int)(c.gpi * c.r_out);
+    }
+    // chunking: ~8 items per SM slot for big passes, >= 2 iterations per item otherwise
     const int64_t per_item = std::max<int64_t>(2 * TH, total / (int64_t)(st->num_sms * 8));
     const int64_t desired = std::max<int64_t>(1, (total + per_item - 1) / per_item);
     const int64_t max_chunks = (c.r_out + c.BPI - 1) / c.BPI;
     int64_t nch = has_out ? (desired + c.n_out - 1) / c.n_out : desired;
+    if ((c.own || c.gpi > 1) && c.r_out * T <= per_item) nch = 1;  // whole groups per item instead
     nch = std::max<int64_t>(1, std::min(nch, max_chunks));
     int64_t bpc = (c.r_out + nch - 1) / nch;
     bpc = (bpc + c.BPI - 1) / c.BPI * c.BPI;
     c.bpc = bpc;
     c.n_chunks = (c.r_out + bpc - 1) / bpc;
+    c.j_per_item = 1;
+    if (c.own && c.n_chunks == 1)
+      c.j_per_item = std::max<int64_t>(1, per_item / std::max<int64_t>(1, c.r_out * T));
+    if (c.gpi > 1) {
+      c.n_chunks = 1;
+      c.bpc = c.r_out;
+      c.j_per_item = std::max<int64_t>(c.gpi, per_item / std::max<int64_t>(1, c.r_out * T) / c.gpi * c.gpi);
+    }
     const double esz = st->esz;
     double bytes = (double)total * esz * ((ps.src_arena == A_CLIQUE ? 1.0 : 0.05) + (ps.write ? 1.0 : 0.0));
-    double part = (has_out && c.n_chunks > 1) ? (double)c.n_out * c.n_chunks * c.n_in * 16.0 : 0.0;
-    double items = (double)c.n_out * c.n_chunks;
+    const int64_t ng = (c.n_chunks + 31) / 32;
+    double part = (has_out && c.n_chunks > 1) ? (double)c.n_out * (c.n_chunks + ng) * c.n_in * 16.0 : 0.0;
+    double items = (double)c.n_out * c.n_chunks / c.j_per_item;
+    // per-item epilogue: block reduction (general path) or nothing (own path);
+    // the last CTA of a group sums <= 32 partial rows of n_in values per level
+    double epi = c.own ? 256.0 : 4096.0;
+    if (c.gpi > 1) epi = 4096.0 * c.j_per_item / c.gpi;  // one smem reduction per iteration
+    double fin = (has_out && c.n_chunks > 1) ? (double)c.n_out * std::min<int64_t>(32, c.n_chunks) * c.n_in * 64.0 : 0.0;
     double pen = 0.0;
     if (T * esz < 128) pen = bytes * (128.0 / (T * esz) - 1.0) * 0.5;
-    c.cost = bytes + part + items * 4096.0 + pen + (double)c.n_out * c.r_out * 16.0;
+    c.cost = bytes + part + items * epi + fin + pen + (double)c.n_out * c.r_out * 16.0;
     if (!found || c.cost < best.cost * 0.999) {
       best = c;
       found = true;
@@ -521,6 +566,8 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
   d.n_blocks_per_jout = best.r_out;
   d.blocks_per_chunk = best.bpc;
   d.blk_stride = 2 + nf;
+  d.own = best.own ? 1 : 0;
+  d.gpi = best.gpi;
   d.ndi = (int)best.inner.size();
   for (int i = 0; i < d.ndi; ++i) {
     const Dim& x = best.inner[i];
@@ -592,22 +639,38 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
     for (auto x : br) bp.bins.push_back((int32_t)x);
   }
   if (has_out && d.n_chunks > 1) {
-    bp.n_part = best.n_out * best.n_chunks * best.n_in;
-    bp.n_cnt = best.n_out;
+    const int64_t ng = (best.n_chunks + 31) / 32;
+    bp.n_part = best.n_out * (best.n_chunks + ng) * best.n_in;
+    bp.n_cnt = best.n_out * (ng + 1);
   }
-  for (int64_t jo = 0; jo < best.n_out; ++jo)
-    for (int64_t ch = 0; ch < best.n_chunks; ++ch) bp.items.push_back(Item{pass_idx, (int)ch, jo});
+  if ((best.own || best.gpi > 1) && best.n_chunks == 1) {
+    for (int64_t jo = 0; jo < best.n_out; jo += best.j_per_item)
+      bp.items.push_back(Item{pass_idx, 0, jo, std::min(best.j_per_item, best.n_out - jo)});
+  } else {
+    for (int64_t jo = 0; jo < best.n_out; ++jo)
+      for (int64_t ch = 0; ch < best.n_chunks; ++ch) bp.items.push_back(Item{pass_idx, (int)ch, jo, 1});
+  }
   return JT_OK;
 }
 
-static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>& waves,
-                         std::unique_ptr<Program>& out) {
-  auto prog = std::make_unique<Program>();
+struct HostProgram {
+  std::vector<WaveRt> waves;
   std::vector<DevPass> passes;
   std::vector<Item> items;
   std::vector<int64_t> blk;
   std::vector<int32_t> bins;
+  std::vector<int> pass_clique;
   int64_t n_part = 0, n_cnt = 0;
+};
+
+static int compile_program(const jt_state* st, const std::vector<std::vector<PassSpec>>& waves, HostProgram& hp,
+                           int occ_override = 0) {
+  auto& passes = hp.passes;
+  auto& items = hp.items;
+  auto& blk = hp.blk;
+  auto& bins = hp.bins;
+  int64_t& n_part = hp.n_part;
+  int64_t& n_cnt = hp.n_cnt;
   for (auto& w : waves) {
     if (w.empty()) continue;
     int vec = st->esz == 4 ? 4 : 2;
@@ -630,13 +693,29 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
       n_part += bp.n_part;
       n_cnt += bp.n_cnt;
       passes.push_back(bp.d);
+      hp.pass_clique.push_back(ps.clique);
       items.insert(items.end(), bp.items.begin(), bp.items.end());
     }
     rt.n_items = (int)(items.size() - rt.item_base);
-    const int occ = wave_max_ctas_per_sm(st->plan->dtype, vec);
+    const int occ = occ_override ? occ_override : wave_max_ctas_per_sm(st->plan->dtype, vec);
     rt.grid = (int)std::min<int64_t>(rt.n_items, (int64_t)occ * st->num_sms);
-    prog->waves.push_back(rt);
+    hp.waves.push_back(rt);
   }
+  return JT_OK;
+}
+
+static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>& waves,
+                         std::unique_ptr<Program>& out) {
+  HostProgram hp;
+  int rc0 = compile_program(st, waves, hp);
+  if (rc0) return rc0;
+  auto prog = std::make_unique<Program>();
+  prog->waves = hp.waves;
+  auto& passes = hp.passes;
+  auto& items = hp.items;
+  auto& blk = hp.blk;
+  auto& bins = hp.bins;
+  const int64_t n_part = hp.n_part, n_cnt = hp.n_cnt;
   auto up = [&](auto** dptr, const auto& vec) -> int {
     using E = typename std::decay_t<decltype(vec)>::value_type;
     const size_t n = std::max<size_t>(vec.size(), 1);
@@ -1553,3 +1632,61 @@ extern "C" int jt_run_message_mu(const double* phi_src, int64_t n_src, double* p
 }
 
 extern "C" const char* jt_version(void) { return "libjtb200 0.1 sm_100a"; }
+
+// ----------------------------------------------------------------- debug --
+// Host-only: compile the propagation program of a (plan, batch, mode) without
+// touching a device and describe every wave/pass.  kind 0: jt_propagate;
+// kind 1: jt_propagate_query over all variables with every variable observed
+// (the batch program).  Used by tools/plan_report.py and the CPU tests.
+extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind, int num_sms, int occ,
+                             char* buf, int64_t len) {
+  if (!plan || !buf || len <= 0 || batch < 1) return JT_ERR_BAD_ARG;
+  jt_state st;
+  st.plan = plan;
+  st.B = batch;
+  st.mode = mode;
+  st.num_sms = num_sms > 0 ? num_sms : 148;
+  layout_state(&st);
+  std::vector<int> qv;
+  if (kind == 1) {
+    for (int v = 0; v < plan->n_vars; ++v) {
+      qv.push_back(v);
+      if (mode == JT_SHARED_BASE) st.ev_clique[v] = smallest_holder(plan, v);
+    }
+  }
+  std::vector<std::vector<PassSpec>> waves;
+  int rc = build_propagate(&st, plan->roots, qv, waves);
+  if (rc) return rc;
+  HostProgram hp;
+  rc = compile_program(&st, waves, hp, occ > 0 ? occ : 2);
+  if (rc) return rc;
+  std::string out;
+  char line[512];
+  for (size_t w = 0; w < hp.waves.size(); ++w) {
+    const WaveRt& rt = hp.waves[w];
+    snprintf(line, sizeof line, "wave %zu vec %d grid %d items %d\n", w, rt.vec, rt.grid, rt.n_items);
+    out += line;
+    const int64_t pe = (w + 1 < hp.waves.size()) ? hp.waves[w + 1].pass_base : (int64_t)hp.passes.size();
+    for (int64_t pi = rt.pass_base; pi < pe; ++pi) {
+      const DevPass& d = hp.passes[pi];
+      int64_t n_items = 0, n_out = 0;
+      for (int64_t i = rt.item_base; i < rt.item_base + rt.n_items; ++i)
+        if (hp.items[i].pass == pi - rt.pass_base) {
+          ++n_items;
+          if (hp.items[i].chunk == 0) n_out += hp.items[i].j_count;
+        }
+      snprintf(line, sizeof line,
+               "  pass clique %d src %d nf %d wr %d out %d T %d n_in %d n_out %lld r_out %lld BPI %d chunks %d "
+               "bpc %lld items %lld ndi %d own %d gpi %d part %lld\n",
+               hp.pass_clique[pi], d.src_arena, d.nf, d.dst_off >= 0, d.out_kind, d.T, d.n_in, (long long)n_out,
+               (long long)d.n_blocks_per_jout, d.BPI, d.n_chunks, (long long)d.blocks_per_chunk,
+               (long long)n_items, d.ndi, d.own, d.gpi,
+               (long long)(d.n_chunks > 1 && d.out_kind ? n_out * d.n_chunks * d.n_in : 0));
+      out += line;
+    }
+  }
+  const int64_t n = std::min<int64_t>((int64_t)out.size(), len - 1);
+  memcpy(buf, out.data(), n);
+  buf[n] = 0;
+  return (int64_t)out.size() < len ? JT_OK : JT_ERR_BAD_ARG;
+}

@@ -40,6 +40,10 @@ struct DevPass {
   int T;                    // positions per block (multiple of VEC)
   int BPI;                  // blocks per CTA iteration
   int blk_stride;           // 2 + nf
+  int gpi;                  // >1: each iteration covers gpi whole output groups (BPI = gpi*r_out),
+                            //     reduced and finalized per iteration; items span j_count groups
+  int own;                  // 1: thread-owned bins (n_in == T == NT*VEC): sync-free epilogue,
+                            //    items span j_count whole output groups
   int ndi;                  // merged inner dims
   int icard[MAXDI];         // innermost last
   int isrc[MAXDI];
@@ -52,6 +56,7 @@ struct Item {               // one CTA work unit
   int pass;
   int chunk;
   int64_t j_out;
+  int64_t j_count;          // OWN passes without chunking: consecutive output groups
 };
 
 struct WaveArgs {

@@ -115,6 +115,145 @@ __device__ __forceinline__ void finalize_entry(const DevPass& P, int64_t j, doub
   }
 }
 
+constexpr int CHUNK_GROUP = 32;
+
+// Deterministic cross-CTA combine of one output group's chunk partials.  The
+// block's n_in values are in red[0..n_in).  Chunks are combined in fixed
+// groups of CHUNK_GROUP (level 1) and the groups in order (level 2); the last
+// CTA to arrive at each level does that level's sum, so no CTA reduces more
+// than CHUNK_GROUP × n_in values.
+template <typename T>
+__device__ void chunk_finalize(const DevPass& P, const Item& item, const WaveArgs& a, double* red,
+                               double* part2, int* s_last, T* aux) {
+  const int tid = threadIdx.x;
+  const int n_in = P.n_in, nch = P.n_chunks;
+  const int ng = (nch + CHUNK_GROUP - 1) / CHUNK_GROUP;
+  const int g = item.chunk / CHUNK_GROUP;
+  const int gsz = min(CHUNK_GROUP, nch - g * CHUNK_GROUP);
+  double* L1 = a.partials + P.part_off + item.j_out * (int64_t)(nch + ng) * n_in;
+  double* L2 = L1 + (int64_t)nch * n_in;
+  int* cnt = a.counters + P.cnt_off + item.j_out * (int64_t)(ng + 1);
+  for (int b = tid; b < n_in; b += NT) L1[(int64_t)item.chunk * n_in + b] = red[b];
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) *s_last = (atomicAdd(&cnt[g], 1) == gsz - 1);
+  __syncthreads();
+  if (!*s_last) return;
+  __threadfence();
+  const double* Lg = L1 + (int64_t)g * CHUNK_GROUP * n_in;
+  reduce_bins([&](int b, int r) { return __ldcg(Lg + (int64_t)r * n_in + b); }, n_in, gsz, red, part2);
+  if (tid == 0) cnt[g] = 0;
+  if (ng > 1) {
+    for (int b = tid; b < n_in; b += NT) L2[(int64_t)g * n_in + b] = red[b];
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) *s_last = (atomicAdd(&cnt[ng], 1) == ng - 1);
+    __syncthreads();
+    if (!*s_last) return;
+    __threadfence();
+    reduce_bins([&](int b, int r) { return __ldcg(L2 + (int64_t)r * n_in + b); }, n_in, ng, red, part2);
+    if (tid == 0) cnt[ng] = 0;
+  }
+  const int64_t j0 = item.j_out * (int64_t)n_in;
+  for (int b = tid; b < n_in; b += NT) finalize_entry<T>(P, j0 + b, red[b], aux, a.qout, a.err);
+}
+
+// Thread-owned bins (P.own): each thread owns the VEC output lanes of its
+// position in every block (n_in == T == NT*VEC), streams KV blocks per
+// iteration and finalizes its own lanes at every output-group boundary —
+// no barriers, no shared memory.  This is the batched layout's natural path.
+template <typename T, int VEC>
+__device__ __forceinline__ void own_item(const DevPass& P, const Item& item, const WaveArgs& a, T* clique,
+                                         const T* base, T* aux, int q_src, int q_dst,
+                                         const uint16_t* qfac /* [f*KV*NT + tid] */, double* red,
+                                         double* part2, int* s_last) {
+  const int tid = threadIdx.x;
+  const int64_t r_out = P.n_blocks_per_jout;
+  const bool chunked = P.n_chunks > 1;
+  int64_t b0, b1;
+  if (!chunked) {
+    b0 = item.j_out * r_out;
+    b1 = (item.j_out + item.j_count) * r_out;
+  } else {
+    b0 = item.j_out * r_out + (int64_t)item.chunk * P.blocks_per_chunk;
+    b1 = min(b0 + P.blocks_per_chunk, (item.j_out + 1) * r_out);
+  }
+  const T* __restrict__ srcA = (P.src_arena == A_BASE ? base : clique) + P.src_off;
+  const bool wr = P.dst_off >= 0;
+  T* __restrict__ dstA = clique + (wr ? P.dst_off : 0);
+  const int64_t* __restrict__ blk = a.blk + P.blk_off;
+  const int bs = P.blk_stride, nf = P.nf;
+  double acc[VEC];
+#pragma unroll
+  for (int l = 0; l < VEC; ++l) acc[l] = 0.0;
+  int64_t next_flush = chunked ? INT64_MAX : (b0 / r_out + 1) * r_out;
+  const int lane0 = tid * VEC;
+  for (int64_t bb = b0; bb < b1; bb += KV) {
+    T v[KV][VEC];
+    bool ok[KV];
+#pragma unroll
+    for (int u = 0; u < KV; ++u) {
+      ok[u] = bb + u < b1;
+      const int64_t* e = blk + (ok[u] ? bb + u : b0) * bs;
+      if (ok[u]) {
+        const T* p = srcA + e[0] + q_src;
+        if (VEC == 1 || P.src_vec) {
+          load_vec<T, VEC>(p, v[u]);
+        } else {
+          const T x = *p;
+#pragma unroll
+          for (int l = 0; l < VEC; ++l) v[u][l] = x;
+        }
+      }
+    }
+#pragma unroll
+    for (int f = 0; f < MAXF; ++f) {
+      if (f < nf) {
+        const T* fb = aux + P.fac_off[f] + qfac[f * KV * NT];
+        const bool fv = (P.fac_vec >> f) & 1u;
+#pragma unroll
+        for (int u = 0; u < KV; ++u) {
+          if (ok[u]) {
+            const T* p = fb + blk[(bb + u) * bs + 2 + f];
+            T g[VEC];
+            if (VEC == 1 || fv) {
+              load_vec_ro<T, VEC>(p, g);
+            } else {
+              const T x = __ldg(p);
+#pragma unroll
+              for (int l = 0; l < VEC; ++l) g[l] = x;
+            }
+#pragma unroll
+            for (int l = 0; l < VEC; ++l) v[u][l] *= g[l];
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < KV; ++u) {
+      if (!ok[u]) continue;
+      if (wr) store_vec<T, VEC>(dstA + blk[(bb + u) * bs + 1] + q_dst, v[u]);
+#pragma unroll
+      for (int l = 0; l < VEC; ++l) acc[l] += (double)v[u][l];
+      if (bb + u + 1 == next_flush) {
+        const int64_t j = ((bb + u) / r_out) * (int64_t)P.n_in + lane0;
+#pragma unroll
+        for (int l = 0; l < VEC; ++l) {
+          finalize_entry<T>(P, j + l, acc[l], aux, a.qout, a.err);
+          acc[l] = 0.0;
+        }
+        next_flush += r_out;
+      }
+    }
+  }
+  if (chunked) {
+#pragma unroll
+    for (int l = 0; l < VEC; ++l) red[lane0 + l] = acc[l];
+    __syncthreads();
+    chunk_finalize<T>(P, item, a, red, part2, s_last, aux);
+  }
+}
+
 template <typename T, int VEC>
 __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
   constexpr int TH = NT * KV * VEC;  // positions per CTA iteration
@@ -174,10 +313,18 @@ __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
       }
     }
 
+    if (P.own) {
+      own_item<T, VEC>(P, item, a, clique, base, aux, q_src[0], q_dst[0], &s_qfac[0][0][tid], red, part2,
+                       &s_last);
+      __syncthreads();
+      continue;
+    }
+
+    const bool multi = P.gpi > 1;
     const int64_t jb = item.j_out * P.n_blocks_per_jout;
     const int64_t b0 = jb + (int64_t)item.chunk * P.blocks_per_chunk;
-    int64_t b1 = b0 + P.blocks_per_chunk;
-    if (b1 > jb + P.n_blocks_per_jout) b1 = jb + P.n_blocks_per_jout;
+    int64_t b1 = multi ? (item.j_out + item.j_count) * P.n_blocks_per_jout : b0 + P.blocks_per_chunk;
+    if (!multi && b1 > jb + P.n_blocks_per_jout) b1 = jb + P.n_blocks_per_jout;
     const T* __restrict__ srcA = (P.src_arena == A_BASE ? base : clique) + P.src_off;
     const bool wr = P.dst_off >= 0;
     T* __restrict__ dstA = clique + (wr ? P.dst_off : 0);
@@ -246,9 +393,47 @@ __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
       for (int k = 0; k < KV; ++k)
 #pragma unroll
         for (int l = 0; l < VEC; ++l) acc[k][l] += (double)v[k][l];
+      if (multi) {
+        // this iteration holds gpi complete output groups: reduce and finalize now
+        const int n_in = P.n_in;
+        const int64_t g0 = (bb - jb) / P.n_blocks_per_jout + item.j_out;
+        const int64_t rem_g = item.j_out + item.j_count - g0;
+        const int ng = (int)(rem_g < P.gpi ? rem_g : P.gpi);
+#pragma unroll
+        for (int k = 0; k < KV; ++k) {
+          if (q_ok[k]) {
+            const int q = tid + k * NT;
+#pragma unroll
+            for (int l = 0; l < VEC; ++l) {
+              red[q * VEC + l] = acc[k][l];
+              acc[k][l] = 0.0;
+            }
+          }
+        }
+        __syncthreads();
+        const int rest = P.T / n_in;
+        const int ro = (int)P.n_blocks_per_jout;
+        const int32_t* __restrict__ bbase = a.bins + P.bin_off;
+        const int32_t* __restrict__ brest = bbase + n_in;
+        const int T_ = P.T;
+        if (n_in == 1) {
+          reduce_bins([&](int g, int r) { return red[(g * ro + r / rest) * T_ + (r % rest)]; }, ng, ro * rest,
+                      red, part2);
+        } else {
+          reduce_bins(
+              [&](int gb, int r) {
+                const int g = gb / n_in, b = gb - (gb / n_in) * n_in;
+                const int slot = g * ro + r / rest;
+                return red[slot * T_ + bbase[b] + brest[r % rest]];
+              },
+              ng * n_in, ro * rest, red, part2);
+        }
+        for (int b = tid; b < ng * n_in; b += NT) finalize_entry<T>(P, g0 * n_in + b, red[b], aux, a.qout, a.err);
+        __syncthreads();
+      }
     }
 
-    if (P.out_kind == OUT_NONE) continue;
+    if (P.out_kind == OUT_NONE || multi) continue;
 
     // ---- block partials -> n_in bins (fixed order) ----
     const int n_in = P.n_in;
@@ -298,23 +483,7 @@ __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
     if (P.n_chunks == 1) {
       for (int b = tid; b < n_in; b += NT) finalize_entry<T>(P, j0 + b, red[b], aux, a.qout, a.err);
     } else {
-      double* part = a.partials + P.part_off + (item.j_out * P.n_chunks + item.chunk) * (int64_t)n_in;
-      for (int b = tid; b < n_in; b += NT) part[b] = red[b];
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) {
-        const int prev = atomicAdd(&a.counters[P.cnt_off + item.j_out], 1);
-        s_last = (prev == P.n_chunks - 1);
-      }
-      __syncthreads();
-      if (s_last) {
-        __threadfence();
-        const double* pj = a.partials + P.part_off + item.j_out * P.n_chunks * (int64_t)n_in;
-        reduce_bins([&](int b, int r) { return __ldcg(pj + (int64_t)r * n_in + b); }, n_in,
-                    P.n_chunks, red, part2);
-        for (int b = tid; b < n_in; b += NT) finalize_entry<T>(P, j0 + b, red[b], aux, a.qout, a.err);
-        if (tid == 0) a.counters[P.cnt_off + item.j_out] = 0;
-      }
+      chunk_finalize<T>(P, item, a, red, part2, &s_last, aux);
     }
     __syncthreads();
   }
