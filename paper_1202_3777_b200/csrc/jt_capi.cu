@@ -158,8 +158,10 @@ struct PassSpec {
 
 struct WaveRt {
   int vec = 1;
-  int grid = 0;
-  int n_items = 0;
+  int grid = 0;      // general kernel
+  int n_items = 0;   // general-kernel items start at item_base
+  int grid_own = 0;  // thread-owned-bins kernel
+  int n_own = 0;     // its items follow the general ones
   int64_t pass_base = 0, item_base = 0;
 };
 
@@ -174,6 +176,7 @@ struct Program {
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t gstream = nullptr;
   int runs = 0;
+  int64_t n_launches = 0;  // kernel launches per run
   ~Program() {
     if (gexec) cudaGraphExecDestroy(gexec);
     cudaFree(d_passes);
@@ -671,6 +674,7 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
   auto& bins = hp.bins;
   int64_t& n_part = hp.n_part;
   int64_t& n_cnt = hp.n_cnt;
+  std::vector<Item> own_items;
   for (auto& w : waves) {
     if (w.empty()) continue;
     int vec = st->esz == 4 ? 4 : 2;
@@ -694,11 +698,17 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
       n_cnt += bp.n_cnt;
       passes.push_back(bp.d);
       hp.pass_clique.push_back(ps.clique);
-      items.insert(items.end(), bp.items.begin(), bp.items.end());
+      (bp.d.own ? own_items : items).insert((bp.d.own ? own_items : items).end(), bp.items.begin(),
+                                            bp.items.end());
     }
     rt.n_items = (int)(items.size() - rt.item_base);
+    rt.n_own = (int)own_items.size();
+    items.insert(items.end(), own_items.begin(), own_items.end());
+    own_items.clear();
     const int occ = occ_override ? occ_override : wave_max_ctas_per_sm(st->plan->dtype, vec);
+    const int occ_o = occ_override ? occ_override : wave_own_max_ctas_per_sm(st->plan->dtype, vec);
     rt.grid = (int)std::min<int64_t>(rt.n_items, (int64_t)occ * st->num_sms);
+    rt.grid_own = (int)std::min<int64_t>(rt.n_own, (int64_t)occ_o * st->num_sms);
     hp.waves.push_back(rt);
   }
   return JT_OK;
@@ -711,6 +721,7 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
   if (rc0) return rc0;
   auto prog = std::make_unique<Program>();
   prog->waves = hp.waves;
+  for (auto& w : hp.waves) prog->n_launches += (w.n_items ? 1 : 0) + (w.n_own ? 1 : 0);
   auto& passes = hp.passes;
   auto& items = hp.items;
   auto& blk = hp.blk;
@@ -750,8 +761,16 @@ static int launch_program_waves(jt_state* st, Program* pr, cudaStream_t s) {
     a.passes = pr->d_passes + w.pass_base;
     a.items = pr->d_items + w.item_base;
     a.n_items = w.n_items;
-    CK(launch_wave(st->plan->dtype, w.vec, a, w.grid, s));
-    st->launches++;
+    if (w.n_items) {
+      CK(launch_wave(st->plan->dtype, w.vec, a, w.grid, s));
+      st->launches++;
+    }
+    if (w.n_own) {
+      a.items = pr->d_items + w.item_base + w.n_items;
+      a.n_items = w.n_own;
+      CK(launch_wave_own(st->plan->dtype, w.vec, a, w.grid_own, s));
+      st->launches++;
+    }
   }
   return JT_OK;
 }
@@ -763,7 +782,7 @@ static int run_program(jt_state* st, Program* pr, cudaStream_t s) {
   if (pr->waves.size() <= 1 || pr->runs < 2) return launch_program_waves(st, pr, s);
   if (pr->gexec && pr->gstream == s) {
     CK(cudaGraphLaunch(pr->gexec, s));
-    st->launches += (int64_t)pr->waves.size();
+    st->launches += pr->n_launches;
     return JT_OK;
   }
   cudaStreamCaptureStatus cs;
@@ -783,7 +802,7 @@ static int run_program(jt_state* st, Program* pr, cudaStream_t s) {
   cudaGraphDestroy(graph);
   pr->gstream = s;
   CK(cudaGraphLaunch(pr->gexec, s));
-  st->launches += (int64_t)pr->waves.size();
+  st->launches += pr->n_launches;
   return JT_OK;
 }
 
@@ -1664,13 +1683,14 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
   char line[512];
   for (size_t w = 0; w < hp.waves.size(); ++w) {
     const WaveRt& rt = hp.waves[w];
-    snprintf(line, sizeof line, "wave %zu vec %d grid %d items %d\n", w, rt.vec, rt.grid, rt.n_items);
+    snprintf(line, sizeof line, "wave %zu vec %d grid %d items %d own-grid %d own-items %d\n", w, rt.vec, rt.grid,
+             rt.n_items, rt.grid_own, rt.n_own);
     out += line;
     const int64_t pe = (w + 1 < hp.waves.size()) ? hp.waves[w + 1].pass_base : (int64_t)hp.passes.size();
     for (int64_t pi = rt.pass_base; pi < pe; ++pi) {
       const DevPass& d = hp.passes[pi];
       int64_t n_items = 0, n_out = 0;
-      for (int64_t i = rt.item_base; i < rt.item_base + rt.n_items; ++i)
+      for (int64_t i = rt.item_base; i < rt.item_base + rt.n_items + rt.n_own; ++i)
         if (hp.items[i].pass == pi - rt.pass_base) {
           ++n_items;
           if (hp.items[i].chunk == 0) n_out += hp.items[i].j_count;

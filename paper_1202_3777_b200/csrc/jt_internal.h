@@ -77,6 +77,8 @@ struct WaveArgs {
 // launchers (jt_kernels.cu)
 cudaError_t launch_wave(int dtype, int vec, const WaveArgs& a, int grid, cudaStream_t s);
 int wave_max_ctas_per_sm(int dtype, int vec);
+cudaError_t launch_wave_own(int dtype, int vec, const WaveArgs& a, int grid, cudaStream_t s);
+int wave_own_max_ctas_per_sm(int dtype, int vec);
 cudaError_t launch_normalize(const double* qout, const int64_t* q_off, const int32_t* q_card,
                              const int32_t* q_col, int nq, int B, int total_cols,
                              int normalize, double* post, int* err, cudaStream_t s);

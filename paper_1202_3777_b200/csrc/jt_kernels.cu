@@ -159,98 +159,133 @@ __device__ void chunk_finalize(const DevPass& P, const Item& item, const WaveArg
 }
 
 // Thread-owned bins (P.own): each thread owns the VEC output lanes of its
-// position in every block (n_in == T == NT*VEC), streams KV blocks per
+// position in every block (n_in == T == NT*VEC), streams OKV blocks per
 // iteration and finalizes its own lanes at every output-group boundary —
-// no barriers, no shared memory.  This is the batched layout's natural path.
+// no barriers, no shared memory in the steady state.  This is the batched
+// layout's natural path (case = innermost index).
+constexpr int OKV = 8;
+
 template <typename T, int VEC>
-__device__ __forceinline__ void own_item(const DevPass& P, const Item& item, const WaveArgs& a, T* clique,
-                                         const T* base, T* aux, int q_src, int q_dst,
-                                         const uint16_t* qfac /* [f*KV*NT + tid] */, double* red,
-                                         double* part2, int* s_last) {
+__global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
+  __shared__ DevPass P;
+  __shared__ double part2[NT];
+  __shared__ int s_last;
+  __shared__ double red[NT * 4];
+  T* __restrict__ clique = reinterpret_cast<T*>(a.clique);
+  const T* __restrict__ base = reinterpret_cast<const T*>(a.base);
+  T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
   const int tid = threadIdx.x;
-  const int64_t r_out = P.n_blocks_per_jout;
-  const bool chunked = P.n_chunks > 1;
-  int64_t b0, b1;
-  if (!chunked) {
-    b0 = item.j_out * r_out;
-    b1 = (item.j_out + item.j_count) * r_out;
-  } else {
-    b0 = item.j_out * r_out + (int64_t)item.chunk * P.blocks_per_chunk;
-    b1 = min(b0 + P.blocks_per_chunk, (item.j_out + 1) * r_out);
-  }
-  const T* __restrict__ srcA = (P.src_arena == A_BASE ? base : clique) + P.src_off;
-  const bool wr = P.dst_off >= 0;
-  T* __restrict__ dstA = clique + (wr ? P.dst_off : 0);
-  const int64_t* __restrict__ blk = a.blk + P.blk_off;
-  const int bs = P.blk_stride, nf = P.nf;
-  double acc[VEC];
-#pragma unroll
-  for (int l = 0; l < VEC; ++l) acc[l] = 0.0;
-  int64_t next_flush = chunked ? INT64_MAX : (b0 / r_out + 1) * r_out;
   const int lane0 = tid * VEC;
-  for (int64_t bb = b0; bb < b1; bb += KV) {
-    T v[KV][VEC];
-    bool ok[KV];
+  int cur = -1;
+  int q_src = 0, q_dst = 0;
+  int qf[MAXF];
+  for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
+    const Item item = a.items[it];
+    if (item.pass != cur) {
+      __syncthreads();
+      const int* sw = reinterpret_cast<const int*>(a.passes + item.pass);
+      int* dw = reinterpret_cast<int*>(&P);
+      for (int w = tid; w < (int)(sizeof(DevPass) / 4); w += NT) dw[w] = sw[w];
+      __syncthreads();
+      cur = item.pass;
+      int rem = lane0, s = 0, dd = 0;
 #pragma unroll
-    for (int u = 0; u < KV; ++u) {
-      ok[u] = bb + u < b1;
-      const int64_t* e = blk + (ok[u] ? bb + u : b0) * bs;
-      if (ok[u]) {
-        const T* p = srcA + e[0] + q_src;
-        if (VEC == 1 || P.src_vec) {
-          load_vec<T, VEC>(p, v[u]);
-        } else {
-          const T x = *p;
+      for (int f = 0; f < MAXF; ++f) qf[f] = 0;
+      for (int d = P.ndi - 1; d >= 0; --d) {
+        const int c = P.icard[d];
+        const int dig = rem % c;
+        rem /= c;
+        s += dig * P.isrc[d];
+        dd += dig * P.idst[d];
 #pragma unroll
-          for (int l = 0; l < VEC; ++l) v[u][l] = x;
-        }
+        for (int f = 0; f < MAXF; ++f)
+          if (f < P.nf) qf[f] += dig * P.ifac[f][d];
       }
+      q_src = s;
+      q_dst = dd;
     }
+    const int64_t r_out = P.n_blocks_per_jout;
+    const bool chunked = P.n_chunks > 1;
+    int64_t b0, b1;
+    if (!chunked) {
+      b0 = item.j_out * r_out;
+      b1 = (item.j_out + item.j_count) * r_out;
+    } else {
+      b0 = item.j_out * r_out + (int64_t)item.chunk * P.blocks_per_chunk;
+      b1 = min(b0 + P.blocks_per_chunk, (item.j_out + 1) * r_out);
+    }
+    const T* __restrict__ srcA = (P.src_arena == A_BASE ? base : clique) + P.src_off + q_src;
+    const bool wr = P.dst_off >= 0;
+    T* __restrict__ dstA = clique + (wr ? P.dst_off : 0) + q_dst;
+    const int64_t* __restrict__ blk = a.blk + P.blk_off;
+    const int bs = P.blk_stride, nf = P.nf;
+    const bool svec = P.src_vec;
+    double acc[VEC];
 #pragma unroll
-    for (int f = 0; f < MAXF; ++f) {
-      if (f < nf) {
-        const T* fb = aux + P.fac_off[f] + qfac[f * KV * NT];
-        const bool fv = (P.fac_vec >> f) & 1u;
+    for (int l = 0; l < VEC; ++l) acc[l] = 0.0;
+    int64_t next_flush = chunked ? INT64_MAX : (b0 / r_out + 1) * r_out;
+    for (int64_t bb = b0; bb < b1; bb += OKV) {
+      T v[OKV][VEC];
 #pragma unroll
-        for (int u = 0; u < KV; ++u) {
-          if (ok[u]) {
-            const T* p = fb + blk[(bb + u) * bs + 2 + f];
-            T g[VEC];
-            if (VEC == 1 || fv) {
-              load_vec_ro<T, VEC>(p, g);
-            } else {
-              const T x = __ldg(p);
+      for (int u = 0; u < OKV; ++u) {
+        if (bb + u < b1) {
+          const T* p = srcA + __ldg(blk + (bb + u) * bs);
+          if (VEC == 1 || svec) {
+            load_vec<T, VEC>(p, v[u]);
+          } else {
+            const T x = *p;
 #pragma unroll
-              for (int l = 0; l < VEC; ++l) g[l] = x;
-            }
-#pragma unroll
-            for (int l = 0; l < VEC; ++l) v[u][l] *= g[l];
+            for (int l = 0; l < VEC; ++l) v[u][l] = x;
           }
         }
       }
-    }
 #pragma unroll
-    for (int u = 0; u < KV; ++u) {
-      if (!ok[u]) continue;
-      if (wr) store_vec<T, VEC>(dstA + blk[(bb + u) * bs + 1] + q_dst, v[u]);
+      for (int f = 0; f < MAXF; ++f) {
+        if (f < nf) {
+          const T* fb = aux + P.fac_off[f] + qf[f];
+          const bool fv = (P.fac_vec >> f) & 1u;
 #pragma unroll
-      for (int l = 0; l < VEC; ++l) acc[l] += (double)v[u][l];
-      if (bb + u + 1 == next_flush) {
-        const int64_t j = ((bb + u) / r_out) * (int64_t)P.n_in + lane0;
+          for (int u = 0; u < OKV; ++u) {
+            if (bb + u < b1) {
+              const T* p = fb + __ldg(blk + (bb + u) * bs + 2 + f);
+              T g[VEC];
+              if (VEC == 1 || fv) {
+                load_vec_ro<T, VEC>(p, g);
+              } else {
+                const T x = __ldg(p);
 #pragma unroll
-        for (int l = 0; l < VEC; ++l) {
-          finalize_entry<T>(P, j + l, acc[l], aux, a.qout, a.err);
-          acc[l] = 0.0;
+                for (int l = 0; l < VEC; ++l) g[l] = x;
+              }
+#pragma unroll
+              for (int l = 0; l < VEC; ++l) v[u][l] *= g[l];
+            }
+          }
         }
-        next_flush += r_out;
+      }
+#pragma unroll
+      for (int u = 0; u < OKV; ++u) {
+        if (bb + u >= b1) continue;
+        if (wr) store_vec<T, VEC>(dstA + __ldg(blk + (bb + u) * bs + 1), v[u]);
+#pragma unroll
+        for (int l = 0; l < VEC; ++l) acc[l] += (double)v[u][l];
+        if (bb + u + 1 == next_flush) {
+          const int64_t j = ((bb + u) / r_out) * (int64_t)P.n_in + lane0;
+#pragma unroll
+          for (int l = 0; l < VEC; ++l) {
+            finalize_entry<T>(P, j + l, acc[l], aux, a.qout, a.err);
+            acc[l] = 0.0;
+          }
+          next_flush += r_out;
+        }
       }
     }
-  }
-  if (chunked) {
+    if (chunked) {
 #pragma unroll
-    for (int l = 0; l < VEC; ++l) red[lane0 + l] = acc[l];
-    __syncthreads();
-    chunk_finalize<T>(P, item, a, red, part2, s_last, aux);
+      for (int l = 0; l < VEC; ++l) red[lane0 + l] = acc[l];
+      __syncthreads();
+      chunk_finalize<T>(P, item, a, red, part2, &s_last, aux);
+      __syncthreads();
+    }
   }
 }
 
@@ -311,13 +346,6 @@ __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
 #pragma unroll
         for (int f = 0; f < MAXF; ++f) s_qfac[f][k][tid] = (uint16_t)fo[f];
       }
-    }
-
-    if (P.own) {
-      own_item<T, VEC>(P, item, a, clique, base, aux, q_src[0], q_dst[0], &s_qfac[0][0][tid], red, part2,
-                       &s_last);
-      __syncthreads();
-      continue;
     }
 
     const bool multi = P.gpi > 1;
@@ -505,6 +533,40 @@ static cudaError_t launch_t(const WaveArgs& a, int grid, cudaStream_t s) {
   }
   wave_kernel<T, VEC><<<grid, NT, wave_smem<VEC>(), s>>>(a);
   return cudaGetLastError();
+}
+
+template <typename T, int VEC>
+static cudaError_t launch_own_t(const WaveArgs& a, int grid, cudaStream_t s) {
+  wave_own_kernel<T, VEC><<<grid, NT, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wave_own(int dtype, int vec, const WaveArgs& a, int grid, cudaStream_t s) {
+  if (grid <= 0 || a.n_items <= 0) return cudaSuccess;
+  if (dtype == 0) {
+    if (vec == 4) return launch_own_t<float, 4>(a, grid, s);
+    if (vec == 2) return launch_own_t<float, 2>(a, grid, s);
+    return launch_own_t<float, 1>(a, grid, s);
+  }
+  if (vec == 2) return launch_own_t<double, 2>(a, grid, s);
+  return launch_own_t<double, 1>(a, grid, s);
+}
+
+template <typename T, int VEC>
+static int occ_own_t() {
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, wave_own_kernel<T, VEC>, NT, 0);
+  return n > 0 ? n : 1;
+}
+
+int wave_own_max_ctas_per_sm(int dtype, int vec) {
+  if (dtype == 0) {
+    if (vec == 4) return occ_own_t<float, 4>();
+    if (vec == 2) return occ_own_t<float, 2>();
+    return occ_own_t<float, 1>();
+  }
+  if (vec == 2) return occ_own_t<double, 2>();
+  return occ_own_t<double, 1>();
 }
 
 cudaError_t launch_wave(int dtype, int vec, const WaveArgs& a, int grid, cudaStream_t s) {
