@@ -162,6 +162,7 @@ struct WaveRt {
   int n_items = 0;   // general-kernel items start at item_base
   int grid_own = 0;  // thread-owned-bins kernel
   int n_own = 0;     // its items follow the general ones
+  int lm_own = 0;    // load shapes of the own passes: 0 mixed, 1 src bcast + vector factors, 2 all vector
   int64_t pass_base = 0, item_base = 0;
 };
 
@@ -170,6 +171,7 @@ struct Program {
   DevPass* d_passes = nullptr;
   Item* d_items = nullptr;
   int64_t* d_blk = nullptr;
+  int32_t* d_blk32 = nullptr;
   int32_t* d_bins = nullptr;
   double* d_part = nullptr;
   int* d_cnt = nullptr;
@@ -182,6 +184,7 @@ struct Program {
     cudaFree(d_passes);
     cudaFree(d_items);
     cudaFree(d_blk);
+    cudaFree(d_blk32);
     cudaFree(d_bins);
     cudaFree(d_part);
     cudaFree(d_cnt);
@@ -372,6 +375,7 @@ static int64_t tensor_stride(const jt_plan* p, const Tensor& t, int var, int64_t
 struct BuiltPass {
   DevPass d;
   std::vector<int64_t> blk;
+  std::vector<int32_t> blk32;
   std::vector<int32_t> bins;
   int64_t n_part = 0;
   int64_t n_cnt = 0;
@@ -519,8 +523,9 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
     c.bpc = bpc;
     c.n_chunks = (c.r_out + bpc - 1) / bpc;
     c.j_per_item = 1;
-    if (c.own && c.n_chunks == 1)
-      c.j_per_item = std::max<int64_t>(1, per_item / std::max<int64_t>(1, c.r_out * T));
+    // own items: ~16 blocks, so concurrently running CTAs walk neighbouring
+    // output groups and share their factor rows in L2
+    if (c.own && c.n_chunks == 1) c.j_per_item = std::max<int64_t>(1, 16 / std::max<int64_t>(1, c.r_out));
     if (c.gpi > 1) {
       c.n_chunks = 1;
       c.bpc = c.r_out;
@@ -625,6 +630,33 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
       }
     }
   }
+  // thread-owned passes read a compact int32 table: every column in units of
+  // the largest power-of-two-free common step (T for lane-strided tensors)
+  if (best.own) {
+    const int ncol = 2 + nf;
+    std::vector<int64_t> unit(ncol, 0);
+    for (int c = 0; c < ncol; ++c) {
+      int64_t gcd = 0;
+      for (int64_t b = 0; b < nblk; ++b) gcd = std::gcd(gcd, bp.blk[b * ncol + c]);
+      unit[c] = gcd > 0 ? gcd : 1;
+      if (unit[c] > (1 << 30)) unit[c] = 1;
+    }
+    bp.blk32.resize(bp.blk.size());
+    bool fits = true;
+    for (int64_t b = 0; b < nblk && fits; ++b)
+      for (int c = 0; c < ncol; ++c) {
+        const int64_t q = bp.blk[b * ncol + c] / unit[c];
+        if (q > INT32_MAX) fits = false;
+        bp.blk32[b * ncol + c] = (int32_t)q;
+      }
+    if (!fits || unit[0] > INT32_MAX || unit[1] > INT32_MAX) return JT_ERR_UNSUPPORTED;
+    d.unit_src = (int)unit[0];
+    d.unit_dst = (int)unit[1];
+    for (int f = 0; f < nf; ++f) {
+      if (unit[2 + f] > INT32_MAX) return JT_ERR_UNSUPPORTED;
+      d.unit_fac[f] = (int)unit[2 + f];
+    }
+  }
   // bin tables: position(b, p) = binbase[b] + binrest[p] over the inner block
   if (has_out && d.n_in > 1) {
     std::vector<int64_t> pstride(d.ndi, 1);
@@ -661,6 +693,7 @@ struct HostProgram {
   std::vector<DevPass> passes;
   std::vector<Item> items;
   std::vector<int64_t> blk;
+  std::vector<int32_t> blk32;
   std::vector<int32_t> bins;
   std::vector<int> pass_clique;
   int64_t n_part = 0, n_cnt = 0;
@@ -689,6 +722,9 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
       int rc = compile_pass(st, ps, vec, local, bp);
       if (rc != JT_OK) return rc;
       bp.d.blk_off = (int64_t)blk.size();
+      bp.d.blk32_off = (int64_t)hp.blk32.size();
+      hp.blk32.insert(hp.blk32.end(), bp.blk32.begin(), bp.blk32.end());
+      if (bp.d.own) bp.blk.clear();  // the own kernel reads only the int32 table
       bp.d.bin_off = (int64_t)bins.size();
       bp.d.part_off = n_part;
       bp.d.cnt_off = n_cnt;
@@ -703,6 +739,18 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
     }
     rt.n_items = (int)(items.size() - rt.item_base);
     rt.n_own = (int)own_items.size();
+    {
+      int lm = -1;
+      for (int64_t pi = rt.pass_base; pi < (int64_t)passes.size(); ++pi) {
+        const DevPass& d = passes[pi];
+        if (!d.own) continue;
+        const bool allf = d.fac_vec == ((1u << d.nf) - 1u);
+        const int m = !allf ? 0 : (d.src_vec ? 2 : 1);
+        lm = lm < 0 ? m : (lm == m ? lm : 0);
+      }
+      rt.lm_own = lm < 0 ? 0 : lm;
+      if (vec != (st->esz == 4 ? 4 : 2)) rt.lm_own = 0;
+    }
     items.insert(items.end(), own_items.begin(), own_items.end());
     own_items.clear();
     const int occ = occ_override ? occ_override : wave_max_ctas_per_sm(st->plan->dtype, vec);
@@ -739,6 +787,7 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
   if ((rc = up(&prog->d_items, items))) return rc;
   if ((rc = up(&prog->d_blk, blk))) return rc;
   if ((rc = up(&prog->d_bins, bins))) return rc;
+  if ((rc = up(&prog->d_blk32, hp.blk32))) return rc;
   CK(cudaMalloc(&prog->d_part, std::max<int64_t>(n_part, 1) * sizeof(double)));
   CK(cudaMalloc(&prog->d_cnt, std::max<int64_t>(n_cnt, 1) * sizeof(int)));
   CK(cudaMemset(prog->d_cnt, 0, std::max<int64_t>(n_cnt, 1) * sizeof(int)));
@@ -757,6 +806,7 @@ static int launch_program_waves(jt_state* st, Program* pr, cudaStream_t s) {
     a.counters = pr->d_cnt;
     a.err = st->d_err;
     a.blk = pr->d_blk;
+    a.blk32 = pr->d_blk32;
     a.bins = pr->d_bins;
     a.passes = pr->d_passes + w.pass_base;
     a.items = pr->d_items + w.item_base;
@@ -768,7 +818,7 @@ static int launch_program_waves(jt_state* st, Program* pr, cudaStream_t s) {
     if (w.n_own) {
       a.items = pr->d_items + w.item_base + w.n_items;
       a.n_items = w.n_own;
-      CK(launch_wave_own(st->plan->dtype, w.vec, a, w.grid_own, s));
+      CK(launch_wave_own(st->plan->dtype, w.vec, w.lm_own, a, w.grid_own, s));
       st->launches++;
     }
   }

@@ -42,6 +42,9 @@ struct DevPass {
   int blk_stride;           // 2 + nf
   int gpi;                  // >1: each iteration covers gpi whole output groups (BPI = gpi*r_out),
                             //     reduced and finalized per iteration; items span j_count groups
+  int64_t blk32_off;        // OWN passes: offset into the int32 block table (entries in units)
+  int unit_src, unit_dst;   // element offset = entry * unit
+  int unit_fac[MAXF];
   int own;                  // 1: thread-owned bins (n_in == T == NT*VEC): sync-free epilogue,
                             //    items span j_count whole output groups
   int ndi;                  // merged inner dims
@@ -68,6 +71,7 @@ struct WaveArgs {
   int* counters;
   int* err;
   const int64_t* blk;
+  const int32_t* blk32;
   const int32_t* bins;
   const DevPass* passes;
   const Item* items;
@@ -77,7 +81,7 @@ struct WaveArgs {
 // launchers (jt_kernels.cu)
 cudaError_t launch_wave(int dtype, int vec, const WaveArgs& a, int grid, cudaStream_t s);
 int wave_max_ctas_per_sm(int dtype, int vec);
-cudaError_t launch_wave_own(int dtype, int vec, const WaveArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_wave_own(int dtype, int vec, int lm, const WaveArgs& a, int grid, cudaStream_t s);
 int wave_own_max_ctas_per_sm(int dtype, int vec);
 cudaError_t launch_normalize(const double* qout, const int64_t* q_off, const int32_t* q_card,
                              const int32_t* q_col, int nq, int B, int total_cols,

@@ -163,14 +163,16 @@ __device__ void chunk_finalize(const DevPass& P, const Item& item, const WaveArg
 // iteration and finalizes its own lanes at every output-group boundary —
 // no barriers, no shared memory in the steady state.  This is the batched
 // layout's natural path (case = innermost index).
-constexpr int OKV = 8;
+constexpr int OKV = 8;      // blocks in flight per iteration
+constexpr int OWIN = 64;    // block-table window staged in shared memory
 
-template <typename T, int VEC>
+template <typename T, int VEC, int LM>
 __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
   __shared__ DevPass P;
   __shared__ double part2[NT];
   __shared__ int s_last;
   __shared__ double red[NT * 4];
+  __shared__ int32_t s_blk[OWIN * (2 + MAXF)];
   T* __restrict__ clique = reinterpret_cast<T*>(a.clique);
   const T* __restrict__ base = reinterpret_cast<const T*>(a.base);
   T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
@@ -217,65 +219,74 @@ __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
     const T* __restrict__ srcA = (P.src_arena == A_BASE ? base : clique) + P.src_off + q_src;
     const bool wr = P.dst_off >= 0;
     T* __restrict__ dstA = clique + (wr ? P.dst_off : 0) + q_dst;
-    const int64_t* __restrict__ blk = a.blk + P.blk_off;
-    const int bs = P.blk_stride, nf = P.nf;
-    const bool svec = P.src_vec;
+    const int bs = 2 + P.nf, nf = P.nf;
+    const int us = P.unit_src, ud = P.unit_dst;
+    const bool svec = LM == 0 ? (bool)P.src_vec : LM == 2;
     double acc[VEC];
 #pragma unroll
     for (int l = 0; l < VEC; ++l) acc[l] = 0.0;
     int64_t next_flush = chunked ? INT64_MAX : (b0 / r_out + 1) * r_out;
-    for (int64_t bb = b0; bb < b1; bb += OKV) {
-      T v[OKV][VEC];
+    for (int64_t w0 = b0; w0 < b1; w0 += OWIN) {
+      const int wn = (int)((b1 - w0) < OWIN ? (b1 - w0) : OWIN);
+      __syncthreads();
+      const int32_t* g = a.blk32 + P.blk32_off + w0 * bs;
+      for (int i = tid; i < wn * bs; i += NT) s_blk[i] = __ldg(g + i);
+      __syncthreads();
+      for (int wb = 0; wb < wn; wb += OKV) {
+        T v[OKV][VEC];
 #pragma unroll
-      for (int u = 0; u < OKV; ++u) {
-        if (bb + u < b1) {
-          const T* p = srcA + __ldg(blk + (bb + u) * bs);
-          if (VEC == 1 || svec) {
-            load_vec<T, VEC>(p, v[u]);
-          } else {
-            const T x = *p;
+        for (int u = 0; u < OKV; ++u) {
+          if (wb + u < wn) {
+            const T* p = srcA + (int64_t)s_blk[(wb + u) * bs] * us;
+            if (VEC == 1 || svec) {
+              load_vec<T, VEC>(p, v[u]);
+            } else {
+              const T x = *p;
 #pragma unroll
-            for (int l = 0; l < VEC; ++l) v[u][l] = x;
-          }
-        }
-      }
-#pragma unroll
-      for (int f = 0; f < MAXF; ++f) {
-        if (f < nf) {
-          const T* fb = aux + P.fac_off[f] + qf[f];
-          const bool fv = (P.fac_vec >> f) & 1u;
-#pragma unroll
-          for (int u = 0; u < OKV; ++u) {
-            if (bb + u < b1) {
-              const T* p = fb + __ldg(blk + (bb + u) * bs + 2 + f);
-              T g[VEC];
-              if (VEC == 1 || fv) {
-                load_vec_ro<T, VEC>(p, g);
-              } else {
-                const T x = __ldg(p);
-#pragma unroll
-                for (int l = 0; l < VEC; ++l) g[l] = x;
-              }
-#pragma unroll
-              for (int l = 0; l < VEC; ++l) v[u][l] *= g[l];
+              for (int l = 0; l < VEC; ++l) v[u][l] = x;
             }
           }
         }
-      }
 #pragma unroll
-      for (int u = 0; u < OKV; ++u) {
-        if (bb + u >= b1) continue;
-        if (wr) store_vec<T, VEC>(dstA + __ldg(blk + (bb + u) * bs + 1), v[u]);
+        for (int f = 0; f < MAXF; ++f) {
+          if (f < nf) {
+            const T* fb = aux + P.fac_off[f] + qf[f];
+            const int uf = P.unit_fac[f];
+            const bool fv = LM == 0 ? (bool)((P.fac_vec >> f) & 1u) : true;
 #pragma unroll
-        for (int l = 0; l < VEC; ++l) acc[l] += (double)v[u][l];
-        if (bb + u + 1 == next_flush) {
-          const int64_t j = ((bb + u) / r_out) * (int64_t)P.n_in + lane0;
+            for (int u = 0; u < OKV; ++u) {
+              if (wb + u < wn) {
+                const T* p = fb + (int64_t)s_blk[(wb + u) * bs + 2 + f] * uf;
+                T gv[VEC];
+                if (VEC == 1 || fv) {
+                  load_vec_ro<T, VEC>(p, gv);
+                } else {
+                  const T x = __ldg(p);
 #pragma unroll
-          for (int l = 0; l < VEC; ++l) {
-            finalize_entry<T>(P, j + l, acc[l], aux, a.qout, a.err);
-            acc[l] = 0.0;
+                  for (int l = 0; l < VEC; ++l) gv[l] = x;
+                }
+#pragma unroll
+                for (int l = 0; l < VEC; ++l) v[u][l] *= gv[l];
+              }
+            }
           }
-          next_flush += r_out;
+        }
+#pragma unroll
+        for (int u = 0; u < OKV; ++u) {
+          if (wb + u >= wn) continue;
+          if (wr) store_vec<T, VEC>(dstA + (int64_t)s_blk[(wb + u) * bs + 1] * ud, v[u]);
+#pragma unroll
+          for (int l = 0; l < VEC; ++l) acc[l] += (double)v[u][l];
+          const int64_t bi = w0 + wb + u;
+          if (bi + 1 == next_flush) {
+            const int64_t j = (bi / r_out) * (int64_t)P.n_in + lane0;
+#pragma unroll
+            for (int l = 0; l < VEC; ++l) {
+              finalize_entry<T>(P, j + l, acc[l], aux, a.qout, a.err);
+              acc[l] = 0.0;
+            }
+            next_flush += r_out;
+          }
         }
       }
     }
@@ -535,27 +546,35 @@ static cudaError_t launch_t(const WaveArgs& a, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <typename T, int VEC>
+template <typename T, int VEC, int LM>
 static cudaError_t launch_own_t(const WaveArgs& a, int grid, cudaStream_t s) {
-  wave_own_kernel<T, VEC><<<grid, NT, 0, s>>>(a);
+  wave_own_kernel<T, VEC, LM><<<grid, NT, 0, s>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_wave_own(int dtype, int vec, const WaveArgs& a, int grid, cudaStream_t s) {
+cudaError_t launch_wave_own(int dtype, int vec, int lm, const WaveArgs& a, int grid, cudaStream_t s) {
   if (grid <= 0 || a.n_items <= 0) return cudaSuccess;
   if (dtype == 0) {
-    if (vec == 4) return launch_own_t<float, 4>(a, grid, s);
-    if (vec == 2) return launch_own_t<float, 2>(a, grid, s);
-    return launch_own_t<float, 1>(a, grid, s);
+    if (vec == 4) {
+      if (lm == 1) return launch_own_t<float, 4, 1>(a, grid, s);
+      if (lm == 2) return launch_own_t<float, 4, 2>(a, grid, s);
+      return launch_own_t<float, 4, 0>(a, grid, s);
+    }
+    if (vec == 2) return launch_own_t<float, 2, 0>(a, grid, s);
+    return launch_own_t<float, 1, 0>(a, grid, s);
   }
-  if (vec == 2) return launch_own_t<double, 2>(a, grid, s);
-  return launch_own_t<double, 1>(a, grid, s);
+  if (vec == 2) {
+    if (lm == 1) return launch_own_t<double, 2, 1>(a, grid, s);
+    if (lm == 2) return launch_own_t<double, 2, 2>(a, grid, s);
+    return launch_own_t<double, 2, 0>(a, grid, s);
+  }
+  return launch_own_t<double, 1, 0>(a, grid, s);
 }
 
 template <typename T, int VEC>
 static int occ_own_t() {
   int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, wave_own_kernel<T, VEC>, NT, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, wave_own_kernel<T, VEC, 0>, NT, 0);
   return n > 0 ? n : 1;
 }
 
