@@ -148,12 +148,15 @@ struct Tensor {
 
 struct PassSpec {
   int clique = 0;
+  std::vector<int> scope;   // non-empty: iterate this scope (a separator) instead of the clique's
+  int64_t src_off = -1;     // A_AUX source: aux offset of the scope's table
   int src_arena = A_CLIQUE;
   bool write = false;
   std::vector<Tensor> factors;
   int out_kind = OUT_NONE;
   Tensor out;
   int64_t ratio_off = -1;
+  int64_t out2_off = -1;
 };
 
 struct WaveRt {
@@ -220,6 +223,13 @@ struct jt_state {
   std::map<std::string, std::unique_ptr<Program>> programs;
   int64_t launches = 0;
   int64_t device_bytes = 0;
+  bool fresh = true;        // separators hold ones (reset/load): collect may skip old/ratio
+  bool seps_stale = false;  // separators logically ones but not yet filled
+  // Two tables per separator (X at sep_off, Y at ratC_off): one holds the
+  // current separator values, the other the last collect ratios.  A fresh
+  // propagation writes the collect messages into the current table and the
+  // distribute results into the other one, then the roles swap.
+  bool sep_in_y = false;
   ~jt_state() {
     programs.clear();
     cudaFree(d_clique);
@@ -238,6 +248,8 @@ struct jt_state {
 };
 
 static int64_t align4(int64_t x) { return (x + 3) & ~int64_t(3); }
+static int64_t sep_cur(const jt_state* st, int sp) { return st->sep_in_y ? st->ratC_off[sp] : st->sep_off[sp]; }
+static int64_t sep_alt(const jt_state* st, int sp) { return st->sep_in_y ? st->sep_off[sp] : st->ratC_off[sp]; }
 
 struct DevGuard {
   int prev = 0;
@@ -385,14 +397,14 @@ struct BuiltPass {
 static std::vector<Dim> pass_dims(const jt_state* st, const PassSpec& ps) {
   const jt_plan* p = st->plan;
   const int64_t B = st->B;
-  const auto& cv = p->cvars[ps.clique];
+  const auto& cv = ps.scope.empty() ? p->cvars[ps.clique] : ps.scope;
   std::vector<int> vars(cv.begin(), cv.end());
   if (B > 1) vars.push_back(-1);
   // lanes per block for the thread-owned path: one vector per thread
   const int64_t L = (int64_t)NT * (st->esz == 4 ? 4 : 2);
   Tensor src;
   src.vars = cv;
-  src.batch = (B > 1) && ps.src_arena == A_CLIQUE;
+  src.batch = (B > 1) && (ps.src_arena == A_CLIQUE || ps.src_arena == A_AUX);
   Tensor dst;
   dst.vars = cv;
   dst.batch = B > 1;
@@ -464,6 +476,7 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
   const int nd = (int)dims.size();
   const int TH = NT * KV * vec;
   const bool has_out = ps.out_kind != OUT_NONE;
+  if (ps.write && !ps.scope.empty()) return JT_ERR_UNSUPPORTED;
   int64_t total = 1;
   for (auto& d : dims) total *= d.card;
 
@@ -555,7 +568,7 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
   std::memset(&d, 0, sizeof(d));
   const jt_plan* p = st->plan;
   d.src_arena = ps.src_arena;
-  d.src_off = ps.src_arena == A_CLIQUE ? st->coff[ps.clique] : st->boff[ps.clique];
+  d.src_off = ps.src_arena == A_AUX ? ps.src_off : ps.src_arena == A_CLIQUE ? st->coff[ps.clique] : st->boff[ps.clique];
   d.dst_off = ps.write ? st->coff[ps.clique] : -1;
   d.nf = nf;
   d.fac_vec = 0;
@@ -567,6 +580,7 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
   d.out_kind = ps.out_kind;
   d.out_off = has_out ? ps.out.off : 0;
   d.ratio_off = ps.ratio_off;
+  d.out2_off = ps.out2_off;
   d.T = (int)best.T;
   d.BPI = best.BPI;
   d.n_in = (int)best.n_in;
@@ -938,7 +952,7 @@ static Orient orient(const jt_plan* p, const std::vector<int>& roots) {
 // written once in distribute.  Cliques with more factors than a pass carries
 // absorb their children's ratios eagerly (in-place) during collect instead.
 static int build_propagate(jt_state* st, const std::vector<int>& roots, const std::vector<int>& qvars,
-                           std::vector<std::vector<PassSpec>>& waves) {
+                           std::vector<std::vector<PassSpec>>& waves, bool fresh = false) {
   const jt_plan* p = st->plan;
   const bool shared = st->mode == JT_SHARED_BASE;
   const int src_arena = shared ? A_BASE : A_CLIQUE;
@@ -956,9 +970,13 @@ static int build_propagate(jt_state* st, const std::vector<int>& roots, const st
       eager[c] = 1;
     }
   }
+  // collect ratio of a child separator: fresh propagations keep it in the
+  // separator table itself (old == 1 ⇒ ratio == new)
+  auto ratC = [&](int sp) { return fresh ? sep_cur(st, sp) : sep_alt(st, sp); };
+  const int c_kind = fresh ? OUT_SEP_FRESH : OUT_SEP;
   auto child_ratios = [&](int c) {
     std::vector<Tensor> f;
-    for (auto& ch : o.children[c]) f.push_back(sep_tensor(st, ch.second, st->ratC_off[ch.second]));
+    for (auto& ch : o.children[c]) f.push_back(sep_tensor(st, ch.second, ratC(ch.second)));
     return f;
   };
   auto ev_factors = [&](int c) {
@@ -997,9 +1015,9 @@ static int build_propagate(jt_state* st, const std::vector<int>& roots, const st
           ps.src_arena = A_CLIQUE;
           ps.write = true;
           for (size_t k = i; k < cf.size(); ++k) ps.factors.push_back(cf[k]);
-          ps.out_kind = OUT_SEP;
-          ps.out = sep_tensor(st, o.psep[c], st->sep_off[o.psep[c]]);
-          ps.ratio_off = st->ratC_off[o.psep[c]];
+          ps.out_kind = c_kind;
+          ps.out = sep_tensor(st, o.psep[c], sep_cur(st, o.psep[c]));
+          ps.ratio_off = sep_alt(st, o.psep[c]);
           main.push_back(ps);
         }
       } else {
@@ -1008,9 +1026,9 @@ static int build_propagate(jt_state* st, const std::vector<int>& roots, const st
         ps.src_arena = src_arena;
         ps.factors = cf;
         ps.factors.insert(ps.factors.end(), ef.begin(), ef.end());
-        ps.out_kind = OUT_SEP;
-        ps.out = sep_tensor(st, o.psep[c], st->sep_off[o.psep[c]]);
-        ps.ratio_off = st->ratC_off[o.psep[c]];
+        ps.out_kind = c_kind;
+        ps.out = sep_tensor(st, o.psep[c], sep_cur(st, o.psep[c]));
+        ps.ratio_off = sep_alt(st, o.psep[c]);
         main.push_back(ps);
       }
     }
@@ -1020,9 +1038,21 @@ static int build_propagate(jt_state* st, const std::vector<int>& roots, const st
     // all lower heights — correct since every child has a lower height.
     waves.push_back(main);
   }
-  // query assignment (fused queries, shared mode)
-  std::vector<std::vector<int>> qby(n);
+  // query assignment (fused queries, shared mode): a variable held by some
+  // separator is read from the smallest such separator's final table (after
+  // propagation every separator equals both adjacent clique marginals,
+  // propagate.py:393-402), otherwise from its smallest clique with all factors
+  std::vector<std::vector<int>> qby(n), qsep(p->n_seps);
   for (int v : qvars) {
+    int bs = -1;
+    if (shared)
+      for (int sp = 0; sp < p->n_seps; ++sp)
+        if (std::binary_search(p->svars[sp].begin(), p->svars[sp].end(), v))
+          if (bs < 0 || p->ssize[sp] < p->ssize[bs]) bs = sp;
+    if (bs >= 0) {
+      qsep[bs].push_back(v);
+      continue;
+    }
     int best = -1;
     for (int c = 0; c < n; ++c)
       if (std::binary_search(p->cvars[c].begin(), p->cvars[c].end(), v))
@@ -1047,7 +1077,8 @@ static int build_propagate(jt_state* st, const std::vector<int>& roots, const st
       ps.factors = fac;
       ps.write = !shared && ch.size() == 1;
       ps.out_kind = OUT_SEP;
-      ps.out = sep_tensor(st, ch[i].second, st->sep_off[ch[i].second]);
+      ps.out = sep_tensor(st, ch[i].second, sep_cur(st, ch[i].second));
+      if (fresh) ps.out2_off = sep_alt(st, ch[i].second);
       ps.ratio_off = st->ratD_off[ch[i].second];
       dw[d].push_back(ps);
     }
@@ -1068,6 +1099,22 @@ static int build_propagate(jt_state* st, const std::vector<int>& roots, const st
       ps.out = var_out_tensor(st, v);
       // materialized: queries read the final table, after its writer
       dw[shared ? d : d + 2].push_back(ps);
+    }
+  }
+  for (int sp = 0; sp < p->n_seps; ++sp) {
+    if (qsep[sp].empty()) continue;
+    // the separator's final table is written by its parent's distribute pass
+    const int a = p->sedge[sp][0], b = p->sedge[sp][1];
+    const int par = o.parent[a] == b ? b : a;
+    for (int v : qsep[sp]) {
+      PassSpec ps;
+      ps.clique = par;
+      ps.scope = p->svars[sp];
+      ps.src_arena = A_AUX;
+      ps.src_off = fresh ? sep_alt(st, sp) : sep_cur(st, sp);
+      ps.out_kind = OUT_RAW;
+      ps.out = var_out_tensor(st, v);
+      dw[o.depth[par] + 1].push_back(ps);
     }
   }
   for (auto& w : dw) waves.push_back(w);
@@ -1106,6 +1153,18 @@ static int get_program(jt_state* st, const std::string& key,
   return JT_OK;
 }
 
+// Fill the current separator tables with ones if a reset deferred it.
+static int ensure_seps(jt_state* st, cudaStream_t s) {
+  if (!st->seps_stale) return JT_OK;
+  const jt_plan* p = st->plan;
+  const int64_t x0 = st->sep_off[0], y0 = st->ratC_off[0], z0 = st->ratD_off[0];
+  const int64_t off = st->sep_in_y ? y0 : x0, n = st->sep_in_y ? z0 - y0 : y0 - x0;
+  CK(launch_fill(p->dtype, (char*)st->d_aux + off * st->esz, n, 1.0, s));
+  st->launches++;
+  st->seps_stale = false;
+  return JT_OK;
+}
+
 // ------------------------------------------------------------------ C ABI --
 extern "C" int jt_state_load(jt_state* st, int case_idx, const double* clique_concat, const double* sep_concat) {
   if (!st || case_idx < -1 || case_idx >= st->B) return JT_ERR_BAD_ARG;
@@ -1119,6 +1178,8 @@ extern "C" int jt_state_load(jt_state* st, int case_idx, const double* clique_co
   if (rc) return rc;
   cudaStream_t s = st->stream;
   const int64_t B = st->B;
+  if ((rc = ensure_seps(st, s))) return rc;
+  st->fresh = (case_idx < 0 && !sep_concat) || (st->fresh && !sep_concat);
   if (clique_concat) {
     CK(cudaMemcpyAsync(st->d_stage, clique_concat, tot_c * 8, cudaMemcpyHostToDevice, s));
     int64_t o = 0;
@@ -1142,7 +1203,7 @@ extern "C" int jt_state_load(jt_state* st, int case_idx, const double* clique_co
   int64_t o = 0;
   for (int sp = 0; sp < p->n_seps; ++sp) {
     const int64_t ns = p->ssize[sp];
-    char* dst = (char*)st->d_aux + (st->sep_off[sp] + (case_idx < 0 ? 0 : case_idx)) * st->esz;
+    char* dst = (char*)st->d_aux + (sep_cur(st, sp) + (case_idx < 0 ? 0 : case_idx)) * st->esz;
     if (sep_concat) {
       CK(launch_convert_d2t(p->dtype, st->d_stage + o, dst, ns, B, case_idx < 0 ? B : 1, s));
     } else if (case_idx < 0) {
@@ -1165,6 +1226,7 @@ extern "C" int jt_state_store(jt_state* st, int case_idx, double* clique_concat,
   if (rc) return rc;
   cudaStream_t s = st->stream;
   const int64_t B = st->B;
+  if ((rc = ensure_seps(st, s))) return rc;
   if (clique_concat) {
     int64_t o = 0;
     for (int c = 0; c < p->n_cliques; ++c) {
@@ -1178,7 +1240,7 @@ extern "C" int jt_state_store(jt_state* st, int case_idx, double* clique_concat,
   if (sep_concat) {
     int64_t o = 0;
     for (int sp = 0; sp < p->n_seps; ++sp) {
-      const char* src = (const char*)st->d_aux + (st->sep_off[sp] + case_idx) * st->esz;
+      const char* src = (const char*)st->d_aux + (sep_cur(st, sp) + case_idx) * st->esz;
       CK(launch_convert_t2d(p->dtype, src, B, st->d_stage + o, p->ssize[sp], s));
       o += p->ssize[sp];
     }
@@ -1200,11 +1262,9 @@ extern "C" int jt_state_reset(jt_state* st, void* stream) {
   DevGuard g(p->device);
   cudaStream_t s = pick_stream(st, stream);
   jt_clear_evidence(st);
-  if (p->n_seps) {
-    const int64_t n = st->ratC_off[0];  // separator tables lead the aux arena
-    CK(launch_fill(p->dtype, st->d_aux, n, 1.0, s));
-    st->launches++;
-  }
+  // separators back to ones: deferred — a fresh propagation never reads them
+  st->seps_stale = p->n_seps > 0;
+  st->fresh = true;
   if (st->mode == JT_SHARED_BASE) return JT_OK;
   Program* pr;
   auto it = st->programs.find("reset");
@@ -1364,8 +1424,13 @@ extern "C" int jt_message(jt_state* st, int src, int tgt, int sep, void* stream)
   if (!((e[0] == src && e[1] == tgt) || (e[0] == tgt && e[1] == src))) return JT_ERR_BAD_ARG;
   if (st->mode != JT_MATERIALIZED) return JT_ERR_UNSUPPORTED;
   DevGuard g(p->device);
+  cudaStream_t s = pick_stream(st, stream);
+  int rc0 = ensure_seps(st, s);
+  if (rc0) return rc0;
+  st->fresh = false;
+  const std::string mkey = key_of("msg", {src, tgt, sep, (int)st->sep_in_y});
   Program* pr;
-  auto it = st->programs.find(key_of("msg", {src, tgt, sep}));
+  auto it = st->programs.find(mkey);
   if (it != st->programs.end()) {
     pr = it->second.get();
   } else {
@@ -1373,7 +1438,7 @@ extern "C" int jt_message(jt_state* st, int src, int tgt, int sep, void* stream)
     PassSpec m;
     m.clique = src;
     m.out_kind = OUT_SEP;
-    m.out = sep_tensor(st, sep, st->sep_off[sep]);
+    m.out = sep_tensor(st, sep, sep_cur(st, sep));
     m.ratio_off = st->msg_ratio_off;
     waves[0].push_back(m);
     PassSpec sc;
@@ -1381,10 +1446,10 @@ extern "C" int jt_message(jt_state* st, int src, int tgt, int sep, void* stream)
     sc.write = true;
     sc.factors.push_back(sep_tensor(st, sep, st->msg_ratio_off));
     waves[1].push_back(sc);
-    int rc = get_program(st, key_of("msg", {src, tgt, sep}), waves, &pr);
+    int rc = get_program(st, mkey, waves, &pr);
     if (rc) return rc;
   }
-  return run_program(st, pr, pick_stream(st, stream));
+  return run_program(st, pr, s);
 }
 
 static int resolve_roots(const jt_state* st, const int32_t* roots_or_null, std::vector<int>& roots) {
@@ -1406,19 +1471,30 @@ extern "C" int jt_propagate(jt_state* st, const int32_t* roots_or_null, void* st
   std::vector<int> roots;
   int rc = resolve_roots(st, roots_or_null, roots);
   if (rc) return rc;
-  const std::string key = key_of("bp", roots, active_ev(st));
+  cudaStream_t s = pick_stream(st, stream);
+  const bool fresh = st->fresh;
+  if (!fresh && (rc = ensure_seps(st, s))) return rc;
+  std::vector<int> tag{(int)fresh, (int)st->sep_in_y};
+  std::vector<int> kv = active_ev(st);
+  kv.insert(kv.end(), tag.begin(), tag.end());
+  const std::string key = key_of("bp", roots, kv);
   Program* pr;
   auto it = st->programs.find(key);
   if (it != st->programs.end()) {
     pr = it->second.get();
   } else {
     std::vector<std::vector<PassSpec>> waves;
-    rc = build_propagate(st, roots, {}, waves);
+    rc = build_propagate(st, roots, {}, waves, fresh);
     if (rc) return rc;
     rc = get_program(st, key, waves, &pr);
     if (rc) return rc;
   }
-  return run_program(st, pr, pick_stream(st, stream));
+  rc = run_program(st, pr, s);
+  if (rc) return rc;
+  if (fresh) st->sep_in_y = !st->sep_in_y;
+  st->fresh = false;
+  st->seps_stale = false;
+  return JT_OK;
 }
 
 static int smallest_holder(const jt_plan* p, int v) {
@@ -1480,7 +1556,9 @@ static int query_program(jt_state* st, int n, const int32_t* var, const int32_t*
   std::vector<int> kk = vs;
   kk.insert(kk.end(), cs.begin(), cs.end());
   const bool shared = st->mode == JT_SHARED_BASE;
-  std::string key = key_of("q", kk, active_ev(st));
+  std::vector<int> kv = active_ev(st);
+  kv.push_back((int)st->sep_in_y);
+  std::string key = key_of("q", kk, kv);
   Program* pr;
   auto it = st->programs.find(key);
   if (it != st->programs.end()) {
@@ -1498,7 +1576,7 @@ static int query_program(jt_state* st, int n, const int32_t* var, const int32_t*
       if (shared) {
         // final table of the clique = base × evidence × Π neighbour ratios
         const int c = cs[i];
-        for (auto& ch : o.children[c]) ps.factors.push_back(sep_tensor(st, ch.second, st->ratC_off[ch.second]));
+        for (auto& ch : o.children[c]) ps.factors.push_back(sep_tensor(st, ch.second, sep_alt(st, ch.second)));
         if (o.parent[c] >= 0) ps.factors.push_back(sep_tensor(st, o.psep[c], st->ratD_off[o.psep[c]]));
         for (int v = 0; v < p->n_vars; ++v)
           if (st->ev_clique[v] == c) ps.factors.push_back(ev_tensor(st, v));
@@ -1563,21 +1641,32 @@ extern "C" int jt_propagate_query(jt_state* st, int n, const int32_t* var, int n
     if (rc) return rc;
     return n ? jt_query_device(st, n, var, nullptr, normalize, out_device, stream) : JT_OK;
   }
-  const std::string key = key_of("bpq", vs, active_ev(st));
+  cudaStream_t s = pick_stream(st, stream);
+  const bool fresh = st->fresh;
+  if (!fresh) {
+    int rc = ensure_seps(st, s);
+    if (rc) return rc;
+  }
+  std::vector<int> kv = active_ev(st);
+  kv.push_back((int)fresh);
+  kv.push_back((int)st->sep_in_y);
+  const std::string key = key_of("bpq", vs, kv);
   Program* pr;
   auto it = st->programs.find(key);
   if (it != st->programs.end()) {
     pr = it->second.get();
   } else {
     std::vector<std::vector<PassSpec>> waves;
-    int rc = build_propagate(st, p->roots, vs, waves);
+    int rc = build_propagate(st, p->roots, vs, waves, fresh);
     if (rc) return rc;
     rc = get_program(st, key, waves, &pr);
     if (rc) return rc;
   }
-  cudaStream_t s = pick_stream(st, stream);
   int rc = run_program(st, pr, s);
   if (rc) return rc;
+  if (fresh) st->sep_in_y = !st->sep_in_y;
+  st->fresh = false;
+  st->seps_stale = false;
   return n ? finish_query(st, n, var, normalize, out_device, s, nullptr) : JT_OK;
 }
 
@@ -1724,7 +1813,7 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
     }
   }
   std::vector<std::vector<PassSpec>> waves;
-  int rc = build_propagate(&st, plan->roots, qv, waves);
+  int rc = build_propagate(&st, plan->roots, qv, waves, kind == 1);
   if (rc) return rc;
   HostProgram hp;
   rc = compile_program(&st, waves, hp, occ > 0 ? occ : 2);

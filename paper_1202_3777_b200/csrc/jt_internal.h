@@ -12,7 +12,10 @@ constexpr int MAXF = 8;     // factors (ratio / evidence tensors) multiplied in 
 constexpr int MAXDI = 8;    // merged inner dimensions per pass
 
 enum ArenaId : int { A_CLIQUE = 0, A_BASE = 1, A_AUX = 2 };
-enum OutKind : int { OUT_NONE = 0, OUT_SEP = 1, OUT_RAW = 2 };
+enum OutKind : int { OUT_NONE = 0, OUT_SEP = 1, OUT_RAW = 2, OUT_SEP_FRESH = 3 };
+// OUT_SEP_FRESH: collect output of a fresh propagation (old separator known to be
+// ones): ratio == star, so only the separator itself is written and consumers
+// read it as the ratio.
 enum ErrBits : int { EB_INCONSISTENT = 1, EB_ZERO_MASS = 2 };
 
 // One pass = one sweep over one clique table: read (src), multiply the
@@ -24,13 +27,14 @@ struct DevPass {
   int64_t fac_off[MAXF];    // element offsets of the factor tensors (aux arena)
   int64_t out_off;          // aux (OUT_SEP) or qout (OUT_RAW) offset of the output
   int64_t ratio_off;        // aux offset of the ratio array written by OUT_SEP
+  int64_t out2_off;         // OUT_SEP: >= 0 writes the new separator here (old stays at out_off)
   int64_t blk_off;          // offset into the block table (int64 entries)
   int64_t bin_off;          // offset into the bin table (int32: binbase[n_in], binrest[T/n_in])
   int64_t part_off;         // offset into the partials arena (doubles)
   int64_t cnt_off;          // offset into the counters arena (ints)
   int64_t n_blocks_per_jout;// rest-outer blocks per output group (r_out)
   int64_t blocks_per_chunk; // multiple of BPI
-  int src_arena;            // A_CLIQUE or A_BASE
+  int src_arena;            // A_CLIQUE, A_BASE or A_AUX (separator-sized sources)
   int src_vec;              // 1: innermost stride 1 (vector load), 0: broadcast
   int nf;
   uint32_t fac_vec;         // bit f set: factor f has the innermost dim (vector), else broadcast

@@ -104,12 +104,14 @@ __device__ __forceinline__ void reduce_bins(F get, int n_bins, int R, double* ou
 template <typename T>
 __device__ __forceinline__ void finalize_entry(const DevPass& P, int64_t j, double star, T* aux,
                                                double* qout, int* err) {
-  if (P.out_kind == OUT_SEP) {
+  if (P.out_kind == OUT_SEP_FRESH) {
+    aux[P.out_off + j] = (T)star;
+  } else if (P.out_kind == OUT_SEP) {
     const double old = (double)aux[P.out_off + j];
     if (old == 0.0 && star != 0.0) atomicOr(err, EB_INCONSISTENT);
     const double r = (old != 0.0) ? star / old : 0.0;
     aux[P.ratio_off + j] = (T)r;
-    aux[P.out_off + j] = (T)star;
+    aux[(P.out2_off >= 0 ? P.out2_off : P.out_off) + j] = (T)star;
   } else {
     qout[P.out_off + j] = star;
   }
@@ -216,7 +218,7 @@ __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
       b0 = item.j_out * r_out + (int64_t)item.chunk * P.blocks_per_chunk;
       b1 = min(b0 + P.blocks_per_chunk, (item.j_out + 1) * r_out);
     }
-    const T* __restrict__ srcA = (P.src_arena == A_BASE ? base : clique) + P.src_off + q_src;
+    const T* __restrict__ srcA = (P.src_arena == A_BASE ? base : P.src_arena == A_AUX ? aux : clique) + P.src_off + q_src;
     const bool wr = P.dst_off >= 0;
     T* __restrict__ dstA = clique + (wr ? P.dst_off : 0) + q_dst;
     const int bs = 2 + P.nf, nf = P.nf;
@@ -364,7 +366,7 @@ __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
     const int64_t b0 = jb + (int64_t)item.chunk * P.blocks_per_chunk;
     int64_t b1 = multi ? (item.j_out + item.j_count) * P.n_blocks_per_jout : b0 + P.blocks_per_chunk;
     if (!multi && b1 > jb + P.n_blocks_per_jout) b1 = jb + P.n_blocks_per_jout;
-    const T* __restrict__ srcA = (P.src_arena == A_BASE ? base : clique) + P.src_off;
+    const T* __restrict__ srcA = (P.src_arena == A_BASE ? base : P.src_arena == A_AUX ? aux : clique) + P.src_off;
     const bool wr = P.dst_off >= 0;
     T* __restrict__ dstA = clique + (wr ? P.dst_off : 0);
     const int64_t* __restrict__ blk = a.blk + P.blk_off;
