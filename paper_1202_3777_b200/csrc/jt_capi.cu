@@ -159,13 +159,18 @@ struct PassSpec {
   int64_t out2_off = -1;
 };
 
+struct LaunchGrp {  // one kernel launch of a wave
+  int own = 0;       // 0: general kernel, 1: thread-owned-bins kernel
+  int lm = 0;        // own kernel load shapes: 0 generic, 1 src bcast + vector factors, 2 all vector
+  int grid = 0;
+  int n_items = 0;
+  int64_t item_off = 0;  // relative to the wave's item_base
+};
+
 struct WaveRt {
   int vec = 1;
-  int grid = 0;      // general kernel
-  int n_items = 0;   // general-kernel items start at item_base
-  int grid_own = 0;  // thread-owned-bins kernel
-  int n_own = 0;     // its items follow the general ones
-  int lm_own = 0;    // load shapes of the own passes: 0 mixed, 1 src bcast + vector factors, 2 all vector
+  int n_items = 0;  // all items of the wave
+  std::vector<LaunchGrp> groups;
   int64_t pass_base = 0, item_base = 0;
 };
 
@@ -721,7 +726,7 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
   auto& bins = hp.bins;
   int64_t& n_part = hp.n_part;
   int64_t& n_cnt = hp.n_cnt;
-  std::vector<Item> own_items;
+  std::vector<Item> grp_items[4];
   for (auto& w : waves) {
     if (w.empty()) continue;
     int vec = st->esz == 4 ? 4 : 2;
@@ -748,29 +753,32 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
       n_cnt += bp.n_cnt;
       passes.push_back(bp.d);
       hp.pass_clique.push_back(ps.clique);
-      (bp.d.own ? own_items : items).insert((bp.d.own ? own_items : items).end(), bp.items.begin(),
-                                            bp.items.end());
-    }
-    rt.n_items = (int)(items.size() - rt.item_base);
-    rt.n_own = (int)own_items.size();
-    {
-      int lm = -1;
-      for (int64_t pi = rt.pass_base; pi < (int64_t)passes.size(); ++pi) {
-        const DevPass& d = passes[pi];
-        if (!d.own) continue;
-        const bool allf = d.fac_vec == ((1u << d.nf) - 1u);
-        const int m = !allf ? 0 : (d.src_vec ? 2 : 1);
-        lm = lm < 0 ? m : (lm == m ? lm : 0);
+      // launch group: general kernel, or own kernel keyed by load shapes
+      int key = 0;
+      if (bp.d.own) {
+        const bool allf = bp.d.fac_vec == ((1u << bp.d.nf) - 1u);
+        const bool full_vec = vec == (st->esz == 4 ? 4 : 2);
+        key = 1 + (full_vec && allf ? (bp.d.src_vec ? 2 : 1) : 0);
       }
-      rt.lm_own = lm < 0 ? 0 : lm;
-      if (vec != (st->esz == 4 ? 4 : 2)) rt.lm_own = 0;
+      auto& g = grp_items[key];
+      g.insert(g.end(), bp.items.begin(), bp.items.end());
     }
-    items.insert(items.end(), own_items.begin(), own_items.end());
-    own_items.clear();
     const int occ = occ_override ? occ_override : wave_max_ctas_per_sm(st->plan->dtype, vec);
     const int occ_o = occ_override ? occ_override : wave_own_max_ctas_per_sm(st->plan->dtype, vec);
-    rt.grid = (int)std::min<int64_t>(rt.n_items, (int64_t)occ * st->num_sms);
-    rt.grid_own = (int)std::min<int64_t>(rt.n_own, (int64_t)occ_o * st->num_sms);
+    for (int key = 0; key < 4; ++key) {
+      auto& g = grp_items[key];
+      if (g.empty()) continue;
+      LaunchGrp lg;
+      lg.own = key > 0;
+      lg.lm = key > 0 ? key - 1 : 0;
+      lg.n_items = (int)g.size();
+      lg.item_off = (int64_t)items.size() - rt.item_base;
+      lg.grid = (int)std::min<int64_t>(lg.n_items, (int64_t)(lg.own ? occ_o : occ) * st->num_sms);
+      items.insert(items.end(), g.begin(), g.end());
+      g.clear();
+      rt.groups.push_back(lg);
+    }
+    rt.n_items = (int)(items.size() - rt.item_base);
     hp.waves.push_back(rt);
   }
   return JT_OK;
@@ -783,7 +791,7 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
   if (rc0) return rc0;
   auto prog = std::make_unique<Program>();
   prog->waves = hp.waves;
-  for (auto& w : hp.waves) prog->n_launches += (w.n_items ? 1 : 0) + (w.n_own ? 1 : 0);
+  for (auto& w : hp.waves) prog->n_launches += (int64_t)w.groups.size();
   auto& passes = hp.passes;
   auto& items = hp.items;
   auto& blk = hp.blk;
@@ -823,16 +831,11 @@ static int launch_program_waves(jt_state* st, Program* pr, cudaStream_t s) {
     a.blk32 = pr->d_blk32;
     a.bins = pr->d_bins;
     a.passes = pr->d_passes + w.pass_base;
-    a.items = pr->d_items + w.item_base;
-    a.n_items = w.n_items;
-    if (w.n_items) {
-      CK(launch_wave(st->plan->dtype, w.vec, a, w.grid, s));
-      st->launches++;
-    }
-    if (w.n_own) {
-      a.items = pr->d_items + w.item_base + w.n_items;
-      a.n_items = w.n_own;
-      CK(launch_wave_own(st->plan->dtype, w.vec, w.lm_own, a, w.grid_own, s));
+    for (const LaunchGrp& g : w.groups) {
+      a.items = pr->d_items + w.item_base + g.item_off;
+      a.n_items = g.n_items;
+      if (g.own) CK(launch_wave_own(st->plan->dtype, w.vec, g.lm, a, g.grid, s));
+      else CK(launch_wave(st->plan->dtype, w.vec, a, g.grid, s));
       st->launches++;
     }
   }
@@ -1822,14 +1825,13 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
   char line[512];
   for (size_t w = 0; w < hp.waves.size(); ++w) {
     const WaveRt& rt = hp.waves[w];
-    snprintf(line, sizeof line, "wave %zu vec %d grid %d items %d own-grid %d own-items %d\n", w, rt.vec, rt.grid,
-             rt.n_items, rt.grid_own, rt.n_own);
+    snprintf(line, sizeof line, "wave %zu vec %d items %d launches %zu\n", w, rt.vec, rt.n_items, rt.groups.size());
     out += line;
     const int64_t pe = (w + 1 < hp.waves.size()) ? hp.waves[w + 1].pass_base : (int64_t)hp.passes.size();
     for (int64_t pi = rt.pass_base; pi < pe; ++pi) {
       const DevPass& d = hp.passes[pi];
       int64_t n_items = 0, n_out = 0;
-      for (int64_t i = rt.item_base; i < rt.item_base + rt.n_items + rt.n_own; ++i)
+      for (int64_t i = rt.item_base; i < rt.item_base + rt.n_items; ++i)
         if (hp.items[i].pass == pi - rt.pass_base) {
           ++n_items;
           if (hp.items[i].chunk == 0) n_out += hp.items[i].j_count;

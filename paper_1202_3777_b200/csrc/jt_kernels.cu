@@ -273,23 +273,31 @@ __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
             }
           }
         }
+        // ≤ OKV-term partial sums in the storage type, folded into the fp64
+        // accumulator once per iteration or output group
+        T part[VEC];
+#pragma unroll
+        for (int l = 0; l < VEC; ++l) part[l] = (T)0;
 #pragma unroll
         for (int u = 0; u < OKV; ++u) {
           if (wb + u >= wn) continue;
           if (wr) store_vec<T, VEC>(dstA + (int64_t)s_blk[(wb + u) * bs + 1] * ud, v[u]);
 #pragma unroll
-          for (int l = 0; l < VEC; ++l) acc[l] += (double)v[u][l];
+          for (int l = 0; l < VEC; ++l) part[l] += v[u][l];
           const int64_t bi = w0 + wb + u;
           if (bi + 1 == next_flush) {
             const int64_t j = (bi / r_out) * (int64_t)P.n_in + lane0;
 #pragma unroll
             for (int l = 0; l < VEC; ++l) {
-              finalize_entry<T>(P, j + l, acc[l], aux, a.qout, a.err);
+              finalize_entry<T>(P, j + l, acc[l] + (double)part[l], aux, a.qout, a.err);
               acc[l] = 0.0;
+              part[l] = (T)0;
             }
             next_flush += r_out;
           }
         }
+#pragma unroll
+        for (int l = 0; l < VEC; ++l) acc[l] += (double)part[l];
       }
     }
     if (chunked) {
