@@ -162,6 +162,7 @@ struct PassSpec {
 struct LaunchGrp {  // one kernel launch of a wave
   int own = 0;       // 0: general kernel, 1: thread-owned-bins kernel
   int lm = 0;        // own kernel load shapes: 0 generic, 1 src bcast + vector factors, 2 all vector
+  int m = 1;         // own kernel vectors per thread per block
   int grid = 0;
   int n_items = 0;
   int64_t item_off = 0;  // relative to the wave's item_base
@@ -488,6 +489,7 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
   struct Cand {
     int k;
     bool own = false;
+    int own_m = 0;
     int gpi = 1;
     int64_t j_per_item = 1;
     int64_t T, n_in, n_out, r_out;
@@ -520,7 +522,13 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
       if (has_out && dims[i].out) c.n_out *= dims[i].card;
       else c.r_out *= dims[i].card;
     }
-    c.own = has_out && c.n_in == T && T == (int64_t)NT * vec;
+    c.own_m = 0;
+    if (has_out && c.n_in == T && T % ((int64_t)NT * vec) == 0) {
+      const int64_t m = T / ((int64_t)NT * vec);
+      // M > 1 only for full-width vectors (the templated load-shape kernels)
+      if (m == 1 || ((m == 2 || m == 4) && vec == (st->esz == 4 ? 4 : 2))) c.own_m = (int)m;
+    }
+    c.own = c.own_m > 0;
     c.BPI = c.own ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(TH / T, c.r_out));
     // several whole output groups per iteration when a group is smaller than an iteration
     c.gpi = 1;
@@ -543,7 +551,8 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
     c.j_per_item = 1;
     // own items: ~16 blocks, so concurrently running CTAs walk neighbouring
     // output groups and share their factor rows in L2
-    if (c.own && c.n_chunks == 1) c.j_per_item = std::max<int64_t>(1, 16 / std::max<int64_t>(1, c.r_out));
+    if (c.own && c.n_chunks == 1)
+      c.j_per_item = std::max<int64_t>(1, (16 / c.own_m) / std::max<int64_t>(1, c.r_out));
     if (c.gpi > 1) {
       c.n_chunks = 1;
       c.bpc = c.r_out;
@@ -594,6 +603,7 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
   d.blocks_per_chunk = best.bpc;
   d.blk_stride = 2 + nf;
   d.own = best.own ? 1 : 0;
+  d.own_m = best.own_m;
   d.gpi = best.gpi;
   d.ndi = (int)best.inner.size();
   for (int i = 0; i < d.ndi; ++i) {
@@ -653,13 +663,7 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
   // the largest power-of-two-free common step (T for lane-strided tensors)
   if (best.own) {
     const int ncol = 2 + nf;
-    std::vector<int64_t> unit(ncol, 0);
-    for (int c = 0; c < ncol; ++c) {
-      int64_t gcd = 0;
-      for (int64_t b = 0; b < nblk; ++b) gcd = std::gcd(gcd, bp.blk[b * ncol + c]);
-      unit[c] = gcd > 0 ? gcd : 1;
-      if (unit[c] > (1 << 30)) unit[c] = 1;
-    }
+    std::vector<int64_t> unit(ncol, 1);  // plain int32 element offsets
     bp.blk32.resize(bp.blk.size());
     bool fits = true;
     for (int64_t b = 0; b < nblk && fits; ++b)
@@ -726,7 +730,7 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
   auto& bins = hp.bins;
   int64_t& n_part = hp.n_part;
   int64_t& n_cnt = hp.n_cnt;
-  std::vector<Item> grp_items[4];
+  std::vector<Item> grp_items[10];
   for (auto& w : waves) {
     if (w.empty()) continue;
     int vec = st->esz == 4 ? 4 : 2;
@@ -758,19 +762,22 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
       if (bp.d.own) {
         const bool allf = bp.d.fac_vec == ((1u << bp.d.nf) - 1u);
         const bool full_vec = vec == (st->esz == 4 ? 4 : 2);
-        key = 1 + (full_vec && allf ? (bp.d.src_vec ? 2 : 1) : 0);
+        const int lm = full_vec && allf ? (bp.d.src_vec ? 2 : 1) : 0;
+        if (lm == 0 && bp.d.own_m != 1) return JT_ERR_UNSUPPORTED;
+        key = 1 + lm + 3 * (bp.d.own_m == 4 ? 2 : bp.d.own_m == 2 ? 1 : 0);
       }
       auto& g = grp_items[key];
       g.insert(g.end(), bp.items.begin(), bp.items.end());
     }
     const int occ = occ_override ? occ_override : wave_max_ctas_per_sm(st->plan->dtype, vec);
     const int occ_o = occ_override ? occ_override : wave_own_max_ctas_per_sm(st->plan->dtype, vec);
-    for (int key = 0; key < 4; ++key) {
+    for (int key = 0; key < 10; ++key) {
       auto& g = grp_items[key];
       if (g.empty()) continue;
       LaunchGrp lg;
       lg.own = key > 0;
-      lg.lm = key > 0 ? key - 1 : 0;
+      lg.lm = key > 0 ? (key - 1) % 3 : 0;
+      lg.m = key > 0 ? (1 << ((key - 1) / 3)) : 1;
       lg.n_items = (int)g.size();
       lg.item_off = (int64_t)items.size() - rt.item_base;
       lg.grid = (int)std::min<int64_t>(lg.n_items, (int64_t)(lg.own ? occ_o : occ) * st->num_sms);
@@ -834,7 +841,7 @@ static int launch_program_waves(jt_state* st, Program* pr, cudaStream_t s) {
     for (const LaunchGrp& g : w.groups) {
       a.items = pr->d_items + w.item_base + g.item_off;
       a.n_items = g.n_items;
-      if (g.own) CK(launch_wave_own(st->plan->dtype, w.vec, g.lm, a, g.grid, s));
+      if (g.own) CK(launch_wave_own(st->plan->dtype, w.vec, g.lm, g.m, a, g.grid, s));
       else CK(launch_wave(st->plan->dtype, w.vec, a, g.grid, s));
       st->launches++;
     }
@@ -1838,10 +1845,10 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
         }
       snprintf(line, sizeof line,
                "  pass clique %d src %d nf %d wr %d out %d T %d n_in %d n_out %lld r_out %lld BPI %d chunks %d "
-               "bpc %lld items %lld ndi %d own %d gpi %d part %lld\n",
+               "bpc %lld items %lld ndi %d own %d/%d gpi %d part %lld\n",
                hp.pass_clique[pi], d.src_arena, d.nf, d.dst_off >= 0, d.out_kind, d.T, d.n_in, (long long)n_out,
                (long long)d.n_blocks_per_jout, d.BPI, d.n_chunks, (long long)d.blocks_per_chunk,
-               (long long)n_items, d.ndi, d.own, d.gpi,
+               (long long)n_items, d.ndi, d.own, d.own_m, d.gpi,
                (long long)(d.n_chunks > 1 && d.out_kind ? n_out * d.n_chunks * d.n_in : 0));
       out += line;
     }

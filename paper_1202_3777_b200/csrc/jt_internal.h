@@ -49,6 +49,7 @@ struct DevPass {
   int64_t blk32_off;        // OWN passes: offset into the int32 block table (entries in units)
   int unit_src, unit_dst;   // element offset = entry * unit
   int unit_fac[MAXF];
+  int own_m;                // own passes: vectors (lane chunks) per thread per block
   int own;                  // 1: thread-owned bins (n_in == T == NT*VEC): sync-free epilogue,
                             //    items span j_count whole output groups
   int ndi;                  // merged inner dims
@@ -85,7 +86,7 @@ struct WaveArgs {
 // launchers (jt_kernels.cu)
 cudaError_t launch_wave(int dtype, int vec, const WaveArgs& a, int grid, cudaStream_t s);
 int wave_max_ctas_per_sm(int dtype, int vec);
-cudaError_t launch_wave_own(int dtype, int vec, int lm, const WaveArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_wave_own(int dtype, int vec, int lm, int m, const WaveArgs& a, int grid, cudaStream_t s);
 int wave_own_max_ctas_per_sm(int dtype, int vec);
 cudaError_t launch_normalize(const double* qout, const int64_t* q_off, const int32_t* q_card,
                              const int32_t* q_col, int nq, int B, int total_cols,

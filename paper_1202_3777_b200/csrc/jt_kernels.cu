@@ -165,24 +165,28 @@ __device__ void chunk_finalize(const DevPass& P, const Item& item, const WaveArg
 // iteration and finalizes its own lanes at every output-group boundary —
 // no barriers, no shared memory in the steady state.  This is the batched
 // layout's natural path (case = innermost index).
-constexpr int OKV = 8;      // blocks in flight per iteration
 constexpr int OWIN = 64;    // block-table window staged in shared memory
 
-template <typename T, int VEC, int LM>
+// M vectors (lane chunks NT*VEC apart) per thread per block; OKV*M = 8 vectors
+// in flight per tensor per iteration.  Block-table entries are int32 element
+// offsets (P.unit_* == 1) staged per window in shared memory.
+template <typename T, int VEC, int LM, int M>
 __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
+  constexpr int OKV = 8 / M;
   __shared__ DevPass P;
   __shared__ double part2[NT];
   __shared__ int s_last;
-  __shared__ double red[NT * 4];
+  __shared__ double red[NT * 4 * 4];
   __shared__ int32_t s_blk[OWIN * (2 + MAXF)];
   T* __restrict__ clique = reinterpret_cast<T*>(a.clique);
   const T* __restrict__ base = reinterpret_cast<const T*>(a.base);
   T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
   const int tid = threadIdx.x;
   const int lane0 = tid * VEC;
+  constexpr int CH = NT * VEC;  // lanes per chunk
   int cur = -1;
-  int q_src = 0, q_dst = 0;
-  int qf[MAXF];
+  int q_src[M], q_dst[M];
+  int qf[MAXF][M];
   for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
     const Item item = a.items[it];
     if (item.pass != cur) {
@@ -192,21 +196,27 @@ __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
       for (int w = tid; w < (int)(sizeof(DevPass) / 4); w += NT) dw[w] = sw[w];
       __syncthreads();
       cur = item.pass;
-      int rem = lane0, s = 0, dd = 0;
 #pragma unroll
-      for (int f = 0; f < MAXF; ++f) qf[f] = 0;
-      for (int d = P.ndi - 1; d >= 0; --d) {
-        const int c = P.icard[d];
-        const int dig = rem % c;
-        rem /= c;
-        s += dig * P.isrc[d];
-        dd += dig * P.idst[d];
+      for (int m = 0; m < (LM == 0 ? M : 1); ++m) {
+        int rem = lane0 + m * CH, s = 0, dd = 0;
+        int fo[MAXF];
 #pragma unroll
-        for (int f = 0; f < MAXF; ++f)
-          if (f < P.nf) qf[f] += dig * P.ifac[f][d];
+        for (int f = 0; f < MAXF; ++f) fo[f] = 0;
+        for (int d = P.ndi - 1; d >= 0; --d) {
+          const int c = P.icard[d];
+          const int dig = rem % c;
+          rem /= c;
+          s += dig * P.isrc[d];
+          dd += dig * P.idst[d];
+#pragma unroll
+          for (int f = 0; f < MAXF; ++f)
+            if (f < P.nf) fo[f] += dig * P.ifac[f][d];
+        }
+        q_src[m] = s;
+        q_dst[m] = dd;
+#pragma unroll
+        for (int f = 0; f < MAXF; ++f) qf[f][m] = fo[f];
       }
-      q_src = s;
-      q_dst = dd;
     }
     const int64_t r_out = P.n_blocks_per_jout;
     const bool chunked = P.n_chunks > 1;
@@ -218,16 +228,19 @@ __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
       b0 = item.j_out * r_out + (int64_t)item.chunk * P.blocks_per_chunk;
       b1 = min(b0 + P.blocks_per_chunk, (item.j_out + 1) * r_out);
     }
-    const T* __restrict__ srcA = (P.src_arena == A_BASE ? base : P.src_arena == A_AUX ? aux : clique) + P.src_off + q_src;
+    const T* __restrict__ srcA = (P.src_arena == A_BASE ? base : P.src_arena == A_AUX ? aux : clique) + P.src_off;
     const bool wr = P.dst_off >= 0;
-    T* __restrict__ dstA = clique + (wr ? P.dst_off : 0) + q_dst;
+    T* __restrict__ dstA = clique + (wr ? P.dst_off : 0);
     const int bs = 2 + P.nf, nf = P.nf;
-    const int us = P.unit_src, ud = P.unit_dst;
     const bool svec = LM == 0 ? (bool)P.src_vec : LM == 2;
-    double acc[VEC];
+    double acc[M][VEC];
 #pragma unroll
-    for (int l = 0; l < VEC; ++l) acc[l] = 0.0;
-    int64_t next_flush = chunked ? INT64_MAX : (b0 / r_out + 1) * r_out;
+    for (int m = 0; m < M; ++m)
+#pragma unroll
+      for (int l = 0; l < VEC; ++l) acc[m][l] = 0.0;
+    // blocks left in the current output group (never reached when chunked)
+    int64_t gidx = b0 / r_out;
+    int left = chunked ? INT32_MAX : (int)((gidx + 1) * r_out - b0);
     for (int64_t w0 = b0; w0 < b1; w0 += OWIN) {
       const int wn = (int)((b1 - w0) < OWIN ? (b1 - w0) : OWIN);
       __syncthreads();
@@ -235,74 +248,94 @@ __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
       for (int i = tid; i < wn * bs; i += NT) s_blk[i] = __ldg(g + i);
       __syncthreads();
       for (int wb = 0; wb < wn; wb += OKV) {
-        T v[OKV][VEC];
+        const int nb = wn - wb < OKV ? wn - wb : OKV;
+        T v[OKV][M][VEC];
 #pragma unroll
         for (int u = 0; u < OKV; ++u) {
-          if (wb + u < wn) {
-            const T* p = srcA + (int64_t)s_blk[(wb + u) * bs] * us;
-            if (VEC == 1 || svec) {
-              load_vec<T, VEC>(p, v[u]);
-            } else {
-              const T x = *p;
+          if (u < nb) {
+            const T* p = srcA + s_blk[(wb + u) * bs];
 #pragma unroll
-              for (int l = 0; l < VEC; ++l) v[u][l] = x;
+            for (int m = 0; m < M; ++m) {
+              if (VEC == 1 || svec) {
+                load_vec<T, VEC>(p + (LM == 0 ? q_src[m] : q_src[0] + m * CH), v[u][m]);
+              } else {
+                const T x = p[LM == 0 ? q_src[m] : q_src[0]];
+#pragma unroll
+                for (int l = 0; l < VEC; ++l) v[u][m][l] = x;
+              }
             }
           }
         }
 #pragma unroll
         for (int f = 0; f < MAXF; ++f) {
           if (f < nf) {
-            const T* fb = aux + P.fac_off[f] + qf[f];
-            const int uf = P.unit_fac[f];
+            const T* fb = aux + P.fac_off[f];
             const bool fv = LM == 0 ? (bool)((P.fac_vec >> f) & 1u) : true;
 #pragma unroll
             for (int u = 0; u < OKV; ++u) {
-              if (wb + u < wn) {
-                const T* p = fb + (int64_t)s_blk[(wb + u) * bs + 2 + f] * uf;
-                T gv[VEC];
-                if (VEC == 1 || fv) {
-                  load_vec_ro<T, VEC>(p, gv);
-                } else {
-                  const T x = __ldg(p);
+              if (u < nb) {
+                const T* p = fb + s_blk[(wb + u) * bs + 2 + f];
 #pragma unroll
-                  for (int l = 0; l < VEC; ++l) gv[l] = x;
+                for (int m = 0; m < M; ++m) {
+                  T gv[VEC];
+                  if (VEC == 1 || fv) {
+                    load_vec_ro<T, VEC>(p + (LM == 0 ? qf[f][m] : qf[f][0] + m * CH), gv);
+                  } else {
+                    const T x = __ldg(p + qf[f][m]);
+#pragma unroll
+                    for (int l = 0; l < VEC; ++l) gv[l] = x;
+                  }
+#pragma unroll
+                  for (int l = 0; l < VEC; ++l) v[u][m][l] *= gv[l];
                 }
-#pragma unroll
-                for (int l = 0; l < VEC; ++l) v[u][l] *= gv[l];
               }
             }
           }
         }
         // ≤ OKV-term partial sums in the storage type, folded into the fp64
         // accumulator once per iteration or output group
-        T part[VEC];
+        T part[M][VEC];
 #pragma unroll
-        for (int l = 0; l < VEC; ++l) part[l] = (T)0;
+        for (int m = 0; m < M; ++m)
+#pragma unroll
+          for (int l = 0; l < VEC; ++l) part[m][l] = (T)0;
 #pragma unroll
         for (int u = 0; u < OKV; ++u) {
-          if (wb + u >= wn) continue;
-          if (wr) store_vec<T, VEC>(dstA + (int64_t)s_blk[(wb + u) * bs + 1] * ud, v[u]);
+          if (u >= nb) continue;
+          if (wr) {
+            T* dp = dstA + s_blk[(wb + u) * bs + 1];
 #pragma unroll
-          for (int l = 0; l < VEC; ++l) part[l] += v[u][l];
-          const int64_t bi = w0 + wb + u;
-          if (bi + 1 == next_flush) {
-            const int64_t j = (bi / r_out) * (int64_t)P.n_in + lane0;
+            for (int m = 0; m < M; ++m) store_vec<T, VEC>(dp + (LM == 0 ? q_dst[m] : q_dst[0] + m * CH), v[u][m]);
+          }
 #pragma unroll
-            for (int l = 0; l < VEC; ++l) {
-              finalize_entry<T>(P, j + l, acc[l] + (double)part[l], aux, a.qout, a.err);
-              acc[l] = 0.0;
-              part[l] = (T)0;
-            }
-            next_flush += r_out;
+          for (int m = 0; m < M; ++m)
+#pragma unroll
+            for (int l = 0; l < VEC; ++l) part[m][l] += v[u][m][l];
+          if (--left == 0) {
+            const int64_t j = gidx * (int64_t)P.n_in + lane0;
+#pragma unroll
+            for (int m = 0; m < M; ++m)
+#pragma unroll
+              for (int l = 0; l < VEC; ++l) {
+                finalize_entry<T>(P, j + m * CH + l, acc[m][l] + (double)part[m][l], aux, a.qout, a.err);
+                acc[m][l] = 0.0;
+                part[m][l] = (T)0;
+              }
+            ++gidx;
+            left = (int)r_out;
           }
         }
 #pragma unroll
-        for (int l = 0; l < VEC; ++l) acc[l] += (double)part[l];
+        for (int m = 0; m < M; ++m)
+#pragma unroll
+          for (int l = 0; l < VEC; ++l) acc[m][l] += (double)part[m][l];
       }
     }
     if (chunked) {
 #pragma unroll
-      for (int l = 0; l < VEC; ++l) red[lane0 + l] = acc[l];
+      for (int m = 0; m < M; ++m)
+#pragma unroll
+        for (int l = 0; l < VEC; ++l) red[lane0 + m * CH + l] = acc[m][l];
       __syncthreads();
       chunk_finalize<T>(P, item, a, red, part2, &s_last, aux);
       __syncthreads();
@@ -556,35 +589,42 @@ static cudaError_t launch_t(const WaveArgs& a, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <typename T, int VEC, int LM>
+template <typename T, int VEC, int LM, int M>
 static cudaError_t launch_own_t(const WaveArgs& a, int grid, cudaStream_t s) {
-  wave_own_kernel<T, VEC, LM><<<grid, NT, 0, s>>>(a);
+  wave_own_kernel<T, VEC, LM, M><<<grid, NT, 0, s>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_wave_own(int dtype, int vec, int lm, const WaveArgs& a, int grid, cudaStream_t s) {
+template <typename T, int VEC, int LM>
+static cudaError_t launch_own_m(int m, const WaveArgs& a, int grid, cudaStream_t s) {
+  if (m == 4) return launch_own_t<T, VEC, LM, 4>(a, grid, s);
+  if (m == 2) return launch_own_t<T, VEC, LM, 2>(a, grid, s);
+  return launch_own_t<T, VEC, LM, 1>(a, grid, s);
+}
+
+cudaError_t launch_wave_own(int dtype, int vec, int lm, int m, const WaveArgs& a, int grid, cudaStream_t s) {
   if (grid <= 0 || a.n_items <= 0) return cudaSuccess;
   if (dtype == 0) {
     if (vec == 4) {
-      if (lm == 1) return launch_own_t<float, 4, 1>(a, grid, s);
-      if (lm == 2) return launch_own_t<float, 4, 2>(a, grid, s);
-      return launch_own_t<float, 4, 0>(a, grid, s);
+      if (lm == 1) return launch_own_m<float, 4, 1>(m, a, grid, s);
+      if (lm == 2) return launch_own_m<float, 4, 2>(m, a, grid, s);
+      return launch_own_t<float, 4, 0, 1>(a, grid, s);
     }
-    if (vec == 2) return launch_own_t<float, 2, 0>(a, grid, s);
-    return launch_own_t<float, 1, 0>(a, grid, s);
+    if (vec == 2) return launch_own_t<float, 2, 0, 1>(a, grid, s);
+    return launch_own_t<float, 1, 0, 1>(a, grid, s);
   }
   if (vec == 2) {
-    if (lm == 1) return launch_own_t<double, 2, 1>(a, grid, s);
-    if (lm == 2) return launch_own_t<double, 2, 2>(a, grid, s);
-    return launch_own_t<double, 2, 0>(a, grid, s);
+    if (lm == 1) return launch_own_m<double, 2, 1>(m, a, grid, s);
+    if (lm == 2) return launch_own_m<double, 2, 2>(m, a, grid, s);
+    return launch_own_t<double, 2, 0, 1>(a, grid, s);
   }
-  return launch_own_t<double, 1, 0>(a, grid, s);
+  return launch_own_t<double, 1, 0, 1>(a, grid, s);
 }
 
 template <typename T, int VEC>
 static int occ_own_t() {
   int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, wave_own_kernel<T, VEC, 0>, NT, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, wave_own_kernel<T, VEC, 0, 1>, NT, 0);
   return n > 0 ? n : 1;
 }
 
