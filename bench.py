@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c5")
     ap.add_argument("--cases", type=int, default=8192, help="evidence cases per GPU per step")
-    ap.add_argument("--batch", type=int, default=1024, help="cases per device micro-batch")
+    ap.add_argument("--batch", type=int, default=2048, help="cases per device micro-batch")
     ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
     ap.add_argument("--mode", default="auto", choices=["auto", "shared", "materialized"])
     ap.add_argument("--cpu-sample", type=int, default=24, help="cases in the CPU baseline sample")
