@@ -570,7 +570,7 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
     double fin = (has_out && c.n_chunks > 1) ? (double)c.n_out * std::min<int64_t>(32, c.n_chunks) * c.n_in * 64.0 : 0.0;
     double pen = 0.0;
     if (T * esz < 128) pen = bytes * (128.0 / (T * esz) - 1.0) * 0.5;
-    c.cost = bytes + part + items * epi + fin + pen + (double)c.n_out * c.r_out * 16.0;
+    c.cost = bytes + part + items * epi + fin + pen + (double)c.n_out * c.r_out * (c.own ? 2048.0 : 16.0);
     if (!found || c.cost < best.cost * 0.999) {
       best = c;
       found = true;
@@ -604,6 +604,15 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
   d.blk_stride = 2 + nf;
   d.own = best.own ? 1 : 0;
   d.own_m = best.own_m;
+  d.flush_fac = 0;
+  if (best.own) {
+    for (int f = 0; f < nf; ++f) {
+      bool constant = true;
+      for (int i = 0; i < best.k; ++i)
+        if (!(has_out && dims[i].out) && dims[i].fac[f] != 0) constant = false;
+      if (constant) d.flush_fac |= 1u << f;
+    }
+  }
   d.gpi = best.gpi;
   d.ndi = (int)best.inner.size();
   for (int i = 0; i < d.ndi; ++i) {
@@ -1090,6 +1099,18 @@ static int build_propagate(jt_state* st, const std::vector<int>& roots, const st
       ps.out = sep_tensor(st, ch[i].second, sep_cur(st, ch[i].second));
       if (fresh) ps.out2_off = sep_alt(st, ch[i].second);
       ps.ratio_off = st->ratD_off[ch[i].second];
+      if (fresh && !ps.write && !eager[c]) {
+        // message to child k: product of the OTHER messages, marginalised
+        // (new/old == Σ without k's own collect message)
+        const int64_t own_off = ratC(ch[i].second);
+        std::vector<Tensor> f2;
+        for (auto& t : fac)
+          if (!(t.off == own_off && t.vars == p->svars[ch[i].second])) f2.push_back(t);
+        if (f2.size() + 1 == fac.size()) {
+          ps.factors = f2;
+          ps.out_kind = OUT_SEP_DFRESH;
+        }
+      }
       dw[d].push_back(ps);
     }
     if (!shared && ch.size() != 1 && !fac.empty()) {
@@ -1845,10 +1866,10 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
         }
       snprintf(line, sizeof line,
                "  pass clique %d src %d nf %d wr %d out %d T %d n_in %d n_out %lld r_out %lld BPI %d chunks %d "
-               "bpc %lld items %lld ndi %d own %d/%d gpi %d part %lld\n",
+               "bpc %lld items %lld ndi %d own %d/%d gpi %d ffac %x part %lld\n",
                hp.pass_clique[pi], d.src_arena, d.nf, d.dst_off >= 0, d.out_kind, d.T, d.n_in, (long long)n_out,
                (long long)d.n_blocks_per_jout, d.BPI, d.n_chunks, (long long)d.blocks_per_chunk,
-               (long long)n_items, d.ndi, d.own, d.own_m, d.gpi,
+               (long long)n_items, d.ndi, d.own, d.own_m, d.gpi, d.flush_fac,
                (long long)(d.n_chunks > 1 && d.out_kind ? n_out * d.n_chunks * d.n_in : 0));
       out += line;
     }

@@ -12,7 +12,10 @@ constexpr int MAXF = 8;     // factors (ratio / evidence tensors) multiplied in 
 constexpr int MAXDI = 8;    // merged inner dimensions per pass
 
 enum ArenaId : int { A_CLIQUE = 0, A_BASE = 1, A_AUX = 2 };
-enum OutKind : int { OUT_NONE = 0, OUT_SEP = 1, OUT_RAW = 2, OUT_SEP_FRESH = 3 };
+enum OutKind : int { OUT_NONE = 0, OUT_SEP = 1, OUT_RAW = 2, OUT_SEP_FRESH = 3, OUT_SEP_DFRESH = 4 };
+// OUT_SEP_DFRESH: distribute output of a fresh propagation; the pass sums
+// WITHOUT the target separator's own collect message c (= old value), so
+// new = c*S and ratio = new/old = S (0 where c == 0): the Hugin division cancels.
 // OUT_SEP_FRESH: collect output of a fresh propagation (old separator known to be
 // ones): ratio == star, so only the separator itself is written and consumers
 // read it as the ratio.
@@ -38,6 +41,8 @@ struct DevPass {
   int src_vec;              // 1: innermost stride 1 (vector load), 0: broadcast
   int nf;
   uint32_t fac_vec;         // bit f set: factor f has the innermost dim (vector), else broadcast
+  uint32_t flush_fac;       // bit f set: factor f is constant over an output group (own passes):
+                            //   multiplied once into the group sum instead of per element
   int out_kind;
   int n_in;                 // output bins per block
   int n_chunks;

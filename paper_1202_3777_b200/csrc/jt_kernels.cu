@@ -106,6 +106,10 @@ __device__ __forceinline__ void finalize_entry(const DevPass& P, int64_t j, doub
                                                double* qout, int* err) {
   if (P.out_kind == OUT_SEP_FRESH) {
     aux[P.out_off + j] = (T)star;
+  } else if (P.out_kind == OUT_SEP_DFRESH) {
+    const double c = (double)aux[P.out_off + j];
+    aux[P.ratio_off + j] = (T)(c != 0.0 ? star : 0.0);
+    aux[(P.out2_off >= 0 ? P.out2_off : P.out_off) + j] = (T)(c * star);
   } else if (P.out_kind == OUT_SEP) {
     const double old = (double)aux[P.out_off + j];
     if (old == 0.0 && star != 0.0) atomicOr(err, EB_INCONSISTENT);
@@ -233,6 +237,20 @@ __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
     T* __restrict__ dstA = clique + (wr ? P.dst_off : 0);
     const int bs = 2 + P.nf, nf = P.nf;
     const bool svec = LM == 0 ? (bool)P.src_vec : LM == 2;
+    const uint32_t ffm = P.flush_fac;
+    // product of the group-constant factors for lane l of vector m, read at the
+    // block-table entry `e` of any block of the group
+    auto flush_mul = [&](const int32_t* e, int m, int l) -> double {
+      double r = 1.0;
+#pragma unroll
+      for (int f = 0; f < MAXF; ++f)
+        if (f < nf && ((ffm >> f) & 1u)) {
+          const bool fv = LM == 0 ? (bool)((P.fac_vec >> f) & 1u) : true;
+          const int o = LM == 0 ? qf[f][m] : qf[f][0] + m * CH;
+          r *= (double)aux[P.fac_off[f] + e[2 + f] + o + (fv ? l : 0)];
+        }
+      return r;
+    };
     double acc[M][VEC];
 #pragma unroll
     for (int m = 0; m < M; ++m)
@@ -268,7 +286,7 @@ __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
         }
 #pragma unroll
         for (int f = 0; f < MAXF; ++f) {
-          if (f < nf) {
+          if (f < nf && !((ffm >> f) & 1u)) {
             const T* fb = aux + P.fac_off[f];
             const bool fv = LM == 0 ? (bool)((P.fac_vec >> f) & 1u) : true;
 #pragma unroll
@@ -313,11 +331,14 @@ __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
             for (int l = 0; l < VEC; ++l) part[m][l] += v[u][m][l];
           if (--left == 0) {
             const int64_t j = gidx * (int64_t)P.n_in + lane0;
+            const int32_t* e = &s_blk[(wb + u) * bs];
 #pragma unroll
             for (int m = 0; m < M; ++m)
 #pragma unroll
               for (int l = 0; l < VEC; ++l) {
-                finalize_entry<T>(P, j + m * CH + l, acc[m][l] + (double)part[m][l], aux, a.qout, a.err);
+                double sum = acc[m][l] + (double)part[m][l];
+                if (ffm) sum *= flush_mul(e, m, l);
+                finalize_entry<T>(P, j + m * CH + l, sum, aux, a.qout, a.err);
                 acc[m][l] = 0.0;
                 part[m][l] = (T)0;
               }
@@ -332,10 +353,12 @@ __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
       }
     }
     if (chunked) {
+      // group-constant factors: apply to this chunk's partial (Σ F·S_c = F·Σ S_c)
+      const int32_t* e = &s_blk[0];
 #pragma unroll
       for (int m = 0; m < M; ++m)
 #pragma unroll
-        for (int l = 0; l < VEC; ++l) red[lane0 + m * CH + l] = acc[m][l];
+        for (int l = 0; l < VEC; ++l) red[lane0 + m * CH + l] = ffm ? acc[m][l] * flush_mul(e, m, l) : acc[m][l];
       __syncthreads();
       chunk_finalize<T>(P, item, a, red, part2, &s_last, aux);
       __syncthreads();
