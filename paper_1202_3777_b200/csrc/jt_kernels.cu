@@ -169,6 +169,55 @@ __device__ void chunk_finalize(const DevPass& P, const Item& item, const WaveArg
 // iteration and finalizes its own lanes at every output-group boundary —
 // no barriers, no shared memory in the steady state.  This is the batched
 // layout's natural path (case = innermost index).
+// VEC consecutive output entries [j, j+VEC) at once (j multiple of VEC): the
+// thread-owned epilogue, with vector loads/stores of the separator arrays.
+template <typename T, int VEC>
+__device__ __forceinline__ void finalize_vec(const DevPass& P, int64_t j, const double (&star)[VEC], T* aux,
+                                             double* qout) {
+  if (P.out_kind == OUT_RAW) {
+#pragma unroll
+    for (int l = 0; l < VEC; ++l) qout[P.out_off + j + l] = star[l];
+    return;
+  }
+  T nw[VEC];
+  if (P.out_kind == OUT_SEP_FRESH) {
+#pragma unroll
+    for (int l = 0; l < VEC; ++l) nw[l] = (T)star[l];
+    store_vec<T, VEC>(aux + P.out_off + j, nw);
+    return;
+  }
+  T old[VEC], rt[VEC];
+  load_vec<T, VEC>(aux + P.out_off + j, old);
+  if (P.out_kind == OUT_SEP_DFRESH) {
+#pragma unroll
+    for (int l = 0; l < VEC; ++l) {
+      const double c = (double)old[l];
+      rt[l] = (T)(c != 0.0 ? star[l] : 0.0);
+      nw[l] = (T)(c * star[l]);
+    }
+  } else {
+#pragma unroll
+    for (int l = 0; l < VEC; ++l) {
+      const double o = (double)old[l];
+      rt[l] = (T)(o != 0.0 ? star[l] / o : 0.0);
+      nw[l] = (T)star[l];
+    }
+  }
+  store_vec<T, VEC>(aux + P.ratio_off + j, rt);
+  store_vec<T, VEC>(aux + (P.out2_off >= 0 ? P.out2_off : P.out_off) + j, nw);
+}
+
+template <typename T, int VEC>
+__device__ __forceinline__ bool any_inconsistent(const DevPass& P, int64_t j, const double (&star)[VEC], const T* aux) {
+  if (P.out_kind != OUT_SEP) return false;
+  T old[VEC];
+  load_vec<T, VEC>(aux + P.out_off + j, old);
+  bool bad = false;
+#pragma unroll
+  for (int l = 0; l < VEC; ++l) bad |= ((double)old[l] == 0.0 && star[l] != 0.0);
+  return bad;
+}
+
 constexpr int OWIN = 64;    // block-table window staged in shared memory
 
 // M vectors (lane chunks NT*VEC apart) per thread per block; OKV*M = 8 vectors
@@ -240,16 +289,23 @@ __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
     const uint32_t ffm = P.flush_fac;
     // product of the group-constant factors for lane l of vector m, read at the
     // block-table entry `e` of any block of the group
-    auto flush_mul = [&](const int32_t* e, int m, int l) -> double {
-      double r = 1.0;
+    auto flush_mul = [&](const int32_t* e, int m, double (&r)[VEC]) {
 #pragma unroll
       for (int f = 0; f < MAXF; ++f)
         if (f < nf && ((ffm >> f) & 1u)) {
           const bool fv = LM == 0 ? (bool)((P.fac_vec >> f) & 1u) : true;
           const int o = LM == 0 ? qf[f][m] : qf[f][0] + m * CH;
-          r *= (double)aux[P.fac_off[f] + e[2 + f] + o + (fv ? l : 0)];
+          const T* p = aux + P.fac_off[f] + e[2 + f] + o;
+          T g[VEC];
+          if (VEC == 1 || fv) {
+            load_vec_ro<T, VEC>(p, g);
+          } else {
+#pragma unroll
+            for (int l = 0; l < VEC; ++l) g[l] = __ldg(p);
+          }
+#pragma unroll
+          for (int l = 0; l < VEC; ++l) r[l] *= (double)g[l];
         }
-      return r;
     };
     double acc[M][VEC];
 #pragma unroll
@@ -333,15 +389,19 @@ __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
             const int64_t j = gidx * (int64_t)P.n_in + lane0;
             const int32_t* e = &s_blk[(wb + u) * bs];
 #pragma unroll
-            for (int m = 0; m < M; ++m)
+            for (int m = 0; m < M; ++m) {
+              double sum[VEC];
+#pragma unroll
+              for (int l = 0; l < VEC; ++l) sum[l] = acc[m][l] + (double)part[m][l];
+              if (ffm) flush_mul(e, m, sum);
+              if (any_inconsistent<T, VEC>(P, j + m * CH, sum, aux)) atomicOr(a.err, EB_INCONSISTENT);
+              finalize_vec<T, VEC>(P, j + m * CH, sum, aux, a.qout);
 #pragma unroll
               for (int l = 0; l < VEC; ++l) {
-                double sum = acc[m][l] + (double)part[m][l];
-                if (ffm) sum *= flush_mul(e, m, l);
-                finalize_entry<T>(P, j + m * CH + l, sum, aux, a.qout, a.err);
                 acc[m][l] = 0.0;
                 part[m][l] = (T)0;
               }
+            }
             ++gidx;
             left = (int)r_out;
           }
@@ -356,9 +416,14 @@ __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
       // group-constant factors: apply to this chunk's partial (Σ F·S_c = F·Σ S_c)
       const int32_t* e = &s_blk[0];
 #pragma unroll
-      for (int m = 0; m < M; ++m)
+      for (int m = 0; m < M; ++m) {
+        double sum[VEC];
 #pragma unroll
-        for (int l = 0; l < VEC; ++l) red[lane0 + m * CH + l] = ffm ? acc[m][l] * flush_mul(e, m, l) : acc[m][l];
+        for (int l = 0; l < VEC; ++l) sum[l] = acc[m][l];
+        if (ffm) flush_mul(e, m, sum);
+#pragma unroll
+        for (int l = 0; l < VEC; ++l) red[lane0 + m * CH + l] = sum[l];
+      }
       __syncthreads();
       chunk_finalize<T>(P, item, a, red, part2, &s_last, aux);
       __syncthreads();
