@@ -58,36 +58,27 @@ __device__ __forceinline__ double warp_sum(double s) {
   return s;
 }
 
-// out[b] = Σ_{r<R} get(b, r), r ascending per thread-group, groups combined in
-// order: deterministic for a given (n_bins, R).  `out` may alias get's source.
+// out[b] = Σ_{r<R} get(b, r): r ascending within a thread group, groups combined
+// in order — deterministic for a given (n_bins, R).  `out` must not alias the
+// values read by `get` (callers reduce from global partials or from `red`
+// into a separate buffer).
 template <class F>
 __device__ __forceinline__ void reduce_bins(F get, int n_bins, int R, double* out, double* part2) {
   const int tid = threadIdx.x;
   if (n_bins >= NT) {
-    constexpr int MAXU = (NT * KV * 4) / NT;
-    double res[MAXU];
-#pragma unroll
-    for (int u = 0; u < MAXU; ++u) {
-      const int b = tid + u * NT;
+    for (int b = tid; b < n_bins; b += NT) {
       double s = 0.0;
-      if (b < n_bins)
-        for (int r = 0; r < R; ++r) s += get(b, r);
-      res[u] = s;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < MAXU; ++u) {
-      const int b = tid + u * NT;
-      if (b < n_bins) out[b] = res[u];
+      for (int r = 0; r < R; ++r) s += get(b, r);
+      out[b] = s;
     }
     __syncthreads();
   } else {
     int G = NT / n_bins;
     if (G > R) G = R;
     if (G < 1) G = 1;
-    double s = 0.0;
     if (tid < n_bins * G) {
       const int b = tid / G, g = tid - (tid / G) * G;
+      double s = 0.0;
       for (int r = g; r < R; r += G) s += get(b, r);
       part2[tid] = s;
     }
@@ -129,7 +120,7 @@ constexpr int CHUNK_GROUP = 32;
 // CTA to arrive at each level does that level's sum, so no CTA reduces more
 // than CHUNK_GROUP × n_in values.
 template <typename T>
-__device__ void chunk_finalize(const DevPass& P, const Item& item, const WaveArgs& a, double* red,
+__device__ __noinline__ void chunk_finalize(const DevPass& P, const Item& item, const WaveArgs& a, double* red,
                                double* part2, int* s_last, T* aux) {
   const int tid = threadIdx.x;
   const int n_in = P.n_in, nch = P.n_chunks;
@@ -220,26 +211,64 @@ __device__ __forceinline__ bool any_inconsistent(const DevPass& P, int64_t j, co
 
 constexpr int OWIN = 64;    // block-table window staged in shared memory
 
+// Group flush of the thread-owned kernel, compiled once (not inlined into the
+// unrolled block loop): multiply the group-constant factors in, check, and
+// write the VEC lanes of each of the M vectors.
+template <typename T, int VEC, int LM, int M>
+__device__ __noinline__ void own_flush(const DevPass& P, const T* __restrict__ aux_c, T* aux, double* qout, int* err,
+                                       const int32_t* e, const int* qfo, int64_t j, double s0, double s1, double s2,
+                                       double s3, double s4, double s5, double s6, double s7, double s8, double s9,
+                                       double s10, double s11, double s12, double s13, double s14, double s15) {
+  constexpr int CH = NT * VEC;
+  const double sv[16] = {s0, s1, s2, s3, s4, s5, s6, s7, s8, s9, s10, s11, s12, s13, s14, s15};
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    double sum[VEC];
+#pragma unroll
+    for (int l = 0; l < VEC; ++l) sum[l] = sv[m * VEC + l];
+    for (int f = 0; f < P.nf; ++f) {
+      if (!((P.flush_fac >> f) & 1u)) continue;
+      const bool fv = LM == 0 ? (bool)((P.fac_vec >> f) & 1u) : true;
+      const T* p = aux_c + P.fac_off[f] + e[2 + f] + qfo[f] + m * CH;
+      T g[VEC];
+      if (VEC == 1 || fv) {
+        load_vec_ro<T, VEC>(p, g);
+      } else {
+#pragma unroll
+        for (int l = 0; l < VEC; ++l) g[l] = __ldg(p);
+      }
+#pragma unroll
+      for (int l = 0; l < VEC; ++l) sum[l] *= (double)g[l];
+    }
+    if (any_inconsistent<T, VEC>(P, j + m * CH, sum, aux)) atomicOr(err, EB_INCONSISTENT);
+    finalize_vec<T, VEC>(P, j + m * CH, sum, aux, qout);
+  }
+}
+
 // M vectors (lane chunks NT*VEC apart) per thread per block; OKV*M = 8 vectors
 // in flight per tensor per iteration.  Block-table entries are int32 element
-// offsets (P.unit_* == 1) staged per window in shared memory.
+// offsets staged per window in shared memory; per-thread inner factor offsets
+// live in shared memory so the factor loop stays a runtime loop (compact code).
 template <typename T, int VEC, int LM, int M>
 __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
+  static_assert(M * VEC <= 16, "flush passes at most 16 lanes");
   constexpr int OKV = 8 / M;
   __shared__ DevPass P;
   __shared__ double part2[NT];
   __shared__ int s_last;
   __shared__ double red[NT * 4 * 4];
   __shared__ int32_t s_blk[OWIN * (2 + MAXF)];
+  __shared__ int s_qf[MAXF][NT];
   T* __restrict__ clique = reinterpret_cast<T*>(a.clique);
   const T* __restrict__ base = reinterpret_cast<const T*>(a.base);
   T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
+  const T* __restrict__ aux_c = aux;
   const int tid = threadIdx.x;
   const int lane0 = tid * VEC;
   constexpr int CH = NT * VEC;  // lanes per chunk
+  static_assert(LM != 0 || M == 1, "generic load shapes use one vector per thread");
   int cur = -1;
-  int q_src[M], q_dst[M];
-  int qf[MAXF][M];
+  int q_src = 0, q_dst = 0;
   for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
     const Item item = a.items[it];
     if (item.pass != cur) {
@@ -249,27 +278,18 @@ __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
       for (int w = tid; w < (int)(sizeof(DevPass) / 4); w += NT) dw[w] = sw[w];
       __syncthreads();
       cur = item.pass;
-#pragma unroll
-      for (int m = 0; m < (LM == 0 ? M : 1); ++m) {
-        int rem = lane0 + m * CH, s = 0, dd = 0;
-        int fo[MAXF];
-#pragma unroll
-        for (int f = 0; f < MAXF; ++f) fo[f] = 0;
-        for (int d = P.ndi - 1; d >= 0; --d) {
-          const int c = P.icard[d];
-          const int dig = rem % c;
-          rem /= c;
-          s += dig * P.isrc[d];
-          dd += dig * P.idst[d];
-#pragma unroll
-          for (int f = 0; f < MAXF; ++f)
-            if (f < P.nf) fo[f] += dig * P.ifac[f][d];
-        }
-        q_src[m] = s;
-        q_dst[m] = dd;
-#pragma unroll
-        for (int f = 0; f < MAXF; ++f) qf[f][m] = fo[f];
+      int rem = lane0, sacc = 0, dd = 0;
+      for (int f = 0; f < MAXF; ++f) s_qf[f][tid] = 0;
+      for (int d = P.ndi - 1; d >= 0; --d) {
+        const int c = P.icard[d];
+        const int dig = rem % c;
+        rem /= c;
+        sacc += dig * P.isrc[d];
+        dd += dig * P.idst[d];
+        for (int f = 0; f < P.nf; ++f) s_qf[f][tid] += dig * P.ifac[f][d];
       }
+      q_src = sacc;
+      q_dst = dd;
     }
     const int64_t r_out = P.n_blocks_per_jout;
     const bool chunked = P.n_chunks > 1;
@@ -281,38 +301,21 @@ __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
       b0 = item.j_out * r_out + (int64_t)item.chunk * P.blocks_per_chunk;
       b1 = min(b0 + P.blocks_per_chunk, (item.j_out + 1) * r_out);
     }
-    const T* __restrict__ srcA = (P.src_arena == A_BASE ? base : P.src_arena == A_AUX ? aux : clique) + P.src_off;
+    const T* __restrict__ srcA =
+        (P.src_arena == A_BASE ? base : P.src_arena == A_AUX ? aux_c : clique) + P.src_off + q_src;
     const bool wr = P.dst_off >= 0;
-    T* __restrict__ dstA = clique + (wr ? P.dst_off : 0);
+    T* __restrict__ dstA = clique + (wr ? P.dst_off : 0) + q_dst;
     const int bs = 2 + P.nf, nf = P.nf;
     const bool svec = LM == 0 ? (bool)P.src_vec : LM == 2;
     const uint32_t ffm = P.flush_fac;
-    // product of the group-constant factors for lane l of vector m, read at the
-    // block-table entry `e` of any block of the group
-    auto flush_mul = [&](const int32_t* e, int m, double (&r)[VEC]) {
+    int qfo[MAXF];
 #pragma unroll
-      for (int f = 0; f < MAXF; ++f)
-        if (f < nf && ((ffm >> f) & 1u)) {
-          const bool fv = LM == 0 ? (bool)((P.fac_vec >> f) & 1u) : true;
-          const int o = LM == 0 ? qf[f][m] : qf[f][0] + m * CH;
-          const T* p = aux + P.fac_off[f] + e[2 + f] + o;
-          T g[VEC];
-          if (VEC == 1 || fv) {
-            load_vec_ro<T, VEC>(p, g);
-          } else {
-#pragma unroll
-            for (int l = 0; l < VEC; ++l) g[l] = __ldg(p);
-          }
-#pragma unroll
-          for (int l = 0; l < VEC; ++l) r[l] *= (double)g[l];
-        }
-    };
+    for (int f = 0; f < MAXF; ++f) qfo[f] = s_qf[f][tid];
     double acc[M][VEC];
 #pragma unroll
     for (int m = 0; m < M; ++m)
 #pragma unroll
       for (int l = 0; l < VEC; ++l) acc[m][l] = 0.0;
-    // blocks left in the current output group (never reached when chunked)
     int64_t gidx = b0 / r_out;
     int left = chunked ? INT32_MAX : (int)((gidx + 1) * r_out - b0);
     for (int64_t w0 = b0; w0 < b1; w0 += OWIN) {
@@ -323,45 +326,44 @@ __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
       __syncthreads();
       for (int wb = 0; wb < wn; wb += OKV) {
         const int nb = wn - wb < OKV ? wn - wb : OKV;
+        const int32_t* eb = &s_blk[wb * bs];
         T v[OKV][M][VEC];
 #pragma unroll
         for (int u = 0; u < OKV; ++u) {
           if (u < nb) {
-            const T* p = srcA + s_blk[(wb + u) * bs];
+            const T* p = srcA + eb[u * bs];
 #pragma unroll
             for (int m = 0; m < M; ++m) {
               if (VEC == 1 || svec) {
-                load_vec<T, VEC>(p + (LM == 0 ? q_src[m] : q_src[0] + m * CH), v[u][m]);
+                load_vec<T, VEC>(p + m * CH, v[u][m]);
               } else {
-                const T x = p[LM == 0 ? q_src[m] : q_src[0]];
+                const T x = *p;
 #pragma unroll
                 for (int l = 0; l < VEC; ++l) v[u][m][l] = x;
               }
             }
           }
         }
+        for (int f = 0; f < nf; ++f) {
+          if ((ffm >> f) & 1u) continue;
+          const T* fb = aux_c + P.fac_off[f] + s_qf[f][tid];
+          const bool fv = LM == 0 ? (bool)((P.fac_vec >> f) & 1u) : true;
 #pragma unroll
-        for (int f = 0; f < MAXF; ++f) {
-          if (f < nf && !((ffm >> f) & 1u)) {
-            const T* fb = aux + P.fac_off[f];
-            const bool fv = LM == 0 ? (bool)((P.fac_vec >> f) & 1u) : true;
+          for (int u = 0; u < OKV; ++u) {
+            if (u < nb) {
+              const T* p = fb + eb[u * bs + 2 + f];
 #pragma unroll
-            for (int u = 0; u < OKV; ++u) {
-              if (u < nb) {
-                const T* p = fb + s_blk[(wb + u) * bs + 2 + f];
+              for (int m = 0; m < M; ++m) {
+                T gv[VEC];
+                if (VEC == 1 || fv) {
+                  load_vec_ro<T, VEC>(p + m * CH, gv);
+                } else {
+                  const T x = __ldg(p);
 #pragma unroll
-                for (int m = 0; m < M; ++m) {
-                  T gv[VEC];
-                  if (VEC == 1 || fv) {
-                    load_vec_ro<T, VEC>(p + (LM == 0 ? qf[f][m] : qf[f][0] + m * CH), gv);
-                  } else {
-                    const T x = __ldg(p + qf[f][m]);
-#pragma unroll
-                    for (int l = 0; l < VEC; ++l) gv[l] = x;
-                  }
-#pragma unroll
-                  for (int l = 0; l < VEC; ++l) v[u][m][l] *= gv[l];
+                  for (int l = 0; l < VEC; ++l) gv[l] = x;
                 }
+#pragma unroll
+                for (int l = 0; l < VEC; ++l) v[u][m][l] *= gv[l];
               }
             }
           }
@@ -377,31 +379,29 @@ __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
         for (int u = 0; u < OKV; ++u) {
           if (u >= nb) continue;
           if (wr) {
-            T* dp = dstA + s_blk[(wb + u) * bs + 1];
+            T* dp = dstA + eb[u * bs + 1];
 #pragma unroll
-            for (int m = 0; m < M; ++m) store_vec<T, VEC>(dp + (LM == 0 ? q_dst[m] : q_dst[0] + m * CH), v[u][m]);
+            for (int m = 0; m < M; ++m) store_vec<T, VEC>(dp + m * CH, v[u][m]);
           }
 #pragma unroll
           for (int m = 0; m < M; ++m)
 #pragma unroll
             for (int l = 0; l < VEC; ++l) part[m][l] += v[u][m][l];
           if (--left == 0) {
-            const int64_t j = gidx * (int64_t)P.n_in + lane0;
-            const int32_t* e = &s_blk[(wb + u) * bs];
+            double sv[16];
 #pragma unroll
-            for (int m = 0; m < M; ++m) {
-              double sum[VEC];
+            for (int i = 0; i < 16; ++i) sv[i] = 0.0;
 #pragma unroll
-              for (int l = 0; l < VEC; ++l) sum[l] = acc[m][l] + (double)part[m][l];
-              if (ffm) flush_mul(e, m, sum);
-              if (any_inconsistent<T, VEC>(P, j + m * CH, sum, aux)) atomicOr(a.err, EB_INCONSISTENT);
-              finalize_vec<T, VEC>(P, j + m * CH, sum, aux, a.qout);
+            for (int m = 0; m < M; ++m)
 #pragma unroll
               for (int l = 0; l < VEC; ++l) {
+                sv[m * VEC + l] = acc[m][l] + (double)part[m][l];
                 acc[m][l] = 0.0;
                 part[m][l] = (T)0;
               }
-            }
+            own_flush<T, VEC, LM, M>(P, aux_c, aux, a.qout, a.err, eb + u * bs, qfo, gidx * (int64_t)P.n_in + lane0,
+                                     sv[0], sv[1], sv[2], sv[3], sv[4], sv[5], sv[6], sv[7], sv[8], sv[9], sv[10],
+                                     sv[11], sv[12], sv[13], sv[14], sv[15]);
             ++gidx;
             left = (int)r_out;
           }
@@ -420,7 +420,13 @@ __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
         double sum[VEC];
 #pragma unroll
         for (int l = 0; l < VEC; ++l) sum[l] = acc[m][l];
-        if (ffm) flush_mul(e, m, sum);
+        for (int f = 0; f < nf; ++f) {
+          if (!((ffm >> f) & 1u)) continue;
+          const bool fv = LM == 0 ? (bool)((P.fac_vec >> f) & 1u) : true;
+          const T* p = aux_c + P.fac_off[f] + e[2 + f] + qfo[f] + m * CH;
+#pragma unroll
+          for (int l = 0; l < VEC; ++l) sum[l] *= (double)__ldg(p + (fv ? l : 0));
+        }
 #pragma unroll
         for (int l = 0; l < VEC; ++l) red[lane0 + m * CH + l] = sum[l];
       }
@@ -439,7 +445,8 @@ __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
   __shared__ int s_last;
   extern __shared__ __align__(16) double dsm[];
   double* red = dsm;                                              // [TH] block partials
-  uint16_t (*s_qfac)[KV][NT] = reinterpret_cast<uint16_t (*)[KV][NT]>(dsm + TH);  // inner factor offsets
+  double* outb = dsm + TH;                                        // [TH] reduced bins
+  uint16_t (*s_qfac)[KV][NT] = reinterpret_cast<uint16_t (*)[KV][NT]>(dsm + 2 * TH);  // inner factor offsets
 
   T* __restrict__ clique = reinterpret_cast<T*>(a.clique);
   const T* __restrict__ base = reinterpret_cast<const T*>(a.base);
@@ -586,19 +593,14 @@ __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
         const int32_t* __restrict__ bbase = a.bins + P.bin_off;
         const int32_t* __restrict__ brest = bbase + n_in;
         const int T_ = P.T;
-        if (n_in == 1) {
-          reduce_bins([&](int g, int r) { return red[(g * ro + r / rest) * T_ + (r % rest)]; }, ng, ro * rest,
-                      red, part2);
-        } else {
-          reduce_bins(
-              [&](int gb, int r) {
-                const int g = gb / n_in, b = gb - (gb / n_in) * n_in;
-                const int slot = g * ro + r / rest;
-                return red[slot * T_ + bbase[b] + brest[r % rest]];
-              },
-              ng * n_in, ro * rest, red, part2);
-        }
-        for (int b = tid; b < ng * n_in; b += NT) finalize_entry<T>(P, g0 * n_in + b, red[b], aux, a.qout, a.err);
+        reduce_bins(
+            [&](int gb, int r) {
+              const int g = gb / n_in, b = gb - (gb / n_in) * n_in;
+              const int slot = g * ro + r / rest;
+              return red[slot * T_ + (n_in == 1 ? 0 : bbase[b]) + (n_in == 1 ? r % rest : brest[r % rest])];
+            },
+            ng * n_in, ro * rest, outb, part2);
+        for (int b = tid; b < ng * n_in; b += NT) finalize_entry<T>(P, g0 * n_in + b, outb[b], aux, a.qout, a.err);
         __syncthreads();
       }
     }
@@ -607,6 +609,7 @@ __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
 
     // ---- block partials -> n_in bins (fixed order) ----
     const int n_in = P.n_in;
+    double* vals = outb;  // reduced bins of this item
     if (n_in == 1) {
       double s = 0.0;
 #pragma unroll
@@ -619,7 +622,7 @@ __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
       if (tid == 0) {
         double t = 0.0;
         for (int w = 0; w < NT / 32; ++w) t += part2[w];
-        red[0] = t;
+        outb[0] = t;
       }
       __syncthreads();
     } else {
@@ -644,15 +647,21 @@ __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
               const int p = r - slot * rest;
               return red[slot * T_ + bbase[b] + brest[p]];
             },
-            n_in, R, red, part2);
+            n_in, R, outb, part2);
+      } else {
+        vals = red;  // identity bins: every position is its own output entry
       }
     }
 
     // ---- output: direct or via chunk partials + last-CTA finalize ----
     const int64_t j0 = item.j_out * (int64_t)n_in;
     if (P.n_chunks == 1) {
-      for (int b = tid; b < n_in; b += NT) finalize_entry<T>(P, j0 + b, red[b], aux, a.qout, a.err);
+      for (int b = tid; b < n_in; b += NT) finalize_entry<T>(P, j0 + b, vals[b], aux, a.qout, a.err);
     } else {
+      if (vals != red) {
+        for (int b = tid; b < n_in; b += NT) red[b] = vals[b];
+        __syncthreads();
+      }
       chunk_finalize<T>(P, item, a, red, part2, &s_last, aux);
     }
     __syncthreads();
@@ -661,7 +670,7 @@ __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
 
 template <int VEC>
 constexpr size_t wave_smem() {
-  return (size_t)NT * KV * VEC * sizeof(double) + (size_t)MAXF * KV * NT * sizeof(uint16_t);
+  return (size_t)2 * NT * KV * VEC * sizeof(double) + (size_t)MAXF * KV * NT * sizeof(uint16_t);
 }
 
 template <typename T, int VEC>
