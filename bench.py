@@ -117,10 +117,51 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- CPU legs ----
-def cpu_case_rate(tree, tables, cases, variables, workers):
-    """Oracle port of the reference's per-case loop (estimator.py:89-96):
-    copy → apply_evidence → belief_propagation → every query_marginal, with the
-    reference's ParallelEngine (propagate.py:97-161) over `workers` threads."""
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _reference_module():
+    """The unmodified reference package (`jtprop`), installed by
+    `pip install --no-deps --target baseline/_ref`; None if absent."""
+    if not os.path.isdir(os.path.join(REF_DIR, "jtprop")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.append(REF_DIR)
+    try:
+        import jtprop.compiler
+        import jtprop.propagate
+        return jtprop
+    except Exception:
+        return None
+
+
+def cpu_case_rate(config, tree, tables, cases, variables, workers):
+    """The reference's per-case loop (estimator.py:89-96): copy → apply_evidence
+    → belief_propagation → every query_marginal, with the reference's
+    ParallelEngine (propagate.py:97-161) over `workers` threads.  Runs the real
+    `jtprop` when it is installed under baseline/_ref (kind "reference"), else
+    the oracle port (kind "port").  Returns (cases/s, seconds, kind)."""
+    ref = _reference_module()
+    if ref is not None:
+        from paper_1202_3777_b200 import synth
+
+        members, cards = synth.config_members(config)
+        rtree = ref.compiler.build_tree(members, cards)
+        rtree.cpt_assignment = dict(tree.cpt_assignment)
+        P = ref.propagate
+        eng = P.make_engine("parallel" if workers > 1 else "sequential", workers=workers)
+        template = P.from_potentials(rtree, tables, engine=eng)
+        t0 = time.perf_counter()
+        for ev in cases:
+            st = template.copy()
+            if ev:
+                P.apply_evidence(st, ev)
+            P.belief_propagation(st)
+            for v in variables:
+                P.query_marginal(st, v)
+        dt = time.perf_counter() - t0
+        eng.close()
+        return len(cases) / dt, dt, "reference"
     from oracle import jtref
 
     eng = jtref.ParallelEngine(workers) if workers > 1 else jtref.SequentialEngine()
@@ -130,7 +171,7 @@ def cpu_case_rate(tree, tables, cases, variables, workers):
         jtref.case_posteriors(template, ev, variables)
     dt = time.perf_counter() - t0
     eng.close()
-    return len(cases) / dt, dt
+    return len(cases) / dt, dt, "port"
 
 
 # -------------------------------------------------------------- GPU leg ----
@@ -199,7 +240,7 @@ def main():
         rates = []
         for s in range(args.warmup + args.steps):
             chunk = cases_all[s * args.ref_sample:(s + 1) * args.ref_sample]
-            r, _ = cpu_case_rate(tree, tables, chunk, range(n_vars), workers)
+            r, _, kind = cpu_case_rate(args.config, tree, tables, chunk, range(n_vars), workers)
             if s >= args.warmup:
                 rates.append(r)
         v = statistics.median(rates)
@@ -211,9 +252,12 @@ def main():
                 "config": {"workload": f"{args.config} Mildew-shaped JT (SURVEY Appendix A), per-case "
                                        "copy→evidence→BP→all posteriors",
                            "cases_per_step": args.ref_sample},
-                "cpu_baseline": {"value": round(v, 4), "unit": "cases/s", "cores": workers, "kind": "port",
-                                 "sample": f"{args.ref_sample} cases/step × {args.steps} steps, oracle/jtref.py "
-                                           "(numpy restatement of jtprop, ParallelEngine)"},
+                "cpu_baseline": {"value": round(v, 4), "unit": "cases/s", "cores": workers, "kind": kind,
+                                 "sample": f"{args.ref_sample} cases/step × {args.steps} steps, "
+                                           + ("unmodified jtprop from baseline/_ref" if kind == "reference"
+                                              else "oracle/jtref.py (numpy restatement of jtprop)")
+                                           + f", ParallelEngine({workers} threads), per-case "
+                                             "copy→evidence→BP→all posteriors"},
                 "e2e": {"value": round(v, 4), "unit": "cases/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -384,11 +428,12 @@ def main():
     if not args.no_cpu_baseline and world == 1:
         workers = os.cpu_count() or 1
         sample = synth.evidence_cases(tree, args.cpu_sample, seed=1234)
-        r, dt = cpu_case_rate(tree, tables, sample, range(n_vars), workers)
-        line["cpu_baseline"] = {"value": round(r, 4), "unit": "cases/s", "cores": workers, "kind": "port",
+        r, dt, kind = cpu_case_rate(args.config, tree, tables, sample, range(n_vars), workers)
+        line["cpu_baseline"] = {"value": round(r, 4), "unit": "cases/s", "cores": workers, "kind": kind,
                                 "sample": f"{args.cpu_sample} cases of the same workload, per-case "
-                                          f"copy→evidence→BP→posteriors, oracle/jtref.py ParallelEngine "
-                                          f"({dt:.1f}s)"}
+                                          f"copy→evidence→BP→posteriors, "
+                                          + ("unmodified jtprop (baseline/_ref)" if kind == "reference"
+                                             else "oracle/jtref.py") + f" ParallelEngine ({dt:.1f}s)"}
     if not args.no_extra and world == 1:
         try:
             line["single_tree"] = single_tree_table()
