@@ -175,7 +175,7 @@ def cpu_case_rate(config, tree, tables, cases, variables, workers):
 
 
 # -------------------------------------------------------------- GPU leg ----
-def single_tree_table(dtype_list=("f32", "f64")):
+def single_tree_table(dtype_list=("f32", "f64"), configs=("c1", "c2", "c3", "c4B", "c4M", "c5")):
     """Per-config single-tree propagations/s (jt_propagate, state reset outside
     the timer, median of CUDA-event timings) and B_alg1 roofline fraction."""
     import ctypes as C
@@ -190,7 +190,7 @@ def single_tree_table(dtype_list=("f32", "f64")):
     pk, _ = peaks()
     out = {}
     L = _lib.lib()
-    for name in ("c1", "c2", "c3", "c4B", "c4M"):
+    for name in configs:
         tree, tables = synth.make_config(name)
         alg = algorithmic_elements(tree)
         for dt in dtype_list:

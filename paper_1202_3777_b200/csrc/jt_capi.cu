@@ -16,6 +16,8 @@
 #include "jt_internal.h"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <array>
 #include <cstring>
 #include <map>
@@ -160,7 +162,8 @@ struct PassSpec {
 };
 
 struct LaunchGrp {  // one kernel launch of a wave
-  int own = 0;       // 0: general kernel, 1: thread-owned-bins kernel
+  int kind = 0;      // 0: general kernel, 1: thread-owned-bins kernel, 2: row kernel
+  int vec = 1;       // lanes per vector load
   int lm = 0;        // own kernel load shapes: 0 generic, 1 src bcast + vector factors, 2 all vector
   int m = 1;         // own kernel vectors per thread per block
   int grid = 0;
@@ -169,7 +172,6 @@ struct LaunchGrp {  // one kernel launch of a wave
 };
 
 struct WaveRt {
-  int vec = 1;
   int n_items = 0;  // all items of the wave
   std::vector<LaunchGrp> groups;
   int64_t pass_base = 0, item_base = 0;
@@ -182,6 +184,7 @@ struct Program {
   int64_t* d_blk = nullptr;
   int32_t* d_blk32 = nullptr;
   int32_t* d_bins = nullptr;
+  int32_t* d_rowtab = nullptr;
   double* d_part = nullptr;
   int* d_cnt = nullptr;
   cudaGraphExec_t gexec = nullptr;
@@ -195,6 +198,7 @@ struct Program {
     cudaFree(d_blk);
     cudaFree(d_blk32);
     cudaFree(d_bins);
+    cudaFree(d_rowtab);
     cudaFree(d_part);
     cudaFree(d_cnt);
   }
@@ -218,6 +222,12 @@ struct jt_state {
   int* d_err = nullptr;
   std::map<std::string, std::pair<int64_t*, int>> qmeta;  // per var list: device metadata, total cols
   cudaStream_t stream = nullptr;
+  // fork/join resources: independent launch groups of one wave run on side
+  // streams (parallel branches once the program is captured as a graph)
+  static constexpr int N_SIDE = 7;
+  cudaStream_t side[N_SIDE] = {};
+  cudaEvent_t ev_fork = nullptr;
+  cudaEvent_t ev_join[N_SIDE] = {};
   std::vector<int64_t> coff, boff, sep_off, ratC_off, ratD_off, ev_off, q_off;
   int64_t msg_ratio_off = 0;
   int64_t n_clique = 0, n_base = 0, n_aux = 0, n_qout = 0;
@@ -249,6 +259,11 @@ struct jt_state {
     cudaFree(d_cards);
     cudaFree(d_obs);
     for (auto& kv : qmeta) cudaFree(kv.second.first);
+    for (int i = 0; i < N_SIDE; ++i) {
+      if (side[i]) cudaStreamDestroy(side[i]);
+      if (ev_join[i]) cudaEventDestroy(ev_join[i]);
+    }
+    if (ev_fork) cudaEventDestroy(ev_fork);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -395,6 +410,7 @@ struct BuiltPass {
   std::vector<int64_t> blk;
   std::vector<int32_t> blk32;
   std::vector<int32_t> bins;
+  std::vector<int32_t> rowtab;
   int64_t n_part = 0;
   int64_t n_cnt = 0;
   std::vector<Item> items;
@@ -475,7 +491,8 @@ static std::vector<Dim> merge_dims(const std::vector<Dim>& in, int nf) {
   return out;
 }
 
-static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pass_idx, BuiltPass& bp) {
+static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pass_idx, BuiltPass& bp,
+                        bool allow_row = true) {
   const int nf = (int)ps.factors.size();
   if (nf > MAXF) return JT_ERR_UNSUPPORTED;
   std::vector<Dim> dims = pass_dims(st, ps);
@@ -489,6 +506,7 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
   struct Cand {
     int k;
     bool own = false;
+    bool row = false;
     int own_m = 0;
     int gpi = 1;
     int64_t j_per_item = 1;
@@ -526,8 +544,13 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
     if (has_out && c.n_in == T && T % ((int64_t)NT * vec) == 0) {
       const int64_t m = T / ((int64_t)NT * vec);
       // M > 1 only for full-width vectors (the templated load-shape kernels)
-      if (m == 1 || ((m == 2 || m == 4) && vec == (st->esz == 4 ? 4 : 2))) c.own_m = (int)m;
+      bool allf = true;  // M > 1 kernels load every factor as a full vector
+      for (int f = 0; f < nf; ++f) allf = allf && dims.back().fac[f] == 1;
+      if (m == 1 || ((m == 2 || m == 4) && vec == (st->esz == 4 ? 4 : 2) && allf)) c.own_m = (int)m;
     }
+    // the thread-owned kernel is validated for one merged inner dimension only
+    // (batched states: the case dim); multi-dim inner blocks take the general kernel
+    if (im.size() > 1) c.own_m = 0;
     c.own = c.own_m > 0;
     c.BPI = c.own ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(TH / T, c.r_out));
     // several whole output groups per iteration when a group is smaller than an iteration
@@ -537,11 +560,22 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
       if (c.gpi * c.n_in > 4096) c.gpi = (int)std::max<int64_t>(1, 4096 / c.n_in);
       if (c.gpi > 1) c.BPI = (int)(c.gpi * c.r_out);
     }
+    // row passes (one output entry per item, or none) run on the lean row kernel
+    const int64_t tw = T / (32 * vec);
+    if (allow_row && !c.own && c.gpi == 1 && (!has_out || c.n_in == 1) && T % (32 * vec) == 0 &&
+        (tw == 1 || tw == 2 || tw == 4 || tw % KROW == 0)) {
+      c.row = true;
+      c.BPI = 1;
+    }
     // chunking: ~8 items per SM slot for big passes, >= 2 iterations per item otherwise
     const int64_t per_item = std::max<int64_t>(2 * TH, total / (int64_t)(st->num_sms * 8));
     const int64_t desired = std::max<int64_t>(1, (total + per_item - 1) / per_item);
     const int64_t max_chunks = (c.r_out + c.BPI - 1) / c.BPI;
     int64_t nch = has_out ? (desired + c.n_out - 1) / c.n_out : desired;
+    // thread-owned column passes: every chunk costs n_in partials, so split only as far
+    // as one item per resident CTA needs (~3 per SM)
+    if (c.own && has_out)
+      nch = std::min<int64_t>(nch, ((int64_t)st->num_sms * 3 + c.n_out - 1) / c.n_out);
     if ((c.own || c.gpi > 1) && c.r_out * T <= per_item) nch = 1;  // whole groups per item instead
     nch = std::max<int64_t>(1, std::min(nch, max_chunks));
     int64_t bpc = (c.r_out + nch - 1) / nch;
@@ -568,9 +602,17 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
     double epi = c.own ? 256.0 : 4096.0;
     if (c.gpi > 1) epi = 4096.0 * c.j_per_item / c.gpi;  // one smem reduction per iteration
     double fin = (has_out && c.n_chunks > 1) ? (double)c.n_out * std::min<int64_t>(32, c.n_chunks) * c.n_in * 64.0 : 0.0;
+    // single-tree states: the measured streaming efficiency of the kernels
+    // (profiles/README.md: general ~2 TB/s, row 3.5-5.7 TB/s) weighs the bytes
+    if (st->B == 1) bytes *= c.row ? 1.0 : c.own ? 1.25 : 2.0;
     double pen = 0.0;
     if (T * esz < 128) pen = bytes * (128.0 / (T * esz) - 1.0) * 0.5;
-    c.cost = bytes + part + items * epi + fin + pen + (double)c.n_out * c.r_out * (c.own ? 2048.0 : 16.0);
+    c.cost = bytes + part + items * epi + fin + pen + (double)c.n_out * c.r_out * (c.own ? (st->B == 1 ? 64.0 : 2048.0) : 16.0);
+    if (getenv("JT_DEBUG_COST"))
+      fprintf(stderr, "cand clique %d T %lld n_in %lld n_out %lld r_out %lld own %d/%d row %d gpi %d nch %lld cost %.3g "
+              "(bytes %.3g part %.3g items %.3g fin %.3g pen %.3g)\n", ps.clique, (long long)c.T, (long long)c.n_in,
+              (long long)c.n_out, (long long)c.r_out, (int)c.own, c.own_m, (int)c.row, c.gpi, (long long)c.n_chunks,
+              c.cost, bytes, part, items * epi, fin, pen);
     if (!found || c.cost < best.cost * 0.999) {
       best = c;
       found = true;
@@ -603,6 +645,7 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
   d.blocks_per_chunk = best.bpc;
   d.blk_stride = 2 + nf;
   d.own = best.own ? 1 : 0;
+  d.row = best.row ? 1 : 0;
   d.own_m = best.own_m;
   d.flush_fac = 0;
   if (best.own) {
@@ -668,9 +711,59 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
       }
     }
   }
+  // row passes: inner-offset table [2+nf][T/VEC] and warp units
+  if (best.row) {
+    const int TV = (int)(best.T / vec);
+    bp.rowtab.assign((size_t)(2 + nf) * TV, 0);
+    d.row_lin = 1;
+    for (int iv = 0; iv < TV; ++iv) {
+      int64_t rem = (int64_t)iv * vec, so = 0, dd = 0, fo[MAXF] = {0};
+      for (int i = d.ndi - 1; i >= 0; --i) {
+        const int64_t dig = rem % d.icard[i];
+        rem /= d.icard[i];
+        so += dig * d.isrc[i];
+        dd += dig * d.idst[i];
+        for (int f = 0; f < nf; ++f) fo[f] += dig * d.ifac[f][i];
+      }
+      if (so != (int64_t)iv * vec || (ps.write && dd != (int64_t)iv * vec) || !d.src_vec || TV / 32 < KROW)
+        d.row_lin = 0;
+      bp.rowtab[iv] = (int32_t)so;
+      bp.rowtab[TV + iv] = (int32_t)dd;
+      for (int f = 0; f < nf; ++f) bp.rowtab[(size_t)(2 + f) * TV + iv] = (int32_t)fo[f];
+    }
+    d.row_fmode = 0;
+    for (int f = 0; f < nf; ++f) {
+      bool lin = true, zero = true;
+      for (int iv = 0; iv < TV; ++iv) {
+        const int32_t x = bp.rowtab[(size_t)(2 + f) * TV + iv];
+        lin = lin && x == iv * vec && ((d.fac_vec >> f) & 1u);
+        zero = zero && x == 0 && !((d.fac_vec >> f) & 1u);  // the VEC lanes of a vector must agree too
+      }
+      d.row_fmode |= (uint32_t)(zero ? 2 : lin ? 1 : 0) << (2 * f);
+    }
+    const int64_t grp_el = best.r_out * best.T;
+    // ~4 units per warp of a full-occupancy grid (3 CTAs x 8 warps per SM), >= one batch each
+    const int64_t unit = std::max<int64_t>((int64_t)32 * vec * KROW, total / ((int64_t)st->num_sms * 24 * 4));
+    if (has_out && grp_el > 2 * unit) {
+      int64_t bpc = std::max<int64_t>(1, unit / best.T);
+      while ((best.r_out + bpc - 1) / bpc > 32 * CHUNK_GROUP) bpc *= 2;
+      d.blocks_per_chunk = bpc;
+      d.n_chunks = (int)((best.r_out + bpc - 1) / bpc);
+    } else if (!has_out) {
+      // no output: any split of the blocks is fine; units of ~unit elements
+      int64_t bpc = std::max<int64_t>(1, unit / best.T);
+      d.blocks_per_chunk = bpc;
+      d.n_chunks = (int)((best.r_out + bpc - 1) / bpc);
+    } else {
+      d.n_chunks = 1;
+      d.blocks_per_chunk = best.r_out;
+    }
+    best.n_chunks = d.n_chunks;
+    best.j_per_item = d.n_chunks == 1 ? std::max<int64_t>(1, unit / grp_el) : 1;
+  }
   // thread-owned passes read a compact int32 table: every column in units of
   // the largest power-of-two-free common step (T for lane-strided tensors)
-  if (best.own) {
+  if (best.own || best.row) {
     const int ncol = 2 + nf;
     std::vector<int64_t> unit(ncol, 1);  // plain int32 element offsets
     bp.blk32.resize(bp.blk.size());
@@ -710,7 +803,7 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
     bp.n_part = best.n_out * (best.n_chunks + ng) * best.n_in;
     bp.n_cnt = best.n_out * (ng + 1);
   }
-  if ((best.own || best.gpi > 1) && best.n_chunks == 1) {
+  if ((best.own || best.gpi > 1 || best.row) && best.n_chunks == 1) {
     for (int64_t jo = 0; jo < best.n_out; jo += best.j_per_item)
       bp.items.push_back(Item{pass_idx, 0, jo, std::min(best.j_per_item, best.n_out - jo)});
   } else {
@@ -720,6 +813,9 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
   return JT_OK;
 }
 
+// waves touching fewer elements than this are launch-latency bound
+constexpr int64_t SMALL_WAVE_ELEMS = int64_t(1) << 21;
+
 struct HostProgram {
   std::vector<WaveRt> waves;
   std::vector<DevPass> passes;
@@ -727,6 +823,7 @@ struct HostProgram {
   std::vector<int64_t> blk;
   std::vector<int32_t> blk32;
   std::vector<int32_t> bins;
+  std::vector<int32_t> rowtab;
   std::vector<int> pass_clique;
   int64_t n_part = 0, n_cnt = 0;
 };
@@ -739,25 +836,38 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
   auto& bins = hp.bins;
   int64_t& n_part = hp.n_part;
   int64_t& n_cnt = hp.n_cnt;
-  std::vector<Item> grp_items[10];
   for (auto& w : waves) {
     if (w.empty()) continue;
-    int vec = st->esz == 4 ? 4 : 2;
-    for (auto& ps : w) vec = std::min(vec, pass_max_vec(st, ps));
     WaveRt rt;
-    rt.vec = vec;
     rt.pass_base = (int64_t)passes.size();
     rt.item_base = (int64_t)items.size();
+    // launch groups of the wave: (kind, vec, lm, m) -> items, in first-seen order
+    std::vector<std::pair<std::array<int, 4>, std::vector<Item>>> grp;
+    // launch-bound (small) waves: one vector width and no row kernel, so the
+    // wave is one or two launches; big waves give every pass its own best kernel
+    int64_t wave_el = 0;
+    int wave_vec = st->esz == 4 ? 4 : 2;
+    for (auto& ps : w) {
+      const auto dd = pass_dims(st, ps);
+      int64_t n = 1;
+      for (auto& x : dd) n *= x.card;
+      wave_el += n;
+      wave_vec = std::min(wave_vec, pass_max_vec(st, ps));
+    }
+    const bool small_wave = wave_el < SMALL_WAVE_ELEMS;
     for (auto& ps : w) {
       BuiltPass bp;
       const int local = (int)(passes.size() - rt.pass_base);
-      int rc = compile_pass(st, ps, vec, local, bp);
+      const int vec = small_wave ? wave_vec : pass_max_vec(st, ps);
+      int rc = compile_pass(st, ps, vec, local, bp, !small_wave);
       if (rc != JT_OK) return rc;
       bp.d.blk_off = (int64_t)blk.size();
       bp.d.blk32_off = (int64_t)hp.blk32.size();
       hp.blk32.insert(hp.blk32.end(), bp.blk32.begin(), bp.blk32.end());
-      if (bp.d.own) bp.blk.clear();  // the own kernel reads only the int32 table
+      if (bp.d.own || bp.d.row) bp.blk.clear();  // these kernels read only the int32 table
       bp.d.bin_off = (int64_t)bins.size();
+      bp.d.row_tab_off = (int64_t)hp.rowtab.size();
+      hp.rowtab.insert(hp.rowtab.end(), bp.rowtab.begin(), bp.rowtab.end());
       bp.d.part_off = n_part;
       bp.d.cnt_off = n_cnt;
       blk.insert(blk.end(), bp.blk.begin(), bp.blk.end());
@@ -766,32 +876,39 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
       n_cnt += bp.n_cnt;
       passes.push_back(bp.d);
       hp.pass_clique.push_back(ps.clique);
-      // launch group: general kernel, or own kernel keyed by load shapes
-      int key = 0;
+      std::array<int, 4> key{bp.d.row ? 2 : 0, vec, bp.d.row ? bp.d.row_lin : 0, 1};
       if (bp.d.own) {
         const bool allf = bp.d.fac_vec == ((1u << bp.d.nf) - 1u);
         const bool full_vec = vec == (st->esz == 4 ? 4 : 2);
         const int lm = full_vec && allf ? (bp.d.src_vec ? 2 : 1) : 0;
         if (lm == 0 && bp.d.own_m != 1) return JT_ERR_UNSUPPORTED;
-        key = 1 + lm + 3 * (bp.d.own_m == 4 ? 2 : bp.d.own_m == 2 ? 1 : 0);
+        key = {1, vec, lm, bp.d.own_m};
       }
-      auto& g = grp_items[key];
-      g.insert(g.end(), bp.items.begin(), bp.items.end());
+      auto it = std::find_if(grp.begin(), grp.end(), [&](const auto& g) { return g.first == key; });
+      if (it == grp.end()) {
+        grp.push_back({key, {}});
+        it = grp.end() - 1;
+      }
+      it->second.insert(it->second.end(), bp.items.begin(), bp.items.end());
     }
-    const int occ = occ_override ? occ_override : wave_max_ctas_per_sm(st->plan->dtype, vec);
-    const int occ_o = occ_override ? occ_override : wave_own_max_ctas_per_sm(st->plan->dtype, vec);
-    for (int key = 0; key < 10; ++key) {
-      auto& g = grp_items[key];
-      if (g.empty()) continue;
+    for (auto& g : grp) {
       LaunchGrp lg;
-      lg.own = key > 0;
-      lg.lm = key > 0 ? (key - 1) % 3 : 0;
-      lg.m = key > 0 ? (1 << ((key - 1) / 3)) : 1;
-      lg.n_items = (int)g.size();
+      lg.kind = g.first[0];
+      lg.vec = g.first[1];
+      lg.lm = g.first[2];
+      lg.m = g.first[3];
+      int occ = occ_override;
+      if (!occ) {
+        const int dt = st->plan->dtype;
+        occ = lg.kind == 1 ? wave_own_max_ctas_per_sm(dt, lg.vec)
+            : lg.kind == 2 ? wave_row_max_ctas_per_sm(dt, lg.vec) : wave_max_ctas_per_sm(dt, lg.vec);
+      }
+      lg.n_items = (int)g.second.size();
       lg.item_off = (int64_t)items.size() - rt.item_base;
-      lg.grid = (int)std::min<int64_t>(lg.n_items, (int64_t)(lg.own ? occ_o : occ) * st->num_sms);
-      items.insert(items.end(), g.begin(), g.end());
-      g.clear();
+      lg.grid = (int)std::min<int64_t>(lg.n_items, (int64_t)occ * st->num_sms);
+      if (lg.kind == 2)  // warp units: enough CTAs for every unit to have a warp, up to full occupancy
+        lg.grid = (int)std::min<int64_t>((lg.n_items + NT / 32 - 1) / (NT / 32), (int64_t)occ * st->num_sms);
+      items.insert(items.end(), g.second.begin(), g.second.end());
       rt.groups.push_back(lg);
     }
     rt.n_items = (int)(items.size() - rt.item_base);
@@ -826,6 +943,7 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
   if ((rc = up(&prog->d_blk, blk))) return rc;
   if ((rc = up(&prog->d_bins, bins))) return rc;
   if ((rc = up(&prog->d_blk32, hp.blk32))) return rc;
+  if ((rc = up(&prog->d_rowtab, hp.rowtab))) return rc;
   CK(cudaMalloc(&prog->d_part, std::max<int64_t>(n_part, 1) * sizeof(double)));
   CK(cudaMalloc(&prog->d_cnt, std::max<int64_t>(n_cnt, 1) * sizeof(int)));
   CK(cudaMemset(prog->d_cnt, 0, std::max<int64_t>(n_cnt, 1) * sizeof(int)));
@@ -833,26 +951,60 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
   return JT_OK;
 }
 
+static int launch_group(jt_state* st, const Program* pr, const WaveRt& w, const LaunchGrp& g, cudaStream_t s) {
+  WaveArgs a;
+  a.clique = st->d_clique;
+  a.base = st->d_base;
+  a.aux = st->d_aux;
+  a.qout = st->d_qout;
+  a.partials = pr->d_part;
+  a.counters = pr->d_cnt;
+  a.err = st->d_err;
+  a.blk = pr->d_blk;
+  a.blk32 = pr->d_blk32;
+  a.bins = pr->d_bins;
+  a.rowtab = pr->d_rowtab;
+  a.passes = pr->d_passes + w.pass_base;
+  a.items = pr->d_items + w.item_base + g.item_off;
+  a.n_items = g.n_items;
+  if (g.kind == 1) CK(launch_wave_own(st->plan->dtype, g.vec, g.lm, g.m, a, g.grid, s));
+  else if (g.kind == 2) CK(launch_wave_row(st->plan->dtype, g.vec, g.lm, a, g.grid, s));
+  else CK(launch_wave(st->plan->dtype, g.vec, a, g.grid, s));
+  st->launches++;
+  return JT_OK;
+}
+
+static int ensure_side(jt_state* st) {
+  if (st->ev_fork) return JT_OK;
+  for (int i = 0; i < jt_state::N_SIDE; ++i) {
+    CK(cudaStreamCreateWithFlags(&st->side[i], cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&st->ev_join[i], cudaEventDisableTiming));
+  }
+  CK(cudaEventCreateWithFlags(&st->ev_fork, cudaEventDisableTiming));
+  return JT_OK;
+}
+
 static int launch_program_waves(jt_state* st, Program* pr, cudaStream_t s) {
   for (auto& w : pr->waves) {
-    WaveArgs a;
-    a.clique = st->d_clique;
-    a.base = st->d_base;
-    a.aux = st->d_aux;
-    a.qout = st->d_qout;
-    a.partials = pr->d_part;
-    a.counters = pr->d_cnt;
-    a.err = st->d_err;
-    a.blk = pr->d_blk;
-    a.blk32 = pr->d_blk32;
-    a.bins = pr->d_bins;
-    a.passes = pr->d_passes + w.pass_base;
-    for (const LaunchGrp& g : w.groups) {
-      a.items = pr->d_items + w.item_base + g.item_off;
-      a.n_items = g.n_items;
-      if (g.own) CK(launch_wave_own(st->plan->dtype, w.vec, g.lm, g.m, a, g.grid, s));
-      else CK(launch_wave(st->plan->dtype, w.vec, a, g.grid, s));
-      st->launches++;
+    const int ng = (int)w.groups.size();
+    if (ng == 1) {
+      int rc = launch_group(st, pr, w, w.groups[0], s);
+      if (rc) return rc;
+      continue;
+    }
+    // independent launch groups: fork onto side streams, join back into s
+    int rc = ensure_side(st);
+    if (rc) return rc;
+    CK(cudaEventRecord(st->ev_fork, s));
+    const int nside = std::min(ng - 1, (int)jt_state::N_SIDE);
+    for (int i = 0; i < nside; ++i) CK(cudaStreamWaitEvent(st->side[i], st->ev_fork, 0));
+    for (int gi = 0; gi < ng; ++gi) {
+      cudaStream_t gs = gi == 0 ? s : st->side[(gi - 1) % jt_state::N_SIDE];
+      if ((rc = launch_group(st, pr, w, w.groups[gi], gs))) return rc;
+    }
+    for (int i = 0; i < nside; ++i) {
+      CK(cudaEventRecord(st->ev_join[i], st->side[i]));
+      CK(cudaStreamWaitEvent(s, st->ev_join[i], 0));
     }
   }
   return JT_OK;
@@ -1826,7 +1978,7 @@ extern "C" const char* jt_version(void) { return "libjtb200 0.1 sm_100a"; }
 // Host-only: compile the propagation program of a (plan, batch, mode) without
 // touching a device and describe every wave/pass.  kind 0: jt_propagate;
 // kind 1: jt_propagate_query over all variables with every variable observed
-// (the batch program).  Used by tools/plan_report.py and the CPU tests.
+// (the batch program); kind 2: jt_propagate on a freshly reset state.  Used by tools/plan_report.py and the CPU tests.
 extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind, int num_sms, int occ,
                              char* buf, int64_t len) {
   if (!plan || !buf || len <= 0 || batch < 1) return JT_ERR_BAD_ARG;
@@ -1844,7 +1996,7 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
     }
   }
   std::vector<std::vector<PassSpec>> waves;
-  int rc = build_propagate(&st, plan->roots, qv, waves, kind == 1);
+  int rc = build_propagate(&st, plan->roots, qv, waves, kind >= 1);
   if (rc) return rc;
   HostProgram hp;
   rc = compile_program(&st, waves, hp, occ > 0 ? occ : 2);
@@ -1853,8 +2005,14 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
   char line[512];
   for (size_t w = 0; w < hp.waves.size(); ++w) {
     const WaveRt& rt = hp.waves[w];
-    snprintf(line, sizeof line, "wave %zu vec %d items %d launches %zu\n", w, rt.vec, rt.n_items, rt.groups.size());
+    snprintf(line, sizeof line, "wave %zu items %d launches %zu:", w, rt.n_items, rt.groups.size());
     out += line;
+    for (const LaunchGrp& g : rt.groups) {
+      snprintf(line, sizeof line, " [%s vec %d items %d grid %d]", g.kind == 1 ? "own" : g.kind == 2 ? "row" : "gen",
+               g.vec, g.n_items, g.grid);
+      out += line;
+    }
+    out += "\n";
     const int64_t pe = (w + 1 < hp.waves.size()) ? hp.waves[w + 1].pass_base : (int64_t)hp.passes.size();
     for (int64_t pi = rt.pass_base; pi < pe; ++pi) {
       const DevPass& d = hp.passes[pi];
@@ -1866,10 +2024,10 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
         }
       snprintf(line, sizeof line,
                "  pass clique %d src %d nf %d wr %d out %d T %d n_in %d n_out %lld r_out %lld BPI %d chunks %d "
-               "bpc %lld items %lld ndi %d own %d/%d gpi %d ffac %x part %lld\n",
+               "bpc %lld items %lld ndi %d own %d/%d row %d gpi %d ffac %x part %lld\n",
                hp.pass_clique[pi], d.src_arena, d.nf, d.dst_off >= 0, d.out_kind, d.T, d.n_in, (long long)n_out,
                (long long)d.n_blocks_per_jout, d.BPI, d.n_chunks, (long long)d.blocks_per_chunk,
-               (long long)n_items, d.ndi, d.own, d.own_m, d.gpi, d.flush_fac,
+               (long long)n_items, d.ndi, d.own, d.own_m, d.row, d.gpi, d.flush_fac,
                (long long)(d.n_chunks > 1 && d.out_kind ? n_out * d.n_chunks * d.n_in : 0));
       out += line;
     }

@@ -55,6 +55,10 @@ struct DevPass {
   int unit_src, unit_dst;   // element offset = entry * unit
   int unit_fac[MAXF];
   int own_m;                // own passes: vectors (lane chunks) per thread per block
+  int row;                  // 1: row pass (n_in <= 1, no gpi, T % (32*VEC) == 0): wave_row_kernel
+  int64_t row_tab_off;      // row passes: offset of the inner-offset table [2+nf][T/VEC] (int32)
+  int row_lin;              // row passes: src and dst inner offsets equal the position (tab rows 0/1 unused)
+  uint32_t row_fmode;       // row passes, 2 bits per factor: 0 table, 1 offset = position, 2 offset = 0
   int own;                  // 1: thread-owned bins (n_in == T == NT*VEC): sync-free epilogue,
                             //    items span j_count whole output groups
   int ndi;                  // merged inner dims
@@ -86,11 +90,16 @@ struct WaveArgs {
   const DevPass* passes;
   const Item* items;
   int n_items;
+  const int32_t* rowtab;    // row kernel inner-offset tables
 };
 
 // launchers (jt_kernels.cu)
 cudaError_t launch_wave(int dtype, int vec, const WaveArgs& a, int grid, cudaStream_t s);
 int wave_max_ctas_per_sm(int dtype, int vec);
+cudaError_t launch_wave_row(int dtype, int vec, int lin, const WaveArgs& a, int grid, cudaStream_t s);
+int wave_row_max_ctas_per_sm(int dtype, int vec);
+constexpr int KROW = 8;
+constexpr int CHUNK_GROUP = 32;  // chunk partials combined in groups of this many (two levels)     // vectors per thread per iteration of the row kernel
 cudaError_t launch_wave_own(int dtype, int vec, int lm, int m, const WaveArgs& a, int grid, cudaStream_t s);
 int wave_own_max_ctas_per_sm(int dtype, int vec);
 cudaError_t launch_normalize(const double* qout, const int64_t* q_off, const int32_t* q_card,

@@ -43,6 +43,15 @@ __device__ __forceinline__ void load_vec_ro(const T* p, T (&v)[VEC]) {
 }
 
 template <typename T, int VEC>
+__device__ __forceinline__ void load_vec_cs(const T* p, T (&v)[VEC]) {
+  using V = typename VecT<T, VEC>::type;
+  V x = __ldcs(reinterpret_cast<const V*>(p));
+  const T* xs = reinterpret_cast<const T*>(&x);
+#pragma unroll
+  for (int l = 0; l < VEC; ++l) v[l] = xs[l];
+}
+
+template <typename T, int VEC>
 __device__ __forceinline__ void store_vec(T* p, const T (&v)[VEC]) {
   using V = typename VecT<T, VEC>::type;
   V x;
@@ -111,8 +120,6 @@ __device__ __forceinline__ void finalize_entry(const DevPass& P, int64_t j, doub
     qout[P.out_off + j] = star;
   }
 }
-
-constexpr int CHUNK_GROUP = 32;
 
 // Deterministic cross-CTA combine of one output group's chunk partials.  The
 // block's n_in values are in red[0..n_in).  Chunks are combined in fixed
@@ -666,6 +673,270 @@ __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
     }
     __syncthreads();
   }
+}
+
+// Row passes: every position of a unit reduces into ONE output entry (n_in <= 1:
+// the separator is a prefix of the merged outer dims — Alg. 1 row sums — or
+// there is no output, e.g. a pure absorb/write pass).  Warp-centric: a unit is
+// one output group (or `j_count` small groups, or one chunk of a huge group)
+// walked by ONE warp, KR vectors per lane in flight per tensor, reduced with
+// shuffles — no barriers, no shared memory.  Units are handed out dynamically
+// (one atomic per unit), so SMs that run ahead take more of them; the results
+// do not depend on which warp took a unit (each group is summed in a fixed
+// order, chunk partials are combined in chunk order), so they are
+// run-to-run deterministic.  Inner offsets of the T positions of a block come
+// from a host-built table (RowTab, L1-resident); block offsets from the block
+// table.
+constexpr int KR = KROW;
+
+template <typename T>
+__device__ __forceinline__ double warp_chunk_combine(const DevPass& P, const Item& u, const WaveArgs& a,
+                                                     double part, bool* last) {
+  // n_in == 1 chunk partials: level 1 groups of CHUNK_GROUP chunks, level 2 the
+  // groups in order; the last warp to arrive at a level sums it (lane i holds
+  // partial i, fixed xor-tree order)
+  const int lane = threadIdx.x & 31;
+  const int nch = P.n_chunks;
+  const int ng = (nch + CHUNK_GROUP - 1) / CHUNK_GROUP;
+  const int g = u.chunk / CHUNK_GROUP;
+  const int gsz = min(CHUNK_GROUP, nch - g * CHUNK_GROUP);
+  double* L1 = a.partials + P.part_off + u.j_out * (int64_t)(nch + ng);
+  double* L2 = L1 + nch;
+  int* cnt = a.counters + P.cnt_off + u.j_out * (int64_t)(ng + 1);
+  if (lane == 0) L1[u.chunk] = part;
+  __threadfence();
+  __syncwarp();
+  int arrived = 0;
+  if (lane == 0) arrived = atomicAdd(&cnt[g], 1);
+  arrived = __shfl_sync(0xffffffffu, arrived, 0);
+  *last = false;
+  if (arrived != gsz - 1) return 0.0;
+  __threadfence();
+  double s = lane < gsz ? __ldcg(L1 + g * CHUNK_GROUP + lane) : 0.0;
+  s = warp_sum(s);
+  if (lane == 0) cnt[g] = 0;
+  if (ng > 1) {
+    if (lane == 0) L2[g] = s;
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) arrived = atomicAdd(&cnt[ng], 1);
+    arrived = __shfl_sync(0xffffffffu, arrived, 0);
+    if (arrived != ng - 1) return 0.0;
+    __threadfence();
+    s = 0.0;
+    for (int i0 = 0; i0 < ng; i0 += 32) {  // ng <= 32 for any realistic split
+      const double x = i0 + lane < ng ? __ldcg(L2 + i0 + lane) : 0.0;
+      s += warp_sum(x);
+    }
+    if (lane == 0) cnt[ng] = 0;
+  }
+  *last = true;
+  return s;
+}
+
+// LIN: the pass's blocks are at least KR vectors per lane (TW >= KR) and the
+// src/dst inner offsets are the positions themselves (the clique's own layout):
+// one block entry per batch, slot addresses are immediates off one pointer.
+template <typename T, int VEC, bool LIN>
+__global__ void __launch_bounds__(NT, 2) wave_row_kernel(const WaveArgs a) {
+  T* __restrict__ clique = reinterpret_cast<T*>(a.clique);
+  const T* __restrict__ base = reinterpret_cast<const T*>(a.base);
+  T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
+  const T* __restrict__ aux_c = aux;
+  const int lane = threadIdx.x & 31;
+  const int n_warps = gridDim.x * (NT / 32);
+  // static round-robin over the warps of the grid: unit i -> warp i mod n_warps
+  for (int ui = blockIdx.x * (NT / 32) + (threadIdx.x >> 5); ui < a.n_items; ui += n_warps) {
+    const Item u = a.items[ui];
+    const DevPass* __restrict__ P = a.passes + u.pass;
+    const int TW = LIN ? P->T / (32 * VEC) : P->T / (32 * VEC);  // {1,2,4} or a multiple of KR
+    const int lg = (LIN || TW >= KR) ? 0 : (TW == 1 ? 0 : TW == 2 ? 1 : 2);
+    const int TV = P->T / VEC;
+    const int64_t r_out = P->n_blocks_per_jout;
+    const bool chunked = P->n_chunks > 1;
+    const T* __restrict__ srcA =
+        (P->src_arena == A_BASE ? base : P->src_arena == A_AUX ? aux_c : clique) + P->src_off;
+    const bool wr = P->dst_off >= 0;
+    T* __restrict__ dstA = clique + (wr ? P->dst_off : 0);
+    const int32_t* __restrict__ blk = a.blk32 + P->blk32_off;
+    const int32_t* __restrict__ tab = a.rowtab + P->row_tab_off;  // [2+nf][T/VEC]
+    const int bs = 2 + P->nf;
+    const int nf = P->nf;
+    const bool svec = VEC == 1 || P->src_vec;
+    const uint32_t fvm = P->fac_vec;
+    const uint32_t fmode = P->row_fmode;
+    const int out_kind = P->out_kind;
+    const int n_groups = chunked ? 1 : (int)u.j_count;
+    for (int gi = 0; gi < n_groups; ++gi) {
+      const int64_t j = u.j_out + gi;
+      int64_t b = j * r_out, b1 = b + r_out;
+      if (chunked) {
+        b += (int64_t)u.chunk * P->blocks_per_chunk;
+        b1 = min(b + P->blocks_per_chunk, (j + 1) * r_out);
+      }
+      double acc = 0.0;
+      int kk = 0;  // TW >= KR: next vector index within block b
+      while (b < b1) {
+        // phase 1: every slot's block entry and inner offset (no data yet), so the
+        // KR data loads below issue back to back instead of each waiting on its index
+        T v[KR][VEC];
+        int ioff[KR];
+        uint32_t okm = (1u << KR) - 1u;
+        int e0 = 0;
+        if (LIN) {
+          e0 = __ldg(blk + b * bs);
+          const T* p0 = srcA + e0 + (kk * 32 + lane) * VEC;
+#pragma unroll
+          for (int k = 0; k < KR; ++k) {
+            ioff[k] = (kk + k) * 32 + lane;
+            load_vec_cs<T, VEC>(p0 + k * 32 * VEC, v[k]);
+          }
+        } else {
+          int soff[KR];
+          okm = 0;
+#pragma unroll
+          for (int k = 0; k < KR; ++k) {
+            const int64_t bk = TW >= KR ? b : b + (k >> lg);
+            const bool ok = bk < b1;
+            okm |= (ok ? 1u : 0u) << k;
+            ioff[k] = (TW >= KR ? kk + k : (k & (TW - 1))) * 32 + lane;
+            soff[k] = __ldg(blk + (ok ? bk : b) * bs) + __ldg(tab + ioff[k]);
+          }
+          // phase 2: the data loads (streaming: evict-first, keeps L1 for the tables)
+#pragma unroll
+          for (int k = 0; k < KR; ++k) {
+            const T* p = srcA + soff[k];
+            if (svec) {
+              load_vec_cs<T, VEC>(p, v[k]);
+            } else {
+              const T x = __ldcs(p);
+#pragma unroll
+              for (int l = 0; l < VEC; ++l) v[k][l] = x;
+            }
+          }
+        }
+        // phase 3: factors (separator ratios / evidence masks: small, L1/L2-resident).
+        // Per factor the host chose how its inner offsets are formed: a table
+        // lookup, the position itself (linear), or zero (constant over the block).
+        for (int f = 0; f < nf; ++f) {
+          const T* fb = aux_c + P->fac_off[f];
+          const int mode = (fmode >> (2 * f)) & 3;
+          if ((LIN || TW >= KR) && mode == 2) {  // one value per block: scalar broadcast
+            const T x = __ldg(fb + __ldg(blk + b * bs + 2 + f));
+#pragma unroll
+            for (int k = 0; k < KR; ++k)
+#pragma unroll
+              for (int l = 0; l < VEC; ++l) v[k][l] *= x;
+            continue;
+          }
+          const int32_t* tf = tab + (int64_t)(2 + f) * TV;
+          const bool fv = (fvm >> f) & 1u;
+          int fo[KR];
+          if (LIN || TW >= KR) {
+            const int e = __ldg(blk + b * bs + 2 + f);
+#pragma unroll
+            for (int k = 0; k < KR; ++k)
+              fo[k] = e + (mode == 1 ? ioff[k] * VEC : mode == 2 ? 0 : __ldg(tf + ioff[k]));
+          } else {
+#pragma unroll
+            for (int k = 0; k < KR; ++k) {
+              const int64_t bk = b + (k >> lg);
+              fo[k] = __ldg(blk + (bk < b1 ? bk : b) * bs + 2 + f) +
+                      (mode == 1 ? ioff[k] * VEC : mode == 2 ? 0 : __ldg(tf + ioff[k]));
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < KR; ++k) {
+            T g[VEC];
+            if (VEC == 1 || fv) {
+              load_vec_ro<T, VEC>(fb + fo[k], g);
+            } else {
+              const T x = __ldg(fb + fo[k]);
+#pragma unroll
+              for (int l = 0; l < VEC; ++l) g[l] = x;
+            }
+#pragma unroll
+            for (int l = 0; l < VEC; ++l) v[k][l] *= g[l];
+          }
+        }
+        if (wr) {
+          if (LIN) {
+            T* q0 = dstA + __ldg(blk + b * bs + 1) + (kk * 32 + lane) * VEC;
+#pragma unroll
+            for (int k = 0; k < KR; ++k) store_vec<T, VEC>(q0 + k * 32 * VEC, v[k]);
+          } else {
+            const int32_t* td = tab + TV;
+#pragma unroll
+            for (int k = 0; k < KR; ++k) {
+              if ((okm >> k) & 1u) {
+                const int64_t bk = TW >= KR ? b : b + (k >> lg);
+                store_vec<T, VEC>(dstA + __ldg(blk + bk * bs + 1) + __ldg(td + ioff[k]), v[k]);
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+          T part = (T)0;
+#pragma unroll
+          for (int l = 0; l < VEC; ++l) part += v[k][l];
+          acc += ((okm >> k) & 1u) ? (double)part : 0.0;
+        }
+        if (LIN || TW >= KR) {
+          kk += KR;
+          if (kk == TW) {
+            kk = 0;
+            ++b;
+          }
+        } else {
+          b += KR >> lg;
+        }
+      }
+      if (out_kind == OUT_NONE) continue;
+      double sum = warp_sum(acc);
+      if (chunked) {
+        bool last;
+        sum = warp_chunk_combine<T>(*P, u, a, sum, &last);
+        if (!last) continue;
+      }
+      if (lane == 0) finalize_entry<T>(*P, j, sum, aux, a.qout, a.err);
+    }
+  }
+}
+
+template <typename T, int VEC>
+static cudaError_t launch_row_t(int lin, const WaveArgs& a, int grid, cudaStream_t s) {
+  if (lin) wave_row_kernel<T, VEC, true><<<grid, NT, 0, s>>>(a);
+  else wave_row_kernel<T, VEC, false><<<grid, NT, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wave_row(int dtype, int vec, int lin, const WaveArgs& a, int grid, cudaStream_t s) {
+  if (grid <= 0 || a.n_items <= 0) return cudaSuccess;
+  if (dtype == 0) {
+    if (vec == 4) return launch_row_t<float, 4>(lin, a, grid, s);
+    if (vec == 2) return launch_row_t<float, 2>(lin, a, grid, s);
+    return launch_row_t<float, 1>(lin, a, grid, s);
+  }
+  if (vec == 2) return launch_row_t<double, 2>(lin, a, grid, s);
+  return launch_row_t<double, 1>(lin, a, grid, s);
+}
+
+template <typename T, int VEC>
+static int occ_row_t() {
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, wave_row_kernel<T, VEC, false>, NT, 0);
+  return n > 0 ? n : 1;
+}
+
+int wave_row_max_ctas_per_sm(int dtype, int vec) {
+  if (dtype == 0) {
+    if (vec == 4) return occ_row_t<float, 4>();
+    if (vec == 2) return occ_row_t<float, 2>();
+    return occ_row_t<float, 1>();
+  }
+  if (vec == 2) return occ_row_t<double, 2>();
+  return occ_row_t<double, 1>();
 }
 
 template <int VEC>

@@ -1,0 +1,55 @@
+"""Host planner (no device): every BASELINE config compiles into a propagation
+program in every mode the engine supports, and the program has the structure
+DESIGN.md §3 describes (waves by height/depth, row passes on the row kernel)."""
+import os
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+
+CONFIGS = ["c1", "c2", "c3", "c4B", "c4M", "c5"]
+
+
+def report(*a, **k):
+    import plan_report
+
+    return plan_report.report(*a, **k)
+
+
+@pytest.mark.parametrize("name", CONFIGS)
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("kind", [0, 1])
+def test_single_tree_program_compiles(name, dtype, kind):
+    text = report(name, batch=1, mode="materialized", kind=kind, dtype=dtype)
+    assert text.startswith("wave 0")
+    assert "pass clique" in text
+
+
+@pytest.mark.parametrize("name", ["c1", "c5", "c4B"])
+@pytest.mark.parametrize("batch", [8, 16, 1024])
+def test_batch_programs_compile(name, batch):
+    for mode in ("shared", "materialized"):
+        if mode == "materialized" and batch > 16 and name != "c1":
+            continue  # a c5 materialized micro-batch of 1024 cases would need 33 GB of clique tables
+        report(name, batch=batch, mode=mode, kind=1, dtype="f32")
+
+
+def test_shared_mode_rejects_cliques_with_too_many_factors():
+    # c2 (Pigs-shaped) has cliques with > 8 neighbours: the batch layer must
+    # fall back to materialized mode (batch.shared_supported)
+    from paper_1202_3777_b200 import synth
+    from paper_1202_3777_b200.batch import shared_supported
+
+    tree, _ = synth.make_config("c2")
+    assert not shared_supported(tree)
+    with pytest.raises(NotImplementedError):
+        report("c2", batch=8, mode="shared", kind=1)
+
+
+def test_large_cliques_use_row_kernel():
+    text = report("c3", batch=1, mode="materialized", kind=0, dtype="f32")
+    rows = [l for l in text.splitlines() if l.startswith("  pass") and " row 1 " in l]
+    assert len(rows) >= 5, text
