@@ -74,6 +74,14 @@ int64_t jt_state_device_bytes(const jt_state* st);
  * case_idx = -1 broadcasts to every case (and, in shared mode, loads the base). */
 int jt_state_load(jt_state* st, int case_idx, const double* clique_concat,
                   const double* sep_concat);
+/* initialize (propagate.py:204-222) on the device: every clique's base table
+ * becomes the product of the CPTs assigned to it (ones when none), then every
+ * case is reset to it (separators ones, no evidence).  CPT k belongs to clique
+ * cpt_clique[k] (tree.cpt_assignment[child]); its variables are
+ * cpt_vars[cpt_off[k] .. cpt_off[k+1]) in the CPT table's own axis order (C order,
+ * last fastest; potential.py:50-55) and its values follow in cpt_values. */
+int jt_state_initialize(jt_state* st, int n_cpts, const int32_t* cpt_clique, const int32_t* cpt_off,
+                        const int32_t* cpt_vars, const double* cpt_values);
 /* Restore every case to the loaded base tables (clique tables from the base
  * replica, separators to ones) and drop all evidence: PropagationState.copy()
  * of a template state (cli.py:194-201), done on device for the whole batch. */

@@ -50,6 +50,10 @@ def __getattr__(name):
         from . import propagate
 
         return getattr(propagate, name)
+    if name == "JunctionTreeEngine":
+        from .estimator import JunctionTreeEngine
+
+        return JunctionTreeEngine
     if name in ("BatchPropagator", "gather_posteriors", "shard_bounds"):
         from . import batch
 
@@ -60,7 +64,7 @@ def __getattr__(name):
 __version__ = "0.1.0"
 __all__ = list(_API) + [
     "BatchPropagator", "Clique", "DeviceError", "FLAT", "INTERLEAVED", "InconsistentDivisionError",
-    "JtpropError", "JunctionTree", "MappingTableSet", "NoCoveringCliqueError", "Scope", "Separator",
+    "JtpropError", "JunctionTree", "JunctionTreeEngine", "MappingTableSet", "NoCoveringCliqueError", "Scope", "Separator",
     "StateOutOfRangeError", "UnknownVariableError", "ZeroMassError", "algorithmic_elements",
     "build_mapping_table", "build_mapping_tables", "build_tree", "directed_messages",
     "gather_posteriors", "relayout_mapping_tables", "shard_bounds",

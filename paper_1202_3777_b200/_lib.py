@@ -47,6 +47,7 @@ SIGNATURES = {
     "jt_apply_evidence_device": (C.c_int, [_vp, C.c_int, _vp, C.c_int, _i32p, _i32p, _vp]),
     "jt_clear_evidence": (C.c_int, [_vp]),
     "jt_state_reset": (C.c_int, [_vp, _vp]),
+    "jt_state_initialize": (C.c_int, [_vp, C.c_int, _i32p, _i32p, _i32p, _f64p]),
     "jt_message": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp]),
     "jt_propagate": (C.c_int, [_vp, _i32p, _vp]),
     "jt_query": (C.c_int, [_vp, C.c_int, _i32p, _i32p, C.c_int, _f64p, _vp]),

@@ -61,7 +61,7 @@ class BatchPropagator:
     """
 
     def __init__(self, tree, clique_tables, batch, dtype="f32", mode="auto", device=0,
-                 query_vars=None):
+                 query_vars=None, net=None):
         _lib.require_device()
         import torch
 
@@ -82,10 +82,20 @@ class BatchPropagator:
         import weakref
 
         self._fin = weakref.finalize(self, _lib.lib().jt_state_destroy, h)
-        cat = f64(np.concatenate([np.asarray(t, dtype=np.float64).ravel() for t in clique_tables]))
-        if cat.size != sum(self.plan.clique_sizes):
-            raise ValueError("clique tables do not match the tree")
-        check(_lib.lib().jt_state_load(self.handle, -1, ptr(cat, C.c_double), None), "jt_state_load")
+        if clique_tables is None:
+            # base tables = CPT products, formed on the device (initialize, propagate.py:204-222)
+            if net is None:
+                raise ValueError("need clique_tables or a network (net=) to initialize from")
+            from .propagate import cpt_arrays
+
+            cl, off, vs, vals, n = cpt_arrays(tree, net)
+            check(_lib.lib().jt_state_initialize(self.handle, n, ptr(cl, C.c_int32), ptr(off, C.c_int32),
+                                                 ptr(vs, C.c_int32), ptr(vals, C.c_double)), "initialize")
+        else:
+            cat = f64(np.concatenate([np.asarray(t, dtype=np.float64).ravel() for t in clique_tables]))
+            if cat.size != sum(self.plan.clique_sizes):
+                raise ValueError("clique tables do not match the tree")
+            check(_lib.lib().jt_state_load(self.handle, -1, ptr(cat, C.c_double), None), "jt_state_load")
         self.query_vars = list(range(len(tree.cards))) if query_vars is None else list(query_vars)
         self.cards = [int(tree.cards[v]) for v in self.query_vars]
         self.cols = int(sum(self.cards))

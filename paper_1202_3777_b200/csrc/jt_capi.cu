@@ -1398,6 +1398,97 @@ extern "C" int jt_state_load(jt_state* st, int case_idx, const double* clique_co
   return JT_OK;
 }
 
+extern "C" int jt_state_initialize(jt_state* st, int n_cpts, const int32_t* cpt_clique, const int32_t* cpt_off,
+                                   const int32_t* cpt_vars, const double* cpt_values) {
+  if (!st || n_cpts < 0 || (n_cpts > 0 && (!cpt_clique || !cpt_off || !cpt_vars || !cpt_values)))
+    return JT_ERR_BAD_ARG;
+  const jt_plan* p = st->plan;
+  DevGuard g(p->device);
+  std::vector<std::vector<int>> by_clique(p->n_cliques);
+  std::vector<int64_t> val_off(n_cpts + 1, 0);
+  for (int k = 0; k < n_cpts; ++k) {
+    const int c = cpt_clique[k];
+    if (c < 0 || c >= p->n_cliques || cpt_off[k + 1] < cpt_off[k]) return JT_ERR_BAD_ARG;
+    int64_t n = 1;
+    for (int i = cpt_off[k]; i < cpt_off[k + 1]; ++i) {
+      const int v = cpt_vars[i];
+      if (v < 0 || v >= p->n_vars || !std::binary_search(p->cvars[c].begin(), p->cvars[c].end(), v))
+        return JT_ERR_BAD_ARG;  // NoCoveringCliqueError territory: the CPT must fit its clique
+      n *= p->cards[v];
+    }
+    val_off[k + 1] = val_off[k] + n;
+    by_clique[c].push_back(k);
+  }
+  std::vector<InitClique> cl(p->n_cliques);
+  std::vector<InitTerm> terms;
+  std::vector<int64_t> vdesc;
+  int64_t max_size = 1;
+  for (int c = 0; c < p->n_cliques; ++c) {
+    const auto& cv = p->cvars[c];
+    std::vector<int64_t> cstride(cv.size(), 1);
+    for (int i = (int)cv.size() - 2; i >= 0; --i) cstride[i] = cstride[i + 1] * p->cards[cv[i + 1]];
+    cl[c].off = st->boff[c];
+    cl[c].size = p->csize[c];
+    cl[c].first_term = (int)terms.size();
+    cl[c].n_terms = (int)by_clique[c].size();
+    max_size = std::max(max_size, p->csize[c]);
+    for (int k : by_clique[c]) {
+      InitTerm t;
+      t.cpt_off = val_off[k];
+      t.first_var = (int)(vdesc.size() / 3);
+      t.nv = cpt_off[k + 1] - cpt_off[k];
+      int64_t ts = 1;
+      std::vector<int64_t> tstr(t.nv);
+      for (int i = t.nv - 1; i >= 0; --i) {
+        tstr[i] = ts;
+        ts *= p->cards[cpt_vars[cpt_off[k] + i]];
+      }
+      for (int i = 0; i < t.nv; ++i) {
+        const int v = cpt_vars[cpt_off[k] + i];
+        const int pos = (int)(std::lower_bound(cv.begin(), cv.end(), v) - cv.begin());
+        vdesc.push_back(cstride[pos]);
+        vdesc.push_back(p->cards[v]);
+        vdesc.push_back(tstr[i]);
+      }
+      terms.push_back(t);
+    }
+  }
+  int rc = ensure_stage(st, std::max<int64_t>(val_off[n_cpts], 1));
+  if (rc) return rc;
+  cudaStream_t s = st->stream;
+  InitClique* d_cl = nullptr;
+  InitTerm* d_terms = nullptr;
+  int64_t* d_vd = nullptr;
+  auto cleanup = [&]() {
+    cudaFree(d_cl);
+    cudaFree(d_terms);
+    cudaFree(d_vd);
+  };
+  cudaError_t e = cudaMalloc(&d_cl, std::max<size_t>(cl.size(), 1) * sizeof(InitClique));
+  if (e == cudaSuccess) e = cudaMalloc(&d_terms, std::max<size_t>(terms.size(), 1) * sizeof(InitTerm));
+  if (e == cudaSuccess) e = cudaMalloc(&d_vd, std::max<size_t>(vdesc.size(), 1) * sizeof(int64_t));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_cl, cl.data(), cl.size() * sizeof(InitClique), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && !terms.empty())
+    e = cudaMemcpyAsync(d_terms, terms.data(), terms.size() * sizeof(InitTerm), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && !vdesc.empty())
+    e = cudaMemcpyAsync(d_vd, vdesc.data(), vdesc.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && val_off[n_cpts] > 0)
+    e = cudaMemcpyAsync(st->d_stage, cpt_values, val_off[n_cpts] * sizeof(double), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = launch_init(st->d_base, p->dtype, st->d_stage, d_cl, p->n_cliques, d_terms, d_vd, max_size, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cleanup();
+  if (e != cudaSuccess) {
+    last_cuda_error() = e;
+    return e == cudaErrorMemoryAllocation ? JT_ERR_OOM : JT_ERR_CUDA;
+  }
+  st->launches++;
+  // every case starts from the new base tables; separators ones, no evidence
+  rc = jt_state_reset(st, nullptr);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(s));
+  return JT_OK;
+}
+
 extern "C" int jt_state_store(jt_state* st, int case_idx, double* clique_concat, double* sep_concat) {
   if (!st || case_idx < 0 || case_idx >= st->B) return JT_ERR_BAD_ARG;
   const jt_plan* p = st->plan;

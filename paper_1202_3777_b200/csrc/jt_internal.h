@@ -93,7 +93,20 @@ struct WaveArgs {
   const int32_t* rowtab;    // row kernel inner-offset tables
 };
 
+// device initialize: one entry per clique, one term per CPT, 3 int64 per CPT variable
+// (clique stride, card, CPT stride)
+struct InitClique {
+  int64_t off, size;
+  int first_term, n_terms;
+};
+struct InitTerm {
+  int64_t cpt_off;
+  int first_var, nv;
+};
+
 // launchers (jt_kernels.cu)
+cudaError_t launch_init(void* base, int dtype, const double* cpt, const InitClique* cl, int n_cliques,
+                        const InitTerm* terms, const int64_t* vdesc, int64_t max_size, cudaStream_t s);
 cudaError_t launch_wave(int dtype, int vec, const WaveArgs& a, int grid, cudaStream_t s);
 int wave_max_ctas_per_sm(int dtype, int vec);
 cudaError_t launch_wave_row(int dtype, int vec, int lin, const WaveArgs& a, int grid, cudaStream_t s);

@@ -14,6 +14,7 @@
 //   (ratio = star/old with 0/0 = 0, nonzero/0 flagged; propagate.py:67-76).
 #include "jt_internal.h"
 #include <cfloat>
+#include <algorithm>
 
 namespace jt {
 
@@ -1164,6 +1165,38 @@ cudaError_t launch_ev_zero(void* aux, int dtype, const int32_t* obs, int n, cons
                            const int32_t* cards, int B, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   ev_zero_kernel<<<(n + 127) / 128, 128, 0, s>>>(aux, dtype, obs, n, var_off, cards, B);
+  return cudaGetLastError();
+}
+
+// ---- initialize (propagate.py:204-222): clique tables = product of assigned CPTs ----
+// One CTA row per clique (blockIdx.y); every entry decodes its digits for each
+// CPT variable (clique stride, card) and gathers the CPT value (CPT stride).
+__global__ void init_kernel(void* base, int dtype, const double* __restrict__ cpt,
+                            const InitClique* __restrict__ cl, const InitTerm* __restrict__ terms,
+                            const int64_t* __restrict__ vdesc) {
+  const InitClique c = cl[blockIdx.y];
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < c.size;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double p = 1.0;
+    for (int t = c.first_term; t < c.first_term + c.n_terms; ++t) {
+      const InitTerm tm = terms[t];
+      int64_t idx = 0;
+      for (int v = 0; v < tm.nv; ++v) {
+        const int64_t* d = vdesc + 3 * (tm.first_var + v);
+        idx += ((e / d[0]) % d[1]) * d[2];
+      }
+      p *= cpt[tm.cpt_off + idx];
+    }
+    if (dtype == 0) ((float*)base)[c.off + e] = (float)p;
+    else ((double*)base)[c.off + e] = p;
+  }
+}
+
+cudaError_t launch_init(void* base, int dtype, const double* cpt, const InitClique* cl, int n_cliques,
+                        const InitTerm* terms, const int64_t* vdesc, int64_t max_size, cudaStream_t s) {
+  if (n_cliques == 0) return cudaSuccess;
+  const unsigned gx = (unsigned)std::min<int64_t>((max_size + 255) / 256, 1024);
+  init_kernel<<<dim3(gx, n_cliques), 256, 0, s>>>(base, dtype, cpt, cl, terms, vdesc);
   return cudaGetLastError();
 }
 

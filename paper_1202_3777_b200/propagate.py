@@ -311,34 +311,38 @@ def _load(state, tables):
     check(_lib.lib().jt_state_load(state.handle, -1, ptr(cat, C.c_double), None), "jt_state_load")
 
 
-def initialize(tree, net, mappings=None, engine=None) -> PropagationState:
-    """All-ones cliques, each CPT multiplied into its assigned clique
-    (propagate.py:204-222).  The CPT products are formed on the host (input
-    preparation, not the propagation path) and uploaded once."""
-    if mappings is None:
-        mappings = build_mapping_tables(tree, layout=FLAT)
-    tables = [np.ones(_scope_size(c.scope)) for c in tree.cliques]
+def cpt_arrays(tree, net):
+    """The network's CPTs as jt_state_initialize arguments: owning clique
+    (tree.cpt_assignment, propagate.py:212-217), variables in the table's own
+    axis order, values concatenated."""
+    cl, off, vs, vals = [], [0], [], []
     for cpt in net.cpts:
         cid = tree.cpt_assignment.get(cpt.child)
         if cid is None:
             raise NoCoveringCliqueError(f"no clique assigned for the CPT of variable {cpt.child}")
-        _multiply_into(tree.cliques[cid].scope, tables[cid], cpt.table.scope, cpt.table.values)
+        scope = cpt.table.scope
+        members = set(tree.cliques[cid].scope.ids)
+        if not set(scope.ids) <= members:
+            raise NoCoveringCliqueError(f"clique {cid} does not cover the CPT of variable {cpt.child}")
+        cl.append(cid)
+        vs.extend(int(v) for v in scope.ids)
+        off.append(len(vs))
+        vals.append(np.ascontiguousarray(cpt.table.values, dtype=np.float64).ravel())
+    values = np.concatenate(vals) if vals else np.zeros(1)
+    return i32(cl or [0]), i32(off), i32(vs or [0]), f64(values), len(cl)
+
+
+def initialize(tree, net, mappings=None, engine=None) -> PropagationState:
+    """All-ones cliques, each CPT multiplied into its assigned clique
+    (propagate.py:204-222).  The products are formed on the device
+    (jt_state_initialize): only the CPTs cross PCIe."""
+    if mappings is None:
+        mappings = build_mapping_tables(tree, layout=FLAT)
+    cl, off, vs, vals, n = cpt_arrays(tree, net)
     state = PropagationState(tree, mappings, _as_engine(engine))
-    _load(state, tables)
+    check(_lib.lib().jt_state_initialize(state.handle, n, ptr(cl, C.c_int32), ptr(off, C.c_int32),
+                                         ptr(vs, C.c_int32), ptr(vals, C.c_double)), "initialize")
     return state
-
-
-def _multiply_into(outer, values, inner, factor):
-    """target[t] *= factor[projection of t onto the factor scope] (potential.py:160-167)."""
-    size = _scope_size(outer)
-    idx = np.arange(size, dtype=np.int64)
-    strides = Scope(outer.ids, outer.cards).strides()
-    istr = Scope(inner.ids, inner.cards).strides()
-    proj = np.zeros(size, dtype=np.int64)
-    for pos, var in enumerate(inner.ids):
-        p = list(outer.ids).index(var)
-        proj += ((idx // strides[p]) % outer.cards[p]) * istr[pos]
-    values *= np.asarray(factor, dtype=np.float64)[proj]
 
 
 def from_potentials(tree, clique_tables, mappings=None, engine=None) -> PropagationState:

@@ -86,3 +86,48 @@ def _skip_gpu_without_device(request):
         import torch
         if not torch.cuda.is_available():
             pytest.skip("no CUDA device")
+
+
+class _Obj:
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+
+class GoldenNetwork:
+    """Duck-typed stand-in for the reference BayesianNetwork (model.py:64-120):
+    `variables[v].name/.cardinality`, `cpts[k].child/.table.scope/.table.values`,
+    `id_of(name)`, `len()` — rebuilt from tests/golden/corpus.json so GPU tests
+    need no reference install."""
+
+    def __init__(self, doc, arrays, k):
+        self.variables = [_Obj(id=i, name=n, cardinality=c) for i, (n, c) in enumerate(doc["variables"])]
+        cards = [c for _, c in doc["variables"]]
+        self.cpts = []
+        for child, ids in doc["cpts"]:
+            scope = _Obj(ids=tuple(ids), cards=tuple(cards[v] for v in ids))
+            self.cpts.append(_Obj(child=child, table=_Obj(scope=scope, values=arrays[f"cpt{k}_{child}"])))
+        self._by_name = {v.name: v.id for v in self.variables}
+
+    def __len__(self):
+        return len(self.variables)
+
+    def id_of(self, name):
+        return self._by_name[name]
+
+
+def load_corpus_networks():
+    """[(name, tree, network, init_tables_concat, estimator_rows, estimator_posteriors)]."""
+    with open(os.path.join(GOLDEN, "corpus.json")) as f:
+        doc = json.load(f)
+    data = np.load(os.path.join(GOLDEN, "corpus.npz"))
+    out = []
+    for k, entry in enumerate(doc):
+        tree = tree_from_json(entry["tree"])
+        net = GoldenNetwork(entry["network"], data, k)
+        est = data[f"est{k}"]
+        rows = [dict() for _ in range(est.shape[0])]
+        for (v, x), r in zip(data[f"estX{k}"], data[f"estXrow{k}"]):
+            if r >= 0:
+                rows[int(r)][int(v)] = int(x)
+        out.append((entry["name"], tree, net, data[f"init{k}"], rows, est))
+    return out

@@ -117,7 +117,19 @@ def corpus():
         apply_evidence(st, {0: 0})
         belief_propagation(st)
         post = np.concatenate([query_marginal(st, v).values for v in range(len(net))])
-        doc.append({"name": name, "tree": tree_json(compiled.tree)})
+        doc.append({"name": name, "tree": tree_json(compiled.tree),
+                    "network": {"variables": [[v.name, v.cardinality] for v in net.variables],
+                                "cpts": [[c.child, list(c.table.scope.ids)] for c in net.cpts]}})
+        for c in net.cpts:
+            arrays[f"cpt{k}_{c.child}"] = np.asarray(c.table.values, dtype=np.float64)
+        # reference estimator (estimator.py:118-134), target = last variable, per-row loop
+        from jtprop.estimator import JunctionTreeEngine
+
+        rows = [{}, {0: 0}] + ([{len(net) - 2: 1}] if len(net) > 2 and net.variables[len(net) - 2].cardinality > 1 else [])
+        est = JunctionTreeEngine(target=net.variables[-1].name).fit(net)
+        arrays[f"est{k}"] = est.predict_proba(rows)
+        arrays[f"estX{k}"] = np.array([[a, b] for r in rows for a, b in r.items()] or [[-1, -1]])
+        arrays[f"estXrow{k}"] = np.array([i for i, r in enumerate(rows) for _ in r.items()] or [-1])
         arrays[f"init{k}"] = init
         arrays[f"post{k}"] = post
         arrays[f"cliques{k}"] = np.concatenate(st.clique_values)
@@ -128,6 +140,9 @@ def corpus():
 
 
 if __name__ == "__main__":
+    if sys.argv[1:] == ["corpus"]:
+        corpus()
+        sys.exit(0)
     mapping_tables()
     corpus()
     for name, n in (("c1", 8), ("c2", 4), ("c4M", 2), ("c5", 8), ("c4B", 1), ("c3", 1)):

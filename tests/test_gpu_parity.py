@@ -288,3 +288,28 @@ def test_calibration_full_size_c3():
     P().check_global_consistency(st, rtol=1e-9)
     got = all_posteriors(st, len(tree.cards))
     assert rel_err(got, data["post0"]) < 1e-10
+
+
+def test_device_initialize_matches_reference():  # initialize, propagate.py:204-222
+    from conftest import load_corpus_networks
+
+    for name, tree, net, init, _, _ in load_corpus_networks():
+        for dtype, tol in (("f64", 1e-14), ("f32", 1e-6)):
+            st = P().initialize(tree, net, engine=P().CudaEngine(dtype=dtype))
+            got = np.concatenate(st.clique_values)
+            assert rel_err(got, init) < tol, (name, dtype)
+            assert all(np.all(s == 1.0) for s in st.sep_values), name
+
+
+def test_estimator_matches_reference_predict_proba():  # estimator.py:118-134
+    from conftest import load_corpus_networks
+    from paper_1202_3777_b200.estimator import JunctionTreeEngine
+
+    for name, tree, net, _, rows, want in load_corpus_networks():
+        est = JunctionTreeEngine(target=net.variables[-1].name, batch=4).fit_compiled(tree, net)
+        got = est.predict_proba(rows)
+        assert got.shape == want.shape
+        assert rel_err(got, want) < 1e-10, name
+        assert np.array_equal(est.predict(rows), want.argmax(axis=1))
+        q = est.query(evidence=rows[-1])
+        assert rel_err(q[net.variables[-1].name], want[-1]) < 1e-10, name
