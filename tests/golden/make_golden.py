@@ -134,6 +134,18 @@ def corpus():
         arrays[f"post{k}"] = post
         arrays[f"cliques{k}"] = np.concatenate(st.clique_values)
         arrays[f"seps{k}"] = np.concatenate(st.sep_values) if st.sep_values else np.zeros(0)
+    # reference tree dumps (io.py:443-474) of two corpus networks: with the
+    # network embedded, and with mapping tables in the interleaved layout
+    from jtprop.io import serialize_tree
+
+    nets = corpus_networks()
+    for k, kw in ((3, {"net": True}), (5, {"net": True, "include_mappings": True, "layout": "interleaved"})):
+        name, net = nets[k]
+        compiled = compile_network(net, layout=kw.get("layout", "flat"))
+        text = serialize_tree(compiled.tree, compiled.mappings, net if kw.get("net") else None,
+                              include_mappings=kw.get("include_mappings", False))
+        with open(os.path.join(HERE, f"tree_dump{k}.jt.json"), "w") as f:
+            f.write(text)
     np.savez_compressed(os.path.join(HERE, "corpus.npz"), **arrays)
     with open(os.path.join(HERE, "corpus.json"), "w") as f:
         json.dump(doc, f)

@@ -313,3 +313,22 @@ def test_estimator_matches_reference_predict_proba():  # estimator.py:118-134
         assert np.array_equal(est.predict(rows), want.argmax(axis=1))
         q = est.query(evidence=rows[-1])
         assert rel_err(q[net.variables[-1].name], want[-1]) < 1e-10, name
+
+
+def test_tree_dump_to_device_plan():  # §8f row 4: .jt.json → cached device plan
+    import os
+
+    from conftest import GOLDEN, load_corpus
+    from paper_1202_3777_b200 import io
+
+    corpus = load_corpus()
+    for k in (3, 5):
+        path = os.path.join(GOLDEN, f"tree_dump{k}.jt.json")
+        plan, tree, net = io.load_plan(path, "f64")
+        assert io.load_plan(path, "f64")[0] is plan  # cached
+        st = P().initialize(tree, net)
+        assert st.plan is plan
+        P().apply_evidence(st, {0: 0})
+        P().belief_propagation(st)
+        got = all_posteriors(st, len(tree.cards))
+        assert rel_err(got, corpus[k][3]) < 1e-10, k
