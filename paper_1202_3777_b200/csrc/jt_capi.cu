@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <iterator>
 #include <cstdlib>
 #include <array>
 #include <cstring>
@@ -169,6 +170,10 @@ struct LaunchGrp {  // one kernel launch of a wave
   int grid = 0;
   int n_items = 0;
   int64_t item_off = 0;  // relative to the wave's item_base
+  // kind 3 (contraction): CPass range and unit count
+  int64_t cpass_off = 0;
+  int n_cpasses = 0;
+  int64_t n_units = 0;
 };
 
 struct WaveRt {
@@ -187,6 +192,9 @@ struct Program {
   int32_t* d_rowtab = nullptr;
   double* d_part = nullptr;
   int* d_cnt = nullptr;
+  CPass* d_cpass = nullptr;
+  int32_t* d_ctab = nullptr;
+  void* d_w = nullptr;
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t gstream = nullptr;
   int runs = 0;
@@ -201,6 +209,9 @@ struct Program {
     cudaFree(d_rowtab);
     cudaFree(d_part);
     cudaFree(d_cnt);
+    cudaFree(d_cpass);
+    cudaFree(d_ctab);
+    cudaFree(d_w);
   }
 };
 
@@ -246,6 +257,9 @@ struct jt_state {
   // propagation writes the collect messages into the current table and the
   // distribute results into the other one, then the roles swap.
   bool sep_in_y = false;
+  // host copy of the base replica (shared-base states): contraction passes
+  // precompute W = base summed over the variables no factor or output sees
+  std::vector<double> h_base;
   ~jt_state() {
     programs.clear();
     cudaFree(d_clique);
@@ -826,7 +840,173 @@ struct HostProgram {
   std::vector<int32_t> rowtab;
   std::vector<int> pass_clique;
   int64_t n_part = 0, n_cnt = 0;
+  std::vector<CPass> cpasses;
+  std::vector<int32_t> ctab;
+  std::vector<double> w;
+  std::vector<int> cpass_clique;
 };
+
+// ----------------------------------------------------- contraction passes --
+static bool contract_eligible(const jt_state* st, const PassSpec& ps) {
+  return st->mode == JT_SHARED_BASE && st->B > 1 && st->B % CVEC == 0 && !st->h_base.empty() &&
+         ps.src_arena == A_BASE && !ps.write && ps.scope.empty() && ps.out_kind != OUT_NONE &&
+         !getenv("JT_NO_CONTRACT");
+}
+
+// Mixed-radix enumeration of a var group: offsets (per tensor) of every index.
+static std::vector<int64_t> group_offsets(const jt_plan* p, const std::vector<int>& vars,
+                                          const std::vector<int64_t>& stride_of_var) {
+  std::vector<int64_t> out{0};
+  for (size_t a = 0; a < vars.size(); ++a) {
+    const int c = p->cards[vars[a]];
+    std::vector<int64_t> nx;
+    nx.reserve(out.size() * c);
+    for (int64_t o : out)
+      for (int d = 0; d < c; ++d) nx.push_back(o + d * stride_of_var[a]);
+    out.swap(nx);
+  }
+  return out;
+}
+
+static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram& hp, CPass& cp) {
+  const jt_plan* p = st->plan;
+  const int64_t B = st->B;
+  const auto& C = p->cvars[ps.clique];
+  const auto& s = ps.out.vars;
+  auto subset = [](const std::vector<int>& a, const std::vector<int>& b) {
+    return std::includes(b.begin(), b.end(), a.begin(), a.end());
+  };
+  std::vector<const Tensor*> G, E;
+  for (auto& f : ps.factors) (subset(f.vars, s) ? E : G).push_back(&f);
+  if ((int)G.size() > CMAXG || (int)E.size() > MAXF) return JT_ERR_UNSUPPORTED;
+  std::vector<int> U;
+  for (auto* f : G) U.insert(U.end(), f->vars.begin(), f->vars.end());
+  std::sort(U.begin(), U.end());
+  U.erase(std::unique(U.begin(), U.end()), U.end());
+  std::vector<int> I, S, K;
+  std::set_intersection(s.begin(), s.end(), U.begin(), U.end(), std::back_inserter(I));
+  std::set_difference(s.begin(), s.end(), U.begin(), U.end(), std::back_inserter(S));
+  std::set_difference(U.begin(), U.end(), s.begin(), s.end(), std::back_inserter(K));
+  const int nG = (int)G.size(), nE = (int)E.size();
+  auto strides = [&](const std::vector<int>& vars, const Tensor& t) {
+    std::vector<int64_t> o;
+    for (int v : vars) o.push_back(tensor_stride(p, t, v, B));
+    return o;
+  };
+  // per-group offset lists of every tensor
+  std::vector<std::vector<int64_t>> gI(nG), gK(nG), eI(nE), eS(nE);
+  for (int g = 0; g < nG; ++g) {
+    gI[g] = group_offsets(p, I, strides(I, *G[g]));
+    gK[g] = group_offsets(p, K, strides(K, *G[g]));
+  }
+  for (int e = 0; e < nE; ++e) {
+    eI[e] = group_offsets(p, I, strides(I, *E[e]));
+    eS[e] = group_offsets(p, S, strides(S, *E[e]));
+  }
+  const std::vector<int64_t> oI = group_offsets(p, I, strides(I, ps.out));
+  const std::vector<int64_t> oS = group_offsets(p, S, strides(S, ps.out));
+  const int64_t nI = (int64_t)oI.size(), nS = (int64_t)oS.size();
+  const int64_t nK = (int64_t)group_offsets(p, K, std::vector<int64_t>(K.size(), 0)).size();
+  if (nI * nK * (nS + 3) > (int64_t)1 << 31) return JT_ERR_UNSUPPORTED;
+  auto fits = [](const std::vector<int64_t>& v) {
+    for (int64_t x : v)
+      if (x > INT32_MAX) return false;
+    return true;
+  };
+  for (int g = 0; g < nG; ++g)
+    if (!fits(gI[g]) || !fits(gK[g])) return JT_ERR_UNSUPPORTED;
+  for (int e = 0; e < nE; ++e)
+    if (!fits(eI[e]) || !fits(eS[e])) return JT_ERR_UNSUPPORTED;
+  if (!fits(oI) || !fits(oS)) return JT_ERR_UNSUPPORTED;
+  // W[i][k][s'] = Σ_R base: walk the clique once, odometer over its variables
+  // rows of S' padded to 4 (one vector load per k); nS == 1 uses the row-per-i kernel
+  const bool rowi = nS == 1;
+  const int64_t nSp = rowi ? 1 : (nS + 3) & ~int64_t(3);
+  const int64_t w0 = (int64_t)hp.w.size();
+  hp.w.resize(w0 + nI * nK * nSp, 0.0);
+  {
+    // per clique position: contribution to i, k, s' linear indices (R: none)
+    std::vector<int64_t> ci(C.size(), 0), ck(C.size(), 0), cs(C.size(), 0);
+    auto lin = [&](const std::vector<int>& grp, int v) {
+      int64_t st_ = 1;
+      bool in = false;
+      for (int a = (int)grp.size() - 1; a >= 0; --a) {
+        if (grp[a] == v) {
+          in = true;
+          break;
+        }
+        st_ *= p->cards[grp[a]];
+      }
+      return in ? st_ : 0;
+    };
+    for (size_t a = 0; a < C.size(); ++a) {
+      ci[a] = lin(I, C[a]);
+      ck[a] = lin(K, C[a]);
+      cs[a] = lin(S, C[a]);
+    }
+    const double* src = st->h_base.data() + st->boff[ps.clique];
+    const int64_t n = p->csize[ps.clique];
+    std::vector<int> dig(C.size(), 0);
+    int64_t xi = 0, xk = 0, xs = 0;
+    double* W = hp.w.data() + w0;
+    for (int64_t e = 0; e < n; ++e) {
+      W[(xi * nK + xk) * nSp + xs] += src[e];
+      for (int a = (int)C.size() - 1; a >= 0; --a) {
+        xi += ci[a];
+        xk += ck[a];
+        xs += cs[a];
+        if (++dig[a] < p->cards[C[a]]) break;
+        const int64_t c = p->cards[C[a]];
+        xi -= ci[a] * c;
+        xk -= ck[a] * c;
+        xs -= cs[a] * c;
+        dig[a] = 0;
+      }
+    }
+  }
+  std::memset(&cp, 0, sizeof(cp));
+  cp.w_off = w0;
+  cp.ti_off = (int64_t)hp.ctab.size();
+  for (int64_t i = 0; i < nI; ++i) {
+    for (int g = 0; g < nG; ++g) hp.ctab.push_back((int32_t)gI[g][i]);
+    for (int e = 0; e < nE; ++e) hp.ctab.push_back((int32_t)eI[e][i]);
+    hp.ctab.push_back((int32_t)oI[i]);
+  }
+  cp.tk_off = (int64_t)hp.ctab.size();
+  for (int64_t k = 0; k < nK; ++k)
+    for (int g = 0; g < nG; ++g) hp.ctab.push_back((int32_t)gK[g][k]);
+  cp.ts_off = (int64_t)hp.ctab.size();
+  for (int64_t x = 0; x < nS; ++x) {
+    for (int e = 0; e < nE; ++e) hp.ctab.push_back((int32_t)eS[e][x]);
+    hp.ctab.push_back((int32_t)oS[x]);
+  }
+  cp.nI = (int)nI;
+  cp.nS = (int)nS;
+  cp.nK = (int)nK;
+  cp.nG = nG;
+  cp.nE = nE;
+  cp.rowi = rowi ? 1 : 0;
+  cp.nT = rowi ? (int)((nI + TMC - 1) / TMC) : (int)((nS + TMC - 1) / TMC);
+  cp.nBC = (int)((B + 32 * CVEC - 1) / (32 * CVEC));
+  // a unit walks a share of the case chunks of its (i, row tile): all of them for
+  // short sums (amortises the unit's setup), one per unit for long ones (parallelism)
+  cp.nCG = nK >= 32 ? cp.nBC : nK >= 8 ? std::min(4, cp.nBC) : 1;
+  cp.n_units = (rowi ? 1 : nI) * cp.nT * cp.nCG;
+  // too few units to fill the GPU (e.g. a posterior over a long factor row):
+  // the chunked thread-owned/general passes parallelise over the clique instead
+  if (cp.n_units < (int64_t)st->num_sms * 8) {
+    hp.w.resize(w0);
+    hp.ctab.resize(cp.ti_off);
+    return JT_ERR_UNSUPPORTED;
+  }
+  cp.out_kind = ps.out_kind;
+  cp.out_off = ps.out.off;
+  cp.ratio_off = ps.ratio_off;
+  cp.out2_off = ps.out2_off;
+  for (int g = 0; g < nG; ++g) cp.gfac_off[g] = G[g]->off;
+  for (int e = 0; e < nE; ++e) cp.efac_off[e] = E[e]->off;
+  return JT_OK;
+}
 
 static int compile_program(const jt_state* st, const std::vector<std::vector<PassSpec>>& waves, HostProgram& hp,
                            int occ_override = 0) {
@@ -855,7 +1035,19 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
       wave_vec = std::min(wave_vec, pass_max_vec(st, ps));
     }
     const bool small_wave = wave_el < SMALL_WAVE_ELEMS;
+    // contraction passes, split by accumulator kind (fp32 sums over > CKF terms fold into fp64)
+    std::vector<CPass> cps[4];
+    std::vector<int> cpc[4];
     for (auto& ps : w) {
+      if (contract_eligible(st, ps)) {
+        CPass cp;
+        if (compile_contract(st, ps, hp, cp) == JT_OK) {
+          const int key = (st->esz == 4 && cp.nK > CKF ? 1 : 0) + 2 * cp.rowi;
+          cps[key].push_back(cp);
+          cpc[key].push_back(ps.clique);
+          continue;
+        }
+      }
       BuiltPass bp;
       const int local = (int)(passes.size() - rt.pass_base);
       const int vec = small_wave ? wave_vec : pass_max_vec(st, ps);
@@ -911,6 +1103,26 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
       items.insert(items.end(), g.second.begin(), g.second.end());
       rt.groups.push_back(lg);
     }
+    for (int key = 0; key < 4; ++key) {
+      const int fold = key & 1;
+      if (cps[key].empty()) continue;
+      LaunchGrp cg;
+      cg.kind = 3;
+      cg.lm = fold;
+      cg.m = key >> 1;
+      cg.cpass_off = (int64_t)hp.cpasses.size();
+      for (size_t q = 0; q < cps[key].size(); ++q) {
+        CPass cp = cps[key][q];
+        cp.unit0 = cg.n_units;
+        cg.n_units += cp.n_units;
+        cg.n_cpasses++;
+        hp.cpasses.push_back(cp);
+        hp.cpass_clique.push_back(cpc[key][q]);
+      }
+      const int occ = occ_override ? occ_override : contract_max_ctas_per_sm(st->plan->dtype, fold);
+      cg.grid = (int)std::min<int64_t>((cg.n_units + NT / 32 - 1) / (NT / 32), (int64_t)occ * st->num_sms);
+      rt.groups.push_back(cg);
+    }
     rt.n_items = (int)(items.size() - rt.item_base);
     hp.waves.push_back(rt);
   }
@@ -944,6 +1156,20 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
   if ((rc = up(&prog->d_bins, bins))) return rc;
   if ((rc = up(&prog->d_blk32, hp.blk32))) return rc;
   if ((rc = up(&prog->d_rowtab, hp.rowtab))) return rc;
+  if ((rc = up(&prog->d_cpass, hp.cpasses))) return rc;
+  if ((rc = up(&prog->d_ctab, hp.ctab))) return rc;
+  {
+    const size_t n = std::max<size_t>(hp.w.size(), 1);
+    CK(cudaMalloc(&prog->d_w, n * st->esz));
+    if (!hp.w.empty()) {
+      if (st->esz == 8) {
+        CK(cudaMemcpy(prog->d_w, hp.w.data(), hp.w.size() * 8, cudaMemcpyHostToDevice));
+      } else {
+        std::vector<float> wf(hp.w.begin(), hp.w.end());
+        CK(cudaMemcpy(prog->d_w, wf.data(), wf.size() * 4, cudaMemcpyHostToDevice));
+      }
+    }
+  }
   CK(cudaMalloc(&prog->d_part, std::max<int64_t>(n_part, 1) * sizeof(double)));
   CK(cudaMalloc(&prog->d_cnt, std::max<int64_t>(n_cnt, 1) * sizeof(int)));
   CK(cudaMemset(prog->d_cnt, 0, std::max<int64_t>(n_cnt, 1) * sizeof(int)));
@@ -952,6 +1178,21 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
 }
 
 static int launch_group(jt_state* st, const Program* pr, const WaveRt& w, const LaunchGrp& g, cudaStream_t s) {
+  if (g.kind == 3) {
+    CArgs c;
+    c.w = pr->d_w;
+    c.aux = st->d_aux;
+    c.qout = st->d_qout;
+    c.err = st->d_err;
+    c.tab = pr->d_ctab;
+    c.passes = pr->d_cpass + g.cpass_off;
+    c.n_passes = g.n_cpasses;
+    c.n_units = g.n_units;
+    c.B = st->B;
+    CK(launch_contract(st->plan->dtype, g.lm, g.m, c, g.grid, s));
+    st->launches++;
+    return JT_OK;
+  }
   WaveArgs a;
   a.clique = st->d_clique;
   a.base = st->d_base;
@@ -1363,6 +1604,16 @@ extern "C" int jt_state_load(jt_state* st, int case_idx, const double* clique_co
   const int64_t B = st->B;
   if ((rc = ensure_seps(st, s))) return rc;
   st->fresh = (case_idx < 0 && !sep_concat) || (st->fresh && !sep_concat);
+  if (clique_concat && case_idx < 0 && shared) {
+    // host copy of the base for contraction passes; programs built on the old base are stale
+    st->h_base.assign(st->n_base, 1.0);
+    int64_t o = 0;
+    for (int c = 0; c < p->n_cliques; ++c) {
+      std::copy(clique_concat + o, clique_concat + o + p->csize[c], st->h_base.begin() + st->boff[c]);
+      o += p->csize[c];
+    }
+    st->programs.clear();
+  }
   if (clique_concat) {
     CK(cudaMemcpyAsync(st->d_stage, clique_concat, tot_c * 8, cudaMemcpyHostToDevice, s));
     int64_t o = 0;
@@ -1482,6 +1733,14 @@ extern "C" int jt_state_initialize(jt_state* st, int n_cpts, const int32_t* cpt_
     return e == cudaErrorMemoryAllocation ? JT_ERR_OOM : JT_ERR_CUDA;
   }
   st->launches++;
+  if (st->mode == JT_SHARED_BASE) {  // host copy of the new base (contraction passes)
+    std::vector<char> raw(st->n_base * st->esz);
+    CK(cudaMemcpy(raw.data(), st->d_base, raw.size(), cudaMemcpyDeviceToHost));
+    st->h_base.resize(st->n_base);
+    for (int64_t i = 0; i < st->n_base; ++i)
+      st->h_base[i] = st->esz == 8 ? ((const double*)raw.data())[i] : (double)((const float*)raw.data())[i];
+    st->programs.clear();
+  }
   // every case starts from the new base tables; separators ones, no evidence
   rc = jt_state_reset(st, nullptr);
   if (rc) return rc;
@@ -2079,6 +2338,7 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
   st.mode = mode;
   st.num_sms = num_sms > 0 ? num_sms : 148;
   layout_state(&st);
+  if (mode == JT_SHARED_BASE) st.h_base.assign(st.n_base, 1.0);  // W values do not matter here
   std::vector<int> qv;
   if (kind == 1) {
     for (int v = 0; v < plan->n_vars; ++v) {
@@ -2094,13 +2354,43 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
   if (rc) return rc;
   std::string out;
   char line[512];
+  {
+    // compulsory HBM traffic per wave: every factor tensor read once, outputs
+    // written once (separator updates also read the old values and write ratios)
+    double tot = 0.0;
+    for (size_t w = 0; w < waves.size(); ++w) {
+      double bytes = 0.0;
+      for (auto& ps : waves[w]) {
+        auto tsize = [&](const Tensor& t) {
+          double n = t.batch ? (double)st.B : 1.0;
+          for (int v : t.vars) n *= plan->cards[v];
+          return n;
+        };
+        for (auto& f : ps.factors) bytes += tsize(f) * st.esz;
+        if (ps.out_kind == OUT_RAW) bytes += tsize(ps.out) * 8;
+        else if (ps.out_kind == OUT_SEP_FRESH) bytes += tsize(ps.out) * st.esz;
+        else if (ps.out_kind != OUT_NONE) bytes += tsize(ps.out) * st.esz * 3;
+        const double csz = (double)plan->csize[ps.clique] * (ps.src_arena == A_BASE ? 1.0 : (double)st.B);
+        if (ps.scope.empty()) bytes += csz * st.esz * (ps.write ? 2 : 1);
+      }
+      tot += bytes;
+      snprintf(line, sizeof line, "compulsory wave %zu MB %.1f\n", w, bytes / 1e6);
+      out += line;
+    }
+    snprintf(line, sizeof line, "compulsory total MB %.1f\n", tot / 1e6);
+    out += line;
+  }
   for (size_t w = 0; w < hp.waves.size(); ++w) {
     const WaveRt& rt = hp.waves[w];
     snprintf(line, sizeof line, "wave %zu items %d launches %zu:", w, rt.n_items, rt.groups.size());
     out += line;
     for (const LaunchGrp& g : rt.groups) {
-      snprintf(line, sizeof line, " [%s vec %d items %d grid %d]", g.kind == 1 ? "own" : g.kind == 2 ? "row" : "gen",
-               g.vec, g.n_items, g.grid);
+      if (g.kind == 3)
+        snprintf(line, sizeof line, " [contract passes %d units %lld grid %d]", g.n_cpasses, (long long)g.n_units,
+                 g.grid);
+      else
+        snprintf(line, sizeof line, " [%s vec %d items %d grid %d]", g.kind == 1 ? "own" : g.kind == 2 ? "row" : "gen",
+                 g.vec, g.n_items, g.grid);
       out += line;
     }
     out += "\n";
@@ -2121,6 +2411,15 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
                (long long)n_items, d.ndi, d.own, d.own_m, d.row, d.gpi, d.flush_fac,
                (long long)(d.n_chunks > 1 && d.out_kind ? n_out * d.n_chunks * d.n_in : 0));
       out += line;
+    }
+    for (const LaunchGrp& g : rt.groups) {
+      if (g.kind != 3) continue;
+      for (int q = 0; q < g.n_cpasses; ++q) {
+        const CPass& c = hp.cpasses[g.cpass_off + q];
+        snprintf(line, sizeof line, "  contract clique %d out %d nI %d nS %d nK %d nG %d nE %d units %lld\n",
+                 hp.cpass_clique[g.cpass_off + q], c.out_kind, c.nI, c.nS, c.nK, c.nG, c.nE, (long long)c.n_units);
+        out += line;
+      }
     }
   }
   const int64_t n = std::min<int64_t>((int64_t)out.size(), len - 1);

@@ -93,6 +93,46 @@ struct WaveArgs {
   const int32_t* rowtab;    // row kernel inner-offset tables
 };
 
+// Contraction pass (shared-base batches): the base replica never
+// changes, so a pass over clique c with factors G (batched, over vars U), output
+// over vars s and epilogue factors E (vars within s) is
+//   out[I, S', b] = Π_E E[., b] · Σ_{K'} W[I, K', S'] · Π_G F_g[I, K', b]
+// with I = s∩U, S' = s∖U, K' = U∖s and W = base summed over R = c∖(s∪U),
+// precomputed on the host.  A warp owns one (i, row tile of TMC rows of S')
+// unit and walks all cases.
+constexpr int TMC = 4;     // W rows per warp unit
+constexpr int CVEC = 4;    // B must be a multiple of this (fp32 lanes per vector; fp64 uses 2)
+constexpr int CMAXG = 4;   // factors multiplied per k (more: the pass takes the general kernels)
+struct CPass {
+  int64_t w_off;            // W arena offset, layout [nI][nK][nS]
+  int64_t ti_off;           // int32 [nI][nG + nE + 1]: G i-offsets, E i-offsets, out i-offset
+  int64_t tk_off;           // int32 [nK][nG]: G k-offsets
+  int64_t ts_off;           // int32 [nS][nE + 1]: E s-offsets, out s-offset
+  int64_t unit0;            // first global unit of this pass in its launch
+  int64_t n_units;
+  int nI, nS, nK, nG, nE, nT, nBC;
+  int nCG;                  // case-chunk groups: a unit walks chunks cg, cg + nCG, ...
+  int rowi;                 // 1: nS == 1, units are TMC consecutive i (W layout [nI][nK])
+  int out_kind;
+  int64_t out_off, ratio_off, out2_off;
+  int64_t gfac_off[MAXF];   // aux offsets of the G factors
+  int64_t efac_off[MAXF];   // aux offsets of the E factors
+};
+struct CArgs {
+  const void* w;
+  void* aux;
+  double* qout;
+  int* err;
+  const int32_t* tab;
+  const CPass* passes;
+  int n_passes;
+  int64_t n_units;
+  int B;
+};
+constexpr int CKF = 16;     // fp32 contraction sums longer than this fold into fp64
+cudaError_t launch_contract(int dtype, int fold, int rowi, const CArgs& a, int grid, cudaStream_t s);
+int contract_max_ctas_per_sm(int dtype, int fold);
+
 // device initialize: one entry per clique, one term per CPT, 3 int64 per CPT variable
 // (clique stride, card, CPT stride)
 struct InitClique {

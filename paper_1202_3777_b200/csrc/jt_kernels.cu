@@ -15,6 +15,7 @@
 #include "jt_internal.h"
 #include <cfloat>
 #include <algorithm>
+#include <type_traits>
 
 namespace jt {
 
@@ -938,6 +939,321 @@ int wave_row_max_ctas_per_sm(int dtype, int vec) {
   }
   if (vec == 2) return occ_row_t<double, 2>();
   return occ_row_t<double, 1>();
+}
+
+// ---- contraction passes (shared-base batches) ----
+// Hugin update of VEC consecutive case lanes of one output entry (element
+// offset j of case 0): the epilogue of every pass kind, written once.
+template <typename T, int VEC>
+__device__ __forceinline__ void finalize_lanes(int kind, int64_t out_off, int64_t ratio_off, int64_t out2_off,
+                                               int64_t j, const double (&star)[VEC], T* aux, double* qout,
+                                               int* err) {
+  if (kind == OUT_RAW) {
+#pragma unroll
+    for (int l = 0; l < VEC; ++l) qout[out_off + j + l] = star[l];
+    return;
+  }
+  T nw[VEC];
+  if (kind == OUT_SEP_FRESH) {
+#pragma unroll
+    for (int l = 0; l < VEC; ++l) nw[l] = (T)star[l];
+    store_vec<T, VEC>(aux + out_off + j, nw);
+    return;
+  }
+  T old[VEC], rt[VEC];
+  load_vec<T, VEC>(aux + out_off + j, old);
+  bool bad = false;
+#pragma unroll
+  for (int l = 0; l < VEC; ++l) {
+    const double o = (double)old[l];
+    if (kind == OUT_SEP_DFRESH) {
+      rt[l] = (T)(o != 0.0 ? star[l] : 0.0);
+      nw[l] = (T)(o * star[l]);
+    } else {
+      bad |= (o == 0.0 && star[l] != 0.0);
+      rt[l] = (T)(o != 0.0 ? star[l] / o : 0.0);
+      nw[l] = (T)star[l];
+    }
+  }
+  if (bad) atomicOr(err, EB_INCONSISTENT);
+  store_vec<T, VEC>(aux + ratio_off + j, rt);
+  store_vec<T, VEC>(aux + (out2_off >= 0 ? out2_off : out_off) + j, nw);
+}
+
+// One warp per unit (i, row tile of TMC rows of S'); the warp walks every chunk
+// of 32*VEC cases, each lane owning VEC consecutive cases.  Per k: the product
+// of the G factor rows (VEC-vectors, coalesced across the warp) times TMC rows
+// of W (one vector load; W rows padded to a multiple of 4) into TMC x VEC
+// accumulators — TMC FMAs per factor load.  k is unrolled by KU so KU x nG
+// loads are in flight per lane.  fp32 sums run in fp32 for KF consecutive k and
+// are folded into fp64.
+template <typename T> struct CTraits;
+template <> struct CTraits<float> { static constexpr int VEC = 4; };
+template <> struct CTraits<double> { static constexpr int VEC = 2; };
+
+template <typename T>
+__device__ __forceinline__ void load_w4(const T* p, T (&w)[TMC]) {
+  if constexpr (sizeof(T) == 4) {
+    const float4 x = __ldg(reinterpret_cast<const float4*>(p));
+    w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
+  } else {
+    const double2 x = __ldg(reinterpret_cast<const double2*>(p));
+    const double2 y = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    w[0] = x.x; w[1] = x.y; w[2] = y.x; w[3] = y.y;
+  }
+}
+
+// FOLD: fp32 with nK > KF — partial sums of KF terms are folded into fp64.
+// Otherwise the sums stay in T (fp64, or fp32 over at most KF terms): fewer
+// registers, three CTAs per SM.
+template <typename T, bool FOLD>
+__global__ void __launch_bounds__(NT, FOLD ? 2 : 3) contract_kernel(const CArgs a) {
+  constexpr int VEC = CTraits<T>::VEC;
+  constexpr int KU = FOLD ? 4 : 2;
+  constexpr int KF = 16;
+  static_assert(TMC == 4, "W rows are loaded as one 4-vector");
+  const T* __restrict__ W = reinterpret_cast<const T*>(a.w);
+  T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
+  const T* __restrict__ aux_c = aux;
+  const int lane = threadIdx.x & 31;
+  const int n_warps = gridDim.x * (NT / 32);
+  int pi = 0;
+  for (int64_t u = blockIdx.x * (NT / 32) + (threadIdx.x >> 5); u < a.n_units; u += n_warps) {
+    while (pi + 1 < a.n_passes && u >= a.passes[pi + 1].unit0) ++pi;
+    while (pi > 0 && u < a.passes[pi].unit0) --pi;
+    const CPass* __restrict__ P = a.passes + pi;
+    const int64_t ul = u - P->unit0;
+    const int nT = P->nT, nCG = P->nCG;
+    const int cg = (int)(ul % nCG);
+    const int t = (int)((ul / nCG) % nT);
+    const int64_t i = ul / ((int64_t)nCG * nT);
+    const int nS = P->nS, nK = P->nK, nG = P->nG, nE = P->nE;
+    const int nSp = (nS + 3) & ~3;
+    const int bstep = 32 * VEC * nCG;  // case chunks cg, cg + nCG, ... of this unit
+    const int s0 = t * TMC;
+    const int rows = min(TMC, nS - s0);
+    const int32_t* __restrict__ ti = a.tab + P->ti_off + i * (nG + nE + 1);
+    const int32_t* __restrict__ tk = a.tab + P->tk_off;
+    const int32_t* __restrict__ ts = a.tab + P->ts_off;
+    const T* __restrict__ wrow = W + P->w_off + i * (int64_t)nK * nSp + s0;
+    const int32_t oI = __ldg(ti + nG + nE);
+    const T* gq[CMAXG];  // factor g at (i, k = 0, case 0)
+#pragma unroll
+    for (int g = 0; g < CMAXG; ++g) gq[g] = aux_c + (g < nG ? P->gfac_off[g] + __ldg(ti + g) : 0);
+    for (int b0 = cg * 32 * VEC + lane * VEC; b0 < a.B; b0 += bstep) {
+      using Acc = typename std::conditional<FOLD, double, T>::type;
+      Acc acc[FOLD ? TMC : 1][FOLD ? VEC : 1];
+      if (FOLD)
+#pragma unroll
+        for (int r = 0; r < (FOLD ? TMC : 1); ++r)
+#pragma unroll
+          for (int l = 0; l < (FOLD ? VEC : 1); ++l) acc[r][l] = 0.0;
+      T part[TMC][VEC];
+#pragma unroll
+      for (int r = 0; r < TMC; ++r)
+#pragma unroll
+        for (int l = 0; l < VEC; ++l) part[r][l] = (T)0;
+      for (int k0 = 0; k0 < nK; k0 += (FOLD ? KF : nK)) {
+        const int k1 = FOLD ? min(nK, k0 + KF) : nK;
+        for (int k = k0; k < k1; k += KU) {
+          T pv[KU][VEC];
+          T w[KU][TMC];
+#pragma unroll
+          for (int q = 0; q < KU; ++q) {
+            const int kq = min(k + q, k1 - 1);  // clamped: loads stay in bounds, the term is masked below
+#pragma unroll
+            for (int l = 0; l < VEC; ++l) pv[q][l] = (T)1;
+#pragma unroll
+            for (int g = 0; g < CMAXG; ++g) {
+              if (g < nG) {
+                T f[VEC];
+                load_vec_ro<T, VEC>(gq[g] + b0 + __ldg(tk + kq * nG + g), f);
+#pragma unroll
+                for (int l = 0; l < VEC; ++l) pv[q][l] *= f[l];
+              }
+            }
+            load_w4<T>(wrow + (int64_t)kq * nSp, w[q]);
+            if (k + q >= k1)
+#pragma unroll
+              for (int r = 0; r < TMC; ++r) w[q][r] = (T)0;
+          }
+#pragma unroll
+          for (int q = 0; q < KU; ++q)
+#pragma unroll
+            for (int r = 0; r < TMC; ++r)
+#pragma unroll
+              for (int l = 0; l < VEC; ++l) part[r][l] += w[q][r] * pv[q][l];
+        }
+        if (FOLD) {
+#pragma unroll
+          for (int r = 0; r < TMC; ++r)
+#pragma unroll
+            for (int l = 0; l < VEC; ++l) {
+              acc[FOLD ? r : 0][FOLD ? l : 0] += (Acc)part[r][l];
+              part[r][l] = (T)0;
+            }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < TMC; ++r) {
+        if (r >= rows) continue;
+        const int32_t* tsr = ts + (int64_t)(s0 + r) * (nE + 1);
+        double v[VEC];
+#pragma unroll
+        for (int l = 0; l < VEC; ++l) v[l] = FOLD ? (double)acc[FOLD ? r : 0][FOLD ? l : 0] : (double)part[r][l];
+        for (int e = 0; e < nE; ++e) {
+          T f[VEC];
+          load_vec_ro<T, VEC>(aux_c + P->efac_off[e] + __ldg(ti + nG + e) + __ldg(tsr + e) + b0, f);
+#pragma unroll
+          for (int l = 0; l < VEC; ++l) v[l] *= (double)f[l];
+        }
+        finalize_lanes<T, VEC>(P->out_kind, P->out_off, P->ratio_off, P->out2_off,
+                               (int64_t)oI + __ldg(tsr + nE) + b0, v, aux, a.qout, a.err);
+      }
+    }
+  }
+}
+
+// Row-per-i contraction passes (nS == 1: every output variable is also a factor
+// variable, e.g. Hugin messages between cliques whose separators cover each
+// other): no W reuse exists, so the unit is TMC consecutive i values and the
+// warp streams their factor rows — KU x TMC x nG independent vector loads in
+// flight per lane — with the same epilogue.
+template <typename T, bool FOLD>
+__global__ void __launch_bounds__(NT, FOLD ? 2 : 3) contract_rowi_kernel(const CArgs a) {
+  constexpr int VEC = CTraits<T>::VEC;
+  constexpr int KU = 2;
+  constexpr int KF = 16;
+  T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
+  const T* __restrict__ aux_c = aux;
+  const T* __restrict__ W = reinterpret_cast<const T*>(a.w);
+  const int lane = threadIdx.x & 31;
+  const int n_warps = gridDim.x * (NT / 32);
+  int pi = 0;
+  for (int64_t u = blockIdx.x * (NT / 32) + (threadIdx.x >> 5); u < a.n_units; u += n_warps) {
+    while (pi + 1 < a.n_passes && u >= a.passes[pi + 1].unit0) ++pi;
+    while (pi > 0 && u < a.passes[pi].unit0) --pi;
+    const CPass* __restrict__ P = a.passes + pi;
+    const int64_t ul = u - P->unit0;
+    const int nCG = P->nCG;
+    const int cg = (int)(ul % nCG);
+    const int64_t i0 = (ul / nCG) * TMC;
+    const int nI = P->nI, nK = P->nK, nG = P->nG, nE = P->nE;
+    const int rows = (int)min((int64_t)TMC, (int64_t)nI - i0);
+    const int32_t* __restrict__ tk = a.tab + P->tk_off;
+    const int32_t* __restrict__ ts = a.tab + P->ts_off;
+    const int tw = nG + nE + 1;
+    const T* gb[CMAXG];
+#pragma unroll
+    for (int g = 0; g < CMAXG; ++g) gb[g] = aux_c + (g < nG ? P->gfac_off[g] : 0);
+    int gI[TMC][CMAXG];
+#pragma unroll
+    for (int r = 0; r < TMC; ++r)
+#pragma unroll
+      for (int g = 0; g < CMAXG; ++g)
+        gI[r][g] = (g < nG && r < rows) ? __ldg(a.tab + P->ti_off + (i0 + r) * tw + g) : 0;
+    const T* __restrict__ wrow = W + P->w_off + i0 * (int64_t)nK;
+    const int bstep = 32 * VEC * nCG;
+    for (int b0 = cg * 32 * VEC + lane * VEC; b0 < a.B; b0 += bstep) {
+      double acc[FOLD ? TMC : 1][FOLD ? VEC : 1];
+      if (FOLD)
+#pragma unroll
+        for (int r = 0; r < (FOLD ? TMC : 1); ++r)
+#pragma unroll
+          for (int l = 0; l < (FOLD ? VEC : 1); ++l) acc[r][l] = 0.0;
+      T part[TMC][VEC];
+#pragma unroll
+      for (int r = 0; r < TMC; ++r)
+#pragma unroll
+        for (int l = 0; l < VEC; ++l) part[r][l] = (T)0;
+      for (int k0 = 0; k0 < nK; k0 += (FOLD ? KF : nK)) {
+        const int k1 = FOLD ? min(nK, k0 + KF) : nK;
+        for (int k = k0; k < k1; k += KU) {
+#pragma unroll
+          for (int q = 0; q < KU; ++q) {
+            const int kq = min(k + q, k1 - 1);
+            const bool kon = k + q < k1;
+            int ko[CMAXG];
+#pragma unroll
+            for (int g = 0; g < CMAXG; ++g) ko[g] = g < nG ? __ldg(tk + kq * nG + g) + b0 : 0;
+#pragma unroll
+            for (int r = 0; r < TMC; ++r) {
+              if (r < rows) {
+                T pv[VEC];
+#pragma unroll
+                for (int l = 0; l < VEC; ++l) pv[l] = (T)1;
+#pragma unroll
+                for (int g = 0; g < CMAXG; ++g) {
+                  if (g < nG) {
+                    T f[VEC];
+                    load_vec_ro<T, VEC>(gb[g] + gI[r][g] + ko[g], f);
+#pragma unroll
+                    for (int l = 0; l < VEC; ++l) pv[l] *= f[l];
+                  }
+                }
+                const T w = kon ? __ldg(wrow + (int64_t)r * nK + kq) : (T)0;
+#pragma unroll
+                for (int l = 0; l < VEC; ++l) part[r][l] += w * pv[l];
+              }
+            }
+          }
+        }
+        if (FOLD) {
+#pragma unroll
+          for (int r = 0; r < TMC; ++r)
+#pragma unroll
+            for (int l = 0; l < VEC; ++l) {
+              acc[FOLD ? r : 0][FOLD ? l : 0] += (double)part[r][l];
+              part[r][l] = (T)0;
+            }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < TMC; ++r) {
+        if (r >= rows) continue;
+        const int32_t* tir = a.tab + P->ti_off + (i0 + r) * tw;
+        double v[VEC];
+#pragma unroll
+        for (int l = 0; l < VEC; ++l) v[l] = FOLD ? acc[FOLD ? r : 0][FOLD ? l : 0] : (double)part[r][l];
+        for (int e = 0; e < nE; ++e) {
+          T f[VEC];
+          load_vec_ro<T, VEC>(aux_c + P->efac_off[e] + __ldg(tir + nG + e) + __ldg(ts + e) + b0, f);
+#pragma unroll
+          for (int l = 0; l < VEC; ++l) v[l] *= (double)f[l];
+        }
+        finalize_lanes<T, VEC>(P->out_kind, P->out_off, P->ratio_off, P->out2_off,
+                               (int64_t)__ldg(tir + nG + nE) + __ldg(ts + nE) + b0, v, aux, a.qout, a.err);
+      }
+    }
+  }
+}
+
+cudaError_t launch_contract(int dtype, int fold, int rowi, const CArgs& a, int grid, cudaStream_t s) {
+  if (grid <= 0 || a.n_units <= 0) return cudaSuccess;
+  if (rowi) {
+    if (dtype == 0) {
+      if (fold) contract_rowi_kernel<float, true><<<grid, NT, 0, s>>>(a);
+      else contract_rowi_kernel<float, false><<<grid, NT, 0, s>>>(a);
+    } else {
+      contract_rowi_kernel<double, false><<<grid, NT, 0, s>>>(a);
+    }
+    return cudaGetLastError();
+  }
+  if (dtype == 0) {
+    if (fold) contract_kernel<float, true><<<grid, NT, 0, s>>>(a);
+    else contract_kernel<float, false><<<grid, NT, 0, s>>>(a);
+  } else {
+    contract_kernel<double, false><<<grid, NT, 0, s>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+int contract_max_ctas_per_sm(int dtype, int fold) {
+  int n = 0;
+  if (dtype == 0 && fold) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_kernel<float, true>, NT, 0);
+  else if (dtype == 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_kernel<float, false>, NT, 0);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_kernel<double, false>, NT, 0);
+  return n > 0 ? n : 1;
 }
 
 template <int VEC>

@@ -332,3 +332,25 @@ def test_tree_dump_to_device_plan():  # §8f row 4: .jt.json → cached device p
         P().belief_propagation(st)
         got = all_posteriors(st, len(tree.cards))
         assert rel_err(got, corpus[k][3]) < 1e-10, k
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_batch_contraction_path_large_batch(dtype):
+    """Shared-base micro-batches large enough for the contraction passes
+    (DESIGN.md §3b): every case matches the reference goldens / the oracle."""
+    from paper_1202_3777_b200.batch import BatchPropagator
+
+    tree, data = load_golden("c5")
+    tables = synth.scaled_potentials(tree, 0)
+    golden = golden_cases(data)
+    extra = synth.evidence_cases(tree, 6, seed=7)
+    template = jtref.from_potentials(tree, tables)
+    want_extra = [jtref.case_posteriors(template, ev, range(len(tree.cards))) for ev in extra]
+    cases = [golden[i % len(golden)][0] for i in range(250)] + extra
+    bp = BatchPropagator(tree, tables, batch=128, dtype=dtype, mode="shared")
+    out = bp.run(cases).cpu().numpy()
+    bp.sync()
+    for i in range(250):
+        assert rel_err(out[i], golden[i % len(golden)][1]) < TOL[dtype], (dtype, i)
+    for i, want in enumerate(want_extra):
+        assert rel_err(out[250 + i], want) < TOL[dtype], (dtype, "extra", i)
