@@ -24,7 +24,7 @@ def report(*a, **k):
 @pytest.mark.parametrize("kind", [0, 1])
 def test_single_tree_program_compiles(name, dtype, kind):
     text = report(name, batch=1, mode="materialized", kind=kind, dtype=dtype)
-    assert text.startswith("wave 0")
+    assert "compulsory total MB" in text and "\nwave 0" in text
     assert "pass clique" in text
 
 
@@ -53,3 +53,10 @@ def test_large_cliques_use_row_kernel():
     text = report("c3", batch=1, mode="materialized", kind=0, dtype="f32")
     rows = [l for l in text.splitlines() if l.startswith("  pass") and " row 1 " in l]
     assert len(rows) >= 5, text
+
+
+def test_batch_program_uses_contraction_passes():
+    text = report("c5", batch=2048, mode="shared", kind=1, dtype="f32")
+    assert "contract clique" in text
+    total = float(next(l for l in text.splitlines() if l.startswith("compulsory total MB")).split()[-1])
+    assert 30000 < total < 60000  # ~46.6 GB per 2048-case micro-batch
