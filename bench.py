@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c5")
     ap.add_argument("--cases", type=int, default=8192, help="evidence cases per GPU per step")
-    ap.add_argument("--batch", type=int, default=2048, help="cases per device micro-batch")
+    ap.add_argument("--batch", type=int, default=4096, help="cases per device micro-batch")
     ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
     ap.add_argument("--mode", default="auto", choices=["auto", "shared", "materialized"])
     ap.add_argument("--cpu-sample", type=int, default=24, help="cases in the CPU baseline sample")
@@ -55,6 +55,39 @@ def parse():
     ap.add_argument("--no-extra", action="store_true", help="skip the single-tree per-config table")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
+
+
+def measured_traffic(config, dtype, batch):
+    """DRAM bytes (read + write) of one micro-batch program, summed from the ncu
+    launch list committed under profiles/ (tools/traffic_from_ncu.py), or None."""
+    p = os.path.join(ROOT, "profiles", f"traffic_{config}_{dtype}_b{batch}.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def compulsory_bytes(tree, batch, dtype, mode):
+    """The planner's compulsory HBM traffic of one micro-batch program (every
+    factor tensor read once, outputs written once)."""
+    try:
+        import ctypes as C
+
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import plan_report
+        from paper_1202_3777_b200 import _lib
+
+        h, _keep = plan_report.plan_handle(tree, dtype)
+        buf = C.create_string_buffer(1 << 22)
+        _lib.check(_lib.lib().jt_debug_plan(h, batch, 1 if mode == "shared" else 0, 1, 148, 2, buf, len(buf)))
+        _lib.lib().jt_plan_destroy(h)
+        for line in buf.value.decode().splitlines():
+            if line.startswith("compulsory total MB"):
+                return float(line.split()[-1]) * 1e6
+    except Exception:
+        return None
+    return None
 
 
 def peaks():
@@ -403,6 +436,8 @@ def main():
     pk, pk_kind = peaks()
     alg_bytes_launch = alg_elems * esz * B
     achieved = alg_bytes_launch / (prog_ms * 1e-3) / 1e9
+    comp = compulsory_bytes(tree, B, args.dtype, bp.mode)
+    traffic = measured_traffic(args.config, args.dtype, B)
     line = {
         "metric": "JT propagations/s (collect+distribute); achieved HBM GB/s vs B200 peak",
         "value": round(value, 2), "unit": "cases/s", "n_gpus": world, "steps": args.steps,
@@ -416,10 +451,16 @@ def main():
                          "(32 MB) L2-resident by design",
                    "parallelism": f"dp{world} (evidence shards, NCCL gather of posteriors)"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": round(achieved / pk["hbm_gbs"], 3), "traffic": None,
-                     "kernel": "wave_kernel program of one micro-batch (jt_propagate_query)",
-                     "alg_bytes_per_launch": alg_bytes_launch, "launch_ms": round(prog_ms, 4),
-                     "peak_kind": pk_kind},
+                     "frac": round(achieved / pk["hbm_gbs"], 3),
+                     "traffic": traffic["bytes_per_launch"] if traffic else None,
+                     "kernel": "propagation program of one micro-batch (jt_propagate_query: contraction, "
+                               "thread-owned and general wave kernels)",
+                     "alg_bytes_per_launch": alg_bytes_launch,
+                     "alg_bytes_def": "B_alg1 x cases (SURVEY.md 8d; materialized-equivalent bytes)",
+                     "compulsory_bytes_per_launch": comp,
+                     "frac_compulsory": round(comp / (prog_ms * 1e-3) / 1e9 / pk["hbm_gbs"], 3) if comp else None,
+                     "traffic_source": traffic.get("source") if traffic else None,
+                     "launch_ms": round(prog_ms, 4), "peak_kind": pk_kind},
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clock_info,

@@ -847,6 +847,10 @@ struct HostProgram {
 };
 
 // ----------------------------------------------------- contraction passes --
+// JT_CONTRACT_TMA=1 selects the experimental TMA-staged contraction kernel
+// (profiles/README.md: not yet faster than the register kernels it would replace)
+static bool use_tma_contract() { return getenv("JT_CONTRACT_TMA") != nullptr; }
+
 static bool contract_eligible(const jt_state* st, const PassSpec& ps) {
   return st->mode == JT_SHARED_BASE && st->B > 1 && st->B % CVEC == 0 && !st->h_base.empty() &&
          ps.src_arena == A_BASE && !ps.write && ps.scope.empty() && ps.out_kind != OUT_NONE &&
@@ -986,15 +990,23 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   cp.nG = nG;
   cp.nE = nE;
   cp.rowi = rowi ? 1 : 0;
-  cp.nT = rowi ? (int)((nI + TMC - 1) / TMC) : (int)((nS + TMC - 1) / TMC);
+  const bool tma = use_tma_contract();
+  const int trows = tma ? (rowi ? TMA_ROWS_R : TMA_ROWS) : TMC;
+  cp.nT = rowi ? (int)((nI + trows - 1) / trows) : (int)((nS + trows - 1) / trows);
   cp.nBC = (int)((B + 32 * CVEC - 1) / (32 * CVEC));
   // a unit walks a share of the case chunks of its (i, row tile): all of them for
   // short sums (amortises the unit's setup), one per unit for long ones (parallelism)
   cp.nCG = nK >= 32 ? cp.nBC : nK >= 8 ? std::min(4, cp.nBC) : 1;
   cp.n_units = (rowi ? 1 : nI) * cp.nT * cp.nCG;
+  int64_t min_units = (int64_t)st->num_sms * 8;
+  if (tma) {  // units are tiles of TMA_ROWS rows x one case tile (2 or 4 KB of cases)
+    const int64_t nct = (B * st->esz + (rowi ? 1024 : 2048) - 1) / (rowi ? 1024 : 2048);
+    cp.n_units = (rowi ? 1 : nI) * cp.nT * nct;
+    min_units = st->num_sms;
+  }
   // too few units to fill the GPU (e.g. a posterior over a long factor row):
   // the chunked thread-owned/general passes parallelise over the clique instead
-  if (cp.n_units < (int64_t)st->num_sms * 8) {
+  if (cp.n_units < min_units) {
     hp.w.resize(w0);
     hp.ctab.resize(cp.ti_off);
     return JT_ERR_UNSUPPORTED;
@@ -1119,8 +1131,13 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
         hp.cpasses.push_back(cp);
         hp.cpass_clique.push_back(cpc[key][q]);
       }
-      const int occ = occ_override ? occ_override : contract_max_ctas_per_sm(st->plan->dtype, fold);
-      cg.grid = (int)std::min<int64_t>((cg.n_units + NT / 32 - 1) / (NT / 32), (int64_t)occ * st->num_sms);
+      if (use_tma_contract()) {
+        const int occ = occ_override ? occ_override : contract_tma_ctas_per_sm(st->plan->dtype, cg.m);
+        cg.grid = (int)std::min<int64_t>(cg.n_units, (int64_t)occ * st->num_sms);
+      } else {
+        const int occ = occ_override ? occ_override : contract_max_ctas_per_sm(st->plan->dtype, fold);
+        cg.grid = (int)std::min<int64_t>((cg.n_units + NT / 32 - 1) / (NT / 32), (int64_t)occ * st->num_sms);
+      }
       rt.groups.push_back(cg);
     }
     rt.n_items = (int)(items.size() - rt.item_base);
@@ -1189,7 +1206,8 @@ static int launch_group(jt_state* st, const Program* pr, const WaveRt& w, const 
     c.n_passes = g.n_cpasses;
     c.n_units = g.n_units;
     c.B = st->B;
-    CK(launch_contract(st->plan->dtype, g.lm, g.m, c, g.grid, s));
+    if (use_tma_contract()) CK(launch_contract_tma(st->plan->dtype, g.m, c, g.grid, s));
+    else CK(launch_contract(st->plan->dtype, g.lm, g.m, c, g.grid, s));
     st->launches++;
     return JT_OK;
   }

@@ -11,7 +11,7 @@ sys.path.insert(0, ROOT)
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c5")
 ap.add_argument("--dtype", default="f32")
-ap.add_argument("--batch", type=int, default=2048)
+ap.add_argument("--batch", type=int, default=4096)
 ap.add_argument("--mode", default="auto")
 ap.add_argument("--single", action="store_true", help="single-tree jt_propagate instead of batch")
 ap.add_argument("--reps", type=int, default=1)
