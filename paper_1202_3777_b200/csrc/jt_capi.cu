@@ -2434,9 +2434,16 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
       if (g.kind != 3) continue;
       for (int q = 0; q < g.n_cpasses; ++q) {
         const CPass& c = hp.cpasses[g.cpass_off + q];
-        snprintf(line, sizeof line, "  contract clique %d out %d nI %d nS %d nK %d nG %d nE %d units %lld\n",
-                 hp.cpass_clique[g.cpass_off + q], c.out_kind, c.nI, c.nS, c.nK, c.nG, c.nE, (long long)c.n_units);
+        snprintf(line, sizeof line, "  contract clique %d out %d nI %d nS %d nK %d nG %d nE %d units %lld rowi %d gI-dep",
+                 hp.cpass_clique[g.cpass_off + q], c.out_kind, c.nI, c.nS, c.nK, c.nG, c.nE, (long long)c.n_units,
+                 c.rowi);
         out += line;
+        for (int gg = 0; gg < c.nG; ++gg) {  // does factor gg depend on i?
+          bool dep = false;
+          for (int ii = 1; ii < c.nI && !dep; ++ii) dep = hp.ctab[c.ti_off + ii * (c.nG + c.nE + 1) + gg] != 0;
+          out += dep ? " 1" : " 0";
+        }
+        out += "\n";
       }
     }
   }

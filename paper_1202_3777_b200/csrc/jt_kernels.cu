@@ -16,6 +16,7 @@
 #include <cfloat>
 #include <algorithm>
 #include <type_traits>
+#include <utility>
 
 namespace jt {
 
@@ -61,6 +62,32 @@ __device__ __forceinline__ void store_vec(T* p, const T (&v)[VEC]) {
 #pragma unroll
   for (int l = 0; l < VEC; ++l) xs[l] = v[l];
   *reinterpret_cast<V*>(p) = x;
+}
+
+// Programmatic dependent launch: wave kernels are launched with the
+// programmatic-serialization attribute, so a kernel's CTAs may be scheduled
+// while the previous wave drains; every such kernel waits for the previous
+// grid's completion (griddepcontrol.wait) before touching any data and lets its
+// own dependents launch right away.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 __device__ __forceinline__ double warp_sum(double s) {
@@ -260,6 +287,7 @@ __device__ __noinline__ void own_flush(const DevPass& P, const T* __restrict__ a
 // live in shared memory so the factor loop stays a runtime loop (compact code).
 template <typename T, int VEC, int LM, int M>
 __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
+  pdl_enter();
   static_assert(M * VEC <= 16, "flush passes at most 16 lanes");
   constexpr int OKV = 8 / M;
   __shared__ DevPass P;
@@ -448,6 +476,7 @@ __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
 
 template <typename T, int VEC>
 __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
+  pdl_enter();
   constexpr int TH = NT * KV * VEC;  // positions per CTA iteration
   __shared__ DevPass P;
   __shared__ double part2[NT];
@@ -741,6 +770,7 @@ __device__ __forceinline__ double warp_chunk_combine(const DevPass& P, const Ite
 // one block entry per batch, slot addresses are immediates off one pointer.
 template <typename T, int VEC, bool LIN>
 __global__ void __launch_bounds__(NT, 2) wave_row_kernel(const WaveArgs a) {
+  pdl_enter();
   T* __restrict__ clique = reinterpret_cast<T*>(a.clique);
   const T* __restrict__ base = reinterpret_cast<const T*>(a.base);
   T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
@@ -908,9 +938,8 @@ __global__ void __launch_bounds__(NT, 2) wave_row_kernel(const WaveArgs a) {
 
 template <typename T, int VEC>
 static cudaError_t launch_row_t(int lin, const WaveArgs& a, int grid, cudaStream_t s) {
-  if (lin) wave_row_kernel<T, VEC, true><<<grid, NT, 0, s>>>(a);
-  else wave_row_kernel<T, VEC, false><<<grid, NT, 0, s>>>(a);
-  return cudaGetLastError();
+  return lin ? launch_pdl(wave_row_kernel<T, VEC, true>, grid, NT, 0, s, a)
+             : launch_pdl(wave_row_kernel<T, VEC, false>, grid, NT, 0, s, a);
 }
 
 cudaError_t launch_wave_row(int dtype, int vec, int lin, const WaveArgs& a, int grid, cudaStream_t s) {
@@ -1008,6 +1037,7 @@ __device__ __forceinline__ void load_w4(const T* p, T (&w)[TMC]) {
 // registers, three CTAs per SM.
 template <typename T, bool FOLD>
 __global__ void __launch_bounds__(NT, FOLD ? 2 : 3) contract_kernel(const CArgs a) {
+  pdl_enter();
   constexpr int VEC = CTraits<T>::VEC;
   constexpr int KU = FOLD ? 4 : 2;
   constexpr int KF = 16;
@@ -1121,6 +1151,7 @@ __global__ void __launch_bounds__(NT, FOLD ? 2 : 3) contract_kernel(const CArgs 
 // flight per lane — with the same epilogue.
 template <typename T, bool FOLD>
 __global__ void __launch_bounds__(NT, FOLD ? 2 : 3) contract_rowi_kernel(const CArgs a) {
+  pdl_enter();
   constexpr int VEC = CTraits<T>::VEC;
   constexpr int KU = 2;
   constexpr int KF = 16;
@@ -1336,6 +1367,7 @@ __device__ __forceinline__ void tma_issue(const CArgs& a, const TmaTile& t, int 
 
 template <typename T, bool ROWI>
 __global__ void __launch_bounds__(TNT, 2) contract_tma_kernel(const CArgs a) {
+  pdl_enter();
   constexpr int VEC = 16 / sizeof(T);
   constexpr int NCt = (ROWI ? 1024 : 2048) / (int)sizeof(T);  // cases per tile (one row = 1 or 2 KB)
   constexpr int LPR = NCt / VEC;                                // threads per row set
@@ -1512,8 +1544,7 @@ static cudaError_t launch_tma_t(const CArgs& a, int grid, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  contract_tma_kernel<T, ROWI><<<grid, TNT, smem, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(contract_tma_kernel<T, ROWI>, grid, TNT, smem, s, a);
 }
 
 int contract_tma_ctas_per_sm(int dtype, int rowi) {
@@ -1549,18 +1580,18 @@ cudaError_t launch_contract(int dtype, int fold, int rowi, const CArgs& a, int g
   if (grid <= 0 || a.n_units <= 0) return cudaSuccess;
   if (rowi) {
     if (dtype == 0) {
-      if (fold) contract_rowi_kernel<float, true><<<grid, NT, 0, s>>>(a);
-      else contract_rowi_kernel<float, false><<<grid, NT, 0, s>>>(a);
+      return fold ? launch_pdl(contract_rowi_kernel<float, true>, grid, NT, 0, s, a)
+                  : launch_pdl(contract_rowi_kernel<float, false>, grid, NT, 0, s, a);
     } else {
-      contract_rowi_kernel<double, false><<<grid, NT, 0, s>>>(a);
+      return launch_pdl(contract_rowi_kernel<double, false>, grid, NT, 0, s, a);
     }
     return cudaGetLastError();
   }
   if (dtype == 0) {
-    if (fold) contract_kernel<float, true><<<grid, NT, 0, s>>>(a);
-    else contract_kernel<float, false><<<grid, NT, 0, s>>>(a);
+    return fold ? launch_pdl(contract_kernel<float, true>, grid, NT, 0, s, a)
+                : launch_pdl(contract_kernel<float, false>, grid, NT, 0, s, a);
   } else {
-    contract_kernel<double, false><<<grid, NT, 0, s>>>(a);
+    return launch_pdl(contract_kernel<double, false>, grid, NT, 0, s, a);
   }
   return cudaGetLastError();
 }
@@ -1587,14 +1618,12 @@ static cudaError_t launch_t(const WaveArgs& a, int grid, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  wave_kernel<T, VEC><<<grid, NT, wave_smem<VEC>(), s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(wave_kernel<T, VEC>, grid, NT, wave_smem<VEC>(), s, a);
 }
 
 template <typename T, int VEC, int LM, int M>
 static cudaError_t launch_own_t(const WaveArgs& a, int grid, cudaStream_t s) {
-  wave_own_kernel<T, VEC, LM, M><<<grid, NT, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(wave_own_kernel<T, VEC, LM, M>, grid, NT, 0, s, a);
 }
 
 template <typename T, int VEC, int LM>
