@@ -991,7 +991,7 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   cp.nE = nE;
   cp.rowi = rowi ? 1 : 0;
   const bool tma = use_tma_contract();
-  const int trows = tma ? (rowi ? TMA_ROWS_R : TMA_ROWS) : TMC;
+  const int trows = tma ? (rowi ? TMA_ROWS_R : TMA_ROWS) : (rowi ? 1 : TMC);  // register rowi: one i per unit
   cp.nT = rowi ? (int)((nI + trows - 1) / trows) : (int)((nS + trows - 1) / trows);
   cp.nBC = (int)((B + 32 * CVEC - 1) / (32 * CVEC));
   // a unit walks a share of the case chunks of its (i, row tile): all of them for

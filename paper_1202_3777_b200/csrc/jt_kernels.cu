@@ -1036,10 +1036,10 @@ __device__ __forceinline__ void load_w4(const T* p, T (&w)[TMC]) {
 // Otherwise the sums stay in T (fp64, or fp32 over at most KF terms): fewer
 // registers, three CTAs per SM.
 template <typename T, bool FOLD>
-__global__ void __launch_bounds__(NT, FOLD ? 2 : 3) contract_kernel(const CArgs a) {
+__global__ void __launch_bounds__(NT, 3) contract_kernel(const CArgs a) {
   pdl_enter();
-  constexpr int VEC = CTraits<T>::VEC;
-  constexpr int KU = FOLD ? 4 : 2;
+  constexpr int VEC = FOLD ? 2 : CTraits<T>::VEC;  // fp64 fold accumulators: two cases per lane
+  constexpr int KU = 2;
   constexpr int KF = 16;
   static_assert(TMC == 4, "W rows are loaded as one 4-vector");
   const T* __restrict__ W = reinterpret_cast<const T*>(a.w);
@@ -1150,10 +1150,12 @@ __global__ void __launch_bounds__(NT, FOLD ? 2 : 3) contract_kernel(const CArgs 
 // warp streams their factor rows — KU x TMC x nG independent vector loads in
 // flight per lane — with the same epilogue.
 template <typename T, bool FOLD>
-__global__ void __launch_bounds__(NT, FOLD ? 2 : 3) contract_rowi_kernel(const CArgs a) {
+__global__ void __launch_bounds__(NT, 3) contract_rowi_kernel(const CArgs a) {
   pdl_enter();
+  // one i per warp unit (few registers: three CTAs per SM), KU values of k in
+  // flight, each with its nG factor-row vectors
   constexpr int VEC = CTraits<T>::VEC;
-  constexpr int KU = 2;
+  constexpr int KU = 4;
   constexpr int KF = 16;
   T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
   const T* __restrict__ aux_c = aux;
@@ -1168,93 +1170,68 @@ __global__ void __launch_bounds__(NT, FOLD ? 2 : 3) contract_rowi_kernel(const C
     const int64_t ul = u - P->unit0;
     const int nCG = P->nCG;
     const int cg = (int)(ul % nCG);
-    const int64_t i0 = (ul / nCG) * TMC;
-    const int nI = P->nI, nK = P->nK, nG = P->nG, nE = P->nE;
-    const int rows = (int)min((int64_t)TMC, (int64_t)nI - i0);
+    const int64_t i = ul / nCG;
+    const int nK = P->nK, nG = P->nG, nE = P->nE;
+    const int tw = nG + nE + 1;
+    const int32_t* __restrict__ tir = a.tab + P->ti_off + i * tw;
     const int32_t* __restrict__ tk = a.tab + P->tk_off;
     const int32_t* __restrict__ ts = a.tab + P->ts_off;
-    const int tw = nG + nE + 1;
-    const T* gb[CMAXG];
+    const T* gq[CMAXG];
 #pragma unroll
-    for (int g = 0; g < CMAXG; ++g) gb[g] = aux_c + (g < nG ? P->gfac_off[g] : 0);
-    int gI[TMC][CMAXG];
-#pragma unroll
-    for (int r = 0; r < TMC; ++r)
-#pragma unroll
-      for (int g = 0; g < CMAXG; ++g)
-        gI[r][g] = (g < nG && r < rows) ? __ldg(a.tab + P->ti_off + (i0 + r) * tw + g) : 0;
-    const T* __restrict__ wrow = W + P->w_off + i0 * (int64_t)nK;
+    for (int g = 0; g < CMAXG; ++g) gq[g] = aux_c + (g < nG ? P->gfac_off[g] + __ldg(tir + g) : 0);
+    const T* __restrict__ wrow = W + P->w_off + i * (int64_t)nK;
     const int bstep = 32 * VEC * nCG;
     for (int b0 = cg * 32 * VEC + lane * VEC; b0 < a.B; b0 += bstep) {
-      double acc[FOLD ? TMC : 1][FOLD ? VEC : 1];
-      if (FOLD)
+      double acc[VEC];
 #pragma unroll
-        for (int r = 0; r < (FOLD ? TMC : 1); ++r)
+      for (int l = 0; l < VEC; ++l) acc[l] = 0.0;
+      T part[VEC];
 #pragma unroll
-          for (int l = 0; l < (FOLD ? VEC : 1); ++l) acc[r][l] = 0.0;
-      T part[TMC][VEC];
+      for (int l = 0; l < VEC; ++l) part[l] = (T)0;
+      int since = 0;
+      for (int k = 0; k < nK; k += KU) {
+        T pv[KU][VEC];
+        T w[KU];
 #pragma unroll
-      for (int r = 0; r < TMC; ++r)
+        for (int q = 0; q < KU; ++q) {
+          const int kq = min(k + q, nK - 1);
 #pragma unroll
-        for (int l = 0; l < VEC; ++l) part[r][l] = (T)0;
-      for (int k0 = 0; k0 < nK; k0 += (FOLD ? KF : nK)) {
-        const int k1 = FOLD ? min(nK, k0 + KF) : nK;
-        for (int k = k0; k < k1; k += KU) {
+          for (int l = 0; l < VEC; ++l) pv[q][l] = (T)1;
 #pragma unroll
-          for (int q = 0; q < KU; ++q) {
-            const int kq = min(k + q, k1 - 1);
-            const bool kon = k + q < k1;
-            int ko[CMAXG];
+          for (int g = 0; g < CMAXG; ++g) {
+            if (g < nG) {
+              T f[VEC];
+              load_vec_ro<T, VEC>(gq[g] + b0 + __ldg(tk + kq * nG + g), f);
 #pragma unroll
-            for (int g = 0; g < CMAXG; ++g) ko[g] = g < nG ? __ldg(tk + kq * nG + g) + b0 : 0;
-#pragma unroll
-            for (int r = 0; r < TMC; ++r) {
-              if (r < rows) {
-                T pv[VEC];
-#pragma unroll
-                for (int l = 0; l < VEC; ++l) pv[l] = (T)1;
-#pragma unroll
-                for (int g = 0; g < CMAXG; ++g) {
-                  if (g < nG) {
-                    T f[VEC];
-                    load_vec_ro<T, VEC>(gb[g] + gI[r][g] + ko[g], f);
-#pragma unroll
-                    for (int l = 0; l < VEC; ++l) pv[l] *= f[l];
-                  }
-                }
-                const T w = kon ? __ldg(wrow + (int64_t)r * nK + kq) : (T)0;
-#pragma unroll
-                for (int l = 0; l < VEC; ++l) part[r][l] += w * pv[l];
-              }
+              for (int l = 0; l < VEC; ++l) pv[q][l] *= f[l];
             }
           }
+          w[q] = k + q < nK ? __ldg(wrow + kq) : (T)0;
         }
-        if (FOLD) {
 #pragma unroll
-          for (int r = 0; r < TMC; ++r)
+        for (int q = 0; q < KU; ++q)
 #pragma unroll
-            for (int l = 0; l < VEC; ++l) {
-              acc[FOLD ? r : 0][FOLD ? l : 0] += (double)part[r][l];
-              part[r][l] = (T)0;
-            }
+          for (int l = 0; l < VEC; ++l) part[l] += w[q] * pv[q][l];
+        if (FOLD && (since += KU) >= KF) {
+#pragma unroll
+          for (int l = 0; l < VEC; ++l) {
+            acc[l] += (double)part[l];
+            part[l] = (T)0;
+          }
+          since = 0;
         }
       }
+      double v[VEC];
 #pragma unroll
-      for (int r = 0; r < TMC; ++r) {
-        if (r >= rows) continue;
-        const int32_t* tir = a.tab + P->ti_off + (i0 + r) * tw;
-        double v[VEC];
+      for (int l = 0; l < VEC; ++l) v[l] = acc[l] + (double)part[l];
+      for (int e = 0; e < nE; ++e) {
+        T f[VEC];
+        load_vec_ro<T, VEC>(aux_c + P->efac_off[e] + __ldg(tir + nG + e) + __ldg(ts + e) + b0, f);
 #pragma unroll
-        for (int l = 0; l < VEC; ++l) v[l] = FOLD ? acc[FOLD ? r : 0][FOLD ? l : 0] : (double)part[r][l];
-        for (int e = 0; e < nE; ++e) {
-          T f[VEC];
-          load_vec_ro<T, VEC>(aux_c + P->efac_off[e] + __ldg(tir + nG + e) + __ldg(ts + e) + b0, f);
-#pragma unroll
-          for (int l = 0; l < VEC; ++l) v[l] *= (double)f[l];
-        }
-        finalize_lanes<T, VEC>(P->out_kind, P->out_off, P->ratio_off, P->out2_off,
-                               (int64_t)__ldg(tir + nG + nE) + __ldg(ts + nE) + b0, v, aux, a.qout, a.err);
+        for (int l = 0; l < VEC; ++l) v[l] *= (double)f[l];
       }
+      finalize_lanes<T, VEC>(P->out_kind, P->out_off, P->ratio_off, P->out2_off,
+                             (int64_t)__ldg(tir + nG + nE) + __ldg(ts + nE) + b0, v, aux, a.qout, a.err);
     }
   }
 }
