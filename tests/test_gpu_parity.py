@@ -354,3 +354,12 @@ def test_batch_contraction_path_large_batch(dtype):
         assert rel_err(out[i], golden[i % len(golden)][1]) < TOL[dtype], (dtype, i)
     for i, want in enumerate(want_extra):
         assert rel_err(out[250 + i], want) < TOL[dtype], (dtype, "extra", i)
+
+
+def test_bench_rows_on_device():  # §8f row 3: bench-style CSV under the device engine
+    from paper_1202_3777_b200 import benchcsv
+
+    tree, tables = synth.make_config("c1")
+    row = benchcsv.bench_tree("c1", tree, tables, repeats=2)
+    assert set(row) == set(benchcsv.BENCH_COLUMNS)
+    assert row["seq_ms"] > 0 and row["par_ms"] > 0 and 0 <= row["overhead_frac"] <= 1
