@@ -911,7 +911,7 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   const std::vector<int64_t> oS = group_offsets(p, S, strides(S, ps.out));
   const int64_t nI = (int64_t)oI.size(), nS = (int64_t)oS.size();
   const int64_t nK = (int64_t)group_offsets(p, K, std::vector<int64_t>(K.size(), 0)).size();
-  if (nI * nK * (nS + 3) > (int64_t)1 << 31) return JT_ERR_UNSUPPORTED;
+  if (nI * nK * (nS + 7) > (int64_t)1 << 31) return JT_ERR_UNSUPPORTED;
   auto fits = [](const std::vector<int64_t>& v) {
     for (int64_t x : v)
       if (x > INT32_MAX) return false;
@@ -923,9 +923,9 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
     if (!fits(eI[e]) || !fits(eS[e])) return JT_ERR_UNSUPPORTED;
   if (!fits(oI) || !fits(oS)) return JT_ERR_UNSUPPORTED;
   // W[i][k][s'] = Σ_R base: walk the clique once, odometer over its variables
-  // rows of S' padded to 4 (one vector load per k); nS == 1 uses the row-per-i kernel
+  // nS == 1 uses the row-per-i kernel
   const bool rowi = nS == 1;
-  const int64_t nSp = rowi ? 1 : (nS + 3) & ~int64_t(3);
+  const int64_t nSp = rowi ? 1 : (nS + 7) & ~int64_t(7);  // W rows padded: two 4-vector loads per k
   const int64_t w0 = (int64_t)hp.w.size();
   hp.w.resize(w0 + nI * nK * nSp, 0.0);
   {
@@ -1135,7 +1135,7 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
         const int occ = occ_override ? occ_override : contract_tma_ctas_per_sm(st->plan->dtype, cg.m);
         cg.grid = (int)std::min<int64_t>(cg.n_units, (int64_t)occ * st->num_sms);
       } else {
-        const int occ = occ_override ? occ_override : contract_max_ctas_per_sm(st->plan->dtype, fold);
+        const int occ = occ_override ? occ_override : contract_max_ctas_per_sm(st->plan->dtype, fold, cg.m);
         cg.grid = (int)std::min<int64_t>((cg.n_units + NT / 32 - 1) / (NT / 32), (int64_t)occ * st->num_sms);
       }
       rt.groups.push_back(cg);

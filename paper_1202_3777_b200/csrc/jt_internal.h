@@ -100,7 +100,7 @@ struct WaveArgs {
 // with I = s∩U, S' = s∖U, K' = U∖s and W = base summed over R = c∖(s∪U),
 // precomputed on the host.  A warp owns one (i, row tile of TMC rows of S')
 // unit and walks all cases.
-constexpr int TMC = 4;     // W rows per warp unit
+constexpr int TMC = 8;     // W rows per warp unit
 constexpr int CVEC = 4;    // B must be a multiple of this (fp32 lanes per vector; fp64 uses 2)
 constexpr int CMAXG = 4;   // factors multiplied per k (more: the pass takes the general kernels)
 struct CPass {
@@ -135,7 +135,7 @@ cudaError_t launch_contract_tma(int dtype, int rowi, const CArgs& a, int grid, c
 int contract_tma_ctas_per_sm(int dtype, int rowi);
 constexpr int TMA_ROWS = 8;    // GEMM-mode rows per TMA contraction tile (jt_kernels.cu TROWS)
 constexpr int TMA_ROWS_R = 4;  // row-per-i mode (TROWS_R)
-int contract_max_ctas_per_sm(int dtype, int fold);
+int contract_max_ctas_per_sm(int dtype, int fold, int rowi);
 
 // device initialize: one entry per clique, one term per CPT, 3 int64 per CPT variable
 // (clique stride, card, CPT stride)

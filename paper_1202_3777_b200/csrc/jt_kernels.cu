@@ -1009,39 +1009,24 @@ __device__ __forceinline__ void finalize_lanes(int kind, int64_t out_off, int64_
   store_vec<T, VEC>(aux + (out2_off >= 0 ? out2_off : out_off) + j, nw);
 }
 
-// One warp per unit (i, row tile of TMC rows of S'); the warp walks every chunk
-// of 32*VEC cases, each lane owning VEC consecutive cases.  Per k: the product
-// of the G factor rows (VEC-vectors, coalesced across the warp) times TMC rows
-// of W (one vector load; W rows padded to a multiple of 4) into TMC x VEC
-// accumulators — TMC FMAs per factor load.  k is unrolled by KU so KU x nG
-// loads are in flight per lane.  fp32 sums run in fp32 for KF consecutive k and
-// are folded into fp64.
 template <typename T> struct CTraits;
 template <> struct CTraits<float> { static constexpr int VEC = 4; };
 template <> struct CTraits<double> { static constexpr int VEC = 2; };
 
-template <typename T>
-__device__ __forceinline__ void load_w4(const T* p, T (&w)[TMC]) {
-  if constexpr (sizeof(T) == 4) {
-    const float4 x = __ldg(reinterpret_cast<const float4*>(p));
-    w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
-  } else {
-    const double2 x = __ldg(reinterpret_cast<const double2*>(p));
-    const double2 y = __ldg(reinterpret_cast<const double2*>(p) + 1);
-    w[0] = x.x; w[1] = x.y; w[2] = y.x; w[3] = y.y;
-  }
-}
-
-// FOLD: fp32 with nK > KF — partial sums of KF terms are folded into fp64.
-// Otherwise the sums stay in T (fp64, or fp32 over at most KF terms): fewer
-// registers, three CTAs per SM.
+// One warp per unit (i, tile of TMC rows of S', share of the case chunks); each
+// lane owns VEC consecutive cases.  Per k: the product of the G factor rows (one
+// VEC-vector per lane, coalesced across the warp) is reused by the TMC rows of W
+// (two 4-vector broadcast loads; W rows padded to a multiple of 8): TMC x VEC
+// FMAs per lane per k against ~nG + 3 loads.  fp32 sums stay in registers for
+// CKF consecutive k and are then folded into per-thread fp64 accumulators in
+// shared memory (fp64 passes accumulate in registers directly).
 template <typename T, bool FOLD>
-__global__ void __launch_bounds__(NT, 3) contract_kernel(const CArgs a) {
+__global__ void __launch_bounds__(NT, 2) contract_kernel(const CArgs a) {
   pdl_enter();
-  constexpr int VEC = FOLD ? 2 : CTraits<T>::VEC;  // fp64 fold accumulators: two cases per lane
+  constexpr int VEC = CTraits<T>::VEC;
   constexpr int KU = 2;
-  constexpr int KF = 16;
-  static_assert(TMC == 4, "W rows are loaded as one 4-vector");
+  static_assert(TMC == 8, "W rows are loaded as two 4-vectors");
+  extern __shared__ double cacc[];  // FOLD: [TMC * VEC][NT] fp64 accumulators
   const T* __restrict__ W = reinterpret_cast<const T*>(a.w);
   T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
   const T* __restrict__ aux_c = aux;
@@ -1058,39 +1043,34 @@ __global__ void __launch_bounds__(NT, 3) contract_kernel(const CArgs a) {
     const int t = (int)((ul / nCG) % nT);
     const int64_t i = ul / ((int64_t)nCG * nT);
     const int nS = P->nS, nK = P->nK, nG = P->nG, nE = P->nE;
-    const int nSp = (nS + 3) & ~3;
-    const int bstep = 32 * VEC * nCG;  // case chunks cg, cg + nCG, ... of this unit
+    const int nSp = (nS + 7) & ~7;
+    const int bstep = 32 * VEC * nCG;
     const int s0 = t * TMC;
     const int rows = min(TMC, nS - s0);
     const int32_t* __restrict__ ti = a.tab + P->ti_off + i * (nG + nE + 1);
     const int32_t* __restrict__ tk = a.tab + P->tk_off;
     const int32_t* __restrict__ ts = a.tab + P->ts_off;
     const T* __restrict__ wrow = W + P->w_off + i * (int64_t)nK * nSp + s0;
-    const int32_t oI = __ldg(ti + nG + nE);
     const T* gq[CMAXG];  // factor g at (i, k = 0, case 0)
 #pragma unroll
     for (int g = 0; g < CMAXG; ++g) gq[g] = aux_c + (g < nG ? P->gfac_off[g] + __ldg(ti + g) : 0);
     for (int b0 = cg * 32 * VEC + lane * VEC; b0 < a.B; b0 += bstep) {
-      using Acc = typename std::conditional<FOLD, double, T>::type;
-      Acc acc[FOLD ? TMC : 1][FOLD ? VEC : 1];
-      if (FOLD)
-#pragma unroll
-        for (int r = 0; r < (FOLD ? TMC : 1); ++r)
-#pragma unroll
-          for (int l = 0; l < (FOLD ? VEC : 1); ++l) acc[r][l] = 0.0;
       T part[TMC][VEC];
 #pragma unroll
       for (int r = 0; r < TMC; ++r)
 #pragma unroll
         for (int l = 0; l < VEC; ++l) part[r][l] = (T)0;
-      for (int k0 = 0; k0 < nK; k0 += (FOLD ? KF : nK)) {
-        const int k1 = FOLD ? min(nK, k0 + KF) : nK;
+      if (FOLD)
+#pragma unroll
+        for (int q = 0; q < TMC * VEC; ++q) cacc[q * NT + threadIdx.x] = 0.0;
+      for (int k0 = 0; k0 < nK; k0 += (FOLD ? CKF : nK)) {
+        const int k1 = FOLD ? min(nK, k0 + CKF) : nK;
         for (int k = k0; k < k1; k += KU) {
           T pv[KU][VEC];
           T w[KU][TMC];
 #pragma unroll
           for (int q = 0; q < KU; ++q) {
-            const int kq = min(k + q, k1 - 1);  // clamped: loads stay in bounds, the term is masked below
+            const int kq = min(k + q, k1 - 1);  // clamped: the term is zeroed below
 #pragma unroll
             for (int l = 0; l < VEC; ++l) pv[q][l] = (T)1;
 #pragma unroll
@@ -1102,7 +1082,20 @@ __global__ void __launch_bounds__(NT, 3) contract_kernel(const CArgs a) {
                 for (int l = 0; l < VEC; ++l) pv[q][l] *= f[l];
               }
             }
-            load_w4<T>(wrow + (int64_t)kq * nSp, w[q]);
+            const T* wk = wrow + (int64_t)kq * nSp;
+            if constexpr (sizeof(T) == 4) {
+              const float4 x = __ldg(reinterpret_cast<const float4*>(wk));
+              const float4 y = __ldg(reinterpret_cast<const float4*>(wk) + 1);
+              w[q][0] = x.x; w[q][1] = x.y; w[q][2] = x.z; w[q][3] = x.w;
+              w[q][4] = y.x; w[q][5] = y.y; w[q][6] = y.z; w[q][7] = y.w;
+            } else {
+#pragma unroll
+              for (int h = 0; h < 4; ++h) {
+                const double2 x = __ldg(reinterpret_cast<const double2*>(wk) + h);
+                w[q][2 * h] = x.x;
+                w[q][2 * h + 1] = x.y;
+              }
+            }
             if (k + q >= k1)
 #pragma unroll
               for (int r = 0; r < TMC; ++r) w[q][r] = (T)0;
@@ -1119,7 +1112,7 @@ __global__ void __launch_bounds__(NT, 3) contract_kernel(const CArgs a) {
           for (int r = 0; r < TMC; ++r)
 #pragma unroll
             for (int l = 0; l < VEC; ++l) {
-              acc[FOLD ? r : 0][FOLD ? l : 0] += (Acc)part[r][l];
+              cacc[(r * VEC + l) * NT + threadIdx.x] += (double)part[r][l];
               part[r][l] = (T)0;
             }
         }
@@ -1130,7 +1123,7 @@ __global__ void __launch_bounds__(NT, 3) contract_kernel(const CArgs a) {
         const int32_t* tsr = ts + (int64_t)(s0 + r) * (nE + 1);
         double v[VEC];
 #pragma unroll
-        for (int l = 0; l < VEC; ++l) v[l] = FOLD ? (double)acc[FOLD ? r : 0][FOLD ? l : 0] : (double)part[r][l];
+        for (int l = 0; l < VEC; ++l) v[l] = FOLD ? cacc[(r * VEC + l) * NT + threadIdx.x] : (double)part[r][l];
         for (int e = 0; e < nE; ++e) {
           T f[VEC];
           load_vec_ro<T, VEC>(aux_c + P->efac_off[e] + __ldg(ti + nG + e) + __ldg(tsr + e) + b0, f);
@@ -1138,7 +1131,7 @@ __global__ void __launch_bounds__(NT, 3) contract_kernel(const CArgs a) {
           for (int l = 0; l < VEC; ++l) v[l] *= (double)f[l];
         }
         finalize_lanes<T, VEC>(P->out_kind, P->out_off, P->ratio_off, P->out2_off,
-                               (int64_t)oI + __ldg(tsr + nE) + b0, v, aux, a.qout, a.err);
+                               (int64_t)__ldg(ti + nG + nE) + __ldg(tsr + nE) + b0, v, aux, a.qout, a.err);
       }
     }
   }
@@ -1399,7 +1392,7 @@ __global__ void __launch_bounds__(TNT, 2) contract_tma_kernel(const CArgs a) {
     const int cl = (tid % LPR) * VEC;  // case offset within the tile
     const int c = t.c0 + cl;
     const bool live = c < a.B;
-    const int nSp = (nS + 3) & ~3;
+    const int nSp = (nS + 7) & ~7;
     T part[RPT][VEC];
 #pragma unroll
     for (int r = 0; r < RPT; ++r)
@@ -1553,31 +1546,46 @@ cudaError_t launch_contract_tma(int dtype, int rowi, const CArgs& a, int grid, c
   return rowi ? launch_tma_t<double, true>(a, grid, s) : launch_tma_t<double, false>(a, grid, s);
 }
 
+constexpr size_t CFOLD_SMEM = (size_t)TMC * 4 * NT * sizeof(double);  // fp32 fold accumulators
+
 cudaError_t launch_contract(int dtype, int fold, int rowi, const CArgs& a, int grid, cudaStream_t s) {
   if (grid <= 0 || a.n_units <= 0) return cudaSuccess;
   if (rowi) {
-    if (dtype == 0) {
+    if (dtype == 0)
       return fold ? launch_pdl(contract_rowi_kernel<float, true>, grid, NT, 0, s, a)
                   : launch_pdl(contract_rowi_kernel<float, false>, grid, NT, 0, s, a);
-    } else {
-      return launch_pdl(contract_rowi_kernel<double, false>, grid, NT, 0, s, a);
-    }
-    return cudaGetLastError();
+    return launch_pdl(contract_rowi_kernel<double, false>, grid, NT, 0, s, a);
   }
   if (dtype == 0) {
-    return fold ? launch_pdl(contract_kernel<float, true>, grid, NT, 0, s, a)
-                : launch_pdl(contract_kernel<float, false>, grid, NT, 0, s, a);
-  } else {
-    return launch_pdl(contract_kernel<double, false>, grid, NT, 0, s, a);
+    if (fold) {
+      static bool attr = false;
+      if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(contract_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)CFOLD_SMEM);
+        if (e != cudaSuccess) return e;
+        attr = true;
+      }
+      return launch_pdl(contract_kernel<float, true>, grid, NT, CFOLD_SMEM, s, a);
+    }
+    return launch_pdl(contract_kernel<float, false>, grid, NT, 0, s, a);
   }
-  return cudaGetLastError();
+  return launch_pdl(contract_kernel<double, false>, grid, NT, 0, s, a);
 }
 
-int contract_max_ctas_per_sm(int dtype, int fold) {
+int contract_max_ctas_per_sm(int dtype, int fold, int rowi) {
   int n = 0;
-  if (dtype == 0 && fold) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_kernel<float, true>, NT, 0);
-  else if (dtype == 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_kernel<float, false>, NT, 0);
-  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_kernel<double, false>, NT, 0);
+  if (rowi) {
+    if (dtype == 0 && fold) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_rowi_kernel<float, true>, NT, 0);
+    else if (dtype == 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_rowi_kernel<float, false>, NT, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_rowi_kernel<double, false>, NT, 0);
+  } else if (dtype == 0 && fold) {
+    cudaFuncSetAttribute(contract_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CFOLD_SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_kernel<float, true>, NT, CFOLD_SMEM);
+  } else if (dtype == 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_kernel<float, false>, NT, 0);
+  } else {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_kernel<double, false>, NT, 0);
+  }
   return n > 0 ? n : 1;
 }
 
