@@ -997,8 +997,28 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   // a unit walks a share of the case chunks of its (i, row tile): all of them for
   // short sums (amortises the unit's setup), one per unit for long ones (parallelism)
   cp.nCG = nK >= 32 ? cp.nBC : nK >= 8 ? std::min(4, cp.nBC) : 1;
+  cp.nKS = 1;
+  cp.kch = (int)nK;
   cp.n_units = (rowi ? 1 : nI) * cp.nT * cp.nCG;
   int64_t min_units = (int64_t)st->num_sms * 8;
+  if (!tma && !rowi && cp.n_units < min_units && nK >= 256) {
+    // long sums with few units (posteriors of a clique-private variable): split K
+    // into chunks of >= 64 k so every warp has work; partials combined in order
+    const int vec = st->esz == 4 ? 4 : 2;
+    cp.nBC = (int)((B + 32 * vec - 1) / (32 * vec));
+    cp.nCG = cp.nBC;  // one case chunk per unit: the combine group is (i, t, chunk)
+    const int64_t base_units = nI * cp.nT * cp.nCG;
+    int64_t nks = std::min<int64_t>((min_units * 4 + base_units - 1) / base_units, (nK + 63) / 64);
+    nks = std::max<int64_t>(2, nks);
+    cp.kch = (int)((nK + nks - 1) / nks);
+    cp.nKS = (int)((nK + cp.kch - 1) / cp.kch);
+    cp.n_units = base_units * cp.nKS;
+    const int64_t groups = base_units;
+    cp.part_off = hp.n_part;
+    hp.n_part += groups * cp.nKS * (int64_t)TMC * 32 * vec;
+    cp.cnt_off = hp.n_cnt;
+    hp.n_cnt += groups;
+  }
   if (tma) {  // units are tiles of TMA_ROWS rows x one case tile (2 or 4 KB of cases)
     const int64_t nct = (B * st->esz + (rowi ? 1024 : 2048) - 1) / (rowi ? 1024 : 2048);
     cp.n_units = (rowi ? 1 : nI) * cp.nT * nct;
@@ -1206,6 +1226,8 @@ static int launch_group(jt_state* st, const Program* pr, const WaveRt& w, const 
     c.n_passes = g.n_cpasses;
     c.n_units = g.n_units;
     c.B = st->B;
+    c.partials = pr->d_part;
+    c.counters = pr->d_cnt;
     if (use_tma_contract()) CK(launch_contract_tma(st->plan->dtype, g.m, c, g.grid, s));
     else CK(launch_contract(st->plan->dtype, g.lm, g.m, c, g.grid, s));
     st->launches++;

@@ -113,6 +113,9 @@ struct CPass {
   int nI, nS, nK, nG, nE, nT, nBC;
   int nCG;                  // case-chunk groups: a unit walks chunks cg, cg + nCG, ...
   int rowi;                 // 1: nS == 1, units are TMC consecutive i (W layout [nI][nK])
+  int nKS;                  // > 1: K split into nKS chunks of kch (units also index the chunk);
+  int kch;                  //   partial sums combined in chunk order by the last warp of a group
+  int64_t part_off, cnt_off;
   int out_kind;
   int64_t out_off, ratio_off, out2_off;
   int64_t gfac_off[MAXF];   // aux offsets of the G factors
@@ -128,6 +131,8 @@ struct CArgs {
   int n_passes;
   int64_t n_units;
   int B;
+  double* partials;         // K-split partial sums
+  int* counters;            // K-split arrival counters (reset by the last warp)
 };
 constexpr int CKF = 16;     // fp32 contraction sums longer than this fold into fp64
 cudaError_t launch_contract(int dtype, int fold, int rowi, const CArgs& a, int grid, cudaStream_t s);

@@ -1038,20 +1038,25 @@ __global__ void __launch_bounds__(NT, 2) contract_kernel(const CArgs a) {
     while (pi > 0 && u < a.passes[pi].unit0) --pi;
     const CPass* __restrict__ P = a.passes + pi;
     const int64_t ul = u - P->unit0;
-    const int nT = P->nT, nCG = P->nCG;
+    const int nT = P->nT, nCG = P->nCG, nKS = P->nKS;
+    // unit = (i, t, ks, cg), case chunk fastest: concurrent warps share factor rows
     const int cg = (int)(ul % nCG);
-    const int t = (int)((ul / nCG) % nT);
-    const int64_t i = ul / ((int64_t)nCG * nT);
-    const int nS = P->nS, nK = P->nK, nG = P->nG, nE = P->nE;
+    const int ks = (int)((ul / nCG) % nKS);
+    const int t = (int)((ul / ((int64_t)nCG * nKS)) % nT);
+    const int64_t i = ul / ((int64_t)nCG * nKS * nT);
+    const int nS = P->nS, nG = P->nG, nE = P->nE;
+    const int kb = ks * P->kch;                      // this unit's k range [kb, kb + nK)
+    const int nK = min(P->nK - kb, P->kch);
+    const int nKall = P->nK;
     const int nSp = (nS + 7) & ~7;
     const int bstep = 32 * VEC * nCG;
     const int s0 = t * TMC;
     const int rows = min(TMC, nS - s0);
     const int32_t* __restrict__ ti = a.tab + P->ti_off + i * (nG + nE + 1);
-    const int32_t* __restrict__ tk = a.tab + P->tk_off;
+    const int32_t* __restrict__ tk = a.tab + P->tk_off + (int64_t)kb * nG;
     const int32_t* __restrict__ ts = a.tab + P->ts_off;
-    const T* __restrict__ wrow = W + P->w_off + i * (int64_t)nK * nSp + s0;
-    const T* gq[CMAXG];  // factor g at (i, k = 0, case 0)
+    const T* __restrict__ wrow = W + P->w_off + (i * (int64_t)nKall + kb) * nSp + s0;
+    const T* gq[CMAXG];  // factor g at (i, k = kb, case 0)
 #pragma unroll
     for (int g = 0; g < CMAXG; ++g) gq[g] = aux_c + (g < nG ? P->gfac_off[g] + __ldg(ti + g) : 0);
     for (int b0 = cg * 32 * VEC + lane * VEC; b0 < a.B; b0 += bstep) {
@@ -1116,6 +1121,35 @@ __global__ void __launch_bounds__(NT, 2) contract_kernel(const CArgs a) {
               part[r][l] = (T)0;
             }
         }
+      }
+      if (nKS > 1) {
+        // K-split: park this chunk's sums; the last warp of the (i, t, case chunk)
+        // group adds the nKS partials in chunk order and runs the epilogue
+        const int64_t grp = ((i * nT + t) * (int64_t)nCG + cg);
+        double* pp = a.partials + P->part_off + (grp * nKS) * (TMC * 32 * VEC);
+#pragma unroll
+        for (int r = 0; r < TMC; ++r)
+#pragma unroll
+          for (int l = 0; l < VEC; ++l)
+            __stcg(pp + (int64_t)ks * (TMC * 32 * VEC) + (r * 32 + lane) * VEC + l,
+                   FOLD ? cacc[(r * VEC + l) * NT + threadIdx.x] : (double)part[r][l]);
+        __threadfence();
+        __syncwarp();
+        int arrived = 0;
+        if (lane == 0) arrived = atomicAdd(a.counters + P->cnt_off + grp, 1);
+        arrived = __shfl_sync(0xffffffffu, arrived, 0);
+        if (arrived != nKS - 1) continue;
+        __threadfence();
+        if (lane == 0) a.counters[P->cnt_off + grp] = 0;
+#pragma unroll
+        for (int r = 0; r < TMC; ++r)
+#pragma unroll
+          for (int l = 0; l < VEC; ++l) {
+            double t_ = 0.0;
+            for (int q = 0; q < nKS; ++q) t_ += __ldcg(pp + (int64_t)q * (TMC * 32 * VEC) + (r * 32 + lane) * VEC + l);
+            if (FOLD) cacc[(r * VEC + l) * NT + threadIdx.x] = t_;
+            else part[r][l] = (T)t_;  // fp64 passes only (fp32 K-split passes always fold)
+          }
       }
 #pragma unroll
       for (int r = 0; r < TMC; ++r) {
