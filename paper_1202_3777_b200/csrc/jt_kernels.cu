@@ -1177,12 +1177,12 @@ __global__ void __launch_bounds__(NT, 2) contract_kernel(const CArgs a) {
 // warp streams their factor rows — KU x TMC x nG independent vector loads in
 // flight per lane — with the same epilogue.
 template <typename T, bool FOLD>
-__global__ void __launch_bounds__(NT, 3) contract_rowi_kernel(const CArgs a) {
+__global__ void __launch_bounds__(NT, FOLD ? 3 : 4) contract_rowi_kernel(const CArgs a) {
   pdl_enter();
-  // one i per warp unit (few registers: three CTAs per SM), KU values of k in
-  // flight, each with its nG factor-row vectors
+  // one i per warp unit (few registers: three or four CTAs per SM), KU values
+  // of k in flight, each with its nG factor-row vectors
   constexpr int VEC = CTraits<T>::VEC;
-  constexpr int KU = 4;
+  constexpr int KU = FOLD ? 4 : 2;
   constexpr int KF = 16;
   T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
   const T* __restrict__ aux_c = aux;
