@@ -303,10 +303,18 @@ def main():
     from paper_1202_3777_b200 import _lib
     from paper_1202_3777_b200.batch import BatchPropagator
 
+    # BENCH_DEVICE_OVERRIDE / BENCH_DIST_BACKEND: smoke-test the multi-rank path on a
+    # single-GPU box (every rank on one device, gloo); production runs use NCCL, one GPU per rank
+    if os.environ.get("BENCH_DEVICE_OVERRIDE") is not None:
+        local = int(os.environ["BENCH_DEVICE_OVERRIDE"])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if world > 1:
