@@ -363,3 +363,37 @@ def test_bench_rows_on_device():  # §8f row 3: bench-style CSV under the device
     row = benchcsv.bench_tree("c1", tree, tables, repeats=2)
     assert set(row) == set(benchcsv.BENCH_COLUMNS)
     assert row["seq_ms"] > 0 and row["par_ms"] > 0 and 0 <= row["overhead_frac"] <= 1
+
+
+@pytest.mark.parametrize("batch", [1, 7, 33])
+def test_batch_odd_sizes_and_partial_micro_batches(batch):
+    """Micro-batches that are not a multiple of the vector width, and a final
+    partial micro-batch (40 cases in steps of `batch`)."""
+    from paper_1202_3777_b200.batch import BatchPropagator
+
+    tree, data = load_golden("c1")
+    tables = synth.scaled_potentials(tree, 0)
+    golden = golden_cases(data)
+    cases = [golden[i % len(golden)][0] for i in range(40)]
+    for mode in ("shared", "materialized"):
+        bp = BatchPropagator(tree, tables, batch=batch, dtype="f64", mode=mode)
+        out = bp.run(cases).cpu().numpy()
+        bp.sync()
+        assert out.shape[0] == 40
+        for i in range(40):
+            assert rel_err(out[i], golden[i % len(golden)][1]) < 1e-10, (mode, batch, i)
+
+
+def test_batch_from_networks_with_components():
+    """Device-initialized batches on the reference corpus (including a network
+    whose tree has two components) against the reference estimator."""
+    from conftest import load_corpus_networks
+    from paper_1202_3777_b200.batch import BatchPropagator
+
+    for name, tree, net, _, rows, want in load_corpus_networks():
+        target = len(net.variables) - 1
+        for mode in ("shared", "materialized"):
+            bp = BatchPropagator(tree, None, batch=4, dtype="f64", mode=mode, query_vars=[target], net=net)
+            got = bp.run(rows).cpu().numpy()
+            bp.sync()
+            assert rel_err(got, want) < 1e-10, (name, mode)
