@@ -636,7 +636,6 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
 
   DevPass& d = bp.d;
   std::memset(&d, 0, sizeof(d));
-  const jt_plan* p = st->plan;
   d.src_arena = ps.src_arena;
   d.src_off = ps.src_arena == A_AUX ? ps.src_off : ps.src_arena == A_CLIQUE ? st->coff[ps.clique] : st->boff[ps.clique];
   d.dst_off = ps.write ? st->coff[ps.clique] : -1;
@@ -680,7 +679,6 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
     d.iout[i] = (int)x.out;
     for (int f = 0; f < nf; ++f) d.ifac[f][i] = (int)x.fac[f];
   }
-  (void)p;
   // block table: j_out-major over the separator dims outside the block, then
   // the remaining outer dims
   std::vector<int> so, ro;
@@ -847,9 +845,6 @@ struct HostProgram {
 };
 
 // ----------------------------------------------------- contraction passes --
-// JT_CONTRACT_TMA=1 selects the experimental TMA-staged contraction kernel
-// (profiles/README.md: not yet faster than the register kernels it would replace)
-static bool use_tma_contract() { return getenv("JT_CONTRACT_TMA") != nullptr; }
 
 static bool contract_eligible(const jt_state* st, const PassSpec& ps) {
   return st->mode == JT_SHARED_BASE && st->B > 1 && st->B % CVEC == 0 && !st->h_base.empty() &&
@@ -990,8 +985,7 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   cp.nG = nG;
   cp.nE = nE;
   cp.rowi = rowi ? 1 : 0;
-  const bool tma = use_tma_contract();
-  const int trows = tma ? (rowi ? TMA_ROWS_R : TMA_ROWS) : (rowi ? 1 : TMC);  // register rowi: one i per unit
+  const int trows = rowi ? 1 : TMC;  // rowi: one i per unit
   cp.nT = rowi ? (int)((nI + trows - 1) / trows) : (int)((nS + trows - 1) / trows);
   cp.nBC = (int)((B + 32 * CVEC - 1) / (32 * CVEC));
   // a unit walks a share of the case chunks of its (i, row tile): all of them for
@@ -1001,7 +995,7 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   cp.kch = (int)nK;
   cp.n_units = (rowi ? 1 : nI) * cp.nT * cp.nCG;
   int64_t min_units = (int64_t)st->num_sms * 8;
-  if (!tma && !rowi && cp.n_units < min_units && nK >= 256) {
+  if (!rowi && cp.n_units < min_units && nK >= 256) {
     // long sums with few units (posteriors of a clique-private variable): split K
     // into chunks of >= 64 k so every warp has work; partials combined in order
     const int vec = st->esz == 4 ? 4 : 2;
@@ -1018,11 +1012,6 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
     hp.n_part += groups * cp.nKS * (int64_t)TMC * 32 * vec;
     cp.cnt_off = hp.n_cnt;
     hp.n_cnt += groups;
-  }
-  if (tma) {  // units are tiles of TMA_ROWS rows x one case tile (2 or 4 KB of cases)
-    const int64_t nct = (B * st->esz + (rowi ? 1024 : 2048) - 1) / (rowi ? 1024 : 2048);
-    cp.n_units = (rowi ? 1 : nI) * cp.nT * nct;
-    min_units = st->num_sms;
   }
   // too few units to fill the GPU (e.g. a posterior over a long factor row):
   // the chunked thread-owned/general passes parallelise over the clique instead
@@ -1151,13 +1140,8 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
         hp.cpasses.push_back(cp);
         hp.cpass_clique.push_back(cpc[key][q]);
       }
-      if (use_tma_contract()) {
-        const int occ = occ_override ? occ_override : contract_tma_ctas_per_sm(st->plan->dtype, cg.m);
-        cg.grid = (int)std::min<int64_t>(cg.n_units, (int64_t)occ * st->num_sms);
-      } else {
-        const int occ = occ_override ? occ_override : contract_max_ctas_per_sm(st->plan->dtype, fold, cg.m);
-        cg.grid = (int)std::min<int64_t>((cg.n_units + NT / 32 - 1) / (NT / 32), (int64_t)occ * st->num_sms);
-      }
+      const int occ = occ_override ? occ_override : contract_max_ctas_per_sm(st->plan->dtype, fold, cg.m);
+      cg.grid = (int)std::min<int64_t>((cg.n_units + NT / 32 - 1) / (NT / 32), (int64_t)occ * st->num_sms);
       rt.groups.push_back(cg);
     }
     rt.n_items = (int)(items.size() - rt.item_base);
@@ -1228,8 +1212,7 @@ static int launch_group(jt_state* st, const Program* pr, const WaveRt& w, const 
     c.B = st->B;
     c.partials = pr->d_part;
     c.counters = pr->d_cnt;
-    if (use_tma_contract()) CK(launch_contract_tma(st->plan->dtype, g.m, c, g.grid, s));
-    else CK(launch_contract(st->plan->dtype, g.lm, g.m, c, g.grid, s));
+    CK(launch_contract(st->plan->dtype, g.lm, g.m, c, g.grid, s));
     st->launches++;
     return JT_OK;
   }

@@ -136,10 +136,6 @@ struct CArgs {
 };
 constexpr int CKF = 16;     // fp32 contraction sums longer than this fold into fp64
 cudaError_t launch_contract(int dtype, int fold, int rowi, const CArgs& a, int grid, cudaStream_t s);
-cudaError_t launch_contract_tma(int dtype, int rowi, const CArgs& a, int grid, cudaStream_t s);
-int contract_tma_ctas_per_sm(int dtype, int rowi);
-constexpr int TMA_ROWS = 8;    // GEMM-mode rows per TMA contraction tile (jt_kernels.cu TROWS)
-constexpr int TMA_ROWS_R = 4;  // row-per-i mode (TROWS_R)
 int contract_max_ctas_per_sm(int dtype, int fold, int rowi);
 
 // device initialize: one entry per clique, one term per CPT, 3 int64 per CPT variable

@@ -1263,323 +1263,6 @@ __global__ void __launch_bounds__(NT, FOLD ? 3 : 4) contract_rowi_kernel(const C
   }
 }
 
-// ---- TMA-staged contraction (the production path for contraction passes) ----
-// The factor rows a stage needs (contiguous runs of cases) are brought into
-// shared memory by 1-D bulk copies (cp.async.bulk, completion on an mbarrier)
-// issued one stage ahead by one thread, so memory-level parallelism no longer
-// depends on registers or occupancy.  A CTA tile is 8 rows x NCt cases:
-//   GEMM mode (nS >= 2): one i, 8 rows of S'; a stage = KCG values of k; each
-//     thread owns VEC cases x 8 rows, computes the factor product of its cases
-//     once per k and reuses it for the 8 rows (W from L1, broadcast).
-//   rowi mode (nS == 1): 8 consecutive i; a stage = one k; each thread owns VEC
-//     cases x 4 rows (two row groups).
-// Tiles are handed out round-robin; the (tile, stage) sequence of a CTA is one
-// continuous two-buffer pipeline, so the next tile's first stage is in flight
-// while the current tile finishes.
-constexpr int TROWS = 8;      // GEMM mode rows per tile (W reuse)
-constexpr int TROWS_R = 4;    // rowi mode: i per tile
-constexpr int KCG = 2;        // GEMM mode: k per stage
-constexpr int NSTAGE = 4;     // stages in flight
-constexpr int STAGE_BYTES = 16 * 1024;
-constexpr int TNT = 128;      // threads per CTA: small CTAs, several per SM, so tiles overlap
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
-struct TmaTile {
-  const CPass* P;
-  int64_t i0;   // GEMM: i; rowi: first i of the tile
-  int s0;       // GEMM: first row of S'
-  int c0;       // first case
-  int nst;      // stages
-  int kcs;      // k per stage (fills STAGE_BYTES)
-};
-
-template <typename T>
-__device__ __forceinline__ void tma_tile_of(const CArgs& a, int64_t tile, int NCt, TmaTile& t) {
-  // tiles: per pass, (i or i-block) x row tiles x case tiles, case tiles fastest
-  int pi = 0;
-  while (pi + 1 < a.n_passes && tile >= a.passes[pi + 1].unit0) ++pi;
-  const CPass* P = a.passes + pi;
-  const int64_t ul = tile - P->unit0;
-  const int nct = (a.B + NCt - 1) / NCt;
-  t.P = P;
-  t.c0 = (int)(ul % nct) * NCt;
-  const int64_t rest = ul / nct;
-  const int per_k = max(1, P->nG) * NCt * (int)sizeof(T) * (P->rowi ? TROWS_R : 1);  // bytes per k
-  t.kcs = max(1, min(STAGE_BYTES / per_k, P->nK));
-  if (P->rowi) {
-    t.i0 = rest * TROWS_R;
-    t.s0 = 0;
-  } else {
-    t.s0 = (int)(rest % P->nT) * TROWS;
-    t.i0 = rest / P->nT;
-  }
-  t.nst = (P->nK + t.kcs - 1) / t.kcs;
-}
-
-// warp 0: issue the bulk copies of stage `st` of tile t into buffer buf — one
-// copy per lane (the lane does its own index-table lookups), after lane 0 has
-// armed the stage's mbarrier with the byte count.
-template <typename T>
-__device__ __forceinline__ void tma_issue(const CArgs& a, const TmaTile& t, int st, int NCt, char* buf,
-                                          uint64_t* bar, int lane) {
-  const CPass* P = t.P;
-  const int nG = P->nG;
-  const int ncase = min(NCt, a.B - t.c0);
-  const uint32_t rb = (uint32_t)ncase * sizeof(T);
-  const int tw = P->nG + P->nE + 1;
-  const int k0 = st * t.kcs, nk = min(t.kcs, P->nK - k0);
-  const int rows = P->rowi ? (int)min((int64_t)TROWS_R, (int64_t)P->nI - t.i0) : 1;
-  const int n_copies = rows * nk * nG;  // slot j = (row * nk + q) * nG + g
-  if (lane == 0) mbar_expect_tx(bar, rb * (uint32_t)n_copies);
-  __syncwarp();
-  for (int j = lane; j < n_copies; j += 32) {
-    const int g = j % nG, q = (j / nG) % nk, row = j / (nG * nk);
-    const int64_t irow = t.i0 + row;
-    const int k = k0 + q;
-    const T* src = reinterpret_cast<const T*>(a.aux) + P->gfac_off[g] + __ldg(a.tab + P->ti_off + irow * tw + g) +
-                   __ldg(a.tab + P->tk_off + (int64_t)k * nG + g) + t.c0;
-    bulk_g2s(buf + (size_t)j * NCt * sizeof(T), src, rb, bar);
-  }
-}
-
-template <typename T, bool ROWI>
-__global__ void __launch_bounds__(TNT, 2) contract_tma_kernel(const CArgs a) {
-  pdl_enter();
-  constexpr int VEC = 16 / sizeof(T);
-  constexpr int NCt = (ROWI ? 1024 : 2048) / (int)sizeof(T);  // cases per tile (one row = 1 or 2 KB)
-  constexpr int LPR = NCt / VEC;                                // threads per row set
-  constexpr int RPT = ROWI ? TROWS_R / (TNT / LPR) : TROWS;     // rows per thread
-  extern __shared__ __align__(128) char smem[];
-  __shared__ uint64_t bars[NSTAGE];
-  T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
-  const T* __restrict__ aux_c = aux;
-  const T* __restrict__ W = reinterpret_cast<const T*>(a.w);
-  const int tid = threadIdx.x;
-  const int n_tiles_total = (int)a.n_units;
-  const int grid = gridDim.x;
-  // this CTA's tiles: blockIdx.x, + grid, ...
-  const int my_tiles = n_tiles_total > (int)blockIdx.x ? (n_tiles_total - 1 - (int)blockIdx.x) / grid + 1 : 0;
-  if (my_tiles == 0) return;
-  if (tid == 0) {
-    for (int b = 0; b < NSTAGE; ++b) mbar_init(&bars[b], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  // producer cursor (warp 0) and consumer cursor walk the same (tile, stage) sequence
-  int p_tile = 0, p_st = 0, issued = 0;
-  TmaTile pt;
-  auto producer_next = [&]() {  // issue the next (tile, stage) into buffer issued % NSTAGE
-    if (p_tile >= my_tiles) return;
-    if (p_st == 0) {
-      const int64_t tile = blockIdx.x + (int64_t)p_tile * grid;
-      tma_tile_of<T>(a, tile, NCt, pt);
-    }
-    tma_issue<T>(a, pt, p_st, NCt, smem + (size_t)(issued % NSTAGE) * STAGE_BYTES, &bars[issued % NSTAGE],
-                 tid & 31);
-    ++issued;
-    if (++p_st >= pt.nst) {
-      p_st = 0;
-      ++p_tile;
-    }
-  };
-  if (tid < 32)
-    for (int q = 0; q < NSTAGE; ++q) producer_next();
-  int consumed = 0;
-  for (int lt = 0; lt < my_tiles; ++lt) {
-    const int64_t tile = blockIdx.x + (int64_t)lt * grid;
-    TmaTile t;
-    tma_tile_of<T>(a, tile, NCt, t);
-    const CPass* __restrict__ P = t.P;
-    const int nG = P->nG, nE = P->nE, nK = P->nK, nS = P->nS;
-    const int tw = nG + nE + 1;
-    const int32_t* __restrict__ ti = a.tab + P->ti_off;
-    const int32_t* __restrict__ ts = a.tab + P->ts_off;
-    constexpr bool rowi = ROWI;
-    const int rg = tid / LPR;          // GEMM: 0, rowi: 0..1
-    const int cl = (tid % LPR) * VEC;  // case offset within the tile
-    const int c = t.c0 + cl;
-    const bool live = c < a.B;
-    const int nSp = (nS + 7) & ~7;
-    T part[RPT][VEC];
-#pragma unroll
-    for (int r = 0; r < RPT; ++r)
-#pragma unroll
-      for (int l = 0; l < VEC; ++l) part[r][l] = (T)0;
-    double acc[RPT][VEC];
-#pragma unroll
-    for (int r = 0; r < RPT; ++r)
-#pragma unroll
-      for (int l = 0; l < VEC; ++l) acc[r][l] = 0.0;
-    for (int st = 0; st < t.nst; ++st) {
-      const int buf = consumed % NSTAGE;
-      mbar_wait(&bars[buf], (uint32_t)((consumed / NSTAGE) & 1));
-      const T* sb = reinterpret_cast<const T*>(smem + (size_t)buf * STAGE_BYTES);
-      if (live) {
-        if (!rowi) {
-          const int k0 = st * t.kcs, nk = min(t.kcs, nK - k0);
-          const T* wb = W + P->w_off + (t.i0 * (int64_t)nK + k0) * nSp + t.s0;
-          for (int q = 0; q < nk; ++q) {
-            T pv[VEC];
-#pragma unroll
-            for (int l = 0; l < VEC; ++l) pv[l] = (T)1;
-            for (int g = 0; g < nG; ++g) {
-              T f[VEC];
-              load_vec<T, VEC>(sb + (size_t)(q * nG + g) * NCt + cl, f);
-#pragma unroll
-              for (int l = 0; l < VEC; ++l) pv[l] *= f[l];
-            }
-            const T* wq = wb + (int64_t)q * nSp;
-#pragma unroll
-            for (int r = 0; r < TROWS; ++r) {
-              const T w = (t.s0 + r < nS) ? __ldg(wq + r) : (T)0;
-#pragma unroll
-              for (int l = 0; l < VEC; ++l) part[r][l] += w * pv[l];
-            }
-          }
-        } else {
-          const int rows = (int)min((int64_t)TROWS_R, (int64_t)P->nI - t.i0);
-          const int k0 = st * t.kcs, nk = min(t.kcs, nK - k0);
-#pragma unroll
-          for (int rr = 0; rr < RPT; ++rr) {
-            const int r = rg * RPT + rr;
-            if (r >= rows) continue;
-            for (int q = 0; q < nk; ++q) {
-              T pv[VEC];
-#pragma unroll
-              for (int l = 0; l < VEC; ++l) pv[l] = (T)1;
-              for (int g = 0; g < nG; ++g) {
-                T f[VEC];
-                load_vec<T, VEC>(sb + (size_t)((r * nk + q) * nG + g) * NCt + cl, f);
-#pragma unroll
-                for (int l = 0; l < VEC; ++l) pv[l] *= f[l];
-              }
-              const T w = __ldg(W + P->w_off + (t.i0 + r) * (int64_t)nK + k0 + q);
-#pragma unroll
-              for (int l = 0; l < VEC; ++l) part[rr][l] += w * pv[l];
-            }
-          }
-        }
-      }
-      ++consumed;
-      // fold fp32 partial sums into fp64 every CKF terms (GEMM: every CKF/KCG stages)
-      if (sizeof(T) == 4) {  // fold the fp32 partial sums (<= kcs terms) into fp64 every stage
-#pragma unroll
-        for (int r = 0; r < RPT; ++r)
-#pragma unroll
-          for (int l = 0; l < VEC; ++l) {
-            acc[r][l] += (double)part[r][l];
-            part[r][l] = (T)0;
-          }
-      }
-      __syncthreads();  // every thread is done with this buffer
-      if (tid < 32) producer_next();
-    }
-    if (sizeof(T) == 8) {
-#pragma unroll
-      for (int r = 0; r < RPT; ++r)
-#pragma unroll
-        for (int l = 0; l < VEC; ++l) acc[r][l] = (double)part[r][l];
-    }
-    if (!live) continue;
-    // epilogue: E factors, then the Hugin update of each row's VEC cases
-#pragma unroll
-    for (int rr = 0; rr < RPT; ++rr) {
-      int64_t i;
-      int srow;
-      if (rowi) {
-        i = t.i0 + rg * RPT + rr;
-        srow = 0;
-        if (i >= P->nI) continue;
-      } else {
-        i = t.i0;
-        srow = t.s0 + rr;
-        if (srow >= nS) continue;
-      }
-      const int32_t* tir = ti + i * tw;
-      const int32_t* tsr = ts + (int64_t)srow * (nE + 1);
-      double v[VEC];
-#pragma unroll
-      for (int l = 0; l < VEC; ++l) v[l] = acc[rr][l];
-      for (int e = 0; e < nE; ++e) {
-        T f[VEC];
-        load_vec_ro<T, VEC>(aux_c + P->efac_off[e] + __ldg(tir + nG + e) + __ldg(tsr + e) + c, f);
-#pragma unroll
-        for (int l = 0; l < VEC; ++l) v[l] *= (double)f[l];
-      }
-      finalize_lanes<T, VEC>(P->out_kind, P->out_off, P->ratio_off, P->out2_off,
-                             (int64_t)__ldg(tir + nG + nE) + __ldg(tsr + nE) + c, v, aux, a.qout, a.err);
-    }
-  }
-}
-
-template <typename T, bool ROWI>
-static cudaError_t launch_tma_t(const CArgs& a, int grid, cudaStream_t s) {
-  const int smem = NSTAGE * STAGE_BYTES;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(contract_tma_kernel<T, ROWI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  return launch_pdl(contract_tma_kernel<T, ROWI>, grid, TNT, smem, s, a);
-}
-
-int contract_tma_ctas_per_sm(int dtype, int rowi) {
-  int n = 0;
-  const int smem = NSTAGE * STAGE_BYTES;
-  if (dtype == 0) {
-    if (rowi) {
-      cudaFuncSetAttribute(contract_tma_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_tma_kernel<float, true>, TNT, smem);
-    } else {
-      cudaFuncSetAttribute(contract_tma_kernel<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_tma_kernel<float, false>, TNT, smem);
-    }
-  } else {
-    if (rowi) {
-      cudaFuncSetAttribute(contract_tma_kernel<double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_tma_kernel<double, true>, TNT, smem);
-    } else {
-      cudaFuncSetAttribute(contract_tma_kernel<double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_tma_kernel<double, false>, TNT, smem);
-    }
-  }
-  return n > 0 ? n : 1;
-}
-
-cudaError_t launch_contract_tma(int dtype, int rowi, const CArgs& a, int grid, cudaStream_t s) {
-  if (grid <= 0 || a.n_units <= 0) return cudaSuccess;
-  if (dtype == 0) return rowi ? launch_tma_t<float, true>(a, grid, s) : launch_tma_t<float, false>(a, grid, s);
-  return rowi ? launch_tma_t<double, true>(a, grid, s) : launch_tma_t<double, false>(a, grid, s);
-}
-
 constexpr size_t CFOLD_SMEM = (size_t)TMC * 4 * NT * sizeof(double);  // fp32 fold accumulators
 
 cudaError_t launch_contract(int dtype, int fold, int rowi, const CArgs& a, int grid, cudaStream_t s) {
