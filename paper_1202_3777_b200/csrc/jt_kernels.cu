@@ -557,13 +557,20 @@ __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
       T v[KV][VEC];
       const int64_t* e[KV];
       bool ok[KV];
+      // block-table lookups of every slot first, then the data loads: the KV
+      // loads issue back to back instead of each waiting on its own lookup
+      int64_t so[KV];
 #pragma unroll
       for (int k = 0; k < KV; ++k) {
         const int64_t bi = bb + q_slot[k];
         ok[k] = q_ok[k] && bi < b1;
         e[k] = blk + (ok[k] ? bi : b0) * bs;
+        so[k] = __ldg(e[k]) + q_src[k];
+      }
+#pragma unroll
+      for (int k = 0; k < KV; ++k) {
         if (ok[k]) {
-          const T* p = srcA + e[k][0] + q_src[k];
+          const T* p = srcA + so[k];
           if (VEC == 1 || P.src_vec) {
             load_vec<T, VEC>(p, v[k]);
           } else {
@@ -581,10 +588,13 @@ __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
         if (f < nf) {
           const T* fb = aux + P.fac_off[f];
           const bool fv = (P.fac_vec >> f) & 1u;
+          int64_t fo[KV];
+#pragma unroll
+          for (int k = 0; k < KV; ++k) fo[k] = __ldg(e[k] + 2 + f) + s_qfac[f][k][tid];
 #pragma unroll
           for (int k = 0; k < KV; ++k) {
             if (ok[k]) {
-              const T* p = fb + e[k][2 + f] + s_qfac[f][k][tid];
+              const T* p = fb + fo[k];
               T g[VEC];
               if (VEC == 1 || fv) {
                 load_vec_ro<T, VEC>(p, g);
