@@ -215,6 +215,23 @@ struct Program {
   }
 };
 
+// Whole-propagation program for a small tree held in one cluster's shared memory
+// (jt_cluster.cu).  ok == false: the tree does not fit / the device cannot run it.
+struct ClusterProg {
+  bool ok = false;
+  int n_ranks = 0, smem = 0, n_segs = 0, n_levels = 0;
+  ClusterSeg* d_segs = nullptr;
+  ClusterMsg* d_msgs = nullptr;
+  ClusterTgt* d_tgts = nullptr;
+  ClusterLevel* d_levels = nullptr;
+  ~ClusterProg() {
+    cudaFree(d_segs);
+    cudaFree(d_msgs);
+    cudaFree(d_tgts);
+    cudaFree(d_levels);
+  }
+};
+
 // ------------------------------------------------------------------ state --
 struct jt_state {
   const jt_plan* plan = nullptr;
@@ -248,6 +265,7 @@ struct jt_state {
   int32_t* d_obs = nullptr;                 // observation staging (case, var, state) + fill list
   int64_t obs_cap = 0;
   std::map<std::string, std::unique_ptr<Program>> programs;
+  std::map<std::string, std::unique_ptr<struct ClusterProg>> cprogs;  // small trees in cluster smem
   int64_t launches = 0;
   int64_t device_bytes = 0;
   bool fresh = true;        // separators hold ones (reset/load): collect may skip old/ratio
@@ -262,6 +280,7 @@ struct jt_state {
   std::vector<double> h_base;
   ~jt_state() {
     programs.clear();
+    cprogs.clear();
     cudaFree(d_clique);
     cudaFree(d_base);
     cudaFree(d_aux);
@@ -2021,6 +2040,188 @@ static int resolve_roots(const jt_state* st, const int32_t* roots_or_null, std::
   return JT_OK;
 }
 
+// Build the cluster program of a single-tree (B == 1, materialized) propagation:
+// bin-pack every clique, separator and ratio table onto the fewest cluster
+// ranks whose shared memory holds them, then list the levels (collect by
+// height, distribute by depth) with their messages and target cliques.
+static int build_cluster_prog(jt_state* st, const std::vector<int>& roots, ClusterProg& cp) {
+  const jt_plan* p = st->plan;
+  cp.ok = false;
+  // opt-in (JT_CLUSTER=1): correct (the GPU suite passes with it) but still slower
+  // than the graph-replayed wave program — see profiles/README.md r05
+  if (st->B != 1 || st->mode != JT_MATERIALIZED || !getenv("JT_CLUSTER")) return JT_OK;
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device);
+  const int64_t cap = (int64_t)(optin - 2048) / st->esz;  // elements per rank
+  if (cap <= 0) return JT_OK;
+  // tables: cliques, separators, ratio scratch (one per separator)
+  struct Tab { int64_t size; int kind, id; int rank = -1; int64_t off = 0; };
+  std::vector<Tab> tabs;
+  for (int c = 0; c < p->n_cliques; ++c) tabs.push_back({p->csize[c], 0, c});
+  for (int sp = 0; sp < p->n_seps; ++sp) tabs.push_back({p->ssize[sp], 1, sp});
+  for (int sp = 0; sp < p->n_seps; ++sp) tabs.push_back({p->ssize[sp], 2, sp});
+  for (auto& t : tabs)
+    if (align4(t.size) > cap) return JT_OK;
+  std::vector<int> order(tabs.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return tabs[a].size > tabs[b].size; });
+  int n_ranks = 0;
+  for (int nr = 1; nr <= CL_MAX_RANKS && !n_ranks; nr *= 2) {  // fewest ranks that hold everything
+    std::vector<int64_t> used(nr, 0);
+    bool fit = true;
+    for (int i : order) {
+      int best = -1;
+      for (int r = 0; r < nr; ++r)
+        if (used[r] + align4(tabs[i].size) <= cap && (best < 0 || used[r] < used[best])) best = r;
+      if (best < 0) {
+        fit = false;
+        break;
+      }
+      tabs[i].rank = best;
+      tabs[i].off = used[best];
+      used[best] += align4(tabs[i].size);
+    }
+    if (fit) {
+      n_ranks = nr;
+      int64_t mx = 0;
+      for (auto u : used) mx = std::max(mx, u);
+      cp.smem = (int)(std::max<int64_t>(mx, 4) * st->esz);
+    }
+  }
+  if (!n_ranks) return JT_OK;
+  if (cluster_prop_supported(p->dtype, n_ranks, cp.smem) <= 0) return JT_OK;
+  cp.n_ranks = n_ranks;
+  auto tab_of = [&](int kind, int id) -> const Tab& { return tabs[(kind == 0 ? 0 : kind == 1 ? p->n_cliques : p->n_cliques + p->n_seps) + id]; };
+  std::vector<ClusterSeg> segs;
+  for (auto& t : tabs) {
+    if (t.kind == 2) continue;
+    ClusterSeg g;
+    g.rank = t.rank;
+    g.lofs = (int)t.off;
+    g.len = (int)t.size;
+    g.arena = t.kind == 0 ? A_CLIQUE : A_AUX;
+    g.gofs = t.kind == 0 ? st->coff[t.id] : sep_cur(st, t.id);
+    g.writeback = 1;
+    segs.push_back(g);
+  }
+  Orient o = orient(p, roots);
+  std::vector<ClusterMsg> msgs;
+  std::vector<ClusterTgt> tgts;
+  std::vector<ClusterLevel> levels;
+  auto strides_of = [&](const std::vector<int>& vars) {
+    std::vector<int64_t> st_(vars.size(), 1);
+    for (int i = (int)vars.size() - 2; i >= 0; --i) st_[i] = st_[i + 1] * p->cards[vars[i + 1]];
+    return st_;
+  };
+  auto make_msg = [&](int src, int sp, ClusterMsg& m) -> bool {
+    std::memset(&m, 0, sizeof(m));
+    const auto& cv = p->cvars[src];
+    const auto& sv = p->svars[sp];
+    if ((int)cv.size() > CL_MAXD) return false;
+    const auto cst = strides_of(cv);
+    const Tab& ts = tab_of(0, src);
+    const Tab& tsep = tab_of(1, sp);
+    const Tab& trat = tab_of(2, sp);
+    m.src_rank = ts.rank;
+    m.src_off = (int)ts.off;
+    m.sep_rank = tsep.rank;
+    m.sep_off = (int)tsep.off;
+    m.rat_rank = trat.rank;
+    m.rat_off = (int)trat.off;
+    m.L = (int)(p->csize[src] / std::max<int64_t>(1, p->ssize[sp]));
+    for (int v : sv) {
+      const int pos = (int)(std::lower_bound(cv.begin(), cv.end(), v) - cv.begin());
+      m.sd_card[m.nsd] = p->cards[v];
+      m.sd_stride[m.nsd] = (int)cst[pos];
+      m.nsd++;
+    }
+    for (size_t i = 0; i < cv.size(); ++i)
+      if (!std::binary_search(sv.begin(), sv.end(), cv[i])) {
+        m.rd_card[m.nrd] = p->cards[cv[i]];
+        m.rd_stride[m.nrd] = (int)cst[i];
+        m.nrd++;
+      }
+    return true;
+  };
+  // one level: (src, tgt, sep) messages
+  auto add_level = [&](const std::vector<std::array<int, 3>>& lm) -> bool {
+    if (lm.empty()) return true;
+    if ((int)lm.size() > 512) return false;  // jt_cluster.cu CL_LVL_MAX
+    ClusterLevel L{};
+    L.m0 = (int)msgs.size();
+    L.t0 = (int)tgts.size();
+    std::map<int, std::vector<int>> into;  // target clique -> message indices
+    for (auto& x : lm) {
+      ClusterMsg m;
+      if (!make_msg(x[0], x[2], m)) return false;
+      const bool lng = m.L > 32;
+      m.short0 = L.n_short;
+      m.long0 = L.n_long;
+      (lng ? L.n_long : L.n_short) += p->ssize[x[2]];
+      into[x[1]].push_back((int)msgs.size());
+      msgs.push_back(m);
+    }
+    L.m1 = (int)msgs.size();
+    for (auto& kv : into) {
+      const int t = kv.first;
+      const auto& tv = p->cvars[t];
+      if ((int)tv.size() > CL_MAXD || (int)kv.second.size() > CL_MAXIN) return false;
+      ClusterTgt G;
+      std::memset(&G, 0, sizeof(G));
+      const Tab& tt = tab_of(0, t);
+      G.rank = tt.rank;
+      G.off = (int)tt.off;
+      G.size = (int)p->csize[t];
+      G.nd = (int)tv.size();
+      for (int d = 0; d < G.nd; ++d) G.card[d] = p->cards[tv[d]];
+      G.nin = (int)kv.second.size();
+      for (int k = 0; k < G.nin; ++k) {
+        G.msg[k] = kv.second[k];
+        const int sp = lm[kv.second[k] - L.m0][2];
+        const auto& sv = p->svars[sp];
+        const auto sst = strides_of(sv);
+        for (int d = 0; d < G.nd; ++d) {
+          auto it = std::lower_bound(sv.begin(), sv.end(), tv[d]);
+          G.sstride[k][d] = (it != sv.end() && *it == tv[d]) ? (int)sst[it - sv.begin()] : 0;
+        }
+      }
+      G.chunk0 = L.n_elem_chunks;
+      L.n_elem_chunks += (G.size + CL_CHUNK - 1) / CL_CHUNK;
+      tgts.push_back(G);
+    }
+    L.t1 = (int)tgts.size();
+    levels.push_back(L);
+    return true;
+  };
+  for (int h = 0; h <= o.max_height; ++h) {  // collect: children of height h send to their parents
+    std::vector<std::array<int, 3>> lm;
+    for (int c = 0; c < p->n_cliques; ++c)
+      if (o.height[c] == h && o.parent[c] >= 0) lm.push_back({c, o.parent[c], o.psep[c]});
+    if (!add_level(lm)) return JT_OK;
+  }
+  for (int d = 0; d <= o.max_depth; ++d) {  // distribute: depth d sends to its children
+    std::vector<std::array<int, 3>> lm;
+    for (int c = 0; c < p->n_cliques; ++c)
+      if (o.depth[c] == d)
+        for (auto& ch : o.children[c]) lm.push_back({c, ch.first, ch.second});
+    if (!add_level(lm)) return JT_OK;
+  }
+  auto up = [&](auto** dptr, const auto& vec) -> int {
+    using E = typename std::decay_t<decltype(vec)>::value_type;
+    CK(cudaMalloc((void**)dptr, std::max<size_t>(vec.size(), 1) * sizeof(E)));
+    if (!vec.empty()) CK(cudaMemcpy(*dptr, vec.data(), vec.size() * sizeof(E), cudaMemcpyHostToDevice));
+    return JT_OK;
+  };
+  int rc;
+  if ((rc = up(&cp.d_segs, segs)) || (rc = up(&cp.d_msgs, msgs)) || (rc = up(&cp.d_tgts, tgts)) ||
+      (rc = up(&cp.d_levels, levels)))
+    return rc;
+  cp.n_segs = (int)segs.size();
+  cp.n_levels = (int)levels.size();
+  cp.ok = true;
+  return JT_OK;
+}
+
 extern "C" int jt_propagate(jt_state* st, const int32_t* roots_or_null, void* stream) {
   if (!st) return JT_ERR_BAD_ARG;
   DevGuard g(st->plan->device);
@@ -2029,6 +2230,35 @@ extern "C" int jt_propagate(jt_state* st, const int32_t* roots_or_null, void* st
   if (rc) return rc;
   cudaStream_t s = pick_stream(st, stream);
   const bool fresh = st->fresh;
+  if (st->B == 1 && st->mode == JT_MATERIALIZED) {
+    // small trees: the whole propagation in one cluster's shared memory, one launch
+    const std::string ckey = key_of("cl", roots, {(int)st->sep_in_y});
+    auto cit = st->cprogs.find(ckey);
+    if (cit == st->cprogs.end()) {
+      auto cpn = std::make_unique<ClusterProg>();
+      if ((rc = build_cluster_prog(st, roots, *cpn))) return rc;
+      cit = st->cprogs.emplace(ckey, std::move(cpn)).first;
+    }
+    ClusterProg* cp = cit->second.get();
+    if (cp->ok) {
+      if ((rc = ensure_seps(st, s))) return rc;
+      ClusterArgs a;
+      a.clique = st->d_clique;
+      a.aux = st->d_aux;
+      a.err = st->d_err;
+      a.segs = cp->d_segs;
+      a.n_segs = cp->n_segs;
+      a.msgs = cp->d_msgs;
+      a.tgts = cp->d_tgts;
+      a.levels = cp->d_levels;
+      a.n_levels = cp->n_levels;
+      CK(launch_cluster_prop(st->plan->dtype, a, cp->n_ranks, cp->smem, s));
+      st->launches++;
+      st->fresh = false;
+      st->seps_stale = false;
+      return JT_OK;
+    }
+  }
   if (!fresh && (rc = ensure_seps(st, s))) return rc;
   std::vector<int> tag{(int)fresh, (int)st->sep_in_y};
   std::vector<int> kv = active_ev(st);

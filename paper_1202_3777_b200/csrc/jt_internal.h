@@ -138,6 +138,49 @@ constexpr int CKF = 16;     // fp32 contraction sums longer than this fold into 
 cudaError_t launch_contract(int dtype, int fold, int rowi, const CArgs& a, int grid, cudaStream_t s);
 int contract_max_ctas_per_sm(int dtype, int fold, int rowi);
 
+// ---- small trees in cluster shared memory (jt_cluster.cu) ----
+constexpr int CL_MAX_RANKS = 16;  // CTAs per cluster (non-portable above 8)
+constexpr int CL_MAXD = 16;       // dims per clique
+constexpr int CL_MAXIN = 16;      // messages into one target in one level
+constexpr int CL_CHUNK = 16;      // target elements per thread item
+constexpr int CL_THREADS = 256;
+struct ClusterSeg {               // a table's home: (rank, local offset) <-> HBM copy
+  int rank, lofs, len, arena, writeback;
+  int64_t gofs;
+};
+struct ClusterMsg {
+  int src_rank, src_off, sep_rank, sep_off, rat_rank, rat_off;
+  int L;                          // row length |src| / |sep|
+  int nsd, nrd;
+  int sd_card[CL_MAXD], sd_stride[CL_MAXD];  // separator digits (separator order) -> src stride
+  int rd_card[CL_MAXD], rd_stride[CL_MAXD];  // remaining src dims (ascending) -> src stride
+  int64_t short0, long0;          // prefix counts of thread-row / warp-row entries in the level
+};
+struct ClusterTgt {
+  int rank, off, size, nd, nin;
+  int card[CL_MAXD];
+  int msg[CL_MAXIN];
+  int sstride[CL_MAXIN][CL_MAXD]; // per incoming message: separator stride of each target dim
+  int64_t chunk0;                 // prefix count of element chunks in the level
+};
+struct ClusterLevel {
+  int m0, m1, t0, t1;
+  int64_t n_short, n_long, n_elem_chunks;
+};
+struct ClusterArgs {
+  void* clique;
+  void* aux;
+  int* err;
+  const ClusterSeg* segs;
+  int n_segs;
+  const ClusterMsg* msgs;
+  const ClusterTgt* tgts;
+  const ClusterLevel* levels;
+  int n_levels;
+};
+cudaError_t launch_cluster_prop(int dtype, const ClusterArgs& a, int n_ranks, int smem_bytes, cudaStream_t s);
+int cluster_prop_supported(int dtype, int n_ranks, int smem_bytes);
+
 // device initialize: one entry per clique, one term per CPT, 3 int64 per CPT variable
 // (clique stride, card, CPT stride)
 struct InitClique {

@@ -397,3 +397,19 @@ def test_batch_from_networks_with_components():
             got = bp.run(rows).cpu().numpy()
             bp.sync()
             assert rel_err(got, want) < 1e-10, (name, mode)
+
+
+def test_cluster_smem_propagation_matches_reference(monkeypatch):
+    """Opt-in whole-tree-in-cluster-shared-memory propagation (JT_CLUSTER=1):
+    same posteriors and final tables as the reference on c1 and c2."""
+    monkeypatch.setenv("JT_CLUSTER", "1")
+    for name in ("c1", "c2"):
+        tree, data = load_golden(name)
+        tables = synth.scaled_potentials(tree, 0)
+        for ev, want in golden_cases(data)[:3]:
+            st = P().from_potentials(tree, tables, engine=P().CudaEngine(dtype="f32"))
+            if ev:
+                P().apply_evidence(st, ev)
+            P().belief_propagation(st)
+            got = all_posteriors(st, len(tree.cards))
+            assert rel_err(got, want) < 1e-5, (name, ev)
