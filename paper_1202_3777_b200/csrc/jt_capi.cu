@@ -219,15 +219,15 @@ struct Program {
 // (jt_cluster.cu).  ok == false: the tree does not fit / the device cannot run it.
 struct ClusterProg {
   bool ok = false;
-  int n_ranks = 0, smem = 0, n_segs = 0, n_levels = 0;
+  int n_ranks = 0, smem = 0, n_levels = 0, table_elems = 0;
   ClusterSeg* d_segs = nullptr;
-  ClusterMsg* d_msgs = nullptr;
-  ClusterTgt* d_tgts = nullptr;
+  int* d_seg_begin = nullptr;
+  int* d_blob = nullptr;
   ClusterLevel* d_levels = nullptr;
   ~ClusterProg() {
     cudaFree(d_segs);
-    cudaFree(d_msgs);
-    cudaFree(d_tgts);
+    cudaFree(d_seg_begin);
+    cudaFree(d_blob);
     cudaFree(d_levels);
   }
 };
@@ -2081,115 +2081,117 @@ static int build_cluster_prog(jt_state* st, const std::vector<int>& roots, Clust
       tabs[i].off = used[best];
       used[best] += align4(tabs[i].size);
     }
-    if (fit) {
-      n_ranks = nr;
-      int64_t mx = 0;
-      for (auto u : used) mx = std::max(mx, u);
-      cp.smem = (int)(std::max<int64_t>(mx, 4) * st->esz);
-    }
+    if (fit) n_ranks = nr;
   }
   if (!n_ranks) return JT_OK;
-  if (cluster_prop_supported(p->dtype, n_ranks, cp.smem) <= 0) return JT_OK;
-  cp.n_ranks = n_ranks;
-  auto tab_of = [&](int kind, int id) -> const Tab& { return tabs[(kind == 0 ? 0 : kind == 1 ? p->n_cliques : p->n_cliques + p->n_seps) + id]; };
+  auto tab_of = [&](int kind, int id) -> const Tab& {
+    return tabs[(kind == 0 ? 0 : kind == 1 ? p->n_cliques : p->n_cliques + p->n_seps) + id];
+  };
+  int64_t table_elems = 0;
+  for (auto& t : tabs) table_elems = std::max<int64_t>(table_elems, t.off + align4(t.size));
+  // segments (HBM <-> shared memory copies), grouped by rank
   std::vector<ClusterSeg> segs;
-  for (auto& t : tabs) {
-    if (t.kind == 2) continue;
-    ClusterSeg g;
-    g.rank = t.rank;
-    g.lofs = (int)t.off;
-    g.len = (int)t.size;
-    g.arena = t.kind == 0 ? A_CLIQUE : A_AUX;
-    g.gofs = t.kind == 0 ? st->coff[t.id] : sep_cur(st, t.id);
-    g.writeback = 1;
-    segs.push_back(g);
+  std::vector<int> seg_begin(n_ranks + 1, 0);
+  for (int r = 0; r < n_ranks; ++r) {
+    seg_begin[r] = (int)segs.size();
+    for (auto& t : tabs) {
+      if (t.kind == 2 || t.rank != r) continue;
+      ClusterSeg g;
+      g.rank = t.rank;
+      g.lofs = (int)t.off;
+      g.len = (int)t.size;
+      g.arena = t.kind == 0 ? A_CLIQUE : A_AUX;
+      g.gofs = t.kind == 0 ? st->coff[t.id] : sep_cur(st, t.id);
+      segs.push_back(g);
+    }
   }
+  seg_begin[n_ranks] = (int)segs.size();
   Orient o = orient(p, roots);
-  std::vector<ClusterMsg> msgs;
-  std::vector<ClusterTgt> tgts;
+  std::vector<int> blob;
   std::vector<ClusterLevel> levels;
+  int max_blob = 0;
   auto strides_of = [&](const std::vector<int>& vars) {
     std::vector<int64_t> st_(vars.size(), 1);
     for (int i = (int)vars.size() - 2; i >= 0; --i) st_[i] = st_[i + 1] * p->cards[vars[i + 1]];
     return st_;
   };
-  auto make_msg = [&](int src, int sp, ClusterMsg& m) -> bool {
-    std::memset(&m, 0, sizeof(m));
-    const auto& cv = p->cvars[src];
-    const auto& sv = p->svars[sp];
-    if ((int)cv.size() > CL_MAXD) return false;
-    const auto cst = strides_of(cv);
-    const Tab& ts = tab_of(0, src);
-    const Tab& tsep = tab_of(1, sp);
-    const Tab& trat = tab_of(2, sp);
-    m.src_rank = ts.rank;
-    m.src_off = (int)ts.off;
-    m.sep_rank = tsep.rank;
-    m.sep_off = (int)tsep.off;
-    m.rat_rank = trat.rank;
-    m.rat_off = (int)trat.off;
-    m.L = (int)(p->csize[src] / std::max<int64_t>(1, p->ssize[sp]));
-    for (int v : sv) {
-      const int pos = (int)(std::lower_bound(cv.begin(), cv.end(), v) - cv.begin());
-      m.sd_card[m.nsd] = p->cards[v];
-      m.sd_stride[m.nsd] = (int)cst[pos];
-      m.nsd++;
-    }
-    for (size_t i = 0; i < cv.size(); ++i)
-      if (!std::binary_search(sv.begin(), sv.end(), cv[i])) {
-        m.rd_card[m.nrd] = p->cards[cv[i]];
-        m.rd_stride[m.nrd] = (int)cst[i];
-        m.nrd++;
-      }
-    return true;
-  };
-  // one level: (src, tgt, sep) messages
+  // one level: (src, tgt, sep) messages -> message records, target records
   auto add_level = [&](const std::vector<std::array<int, 3>>& lm) -> bool {
     if (lm.empty()) return true;
-    if ((int)lm.size() > 512) return false;  // jt_cluster.cu CL_LVL_MAX
     ClusterLevel L{};
-    L.m0 = (int)msgs.size();
-    L.t0 = (int)tgts.size();
-    std::map<int, std::vector<int>> into;  // target clique -> message indices
-    for (auto& x : lm) {
-      ClusterMsg m;
-      if (!make_msg(x[0], x[2], m)) return false;
-      const bool lng = m.L > 32;
-      m.short0 = L.n_short;
-      m.long0 = L.n_long;
-      (lng ? L.n_long : L.n_short) += p->ssize[x[2]];
-      into[x[1]].push_back((int)msgs.size());
-      msgs.push_back(m);
+    L.blob_off = (int64_t)blob.size();
+    L.n_msgs = (int)lm.size();
+    std::vector<int> lb((size_t)L.n_msgs * CL_MREC, 0);
+    std::map<int, std::vector<int>> into;  // target clique -> message ordinals
+    for (int mi = 0; mi < L.n_msgs; ++mi) {
+      const int src = lm[mi][0], sp = lm[mi][2];
+      const auto& cv = p->cvars[src];
+      const auto& sv = p->svars[sp];
+      if ((int)cv.size() > CL_MAXD) return false;
+      const auto cst = strides_of(cv);
+      int* M = lb.data() + (size_t)mi * CL_MREC;
+      const Tab &ts = tab_of(0, src), &tsep = tab_of(1, sp), &trat = tab_of(2, sp);
+      M[0] = ts.rank; M[1] = (int)ts.off; M[2] = tsep.rank; M[3] = (int)tsep.off;
+      M[4] = trat.rank; M[5] = (int)trat.off;
+      M[6] = (int)(p->csize[src] / std::max<int64_t>(1, p->ssize[sp]));
+      int nsd = 0, nrd = 0;
+      for (int v : sv) {
+        const int pos = (int)(std::lower_bound(cv.begin(), cv.end(), v) - cv.begin());
+        M[11 + nsd] = p->cards[v];
+        M[11 + CL_MAXD + nsd] = (int)cst[pos];
+        ++nsd;
+      }
+      for (size_t i = 0; i < cv.size(); ++i)
+        if (!std::binary_search(sv.begin(), sv.end(), cv[i])) {
+          M[11 + 2 * CL_MAXD + nrd] = p->cards[cv[i]];
+          M[11 + 3 * CL_MAXD + nrd] = (int)cst[i];
+          ++nrd;
+        }
+      M[7] = nsd;
+      M[8] = nrd;
+      const bool lng = M[6] > 32;
+      M[9] = (int)L.n_short;
+      M[10] = (int)L.n_long;
+      (lng ? L.n_long : L.n_short) += p->ssize[sp];
+      into[lm[mi][1]].push_back(mi);
     }
-    L.m1 = (int)msgs.size();
+    L.n_tgts = (int)into.size();
+    const size_t toff_at = lb.size();
+    lb.resize(lb.size() + L.n_tgts, 0);
+    int ti = 0;
     for (auto& kv : into) {
       const int t = kv.first;
       const auto& tv = p->cvars[t];
-      if ((int)tv.size() > CL_MAXD || (int)kv.second.size() > CL_MAXIN) return false;
-      ClusterTgt G;
-      std::memset(&G, 0, sizeof(G));
+      const int nd = (int)tv.size(), nin = (int)kv.second.size();
+      if (nd > CL_MAXD || nin > CL_MAXIN) return false;
+      lb[toff_at + ti++] = (int)lb.size();
       const Tab& tt = tab_of(0, t);
-      G.rank = tt.rank;
-      G.off = (int)tt.off;
-      G.size = (int)p->csize[t];
-      G.nd = (int)tv.size();
-      for (int d = 0; d < G.nd; ++d) G.card[d] = p->cards[tv[d]];
-      G.nin = (int)kv.second.size();
-      for (int k = 0; k < G.nin; ++k) {
-        G.msg[k] = kv.second[k];
-        const int sp = lm[kv.second[k] - L.m0][2];
+      lb.push_back(tt.rank);
+      lb.push_back((int)tt.off);
+      lb.push_back((int)p->csize[t]);
+      lb.push_back(nd);
+      lb.push_back(nin);
+      lb.push_back((int)L.n_elem_chunks);
+      for (int d = 0; d < nd; ++d) lb.push_back(p->cards[tv[d]]);
+      for (int k = 0; k < nin; ++k) {
+        const int mi = kv.second[k];
+        const int sp = lm[mi][2];
+        const Tab& trat = tab_of(2, sp);
+        lb.push_back(trat.rank);
+        lb.push_back((int)trat.off);
         const auto& sv = p->svars[sp];
         const auto sst = strides_of(sv);
-        for (int d = 0; d < G.nd; ++d) {
+        for (int d = 0; d < nd; ++d) {
           auto it = std::lower_bound(sv.begin(), sv.end(), tv[d]);
-          G.sstride[k][d] = (it != sv.end() && *it == tv[d]) ? (int)sst[it - sv.begin()] : 0;
+          lb.push_back((it != sv.end() && *it == tv[d]) ? (int)sst[it - sv.begin()] : 0);
         }
       }
-      G.chunk0 = L.n_elem_chunks;
-      L.n_elem_chunks += (G.size + CL_CHUNK - 1) / CL_CHUNK;
-      tgts.push_back(G);
+      L.n_elem_chunks += (p->csize[t] + CL_CHUNK - 1) / CL_CHUNK;
     }
-    L.t1 = (int)tgts.size();
+    while (lb.size() % 4) lb.push_back(0);  // int4 staging
+    L.blob_len = (int)lb.size();
+    max_blob = std::max(max_blob, L.blob_len);
+    blob.insert(blob.end(), lb.begin(), lb.end());
     levels.push_back(L);
     return true;
   };
@@ -2206,6 +2208,12 @@ static int build_cluster_prog(jt_state* st, const std::vector<int>& roots, Clust
         for (auto& ch : o.children[c]) lm.push_back({c, ch.first, ch.second});
     if (!add_level(lm)) return JT_OK;
   }
+  (void)max_blob;
+  const int64_t smem = align4(table_elems) * st->esz;
+  cp.smem = (int)smem;
+  cp.table_elems = (int)align4(table_elems);
+  if (cluster_prop_supported(p->dtype, n_ranks, cp.smem) <= 0) return JT_OK;
+  cp.n_ranks = n_ranks;
   auto up = [&](auto** dptr, const auto& vec) -> int {
     using E = typename std::decay_t<decltype(vec)>::value_type;
     CK(cudaMalloc((void**)dptr, std::max<size_t>(vec.size(), 1) * sizeof(E)));
@@ -2213,10 +2221,9 @@ static int build_cluster_prog(jt_state* st, const std::vector<int>& roots, Clust
     return JT_OK;
   };
   int rc;
-  if ((rc = up(&cp.d_segs, segs)) || (rc = up(&cp.d_msgs, msgs)) || (rc = up(&cp.d_tgts, tgts)) ||
+  if ((rc = up(&cp.d_segs, segs)) || (rc = up(&cp.d_seg_begin, seg_begin)) || (rc = up(&cp.d_blob, blob)) ||
       (rc = up(&cp.d_levels, levels)))
     return rc;
-  cp.n_segs = (int)segs.size();
   cp.n_levels = (int)levels.size();
   cp.ok = true;
   return JT_OK;
@@ -2247,11 +2254,11 @@ extern "C" int jt_propagate(jt_state* st, const int32_t* roots_or_null, void* st
       a.aux = st->d_aux;
       a.err = st->d_err;
       a.segs = cp->d_segs;
-      a.n_segs = cp->n_segs;
-      a.msgs = cp->d_msgs;
-      a.tgts = cp->d_tgts;
+      a.seg_begin = cp->d_seg_begin;
+      a.blob = cp->d_blob;
       a.levels = cp->d_levels;
       a.n_levels = cp->n_levels;
+      a.table_elems = cp->table_elems;
       CK(launch_cluster_prop(st->plan->dtype, a, cp->n_ranks, cp->smem, s));
       st->launches++;
       st->fresh = false;

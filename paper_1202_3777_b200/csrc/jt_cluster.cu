@@ -25,90 +25,86 @@ __device__ __forceinline__ T* rank_ptr(T* const* bases, int rank, int off) {
   return bases[rank] + off;
 }
 
-// last index i in [lo, hi) with pre[i] <= q (pre ascending, pre[lo] <= q)
-__device__ __forceinline__ int upper_idx(const int64_t* pre, int lo, int hi, int64_t q) {
+// last index i in [0, n) with key(i) <= q (keys ascending, key(0) <= q)
+template <class K>
+__device__ __forceinline__ int upper_idx(K key, int n, int64_t q) {
+  int lo = 0, hi = n;
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
-    if (pre[mid] <= q) lo = mid;
+    if (key(mid) <= q) lo = mid;
     else hi = mid;
   }
   return lo;
 }
 
-constexpr int CL_LVL_MAX = 512;  // messages / targets of one level staged in shared memory
-
 template <typename T>
-__global__ void cluster_prop_kernel(const ClusterArgs a) {
+__global__ void __launch_bounds__(CL_THREADS) cluster_prop_kernel(const ClusterArgs a) {
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char csm[];
   __shared__ T* bases[CL_MAX_RANKS];
-  // per-level prefix tables (item -> message / target by binary search in smem)
-  __shared__ int64_t s_short[CL_LVL_MAX], s_long[CL_LVL_MAX], s_chunk[CL_LVL_MAX];
   const int rank = (int)cl.block_rank();
   const int nr = (int)cl.num_blocks();
   const int tid = threadIdx.x;
   const int nthr = nr * blockDim.x;
   const int gtid = rank * blockDim.x + tid;
-  const int lane = tid & 31;
+  const int lane = tid & 31, warp = tid >> 5;
   const int gwarp = gtid >> 5, nwarps = nthr >> 5;
   T* my = reinterpret_cast<T*>(csm);
   if (tid < nr) bases[tid] = cl.map_shared_rank(my, tid);
   T* clique = reinterpret_cast<T*>(a.clique);
   T* aux = reinterpret_cast<T*>(a.aux);
-  // load this rank's tables from HBM
-  for (int s = 0; s < a.n_segs; ++s) {
-    const ClusterSeg g = a.segs[s];
-    if (g.rank != rank) continue;
+  const int s0 = a.seg_begin[rank], s1 = a.seg_begin[rank + 1];
+  for (int si = s0 + warp; si < s1; si += blockDim.x / 32) {  // a warp per table
+    const ClusterSeg g = a.segs[si];
     const T* src = (g.arena == A_CLIQUE ? clique : aux) + g.gofs;
-    for (int e = tid; e < g.len; e += blockDim.x) my[g.lofs + e] = src[e];
+    for (int e = lane; e < g.len; e += 32) my[g.lofs + e] = src[e];
   }
   cl.sync();
   for (int lv = 0; lv < a.n_levels; ++lv) {
     const ClusterLevel L = a.levels[lv];
-    for (int i = tid; i < L.m1 - L.m0; i += blockDim.x) {
-      s_short[i] = a.msgs[L.m0 + i].short0;
-      s_long[i] = a.msgs[L.m0 + i].long0;
-    }
-    for (int i = tid; i < L.t1 - L.t0; i += blockDim.x) s_chunk[i] = a.tgts[L.t0 + i].chunk0;
-    __syncthreads();
+    // the level's descriptors: read through L1 (every thread of the SM touches the same few lines)
+    const int* __restrict__ blob = a.blob + L.blob_off;
+    const int nm = L.n_msgs;
+    const int* toff = blob + nm * CL_MREC;  // target record offsets
     // ---- phase A: marginalize every message of the level onto its separator ----
     for (int pass = 0; pass < 2; ++pass) {  // 0: short rows (thread/entry), 1: long rows (warp/entry)
       const int64_t total = pass == 0 ? L.n_short : L.n_long;
       const int64_t stride = pass == 0 ? nthr : nwarps;
+      const int koff = pass == 0 ? 9 : 10;
       for (int64_t q = pass == 0 ? gtid : gwarp; q < total; q += stride) {
-        // locate (message, entry): messages of the level are in [m0, m1), with
-        // prefix counts of short / long entries
-        const int m = L.m0 + upper_idx(pass == 0 ? s_short : s_long, 0, L.m1 - L.m0, q);
-        const ClusterMsg M = a.msgs[m];  // one bulk copy: no dependent loads per field
-        const int j = (int)(q - (pass == 0 ? M.short0 : M.long0));
-        // row base of entry j: separator digits (separator order, last fastest)
+        const int m = upper_idx([&](int i) { return (int64_t)blob[i * CL_MREC + koff]; }, nm, q);
+        const int* M = blob + m * CL_MREC;
+        const int j = (int)(q - M[koff]);
+        const int nsd = M[7], nrd = M[8], Lr = M[6];
         int rem = j, base = 0;
-        for (int d = M.nsd - 1; d >= 0; --d) {
-          const int c = M.sd_card[d];
-          base += (rem % c) * M.sd_stride[d];
+        for (int d = nsd - 1; d >= 0; --d) {  // separator digits (separator order, last fastest)
+          const int c = M[11 + d];
+          base += (rem % c) * M[11 + CL_MAXD + d];
           rem /= c;
         }
-        const T* src = rank_ptr<T>(bases, M.src_rank, M.src_off);
+        const T* src = rank_ptr<T>(bases, M[0], M[1]);
+        const int* rc = M + 11 + 2 * CL_MAXD;
+        const int* rs = M + 11 + 3 * CL_MAXD;
         double star = 0.0;
         if (pass == 0) {
           int dig[CL_MAXD];
           int off = base;
-          for (int d = 0; d < M.nrd; ++d) dig[d] = 0;
-          for (int p = 0; p < M.L; ++p) {
+          for (int d = 0; d < nrd; ++d) dig[d] = 0;
+          for (int p = 0; p < Lr; ++p) {
             star += (double)src[off];
-            for (int d = M.nrd - 1; d >= 0; --d) {  // odometer over the rest dims
-              off += M.rd_stride[d];
-              if (++dig[d] < M.rd_card[d]) break;
-              off -= M.rd_stride[d] * M.rd_card[d];
+            for (int d = nrd - 1; d >= 0; --d) {  // odometer over the rest dims
+              off += rs[d];
+              if (++dig[d] < rc[d]) break;
+              off -= rs[d] * rc[d];
               dig[d] = 0;
             }
           }
         } else {
-          for (int p = lane; p < M.L; p += 32) {
+          for (int p = lane; p < Lr; p += 32) {
             int r2 = p, off = base;
-            for (int d = M.nrd - 1; d >= 0; --d) {
-              const int c = M.rd_card[d];
-              off += (r2 % c) * M.rd_stride[d];
+            for (int d = nrd - 1; d >= 0; --d) {
+              const int c = rc[d];
+              off += (r2 % c) * rs[d];
               r2 /= c;
             }
             star += (double)src[off];
@@ -117,8 +113,8 @@ __global__ void cluster_prop_kernel(const ClusterArgs a) {
           for (int o = 16; o > 0; o >>= 1) star += __shfl_xor_sync(0xffffffffu, star, o);
           if (lane != 0) continue;
         }
-        T* sep = rank_ptr<T>(bases, M.sep_rank, M.sep_off);
-        T* rat = rank_ptr<T>(bases, M.rat_rank, M.rat_off);
+        T* sep = rank_ptr<T>(bases, M[2], M[3]);
+        T* rat = rank_ptr<T>(bases, M[4], M[5]);
         const double old = (double)sep[j];
         if (old == 0.0 && star != 0.0) atomicOr(a.err, EB_INCONSISTENT);
         rat[j] = (T)(old != 0.0 ? star / old : 0.0);
@@ -128,49 +124,46 @@ __global__ void cluster_prop_kernel(const ClusterArgs a) {
     cl.sync();
     // ---- phase B: every target element times the ratios of its incoming messages ----
     for (int64_t q = gtid; q < L.n_elem_chunks; q += nthr) {
-      const int t = L.t0 + upper_idx(s_chunk, 0, L.t1 - L.t0, q);
-      const ClusterTgt& G = a.tgts[t];
-      const int e0 = (int)(q - G.chunk0) * CL_CHUNK;
-      const int e1 = min(G.size, e0 + CL_CHUNK);
+      const int t = upper_idx([&](int i) { return (int64_t)blob[toff[i] + 5]; }, L.n_tgts, q);
+      const int* G = blob + toff[t];
+      const int size = G[2], nd = G[3], nin = G[4];
+      const int* card = G + 6;
+      const int e0 = (int)(q - G[5]) * CL_CHUNK;
+      const int e1 = min(size, e0 + CL_CHUNK);
       int dig[CL_MAXD];
       int rem = e0;
-      for (int d = G.nd - 1; d >= 0; --d) {
-        dig[d] = rem % G.card[d];
-        rem /= G.card[d];
+      for (int d = nd - 1; d >= 0; --d) {
+        dig[d] = rem % card[d];
+        rem /= card[d];
       }
-      const int nin = G.nin, nd = G.nd;
       int sidx[CL_MAXIN];
       const T* rp[CL_MAXIN];
-      int card[CL_MAXD];
-      for (int d = 0; d < nd; ++d) card[d] = G.card[d];
       for (int k = 0; k < nin; ++k) {
+        const int* R = G + 6 + nd + k * (2 + nd);
         int x = 0;
-        for (int d = 0; d < nd; ++d) x += dig[d] * G.sstride[k][d];
+        for (int d = 0; d < nd; ++d) x += dig[d] * R[2 + d];
         sidx[k] = x;
-        const int mi = G.msg[k];
-        rp[k] = rank_ptr<T>(bases, a.msgs[mi].rat_rank, a.msgs[mi].rat_off);
+        rp[k] = rank_ptr<T>(bases, R[0], R[1]);
       }
-      T* tg = rank_ptr<T>(bases, G.rank, G.off);
+      T* tg = rank_ptr<T>(bases, G[0], G[1]);
       for (int e = e0; e < e1; ++e) {
         T v = tg[e];
         for (int k = 0; k < nin; ++k) v *= rp[k][sidx[k]];
         tg[e] = v;
         for (int d = nd - 1; d >= 0; --d) {  // odometer: digits and separator indices
-          for (int k = 0; k < nin; ++k) sidx[k] += G.sstride[k][d];
+          for (int k = 0; k < nin; ++k) sidx[k] += G[6 + nd + k * (2 + nd) + 2 + d];
           if (++dig[d] < card[d]) break;
-          for (int k = 0; k < nin; ++k) sidx[k] -= G.sstride[k][d] * card[d];
+          for (int k = 0; k < nin; ++k) sidx[k] -= G[6 + nd + k * (2 + nd) + 2 + d] * card[d];
           dig[d] = 0;
         }
       }
     }
     cl.sync();
   }
-  // write this rank's tables back (ratio scratch stays on chip)
-  for (int s = 0; s < a.n_segs; ++s) {
-    const ClusterSeg g = a.segs[s];
-    if (g.rank != rank || !g.writeback) continue;
+  for (int si = s0 + warp; si < s1; si += blockDim.x / 32) {  // write back (ratio scratch stays on chip)
+    const ClusterSeg g = a.segs[si];
     T* dst = (g.arena == A_CLIQUE ? clique : aux) + g.gofs;
-    for (int e = tid; e < g.len; e += blockDim.x) dst[e] = my[g.lofs + e];
+    for (int e = lane; e < g.len; e += 32) dst[e] = my[g.lofs + e];
   }
 }
 

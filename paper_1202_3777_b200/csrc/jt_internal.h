@@ -140,43 +140,40 @@ int contract_max_ctas_per_sm(int dtype, int fold, int rowi);
 
 // ---- small trees in cluster shared memory (jt_cluster.cu) ----
 constexpr int CL_MAX_RANKS = 16;  // CTAs per cluster (non-portable above 8)
-constexpr int CL_MAXD = 16;       // dims per clique
+constexpr int CL_MAXD = 12;       // dims per clique
 constexpr int CL_MAXIN = 16;      // messages into one target in one level
 constexpr int CL_CHUNK = 16;      // target elements per thread item
 constexpr int CL_THREADS = 256;
+// Per-level descriptor blob (int32), staged into shared memory at the start of
+// the level.  Message records are CL_MREC ints:
+//   [0] src_rank [1] src_off [2] sep_rank [3] sep_off [4] rat_rank [5] rat_off
+//   [6] L (row length) [7] nsd [8] nrd [9] short0 [10] long0
+//   [11 + d] sd_card, [11 + CL_MAXD + d] sd_stride, [11 + 2 CL_MAXD + d] rd_card,
+//   [11 + 3 CL_MAXD + d] rd_stride
+// Target records follow (offsets in a table after the messages):
+//   rank off size nd nin chunk0 card[nd] then per incoming message:
+//   rat_rank rat_off sstride[nd]
+constexpr int CL_MREC = 11 + 4 * CL_MAXD;
 struct ClusterSeg {               // a table's home: (rank, local offset) <-> HBM copy
-  int rank, lofs, len, arena, writeback;
+  int rank, lofs, len, arena;
   int64_t gofs;
 };
-struct ClusterMsg {
-  int src_rank, src_off, sep_rank, sep_off, rat_rank, rat_off;
-  int L;                          // row length |src| / |sep|
-  int nsd, nrd;
-  int sd_card[CL_MAXD], sd_stride[CL_MAXD];  // separator digits (separator order) -> src stride
-  int rd_card[CL_MAXD], rd_stride[CL_MAXD];  // remaining src dims (ascending) -> src stride
-  int64_t short0, long0;          // prefix counts of thread-row / warp-row entries in the level
-};
-struct ClusterTgt {
-  int rank, off, size, nd, nin;
-  int card[CL_MAXD];
-  int msg[CL_MAXIN];
-  int sstride[CL_MAXIN][CL_MAXD]; // per incoming message: separator stride of each target dim
-  int64_t chunk0;                 // prefix count of element chunks in the level
-};
 struct ClusterLevel {
-  int m0, m1, t0, t1;
+  int64_t blob_off;               // int offset of the level's blob
+  int blob_len;                   // ints
+  int n_msgs, n_tgts;             // message records, then n_tgts target-record offsets, then records
   int64_t n_short, n_long, n_elem_chunks;
 };
 struct ClusterArgs {
   void* clique;
   void* aux;
   int* err;
-  const ClusterSeg* segs;
-  int n_segs;
-  const ClusterMsg* msgs;
-  const ClusterTgt* tgts;
+  const ClusterSeg* segs;         // sorted by rank
+  const int* seg_begin;           // [n_ranks + 1]
+  const int* blob;
   const ClusterLevel* levels;
   int n_levels;
+  int table_elems;                // shared-memory elements of the largest rank's tables
 };
 cudaError_t launch_cluster_prop(int dtype, const ClusterArgs& a, int n_ranks, int smem_bytes, cudaStream_t s);
 int cluster_prop_supported(int dtype, int n_ranks, int smem_bytes);
