@@ -906,6 +906,27 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   std::set_difference(s.begin(), s.end(), U.begin(), U.end(), std::back_inserter(S));
   std::set_difference(U.begin(), U.end(), s.begin(), s.end(), std::back_inserter(K));
   const int nG = (int)G.size(), nE = (int)E.size();
+  // enumeration order of i (any order works: every i-dependent offset comes from
+  // the per-i table): the variables that index the largest factor tensors vary
+  // slowest, so consecutive i (consecutive warps) re-read the same factor rows
+  // while they are still in L2
+  {
+    std::vector<std::pair<double, int>> cost;
+    for (size_t a = 0; a < I.size(); ++a) {
+      double c = 0.0;
+      for (auto* f : G)
+        if (std::binary_search(f->vars.begin(), f->vars.end(), I[a])) {
+          double n = (double)B;
+          for (int v : f->vars) n *= p->cards[v];
+          c += n;
+        }
+      cost.push_back({-c, (int)a});  // most expensive first (outermost)
+    }
+    std::stable_sort(cost.begin(), cost.end());
+    std::vector<int> Io;
+    for (auto& x : cost) Io.push_back(I[x.second]);
+    if (!getenv("JT_NO_IPERM")) I.swap(Io);
+  }
   auto strides = [&](const std::vector<int>& vars, const Tensor& t) {
     std::vector<int64_t> o;
     for (int v : vars) o.push_back(tensor_stride(p, t, v, B));
