@@ -72,7 +72,7 @@ def load_library(path: str | None = None):
     with _lock:
         if _lib is not None and path is None:
             return _lib
-        p = path or LIB_PATH
+        p = path or os.environ.get("JT_LIB") or LIB_PATH  # JT_LIB: kernel-variant sweeps (tools/)
         if not os.path.exists(p):
             raise DeviceError(
                 f"{LIB_NAME} not built ({p}); run `python -c 'import __graft_entry__ as g; g.build()'`")

@@ -1030,11 +1030,17 @@ template <> struct CTraits<double> { static constexpr int VEC = 2; };
 // FMAs per lane per k against ~nG + 3 loads.  fp32 sums stay in registers for
 // CKF consecutive k and are then folded into per-thread fp64 accumulators in
 // shared memory (fp64 passes accumulate in registers directly).
+#ifndef CON_KU
+#define CON_KU 1
+#endif
+#ifndef CON_MINB
+#define CON_MINB 2
+#endif
 template <typename T, bool FOLD>
-__global__ void __launch_bounds__(NT, 2) contract_kernel(const CArgs a) {
+__global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
   pdl_enter();
   constexpr int VEC = CTraits<T>::VEC;
-  constexpr int KU = 2;
+  constexpr int KU = CON_KU;
   static_assert(TMC == 8, "W rows are loaded as two 4-vectors");
   extern __shared__ double cacc[];  // FOLD: [TMC * VEC][NT] fp64 accumulators
   const T* __restrict__ W = reinterpret_cast<const T*>(a.w);
@@ -1186,13 +1192,28 @@ __global__ void __launch_bounds__(NT, 2) contract_kernel(const CArgs a) {
 // other): no W reuse exists, so the unit is TMC consecutive i values and the
 // warp streams their factor rows — KU x TMC x nG independent vector loads in
 // flight per lane — with the same epilogue.
+// occupancy / loads-in-flight trade-offs, chosen by a variant sweep on the c5
+// batch program (tools/build_variant.sh, tools/sweep_variants.sh; profiles r06):
+// one or two k per step at 4-8 CTAs/SM beat deeper per-warp unrolling
+#ifndef ROWI_KU_NF
+#define ROWI_KU_NF 1
+#endif
+#ifndef ROWI_MINB_NF
+#define ROWI_MINB_NF 8
+#endif
+#ifndef ROWI_KU_F
+#define ROWI_KU_F 2
+#endif
+#ifndef ROWI_MINB_F
+#define ROWI_MINB_F 4
+#endif
 template <typename T, bool FOLD>
-__global__ void __launch_bounds__(NT, FOLD ? 3 : 4) contract_rowi_kernel(const CArgs a) {
+__global__ void __launch_bounds__(NT, FOLD ? ROWI_MINB_F : ROWI_MINB_NF) contract_rowi_kernel(const CArgs a) {
   pdl_enter();
   // one i per warp unit (few registers: three or four CTAs per SM), KU values
   // of k in flight, each with its nG factor-row vectors
   constexpr int VEC = CTraits<T>::VEC;
-  constexpr int KU = FOLD ? 4 : 2;
+  constexpr int KU = FOLD ? ROWI_KU_F : ROWI_KU_NF;
   constexpr int KF = 16;
   T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
   const T* __restrict__ aux_c = aux;
