@@ -525,12 +525,12 @@ static std::vector<Dim> merge_dims(const std::vector<Dim>& in, int nf) {
 }
 
 static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pass_idx, BuiltPass& bp,
-                        bool allow_row = true) {
+                        bool allow_row = true, int kv = KV) {
   const int nf = (int)ps.factors.size();
   if (nf > MAXF) return JT_ERR_UNSUPPORTED;
   std::vector<Dim> dims = pass_dims(st, ps);
   const int nd = (int)dims.size();
-  const int TH = NT * KV * vec;
+  const int TH = NT * kv * vec;
   const bool has_out = ps.out_kind != OUT_NONE;
   if (ps.write && !ps.scope.empty()) return JT_ERR_UNSUPPORTED;
   int64_t total = 1;
@@ -678,6 +678,7 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
   d.blk_stride = 2 + nf;
   d.own = best.own ? 1 : 0;
   d.row = best.row ? 1 : 0;
+  d.kv = kv;
   d.own_m = best.own_m;
   d.flush_fac = 0;
   if (best.own) {
@@ -1112,7 +1113,9 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
       BuiltPass bp;
       const int local = (int)(passes.size() - rt.pass_base);
       const int vec = small_wave ? wave_vec : pass_max_vec(st, ps);
-      int rc = compile_pass(st, ps, vec, local, bp, !small_wave);
+      // single trees, small (latency-bound) waves or scalar passes: the general kernel
+      // at 2 vectors per thread, 3 CTAs per SM (more warps in flight)
+      int rc = compile_pass(st, ps, vec, local, bp, !small_wave, st->B == 1 && (small_wave || vec == 1) ? 2 : KV);
       if (rc != JT_OK) return rc;
       bp.d.blk_off = (int64_t)blk.size();
       bp.d.blk32_off = (int64_t)hp.blk32.size();
@@ -1129,7 +1132,7 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
       n_cnt += bp.n_cnt;
       passes.push_back(bp.d);
       hp.pass_clique.push_back(ps.clique);
-      std::array<int, 4> key{bp.d.row ? 2 : 0, vec, bp.d.row ? bp.d.row_lin : 0, 1};
+      std::array<int, 4> key{bp.d.row ? 2 : 0, vec, bp.d.row ? bp.d.row_lin : 0, bp.d.row ? 1 : bp.d.kv};
       if (bp.d.own) {
         const bool allf = bp.d.fac_vec == ((1u << bp.d.nf) - 1u);
         const bool full_vec = vec == (st->esz == 4 ? 4 : 2);
@@ -1154,7 +1157,7 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
       if (!occ) {
         const int dt = st->plan->dtype;
         occ = lg.kind == 1 ? wave_own_max_ctas_per_sm(dt, lg.vec)
-            : lg.kind == 2 ? wave_row_max_ctas_per_sm(dt, lg.vec) : wave_max_ctas_per_sm(dt, lg.vec);
+            : lg.kind == 2 ? wave_row_max_ctas_per_sm(dt, lg.vec) : wave_max_ctas_per_sm(dt, lg.vec, lg.m);
       }
       lg.n_items = (int)g.second.size();
       lg.item_off = (int64_t)items.size() - rt.item_base;
@@ -1273,7 +1276,7 @@ static int launch_group(jt_state* st, const Program* pr, const WaveRt& w, const 
   a.n_items = g.n_items;
   if (g.kind == 1) CK(launch_wave_own(st->plan->dtype, g.vec, g.lm, g.m, a, g.grid, s));
   else if (g.kind == 2) CK(launch_wave_row(st->plan->dtype, g.vec, g.lm, a, g.grid, s));
-  else CK(launch_wave(st->plan->dtype, g.vec, a, g.grid, s));
+  else CK(launch_wave(st->plan->dtype, g.vec, g.m, a, g.grid, s));
   st->launches++;
   return JT_OK;
 }

@@ -7,7 +7,7 @@
 namespace jt {
 
 constexpr int NT = 256;     // threads per CTA of the wave kernel
-constexpr int KV = 4;       // vectors owned per thread per iteration
+constexpr int KV = 4;       // vectors owned per thread per iteration (large waves; small waves use 2)
 constexpr int MAXF = 8;     // factors (ratio / evidence tensors) multiplied in per pass
 constexpr int MAXDI = 8;    // merged inner dimensions per pass
 
@@ -55,6 +55,7 @@ struct DevPass {
   int unit_src, unit_dst;   // element offset = entry * unit
   int unit_fac[MAXF];
   int own_m;                // own passes: vectors (lane chunks) per thread per block
+  int kv;                   // general kernel: vectors per thread per iteration (2 or 4)
   int row;                  // 1: row pass (n_in <= 1, no gpi, T % (32*VEC) == 0): wave_row_kernel
   int64_t row_tab_off;      // row passes: offset of the inner-offset table [2+nf][T/VEC] (int32)
   int row_lin;              // row passes: src and dst inner offsets equal the position (tab rows 0/1 unused)
@@ -192,11 +193,14 @@ struct InitTerm {
 // launchers (jt_kernels.cu)
 cudaError_t launch_init(void* base, int dtype, const double* cpt, const InitClique* cl, int n_cliques,
                         const InitTerm* terms, const int64_t* vdesc, int64_t max_size, cudaStream_t s);
-cudaError_t launch_wave(int dtype, int vec, const WaveArgs& a, int grid, cudaStream_t s);
-int wave_max_ctas_per_sm(int dtype, int vec);
+cudaError_t launch_wave(int dtype, int vec, int kv, const WaveArgs& a, int grid, cudaStream_t s);
+int wave_max_ctas_per_sm(int dtype, int vec, int kv);
 cudaError_t launch_wave_row(int dtype, int vec, int lin, const WaveArgs& a, int grid, cudaStream_t s);
 int wave_row_max_ctas_per_sm(int dtype, int vec);
-constexpr int KROW = 8;
+#ifndef KROW_V
+#define KROW_V 8
+#endif
+constexpr int KROW = KROW_V;
 constexpr int CHUNK_GROUP = 32;  // chunk partials combined in groups of this many (two levels)     // vectors per thread per iteration of the row kernel
 cudaError_t launch_wave_own(int dtype, int vec, int lm, int m, const WaveArgs& a, int grid, cudaStream_t s);
 int wave_own_max_ctas_per_sm(int dtype, int vec);

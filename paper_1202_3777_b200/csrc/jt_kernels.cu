@@ -474,17 +474,19 @@ __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
   }
 }
 
-template <typename T, int VEC>
-__global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
+// KVT vectors per thread per iteration: 4 for large waves; 2 at three CTAs per
+// SM for small, latency-bound waves (more warps in flight, less work per step)
+template <typename T, int VEC, int KVT>
+__global__ void __launch_bounds__(NT, KVT == 2 ? 3 : 2) wave_kernel(const WaveArgs a) {
   pdl_enter();
-  constexpr int TH = NT * KV * VEC;  // positions per CTA iteration
+  constexpr int TH = NT * KVT * VEC;  // positions per CTA iteration
   __shared__ DevPass P;
   __shared__ double part2[NT];
   __shared__ int s_last;
   extern __shared__ __align__(16) double dsm[];
   double* red = dsm;                                              // [TH] block partials
   double* outb = dsm + TH;                                        // [TH] reduced bins
-  uint16_t (*s_qfac)[KV][NT] = reinterpret_cast<uint16_t (*)[KV][NT]>(dsm + 2 * TH);  // inner factor offsets
+  uint16_t (*s_qfac)[KVT][NT] = reinterpret_cast<uint16_t (*)[KVT][NT]>(dsm + 2 * TH);  // inner factor offsets
 
   T* __restrict__ clique = reinterpret_cast<T*>(a.clique);
   const T* __restrict__ base = reinterpret_cast<const T*>(a.base);
@@ -492,9 +494,9 @@ __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
   const int tid = threadIdx.x;
 
   int cur = -1;
-  int q_slot[KV];
-  bool q_ok[KV];
-  int q_src[KV], q_dst[KV];
+  int q_slot[KVT];
+  bool q_ok[KVT];
+  int q_src[KVT], q_dst[KVT];
 
   for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
     const Item item = a.items[it];
@@ -508,7 +510,7 @@ __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
       const int TV = P.T / VEC;
       const int nq = P.BPI * TV;
 #pragma unroll
-      for (int k = 0; k < KV; ++k) {
+      for (int k = 0; k < KVT; ++k) {
         const int q = tid + k * NT;
         q_ok[k] = q < nq;
         const int slot = q_ok[k] ? q / TV : 0;
@@ -547,28 +549,28 @@ __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
     const int bs = P.blk_stride;
     const int nf = P.nf;
 
-    double acc[KV][VEC];
+    double acc[KVT][VEC];
 #pragma unroll
-    for (int k = 0; k < KV; ++k)
+    for (int k = 0; k < KVT; ++k)
 #pragma unroll
       for (int l = 0; l < VEC; ++l) acc[k][l] = 0.0;
 
     for (int64_t bb = b0; bb < b1; bb += P.BPI) {
-      T v[KV][VEC];
-      const int64_t* e[KV];
-      bool ok[KV];
-      // block-table lookups of every slot first, then the data loads: the KV
+      T v[KVT][VEC];
+      const int64_t* e[KVT];
+      bool ok[KVT];
+      // block-table lookups of every slot first, then the data loads: the KVT
       // loads issue back to back instead of each waiting on its own lookup
-      int64_t so[KV];
+      int64_t so[KVT];
 #pragma unroll
-      for (int k = 0; k < KV; ++k) {
+      for (int k = 0; k < KVT; ++k) {
         const int64_t bi = bb + q_slot[k];
         ok[k] = q_ok[k] && bi < b1;
         e[k] = blk + (ok[k] ? bi : b0) * bs;
         so[k] = __ldg(e[k]) + q_src[k];
       }
 #pragma unroll
-      for (int k = 0; k < KV; ++k) {
+      for (int k = 0; k < KVT; ++k) {
         if (ok[k]) {
           const T* p = srcA + so[k];
           if (VEC == 1 || P.src_vec) {
@@ -588,11 +590,11 @@ __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
         if (f < nf) {
           const T* fb = aux + P.fac_off[f];
           const bool fv = (P.fac_vec >> f) & 1u;
-          int64_t fo[KV];
+          int64_t fo[KVT];
 #pragma unroll
-          for (int k = 0; k < KV; ++k) fo[k] = __ldg(e[k] + 2 + f) + s_qfac[f][k][tid];
+          for (int k = 0; k < KVT; ++k) fo[k] = __ldg(e[k] + 2 + f) + s_qfac[f][k][tid];
 #pragma unroll
-          for (int k = 0; k < KV; ++k) {
+          for (int k = 0; k < KVT; ++k) {
             if (ok[k]) {
               const T* p = fb + fo[k];
               T g[VEC];
@@ -611,11 +613,11 @@ __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
       }
       if (wr) {
 #pragma unroll
-        for (int k = 0; k < KV; ++k)
+        for (int k = 0; k < KVT; ++k)
           if (ok[k]) store_vec<T, VEC>(dstA + e[k][1] + q_dst[k], v[k]);
       }
 #pragma unroll
-      for (int k = 0; k < KV; ++k)
+      for (int k = 0; k < KVT; ++k)
 #pragma unroll
         for (int l = 0; l < VEC; ++l) acc[k][l] += (double)v[k][l];
       if (multi) {
@@ -625,7 +627,7 @@ __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
         const int64_t rem_g = item.j_out + item.j_count - g0;
         const int ng = (int)(rem_g < P.gpi ? rem_g : P.gpi);
 #pragma unroll
-        for (int k = 0; k < KV; ++k) {
+        for (int k = 0; k < KVT; ++k) {
           if (q_ok[k]) {
             const int q = tid + k * NT;
 #pragma unroll
@@ -661,7 +663,7 @@ __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
     if (n_in == 1) {
       double s = 0.0;
 #pragma unroll
-      for (int k = 0; k < KV; ++k)
+      for (int k = 0; k < KVT; ++k)
 #pragma unroll
         for (int l = 0; l < VEC; ++l) s += acc[k][l];
       s = warp_sum(s);
@@ -675,7 +677,7 @@ __global__ void __launch_bounds__(NT) wave_kernel(const WaveArgs a) {
       __syncthreads();
     } else {
 #pragma unroll
-      for (int k = 0; k < KV; ++k) {
+      for (int k = 0; k < KVT; ++k) {
         if (q_ok[k]) {
           const int q = tid + k * NT;
 #pragma unroll
@@ -779,7 +781,10 @@ __device__ __forceinline__ double warp_chunk_combine(const DevPass& P, const Ite
 // src/dst inner offsets are the positions themselves (the clique's own layout):
 // one block entry per batch, slot addresses are immediates off one pointer.
 template <typename T, int VEC, bool LIN>
-__global__ void __launch_bounds__(NT, 2) wave_row_kernel(const WaveArgs a) {
+#ifndef ROW_MINB
+#define ROW_MINB 2
+#endif
+__global__ void __launch_bounds__(NT, ROW_MINB) wave_row_kernel(const WaveArgs a) {
   pdl_enter();
   T* __restrict__ clique = reinterpret_cast<T*>(a.clique);
   const T* __restrict__ base = reinterpret_cast<const T*>(a.base);
@@ -1337,21 +1342,21 @@ int contract_max_ctas_per_sm(int dtype, int fold, int rowi) {
   return n > 0 ? n : 1;
 }
 
-template <int VEC>
+template <int VEC, int KVT>
 constexpr size_t wave_smem() {
-  return (size_t)2 * NT * KV * VEC * sizeof(double) + (size_t)MAXF * KV * NT * sizeof(uint16_t);
+  return (size_t)2 * NT * KVT * VEC * sizeof(double) + (size_t)MAXF * KVT * NT * sizeof(uint16_t);
 }
 
-template <typename T, int VEC>
+template <typename T, int VEC, int KVT>
 static cudaError_t launch_t(const WaveArgs& a, int grid, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(wave_kernel<T, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)wave_smem<VEC>());
+    cudaError_t e = cudaFuncSetAttribute(wave_kernel<T, VEC, KVT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)wave_smem<VEC, KVT>());
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_pdl(wave_kernel<T, VEC>, grid, NT, wave_smem<VEC>(), s, a);
+  return launch_pdl(wave_kernel<T, VEC, KVT>, grid, NT, wave_smem<VEC, KVT>(), s, a);
 }
 
 template <typename T, int VEC, int LM, int M>
@@ -1402,34 +1407,43 @@ int wave_own_max_ctas_per_sm(int dtype, int vec) {
   return occ_own_t<double, 1>();
 }
 
-cudaError_t launch_wave(int dtype, int vec, const WaveArgs& a, int grid, cudaStream_t s) {
-  if (grid <= 0 || a.n_items <= 0) return cudaSuccess;
+template <int KVT>
+static cudaError_t launch_kv(int dtype, int vec, const WaveArgs& a, int grid, cudaStream_t s) {
   if (dtype == 0) {
-    if (vec == 4) return launch_t<float, 4>(a, grid, s);
-    if (vec == 2) return launch_t<float, 2>(a, grid, s);
-    return launch_t<float, 1>(a, grid, s);
+    if (vec == 4) return launch_t<float, 4, KVT>(a, grid, s);
+    if (vec == 2) return launch_t<float, 2, KVT>(a, grid, s);
+    return launch_t<float, 1, KVT>(a, grid, s);
   }
-  if (vec == 2) return launch_t<double, 2>(a, grid, s);
-  return launch_t<double, 1>(a, grid, s);
+  if (vec == 2) return launch_t<double, 2, KVT>(a, grid, s);
+  return launch_t<double, 1, KVT>(a, grid, s);
 }
 
-template <typename T, int VEC>
+cudaError_t launch_wave(int dtype, int vec, int kv, const WaveArgs& a, int grid, cudaStream_t s) {
+  if (grid <= 0 || a.n_items <= 0) return cudaSuccess;
+  return kv == 2 ? launch_kv<2>(dtype, vec, a, grid, s) : launch_kv<4>(dtype, vec, a, grid, s);
+}
+
+template <typename T, int VEC, int KVT>
 static int occ_t() {
   int n = 0;
-  cudaFuncSetAttribute(wave_kernel<T, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wave_smem<VEC>());
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, wave_kernel<T, VEC>, NT, wave_smem<VEC>());
+  cudaFuncSetAttribute(wave_kernel<T, VEC, KVT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)wave_smem<VEC, KVT>());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, wave_kernel<T, VEC, KVT>, NT, wave_smem<VEC, KVT>());
   return n > 0 ? n : 1;
 }
 
-int wave_max_ctas_per_sm(int dtype, int vec) {
+template <int KVT>
+static int occ_kv(int dtype, int vec) {
   if (dtype == 0) {
-    if (vec == 4) return occ_t<float, 4>();
-    if (vec == 2) return occ_t<float, 2>();
-    return occ_t<float, 1>();
+    if (vec == 4) return occ_t<float, 4, KVT>();
+    if (vec == 2) return occ_t<float, 2, KVT>();
+    return occ_t<float, 1, KVT>();
   }
-  if (vec == 2) return occ_t<double, 2>();
-  return occ_t<double, 1>();
+  if (vec == 2) return occ_t<double, 2, KVT>();
+  return occ_t<double, 1, KVT>();
 }
+
+int wave_max_ctas_per_sm(int dtype, int vec, int kv) { return kv == 2 ? occ_kv<2>(dtype, vec) : occ_kv<4>(dtype, vec); }
 
 // ---- posteriors: raw marginals [var][card][B] -> normalized [B][Σcard] ----
 // normalize (potential.py:181-186): total <= 0 raises ZeroMassError; here the
