@@ -846,7 +846,10 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
 }
 
 // waves touching fewer elements than this are launch-latency bound
-constexpr int64_t SMALL_WAVE_ELEMS = int64_t(1) << 21;
+#ifndef SMALL_WAVE_LOG2
+#define SMALL_WAVE_LOG2 21
+#endif
+constexpr int64_t SMALL_WAVE_ELEMS = int64_t(1) << SMALL_WAVE_LOG2;
 
 struct HostProgram {
   std::vector<WaveRt> waves;

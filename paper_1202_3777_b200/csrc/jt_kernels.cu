@@ -474,10 +474,13 @@ __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
   }
 }
 
+#ifndef WK2_MINB
+#define WK2_MINB 3
+#endif
 // KVT vectors per thread per iteration: 4 for large waves; 2 at three CTAs per
 // SM for small, latency-bound waves (more warps in flight, less work per step)
 template <typename T, int VEC, int KVT>
-__global__ void __launch_bounds__(NT, KVT == 2 ? 3 : 2) wave_kernel(const WaveArgs a) {
+__global__ void __launch_bounds__(NT, KVT == 2 ? WK2_MINB : 2) wave_kernel(const WaveArgs a) {
   pdl_enter();
   constexpr int TH = NT * KVT * VEC;  // positions per CTA iteration
   __shared__ DevPass P;
