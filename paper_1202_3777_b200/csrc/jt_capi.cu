@@ -1073,6 +1073,63 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   return JT_OK;
 }
 
+// Disjointness check of one program (the device analogue of the reference's
+// ParallelEngine(validate=True), propagate.py:135-140): within a wave no two
+// passes write the same tensor element, and no pass reads what another pass of
+// the same wave writes.  Runs at every program build (host only, O(passes^2)).
+static int validate_waves(const jt_state* st, const std::vector<std::vector<PassSpec>>& waves) {
+  const jt_plan* p = st->plan;
+  struct Iv { int arena; int64_t lo, hi; };
+  auto tsize = [&](const Tensor& t) {
+    int64_t n = t.batch ? st->B : 1;
+    for (int v : t.vars) n *= p->cards[v];
+    return n;
+  };
+  auto overlap = [](const Iv& a, const Iv& b) { return a.arena == b.arena && a.lo < b.hi && b.lo < a.hi; };
+  for (const auto& w : waves) {
+    std::vector<std::vector<Iv>> wr(w.size()), rd(w.size());
+    for (size_t i = 0; i < w.size(); ++i) {
+      const PassSpec& ps = w[i];
+      const int64_t csz = p->csize[ps.clique] * (st->mode == JT_MATERIALIZED ? st->B : 1);
+      if (ps.write) wr[i].push_back({A_CLIQUE, st->coff[ps.clique], st->coff[ps.clique] + csz});
+      if (ps.src_arena == A_AUX) {
+        Tensor t;
+        t.vars = ps.scope;
+        t.batch = st->B > 1;
+        rd[i].push_back({A_AUX, ps.src_off, ps.src_off + tsize(t)});
+      } else if (ps.src_arena == A_CLIQUE) {
+        rd[i].push_back({A_CLIQUE, st->coff[ps.clique], st->coff[ps.clique] + csz});
+      }
+      for (const auto& f : ps.factors) rd[i].push_back({A_AUX, f.off, f.off + tsize(f)});
+      if (ps.out_kind == OUT_RAW) {
+        wr[i].push_back({-1, ps.out.off, ps.out.off + tsize(ps.out)});
+      } else if (ps.out_kind != OUT_NONE) {
+        const int64_t n = tsize(ps.out);
+        if (ps.out_kind == OUT_SEP_FRESH) {
+          wr[i].push_back({A_AUX, ps.out.off, ps.out.off + n});
+        } else {
+          rd[i].push_back({A_AUX, ps.out.off, ps.out.off + n});
+          if (ps.out2_off < 0) wr[i].push_back({A_AUX, ps.out.off, ps.out.off + n});
+          else wr[i].push_back({A_AUX, ps.out2_off, ps.out2_off + n});
+          wr[i].push_back({A_AUX, ps.ratio_off, ps.ratio_off + n});
+        }
+      }
+    }
+    for (size_t i = 0; i < w.size(); ++i)
+      for (size_t j = 0; j < w.size(); ++j) {
+        if (i == j) continue;
+        for (const Iv& a : wr[i]) {
+          for (const Iv& b : rd[j])
+            if (overlap(a, b)) return JT_ERR_BAD_ARG;
+          if (j > i)
+            for (const Iv& b : wr[j])
+              if (overlap(a, b)) return JT_ERR_BAD_ARG;
+        }
+      }
+  }
+  return JT_OK;
+}
+
 static int compile_program(const jt_state* st, const std::vector<std::vector<PassSpec>>& waves, HostProgram& hp,
                            int occ_override = 0) {
   auto& passes = hp.passes;
@@ -1199,7 +1256,9 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
 static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>& waves,
                          std::unique_ptr<Program>& out) {
   HostProgram hp;
-  int rc0 = compile_program(st, waves, hp);
+  int rc0 = validate_waves(st, waves);
+  if (rc0) return rc0;
+  rc0 = compile_program(st, waves, hp);
   if (rc0) return rc0;
   auto prog = std::make_unique<Program>();
   prog->waves = hp.waves;
@@ -2635,6 +2694,8 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
   }
   std::vector<std::vector<PassSpec>> waves;
   int rc = build_propagate(&st, plan->roots, qv, waves, kind >= 1);
+  if (rc) return rc;
+  rc = validate_waves(&st, waves);
   if (rc) return rc;
   HostProgram hp;
   rc = compile_program(&st, waves, hp, occ > 0 ? occ : 2);
