@@ -164,7 +164,7 @@ struct PassSpec {
 
 struct LaunchGrp {  // one kernel launch of a wave
   int kind = 0;      // 0: general kernel, 1: thread-owned-bins kernel, 2: row kernel
-  int vec = 1;       // lanes per vector load
+  int vec = 1;       // lanes per vector load (kind 3: factors per k, nG)
   int lm = 0;        // own kernel load shapes: 0 generic, 1 src bcast + vector factors, 2 all vector
   int m = 1;         // own kernel vectors per thread per block
   int grid = 0;
@@ -1158,13 +1158,16 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
     }
     const bool small_wave = wave_el < SMALL_WAVE_ELEMS;
     // contraction passes, split by accumulator kind (fp32 sums over > CKF terms fold into fp64)
-    std::vector<CPass> cps[4];
-    std::vector<int> cpc[4];
+    // contraction launch groups keyed by (fold, rowi, nG): fold = fp32 sums over > CKF
+    // terms fold into fp64; nG is a compile-time parameter of the tile kernel
+    constexpr int NGK = CMAXG + 1;
+    std::vector<CPass> cps[4 * NGK];
+    std::vector<int> cpc[4 * NGK];
     for (auto& ps : w) {
       if (contract_eligible(st, ps)) {
         CPass cp;
         if (compile_contract(st, ps, hp, cp) == JT_OK) {
-          const int key = (st->esz == 4 && cp.nK > CKF ? 1 : 0) + 2 * cp.rowi;
+          const int key = ((st->esz == 4 && cp.nK > CKF ? 1 : 0) + 2 * cp.rowi) * NGK + (cp.rowi ? 0 : cp.nG);
           cps[key].push_back(cp);
           cpc[key].push_back(ps.clique);
           continue;
@@ -1227,13 +1230,14 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
       items.insert(items.end(), g.second.begin(), g.second.end());
       rt.groups.push_back(lg);
     }
-    for (int key = 0; key < 4; ++key) {
-      const int fold = key & 1;
+    for (int key = 0; key < 4 * NGK; ++key) {
+      const int fold = (key / NGK) & 1;
       if (cps[key].empty()) continue;
       LaunchGrp cg;
       cg.kind = 3;
       cg.lm = fold;
-      cg.m = key >> 1;
+      cg.m = (key / NGK) >> 1;
+      cg.vec = key % NGK;
       cg.cpass_off = (int64_t)hp.cpasses.size();
       for (size_t q = 0; q < cps[key].size(); ++q) {
         CPass cp = cps[key][q];
@@ -1243,7 +1247,7 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
         hp.cpasses.push_back(cp);
         hp.cpass_clique.push_back(cpc[key][q]);
       }
-      const int occ = occ_override ? occ_override : contract_max_ctas_per_sm(st->plan->dtype, fold, cg.m);
+      const int occ = occ_override ? occ_override : contract_max_ctas_per_sm(st->plan->dtype, fold, cg.m, cg.vec);
       cg.grid = (int)std::min<int64_t>((cg.n_units + NT / 32 - 1) / (NT / 32), (int64_t)occ * st->num_sms);
       rt.groups.push_back(cg);
     }
@@ -1317,7 +1321,7 @@ static int launch_group(jt_state* st, const Program* pr, const WaveRt& w, const 
     c.B = st->B;
     c.partials = pr->d_part;
     c.counters = pr->d_cnt;
-    CK(launch_contract(st->plan->dtype, g.lm, g.m, c, g.grid, s));
+    CK(launch_contract(st->plan->dtype, g.lm, g.m, g.vec, c, g.grid, s));
     st->launches++;
     return JT_OK;
   }

@@ -136,8 +136,9 @@ struct CArgs {
   int* counters;            // K-split arrival counters (reset by the last warp)
 };
 constexpr int CKF = 16;     // fp32 contraction sums longer than this fold into fp64
-cudaError_t launch_contract(int dtype, int fold, int rowi, const CArgs& a, int grid, cudaStream_t s);
-int contract_max_ctas_per_sm(int dtype, int fold, int rowi);
+// ng: factors per k (0..CMAXG) of every pass of the launch (compile-time in the kernel; ignored for rowi)
+cudaError_t launch_contract(int dtype, int fold, int rowi, int ng, const CArgs& a, int grid, cudaStream_t s);
+int contract_max_ctas_per_sm(int dtype, int fold, int rowi, int ng);
 
 // ---- small trees in cluster shared memory (jt_cluster.cu) ----
 constexpr int CL_MAX_RANKS = 16;  // CTAs per cluster (non-portable above 8)

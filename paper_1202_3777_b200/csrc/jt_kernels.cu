@@ -990,71 +990,150 @@ int wave_row_max_ctas_per_sm(int dtype, int vec) {
 
 // ---- contraction passes (shared-base batches) ----
 // Hugin update of VEC consecutive case lanes of one output entry (element
-// offset j of case 0): the epilogue of every pass kind, written once.
-template <typename T, int VEC>
-__device__ __forceinline__ void finalize_lanes(int kind, int64_t out_off, int64_t ratio_off, int64_t out2_off,
-                                               int64_t j, const double (&star)[VEC], T* aux, double* qout,
-                                               int* err) {
+// offset j of case 0) from sums in the accumulator type A (fp32 sums of the
+// unfolded fp32 kernels stay fp32: the ratio and product are the same IEEE
+// results as via fp64); returns "nonzero / 0 seen" for the caller to flag once.
+template <typename T, typename A, int VEC>
+__device__ __forceinline__ bool finalize_lanes(int kind, int64_t out_off, int64_t ratio_off, int64_t out2_off,
+                                               int64_t j, const A (&star)[VEC], const T (&old)[VEC], T* aux,
+                                               double* qout) {
   if (kind == OUT_RAW) {
 #pragma unroll
-    for (int l = 0; l < VEC; ++l) qout[out_off + j + l] = star[l];
-    return;
+    for (int l = 0; l < VEC; ++l) qout[out_off + j + l] = (double)star[l];
+    return false;
   }
   T nw[VEC];
   if (kind == OUT_SEP_FRESH) {
 #pragma unroll
     for (int l = 0; l < VEC; ++l) nw[l] = (T)star[l];
     store_vec<T, VEC>(aux + out_off + j, nw);
-    return;
+    return false;
   }
-  T old[VEC], rt[VEC];
-  load_vec<T, VEC>(aux + out_off + j, old);
+  T rt[VEC];
   bool bad = false;
 #pragma unroll
   for (int l = 0; l < VEC; ++l) {
-    const double o = (double)old[l];
+    const A o = (A)old[l];
     if (kind == OUT_SEP_DFRESH) {
-      rt[l] = (T)(o != 0.0 ? star[l] : 0.0);
+      rt[l] = (T)(o != (A)0 ? star[l] : (A)0);
       nw[l] = (T)(o * star[l]);
     } else {
-      bad |= (o == 0.0 && star[l] != 0.0);
-      rt[l] = (T)(o != 0.0 ? star[l] / o : 0.0);
+      bad |= (o == (A)0 && star[l] != (A)0);
+      rt[l] = (T)(o != (A)0 ? star[l] / o : (A)0);
       nw[l] = (T)star[l];
     }
   }
-  if (bad) atomicOr(err, EB_INCONSISTENT);
   store_vec<T, VEC>(aux + ratio_off + j, rt);
   store_vec<T, VEC>(aux + (out2_off >= 0 ? out2_off : out_off) + j, nw);
+  return bad;
 }
 
 template <typename T> struct CTraits;
 template <> struct CTraits<float> { static constexpr int VEC = 4; };
 template <> struct CTraits<double> { static constexpr int VEC = 2; };
 
-// One warp per unit (i, tile of TMC rows of S', share of the case chunks); each
-// lane owns VEC consecutive cases.  Per k: the product of the G factor rows (one
-// VEC-vector per lane, coalesced across the warp) is reused by the TMC rows of W
-// (two 4-vector broadcast loads; W rows padded to a multiple of 8): TMC x VEC
-// FMAs per lane per k against ~nG + 3 loads.  fp32 sums stay in registers for
-// CKF consecutive k and are then folded into per-thread fp64 accumulators in
-// shared memory (fp64 passes accumulate in registers directly).
-#ifndef CON_KU
-#define CON_KU 1
+// Per-warp cp.async ring of the contraction kernel: stage = NG factor-row
+// slices (16 B per lane each) + the TMC-entry W row; depth by a per-warp budget
+// (fold kernels also hold 64 KB of fp64 accumulators per CTA).
+#ifndef CON_RING_NF
+#define CON_RING_NF 2048
 #endif
+#ifndef CON_RING_F
+#define CON_RING_F 2048
+#endif
+template <typename T, int NG, bool FOLD> struct CRing {
+  static constexpr int SB = NG * 512;  // one stage: NG factor slices of 16 B per lane
+  static constexpr int BUDGET = FOLD ? CON_RING_F : CON_RING_NF;
+  static constexpr int D = NG == 0 ? 2 : (BUDGET / SB > 8 ? 8 : (BUDGET / SB < 2 ? 2 : BUDGET / SB));
+  static constexpr size_t BYTES = (size_t)(NT / 32) * D * SB;
+};
+constexpr size_t CFOLD_SMEM = (size_t)TMC * 4 * NT * sizeof(double);  // fp32 fold accumulators
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// One warp per unit (i, tile of TMC rows of S', share of the case chunks); each
+// Epilogue of one half tile (TMC/2 rows) for one output kind: the rows' old
+// separator values are loaded before any store (stores would otherwise order
+// the loads behind them); returns "nonzero / 0 seen".
+template <typename T, typename A, int VEC, int KIND, bool FOLD, int NG>
+__device__ __forceinline__ bool contract_epilogue_half(const CPass* __restrict__ P, const CArgs& a, int h, int rows,
+                                                       int s0, const int32_t* __restrict__ ti,
+                                                       const int32_t* __restrict__ ts, int b0,
+                                                       const T (&part)[TMC][VEC], const double* cacc) {
+  T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
+  const T* __restrict__ aux_c = aux;
+  const int nE = P->nE;
+  int jo[TMC / 2];
+  const int jb = __ldg(ti + NG + nE);
+#pragma unroll
+  for (int r = 0; r < TMC / 2; ++r) jo[r] = h + r < rows ? jb + __ldg(ts + (int64_t)(s0 + h + r) * (nE + 1) + nE) : 0;
+  T old[TMC / 2][VEC];
+#pragma unroll
+  for (int r = 0; r < TMC / 2; ++r) {
+    if ((KIND == OUT_SEP || KIND == OUT_SEP_DFRESH) && h + r < rows)
+      load_vec<T, VEC>(aux_c + P->out_off + jo[r] + b0, old[r]);
+    else
+#pragma unroll
+      for (int l = 0; l < VEC; ++l) old[r][l] = (T)0;
+  }
+  bool bad = false;
+#pragma unroll
+  for (int r = 0; r < TMC / 2; ++r) {
+    if (h + r >= rows) continue;
+    A v[VEC];
+#pragma unroll
+    for (int l = 0; l < VEC; ++l) v[l] = FOLD ? (A)cacc[((h + r) * VEC + l) * NT + threadIdx.x] : (A)part[h + r][l];
+    if (nE > 0) {
+      const int32_t* tsr = ts + (int64_t)(s0 + h + r) * (nE + 1);
+      for (int e = 0; e < nE; ++e) {
+        T f[VEC];
+        load_vec_ro<T, VEC>(aux_c + P->efac_off[e] + __ldg(ti + NG + e) + __ldg(tsr + e) + b0, f);
+#pragma unroll
+        for (int l = 0; l < VEC; ++l) v[l] *= (A)f[l];
+      }
+    }
+    bad |= finalize_lanes<T, A, VEC>(KIND, P->out_off, P->ratio_off, P->out2_off, (int64_t)jo[r] + b0, v, old[r], aux,
+                                     a.qout);
+  }
+  return bad;
+}
+
+// One warp per unit (i, tile of TMC rows of S', share of the case chunks); each
+// lane owns VEC consecutive cases.  Per k: the product of the NG factor rows
+// (one VEC-vector per lane, coalesced across the warp) is reused by the TMC
+// rows of W: TMC x VEC FMAs per lane per k.  Factor slices stream through a
+// lane-private cp.async ring D stages deep (each lane consumes only what it
+// copied: no barriers, no registers held), so D k-steps of factor loads are in
+// flight per warp; the W row (a warp-uniform 8-entry broadcast, L1-resident
+// across the unit's case-chunk warps) is prefetched one k ahead in registers.
+// fp32 sums stay in registers for CKF consecutive k and are then folded into
+// per-thread fp64 accumulators in shared memory (fp64 passes accumulate in
+// registers).
 #ifndef CON_MINB
 #define CON_MINB 2
 #endif
-template <typename T, bool FOLD>
+template <typename T, bool FOLD, int NG>
 __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
   pdl_enter();
   constexpr int VEC = CTraits<T>::VEC;
-  constexpr int KU = CON_KU;
-  static_assert(TMC == 8, "W rows are loaded as two 4-vectors");
-  extern __shared__ double cacc[];  // FOLD: [TMC * VEC][NT] fp64 accumulators
-  const T* __restrict__ W = reinterpret_cast<const T*>(a.w);
-  T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
-  const T* __restrict__ aux_c = aux;
+  constexpr int WV = sizeof(T) == 4 ? 4 : 2;  // W row loaded as TMC / WV vectors
+  using R = CRing<T, NG, FOLD>;
+  using A = typename std::conditional<FOLD || sizeof(T) == 8, double, T>::type;  // epilogue type
+  static_assert(TMC == 8, "W rows are TMC entries");
+  extern __shared__ __align__(16) unsigned char csm_c[];
+  double* cacc = reinterpret_cast<double*>(csm_c);  // FOLD: [TMC * VEC][NT] fp64 accumulators
   const int lane = threadIdx.x & 31;
+  // this lane's slot of stage 0, slice 0; stage q slice g at + q * SB + g * 512
+  unsigned char* const ring =
+      csm_c + (FOLD ? CFOLD_SMEM : 0) + (size_t)(threadIdx.x >> 5) * R::D * R::SB + lane * 16;
+  const T* __restrict__ W = reinterpret_cast<const T*>(a.w);
+  const T* __restrict__ aux_c = reinterpret_cast<const T*>(a.aux);
   const int n_warps = gridDim.x * (NT / 32);
   int pi = 0;
   for (int64_t u = blockIdx.x * (NT / 32) + (threadIdx.x >> 5); u < a.n_units; u += n_warps) {
@@ -1068,7 +1147,7 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
     const int ks = (int)((ul / nCG) % nKS);
     const int t = (int)((ul / ((int64_t)nCG * nKS)) % nT);
     const int64_t i = ul / ((int64_t)nCG * nKS * nT);
-    const int nS = P->nS, nG = P->nG, nE = P->nE;
+    const int nS = P->nS, nE = P->nE;
     const int kb = ks * P->kch;                      // this unit's k range [kb, kb + nK)
     const int nK = min(P->nK - kb, P->kch);
     const int nKall = P->nK;
@@ -1076,14 +1155,25 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
     const int bstep = 32 * VEC * nCG;
     const int s0 = t * TMC;
     const int rows = min(TMC, nS - s0);
-    const int32_t* __restrict__ ti = a.tab + P->ti_off + i * (nG + nE + 1);
-    const int32_t* __restrict__ tk = a.tab + P->tk_off + (int64_t)kb * nG;
+    const int32_t* __restrict__ ti = a.tab + P->ti_off + i * (NG + nE + 1);
+    const int32_t* __restrict__ tk = a.tab + P->tk_off + (int64_t)kb * NG;
     const int32_t* __restrict__ ts = a.tab + P->ts_off;
     const T* __restrict__ wrow = W + P->w_off + (i * (int64_t)nKall + kb) * nSp + s0;
-    const T* gq[CMAXG];  // factor g at (i, k = kb, case 0)
+    const T* gq[NG > 0 ? NG : 1];  // factor g at (i, k = kb, case 0)
 #pragma unroll
-    for (int g = 0; g < CMAXG; ++g) gq[g] = aux_c + (g < nG ? P->gfac_off[g] + __ldg(ti + g) : 0);
+    for (int g = 0; g < NG; ++g) gq[g] = aux_c + P->gfac_off[g] + __ldg(ti + g);
     for (int b0 = cg * 32 * VEC + lane * VEC; b0 < a.B; b0 += bstep) {
+      auto issue = [&](int k, unsigned char* sp) {
+#pragma unroll
+        for (int g = 0; g < NG; ++g) cp_async16(sp + g * 512, gq[g] + b0 + __ldg(tk + k * NG + g));
+      };
+      if (NG > 0) {
+#pragma unroll
+        for (int q = 0; q < R::D - 1; ++q) {
+          if (q < nK) issue(q, ring + q * R::SB);
+          cp_async_commit();
+        }
+      }
       T part[TMC][VEC];
 #pragma unroll
       for (int r = 0; r < TMC; ++r)
@@ -1092,51 +1182,54 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
       if (FOLD)
 #pragma unroll
         for (int q = 0; q < TMC * VEC; ++q) cacc[q * NT + threadIdx.x] = 0.0;
-      for (int k0 = 0; k0 < nK; k0 += (FOLD ? CKF : nK)) {
-        const int k1 = FOLD ? min(nK, k0 + CKF) : nK;
-        for (int k = k0; k < k1; k += KU) {
-          T pv[KU][VEC];
-          T w[KU][TMC];
+      T wn[TMC];  // W row of the next k
 #pragma unroll
-          for (int q = 0; q < KU; ++q) {
-            const int kq = min(k + q, k1 - 1);  // clamped: the term is zeroed below
+      for (int h = 0; h < TMC / WV; ++h) {
+        T x[WV];
+        load_vec_ro<T, WV>(wrow + h * WV, x);
 #pragma unroll
-            for (int l = 0; l < VEC; ++l) pv[q][l] = (T)1;
+        for (int l = 0; l < WV; ++l) wn[h * WV + l] = x[l];
+      }
+      unsigned char* sp = ring;                          // stage of k
+      unsigned char* spn = ring + (R::D - 1) * R::SB;    // stage refilled at k (k + D - 1)
+      int since = 0;
+      for (int k = 0; k < nK; ++k) {
+        T w[TMC];
 #pragma unroll
-            for (int g = 0; g < CMAXG; ++g) {
-              if (g < nG) {
-                T f[VEC];
-                load_vec_ro<T, VEC>(gq[g] + b0 + __ldg(tk + kq * nG + g), f);
+        for (int r = 0; r < TMC; ++r) w[r] = wn[r];
+        if (k + 1 < nK) {
 #pragma unroll
-                for (int l = 0; l < VEC; ++l) pv[q][l] *= f[l];
-              }
-            }
-            const T* wk = wrow + (int64_t)kq * nSp;
-            if constexpr (sizeof(T) == 4) {
-              const float4 x = __ldg(reinterpret_cast<const float4*>(wk));
-              const float4 y = __ldg(reinterpret_cast<const float4*>(wk) + 1);
-              w[q][0] = x.x; w[q][1] = x.y; w[q][2] = x.z; w[q][3] = x.w;
-              w[q][4] = y.x; w[q][5] = y.y; w[q][6] = y.z; w[q][7] = y.w;
-            } else {
+          for (int h = 0; h < TMC / WV; ++h) {
+            T x[WV];
+            load_vec_ro<T, WV>(wrow + (int64_t)(k + 1) * nSp + h * WV, x);
 #pragma unroll
-              for (int h = 0; h < 4; ++h) {
-                const double2 x = __ldg(reinterpret_cast<const double2*>(wk) + h);
-                w[q][2 * h] = x.x;
-                w[q][2 * h + 1] = x.y;
-              }
-            }
-            if (k + q >= k1)
-#pragma unroll
-              for (int r = 0; r < TMC; ++r) w[q][r] = (T)0;
+            for (int l = 0; l < WV; ++l) wn[h * WV + l] = x[l];
           }
-#pragma unroll
-          for (int q = 0; q < KU; ++q)
-#pragma unroll
-            for (int r = 0; r < TMC; ++r)
-#pragma unroll
-              for (int l = 0; l < VEC; ++l) part[r][l] += w[q][r] * pv[q][l];
         }
-        if (FOLD) {
+        T pv[VEC];
+#pragma unroll
+        for (int l = 0; l < VEC; ++l) pv[l] = (T)1;
+        if (NG > 0) {
+          cp_async_wait<R::D - 2>();
+#pragma unroll
+          for (int g = 0; g < NG; ++g) {
+            T f[VEC];
+            load_vec<T, VEC>(reinterpret_cast<const T*>(sp + g * 512), f);
+#pragma unroll
+            for (int l = 0; l < VEC; ++l) pv[l] *= f[l];
+          }
+          // refill the stage consumed last iteration (this lane's own slot)
+          if (k + R::D - 1 < nK) issue(k + R::D - 1, spn);
+          cp_async_commit();
+          spn = sp;
+          sp = sp + R::SB == ring + R::D * R::SB ? ring : sp + R::SB;
+        }
+#pragma unroll
+        for (int r = 0; r < TMC; ++r)
+#pragma unroll
+          for (int l = 0; l < VEC; ++l) part[r][l] += w[r] * pv[l];
+        if (FOLD && ++since == CKF) {
+          since = 0;
 #pragma unroll
           for (int r = 0; r < TMC; ++r)
 #pragma unroll
@@ -1146,6 +1239,14 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
             }
         }
       }
+      if (FOLD)
+#pragma unroll
+        for (int r = 0; r < TMC; ++r)
+#pragma unroll
+          for (int l = 0; l < VEC; ++l) {
+            cacc[(r * VEC + l) * NT + threadIdx.x] += (double)part[r][l];
+            part[r][l] = (T)0;
+          }
       if (nKS > 1) {
         // K-split: park this chunk's sums; the last warp of the (i, t, case chunk)
         // group adds the nKS partials in chunk order and runs the epilogue
@@ -1175,22 +1276,29 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
             else part[r][l] = (T)t_;  // fp64 passes only (fp32 K-split passes always fold)
           }
       }
+      bool bad = false;
+      switch (P->out_kind) {  // warp-uniform: one specialised epilogue per kind
+        case OUT_SEP_FRESH:
 #pragma unroll
-      for (int r = 0; r < TMC; ++r) {
-        if (r >= rows) continue;
-        const int32_t* tsr = ts + (int64_t)(s0 + r) * (nE + 1);
-        double v[VEC];
+          for (int h = 0; h < TMC; h += TMC / 2)
+            contract_epilogue_half<T, A, VEC, OUT_SEP_FRESH, FOLD, NG>(P, a, h, rows, s0, ti, ts, b0, part, cacc);
+          break;
+        case OUT_RAW:
 #pragma unroll
-        for (int l = 0; l < VEC; ++l) v[l] = FOLD ? cacc[(r * VEC + l) * NT + threadIdx.x] : (double)part[r][l];
-        for (int e = 0; e < nE; ++e) {
-          T f[VEC];
-          load_vec_ro<T, VEC>(aux_c + P->efac_off[e] + __ldg(ti + nG + e) + __ldg(tsr + e) + b0, f);
+          for (int h = 0; h < TMC; h += TMC / 2)
+            contract_epilogue_half<T, A, VEC, OUT_RAW, FOLD, NG>(P, a, h, rows, s0, ti, ts, b0, part, cacc);
+          break;
+        case OUT_SEP_DFRESH:
 #pragma unroll
-          for (int l = 0; l < VEC; ++l) v[l] *= (double)f[l];
-        }
-        finalize_lanes<T, VEC>(P->out_kind, P->out_off, P->ratio_off, P->out2_off,
-                               (int64_t)__ldg(ti + nG + nE) + __ldg(tsr + nE) + b0, v, aux, a.qout, a.err);
+          for (int h = 0; h < TMC; h += TMC / 2)
+            contract_epilogue_half<T, A, VEC, OUT_SEP_DFRESH, FOLD, NG>(P, a, h, rows, s0, ti, ts, b0, part, cacc);
+          break;
+        default:
+#pragma unroll
+          for (int h = 0; h < TMC; h += TMC / 2)
+            bad |= contract_epilogue_half<T, A, VEC, OUT_SEP, FOLD, NG>(P, a, h, rows, s0, ti, ts, b0, part, cacc);
       }
+      if (bad) atomicOr(a.err, EB_INCONSISTENT);
     }
   }
 }
@@ -1296,15 +1404,57 @@ __global__ void __launch_bounds__(NT, FOLD ? ROWI_MINB_F : ROWI_MINB_NF) contrac
 #pragma unroll
         for (int l = 0; l < VEC; ++l) v[l] *= (double)f[l];
       }
-      finalize_lanes<T, VEC>(P->out_kind, P->out_off, P->ratio_off, P->out2_off,
-                             (int64_t)__ldg(tir + nG + nE) + __ldg(ts + nE) + b0, v, aux, a.qout, a.err);
+      const int64_t j = (int64_t)__ldg(tir + nG + nE) + __ldg(ts + nE) + b0;
+      T old[VEC] = {};
+      if (P->out_kind == OUT_SEP || P->out_kind == OUT_SEP_DFRESH) load_vec<T, VEC>(aux_c + P->out_off + j, old);
+      if (finalize_lanes<T, double, VEC>(P->out_kind, P->out_off, P->ratio_off, P->out2_off, j, v, old, aux, a.qout))
+        atomicOr(a.err, EB_INCONSISTENT);
     }
   }
 }
 
-constexpr size_t CFOLD_SMEM = (size_t)TMC * 4 * NT * sizeof(double);  // fp32 fold accumulators
+template <typename T, bool FOLD, int NG>
+static size_t contract_smem() {
+  return (FOLD ? CFOLD_SMEM : 0) + CRing<T, NG, FOLD>::BYTES;
+}
 
-cudaError_t launch_contract(int dtype, int fold, int rowi, const CArgs& a, int grid, cudaStream_t s) {
+template <typename T, bool FOLD, int NG>
+static cudaError_t contract_prepare() {
+  static bool done = false;  // one attribute call per instantiation (host thread of the plan owner)
+  if (done) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(contract_kernel<T, FOLD, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)contract_smem<T, FOLD, NG>());
+  if (e == cudaSuccess) done = true;
+  return e;
+}
+
+template <typename T, bool FOLD, int NG>
+static cudaError_t launch_contract_t(const CArgs& a, int grid, cudaStream_t s) {
+  cudaError_t e = contract_prepare<T, FOLD, NG>();
+  if (e != cudaSuccess) return e;
+  return launch_pdl(contract_kernel<T, FOLD, NG>, grid, NT, contract_smem<T, FOLD, NG>(), s, a);
+}
+
+template <typename T, bool FOLD, int NG>
+static int occ_contract_t() {
+  if (contract_prepare<T, FOLD, NG>() != cudaSuccess) return 1;
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_kernel<T, FOLD, NG>, NT, contract_smem<T, FOLD, NG>());
+  return n > 0 ? n : 1;
+}
+
+template <typename T, bool FOLD, class F>
+static auto by_ng(int ng, F f) {
+  switch (ng) {
+    case 0: return f(std::integral_constant<int, 0>());
+    case 1: return f(std::integral_constant<int, 1>());
+    case 2: return f(std::integral_constant<int, 2>());
+    case 3: return f(std::integral_constant<int, 3>());
+    default: return f(std::integral_constant<int, 4>());
+  }
+}
+
+cudaError_t launch_contract(int dtype, int fold, int rowi, int ng, const CArgs& a, int grid, cudaStream_t s) {
   if (grid <= 0 || a.n_units <= 0) return cudaSuccess;
   if (rowi) {
     if (dtype == 0)
@@ -1312,37 +1462,24 @@ cudaError_t launch_contract(int dtype, int fold, int rowi, const CArgs& a, int g
                   : launch_pdl(contract_rowi_kernel<float, false>, grid, NT, 0, s, a);
     return launch_pdl(contract_rowi_kernel<double, false>, grid, NT, 0, s, a);
   }
-  if (dtype == 0) {
-    if (fold) {
-      static bool attr = false;
-      if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(contract_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)CFOLD_SMEM);
-        if (e != cudaSuccess) return e;
-        attr = true;
-      }
-      return launch_pdl(contract_kernel<float, true>, grid, NT, CFOLD_SMEM, s, a);
-    }
-    return launch_pdl(contract_kernel<float, false>, grid, NT, 0, s, a);
-  }
-  return launch_pdl(contract_kernel<double, false>, grid, NT, 0, s, a);
+  if (dtype == 0 && fold)
+    return by_ng<float, true>(ng, [&](auto c) { return launch_contract_t<float, true, decltype(c)::value>(a, grid, s); });
+  if (dtype == 0)
+    return by_ng<float, false>(ng, [&](auto c) { return launch_contract_t<float, false, decltype(c)::value>(a, grid, s); });
+  return by_ng<double, false>(ng, [&](auto c) { return launch_contract_t<double, false, decltype(c)::value>(a, grid, s); });
 }
 
-int contract_max_ctas_per_sm(int dtype, int fold, int rowi) {
+int contract_max_ctas_per_sm(int dtype, int fold, int rowi, int ng) {
   int n = 0;
   if (rowi) {
     if (dtype == 0 && fold) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_rowi_kernel<float, true>, NT, 0);
     else if (dtype == 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_rowi_kernel<float, false>, NT, 0);
     else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_rowi_kernel<double, false>, NT, 0);
-  } else if (dtype == 0 && fold) {
-    cudaFuncSetAttribute(contract_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CFOLD_SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_kernel<float, true>, NT, CFOLD_SMEM);
-  } else if (dtype == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_kernel<float, false>, NT, 0);
-  } else {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_kernel<double, false>, NT, 0);
+    return n > 0 ? n : 1;
   }
-  return n > 0 ? n : 1;
+  if (dtype == 0 && fold) return by_ng<float, true>(ng, [&](auto c) { return occ_contract_t<float, true, decltype(c)::value>(); });
+  if (dtype == 0) return by_ng<float, false>(ng, [&](auto c) { return occ_contract_t<float, false, decltype(c)::value>(); });
+  return by_ng<double, false>(ng, [&](auto c) { return occ_contract_t<double, false, decltype(c)::value>(); });
 }
 
 template <int VEC, int KVT>
