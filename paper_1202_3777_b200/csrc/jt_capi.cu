@@ -174,6 +174,7 @@ struct LaunchGrp {  // one kernel launch of a wave
   int64_t cpass_off = 0;
   int n_cpasses = 0;
   int64_t n_units = 0;
+  int interleave = 0;  // CArgs::interleave
 };
 
 struct WaveRt {
@@ -929,6 +930,7 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
     std::stable_sort(cost.begin(), cost.end());
     std::vector<int> Io;
     for (auto& x : cost) Io.push_back(I[x.second]);
+    if (getenv("JT_IPERM_REV")) std::reverse(Io.begin(), Io.end());
     if (!getenv("JT_NO_IPERM")) I.swap(Io);
   }
   auto strides = [&](const std::vector<int>& vars, const Tensor& t) {
@@ -1247,6 +1249,15 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
         hp.cpasses.push_back(cp);
         hp.cpass_clique.push_back(cpc[key][q]);
       }
+      // passes of one clique with equal unit counts (e.g. the distribute messages to
+      // children with equal separators) read the same factor tensors: interleave their
+      // units so the second reader finds them in L1/L2
+      if (cps[key].size() > 1 && !getenv("JT_NO_INTERLEAVE")) {
+        bool same = true;
+        for (size_t q = 1; q < cps[key].size(); ++q)
+          same = same && cps[key][q].n_units == cps[key][0].n_units && cpc[key][q] == cpc[key][0];
+        cg.interleave = same ? 1 : 0;
+      }
       const int occ = occ_override ? occ_override : contract_max_ctas_per_sm(st->plan->dtype, fold, cg.m, cg.vec);
       cg.grid = (int)std::min<int64_t>((cg.n_units + NT / 32 - 1) / (NT / 32), (int64_t)occ * st->num_sms);
       rt.groups.push_back(cg);
@@ -1321,6 +1332,7 @@ static int launch_group(jt_state* st, const Program* pr, const WaveRt& w, const 
     c.B = st->B;
     c.partials = pr->d_part;
     c.counters = pr->d_cnt;
+    c.interleave = g.interleave;
     CK(launch_contract(st->plan->dtype, g.lm, g.m, g.vec, c, g.grid, s));
     st->launches++;
     return JT_OK;
@@ -2738,8 +2750,8 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
     out += line;
     for (const LaunchGrp& g : rt.groups) {
       if (g.kind == 3)
-        snprintf(line, sizeof line, " [contract passes %d units %lld grid %d]", g.n_cpasses, (long long)g.n_units,
-                 g.grid);
+        snprintf(line, sizeof line, " [contract passes %d units %lld grid %d%s]", g.n_cpasses, (long long)g.n_units,
+                 g.grid, g.interleave ? " interleaved" : "");
       else
         snprintf(line, sizeof line, " [%s vec %d items %d grid %d]", g.kind == 1 ? "own" : g.kind == 2 ? "row" : "gen",
                  g.vec, g.n_items, g.grid);

@@ -134,6 +134,8 @@ struct CArgs {
   int B;
   double* partials;         // K-split partial sums
   int* counters;            // K-split arrival counters (reset by the last warp)
+  int interleave;           // 1: every pass has n_units / n_passes units and unit u belongs to
+                            // pass u % n_passes (passes reading the same tensors run side by side)
 };
 constexpr int CKF = 16;     // fp32 contraction sums longer than this fold into fp64
 // ng: factors per k (0..CMAXG) of every pass of the launch (compile-time in the kernel; ignored for rowi)

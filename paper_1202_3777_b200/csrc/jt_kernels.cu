@@ -1058,6 +1058,17 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 // One warp per unit (i, tile of TMC rows of S', share of the case chunks); each
+// epilogue inputs (old separator values, E factors) are read once: streaming
+// loads keep them from evicting the units' W rows from L1
+#ifndef CON_EPI_CS
+#define CON_EPI_CS 1
+#endif
+template <typename T, int VEC>
+__device__ __forceinline__ void con_epi_load(const T* p, T (&v)[VEC]) {
+  if (CON_EPI_CS) load_vec_cs<T, VEC>(p, v);
+  else load_vec<T, VEC>(p, v);
+}
+
 // Epilogue of one half tile (TMC/2 rows) for one output kind: the rows' old
 // separator values are loaded before any store (stores would otherwise order
 // the loads behind them); returns "nonzero / 0 seen".
@@ -1077,7 +1088,7 @@ __device__ __forceinline__ bool contract_epilogue_half(const CPass* __restrict__
 #pragma unroll
   for (int r = 0; r < TMC / 2; ++r) {
     if ((KIND == OUT_SEP || KIND == OUT_SEP_DFRESH) && h + r < rows)
-      load_vec<T, VEC>(aux_c + P->out_off + jo[r] + b0, old[r]);
+      con_epi_load<T, VEC>(aux_c + P->out_off + jo[r] + b0, old[r]);
     else
 #pragma unroll
       for (int l = 0; l < VEC; ++l) old[r][l] = (T)0;
@@ -1093,7 +1104,7 @@ __device__ __forceinline__ bool contract_epilogue_half(const CPass* __restrict__
       const int32_t* tsr = ts + (int64_t)(s0 + h + r) * (nE + 1);
       for (int e = 0; e < nE; ++e) {
         T f[VEC];
-        load_vec_ro<T, VEC>(aux_c + P->efac_off[e] + __ldg(ti + NG + e) + __ldg(tsr + e) + b0, f);
+        con_epi_load<T, VEC>(aux_c + P->efac_off[e] + __ldg(ti + NG + e) + __ldg(tsr + e) + b0, f);
 #pragma unroll
         for (int l = 0; l < VEC; ++l) v[l] *= (A)f[l];
       }
@@ -1118,6 +1129,9 @@ __device__ __forceinline__ bool contract_epilogue_half(const CPass* __restrict__
 #ifndef CON_MINB
 #define CON_MINB 2
 #endif
+#ifndef CON_WPF
+#define CON_WPF 1
+#endif
 template <typename T, bool FOLD, int NG>
 __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
   pdl_enter();
@@ -1137,10 +1151,16 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
   const int n_warps = gridDim.x * (NT / 32);
   int pi = 0;
   for (int64_t u = blockIdx.x * (NT / 32) + (threadIdx.x >> 5); u < a.n_units; u += n_warps) {
-    while (pi + 1 < a.n_passes && u >= a.passes[pi + 1].unit0) ++pi;
-    while (pi > 0 && u < a.passes[pi].unit0) --pi;
+    int64_t ul;
+    if (a.interleave) {
+      pi = (int)(u % a.n_passes);
+      ul = u / a.n_passes;
+    } else {
+      while (pi + 1 < a.n_passes && u >= a.passes[pi + 1].unit0) ++pi;
+      while (pi > 0 && u < a.passes[pi].unit0) --pi;
+      ul = u - a.passes[pi].unit0;
+    }
     const CPass* __restrict__ P = a.passes + pi;
-    const int64_t ul = u - P->unit0;
     const int nT = P->nT, nCG = P->nCG, nKS = P->nKS;
     // unit = (i, t, ks, cg), case chunk fastest: concurrent warps share factor rows
     const int cg = (int)(ul % nCG);
@@ -1182,28 +1202,34 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
       if (FOLD)
 #pragma unroll
         for (int q = 0; q < TMC * VEC; ++q) cacc[q * NT + threadIdx.x] = 0.0;
-      T wn[TMC];  // W row of the next k
+      T wn[CON_WPF][TMC];  // W rows of the next CON_WPF k
 #pragma unroll
-      for (int h = 0; h < TMC / WV; ++h) {
-        T x[WV];
-        load_vec_ro<T, WV>(wrow + h * WV, x);
+      for (int q = 0; q < CON_WPF; ++q)
 #pragma unroll
-        for (int l = 0; l < WV; ++l) wn[h * WV + l] = x[l];
-      }
+        for (int h = 0; h < TMC / WV; ++h) {
+          T x[WV];
+          if (q < nK) load_vec_ro<T, WV>(wrow + (int64_t)q * nSp + h * WV, x);
+#pragma unroll
+          for (int l = 0; l < WV; ++l) wn[q][h * WV + l] = q < nK ? x[l] : (T)0;
+        }
       unsigned char* sp = ring;                          // stage of k
       unsigned char* spn = ring + (R::D - 1) * R::SB;    // stage refilled at k (k + D - 1)
       int since = 0;
       for (int k = 0; k < nK; ++k) {
         T w[TMC];
 #pragma unroll
-        for (int r = 0; r < TMC; ++r) w[r] = wn[r];
-        if (k + 1 < nK) {
+        for (int r = 0; r < TMC; ++r) w[r] = wn[0][r];
+#pragma unroll
+        for (int q = 0; q + 1 < CON_WPF; ++q)
+#pragma unroll
+          for (int r = 0; r < TMC; ++r) wn[q][r] = wn[q + 1][r];
+        if (k + CON_WPF < nK) {
 #pragma unroll
           for (int h = 0; h < TMC / WV; ++h) {
             T x[WV];
-            load_vec_ro<T, WV>(wrow + (int64_t)(k + 1) * nSp + h * WV, x);
+            load_vec_ro<T, WV>(wrow + (int64_t)(k + CON_WPF) * nSp + h * WV, x);
 #pragma unroll
-            for (int l = 0; l < WV; ++l) wn[h * WV + l] = x[l];
+            for (int l = 0; l < WV; ++l) wn[CON_WPF - 1][h * WV + l] = x[l];
           }
         }
         T pv[VEC];
@@ -1338,10 +1364,16 @@ __global__ void __launch_bounds__(NT, FOLD ? ROWI_MINB_F : ROWI_MINB_NF) contrac
   const int n_warps = gridDim.x * (NT / 32);
   int pi = 0;
   for (int64_t u = blockIdx.x * (NT / 32) + (threadIdx.x >> 5); u < a.n_units; u += n_warps) {
-    while (pi + 1 < a.n_passes && u >= a.passes[pi + 1].unit0) ++pi;
-    while (pi > 0 && u < a.passes[pi].unit0) --pi;
+    int64_t ul;
+    if (a.interleave) {
+      pi = (int)(u % a.n_passes);
+      ul = u / a.n_passes;
+    } else {
+      while (pi + 1 < a.n_passes && u >= a.passes[pi + 1].unit0) ++pi;
+      while (pi > 0 && u < a.passes[pi].unit0) --pi;
+      ul = u - a.passes[pi].unit0;
+    }
     const CPass* __restrict__ P = a.passes + pi;
-    const int64_t ul = u - P->unit0;
     const int nCG = P->nCG;
     const int cg = (int)(ul % nCG);
     const int64_t i = ul / nCG;
