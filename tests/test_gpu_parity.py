@@ -335,9 +335,12 @@ def test_tree_dump_to_device_plan():  # §8f row 4: .jt.json → cached device p
 
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
-def test_batch_contraction_path_large_batch(dtype):
+@pytest.mark.parametrize("batch", [128, 132])
+def test_batch_contraction_path_large_batch(dtype, batch):
     """Shared-base micro-batches large enough for the contraction passes
-    (DESIGN.md §3b): every case matches the reference goldens / the oracle."""
+    (DESIGN.md §3b): every case matches the reference goldens / the oracle.
+    132 cases: the last case chunk is partial (lanes past B leave the case loop
+    before the K-split combine)."""
     from paper_1202_3777_b200.batch import BatchPropagator
 
     tree, data = load_golden("c5")
@@ -347,7 +350,7 @@ def test_batch_contraction_path_large_batch(dtype):
     template = jtref.from_potentials(tree, tables)
     want_extra = [jtref.case_posteriors(template, ev, range(len(tree.cards))) for ev in extra]
     cases = [golden[i % len(golden)][0] for i in range(250)] + extra
-    bp = BatchPropagator(tree, tables, batch=128, dtype=dtype, mode="shared")
+    bp = BatchPropagator(tree, tables, batch=batch, dtype=dtype, mode="shared")
     out = bp.run(cases).cpu().numpy()
     bp.sync()
     for i in range(250):
