@@ -1041,7 +1041,10 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   cp.kch = (int)nK;
   cp.n_units = (rowi ? 1 : nI) * cp.nT * cp.nCG;
   int64_t min_units = (int64_t)st->num_sms * 8;
-  if (!rowi && cp.n_units < min_units && nK >= 256) {
+  // (the K-split combine is a warp collective: every lane must own cases, so B
+  // must fill whole case chunks; otherwise the pass takes the general kernels)
+  const int kvec = st->esz == 4 ? 4 : 2;
+  if (!rowi && cp.n_units < min_units && nK >= 256 && B % (32 * kvec) == 0) {
     // long sums with few units (posteriors of a clique-private variable): split K
     // into chunks of >= 64 k so every warp has work; partials combined in order
     const int vec = st->esz == 4 ? 4 : 2;

@@ -1075,7 +1075,7 @@ __device__ __forceinline__ void con_epi_load(const T* p, T (&v)[VEC]) {
 template <typename T, typename A, int VEC, int KIND, bool FOLD, int NG>
 __device__ __forceinline__ bool contract_epilogue_half(const CPass* __restrict__ P, const CArgs& a, int h, int rows,
                                                        int s0, const int32_t* __restrict__ ti,
-                                                       const int32_t* __restrict__ ts, int b0, bool lane_ok,
+                                                       const int32_t* __restrict__ ts, int b0,
                                                        const T (&part)[TMC][VEC], const double* cacc) {
   T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
   const T* __restrict__ aux_c = aux;
@@ -1096,7 +1096,7 @@ __device__ __forceinline__ bool contract_epilogue_half(const CPass* __restrict__
   bool bad = false;
 #pragma unroll
   for (int r = 0; r < TMC / 2; ++r) {
-    if (h + r >= rows || !lane_ok) continue;
+    if (h + r >= rows) continue;
     A v[VEC];
 #pragma unroll
     for (int l = 0; l < VEC; ++l) v[l] = FOLD ? (A)cacc[((h + r) * VEC + l) * NT + threadIdx.x] : (A)part[h + r][l];
@@ -1182,11 +1182,7 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
     const T* gq[NG > 0 ? NG : 1];  // factor g at (i, k = kb, case 0)
 #pragma unroll
     for (int g = 0; g < NG; ++g) gq[g] = aux_c + P->gfac_off[g] + __ldg(ti + g);
-    // the whole warp walks the case chunks together (the K-split combine is a warp
-    // collective); lanes past the last case compute on a clamped copy, store nothing
-    for (int bb = cg * 32 * VEC; bb < a.B; bb += bstep) {
-      const bool lane_ok = bb + lane * VEC < a.B;
-      const int b0 = lane_ok ? bb + lane * VEC : a.B - VEC;
+    for (int b0 = cg * 32 * VEC + lane * VEC; b0 < a.B; b0 += bstep) {
       auto issue = [&](int k, unsigned char* sp) {
 #pragma unroll
         for (int g = 0; g < NG; ++g) cp_async16(sp + g * 512, gq[g] + b0 + __ldg(tk + k * NG + g));
@@ -1289,7 +1285,7 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
             __stcg(pp + (int64_t)ks * (TMC * 32 * VEC) + (r * 32 + lane) * VEC + l,
                    FOLD ? cacc[(r * VEC + l) * NT + threadIdx.x] : (double)part[r][l]);
         __threadfence();
-        __syncwarp();
+        __syncwarp();  // K-split passes need B % (32 VEC) == 0 (compile_contract): every lane is here
         int arrived = 0;
         if (lane == 0) arrived = atomicAdd(a.counters + P->cnt_off + grp, 1);
         arrived = __shfl_sync(0xffffffffu, arrived, 0);
@@ -1311,22 +1307,22 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
         case OUT_SEP_FRESH:
 #pragma unroll
           for (int h = 0; h < TMC; h += TMC / 2)
-            contract_epilogue_half<T, A, VEC, OUT_SEP_FRESH, FOLD, NG>(P, a, h, rows, s0, ti, ts, b0, lane_ok, part, cacc);
+            contract_epilogue_half<T, A, VEC, OUT_SEP_FRESH, FOLD, NG>(P, a, h, rows, s0, ti, ts, b0, part, cacc);
           break;
         case OUT_RAW:
 #pragma unroll
           for (int h = 0; h < TMC; h += TMC / 2)
-            contract_epilogue_half<T, A, VEC, OUT_RAW, FOLD, NG>(P, a, h, rows, s0, ti, ts, b0, lane_ok, part, cacc);
+            contract_epilogue_half<T, A, VEC, OUT_RAW, FOLD, NG>(P, a, h, rows, s0, ti, ts, b0, part, cacc);
           break;
         case OUT_SEP_DFRESH:
 #pragma unroll
           for (int h = 0; h < TMC; h += TMC / 2)
-            contract_epilogue_half<T, A, VEC, OUT_SEP_DFRESH, FOLD, NG>(P, a, h, rows, s0, ti, ts, b0, lane_ok, part, cacc);
+            contract_epilogue_half<T, A, VEC, OUT_SEP_DFRESH, FOLD, NG>(P, a, h, rows, s0, ti, ts, b0, part, cacc);
           break;
         default:
 #pragma unroll
           for (int h = 0; h < TMC; h += TMC / 2)
-            bad |= contract_epilogue_half<T, A, VEC, OUT_SEP, FOLD, NG>(P, a, h, rows, s0, ti, ts, b0, lane_ok, part, cacc);
+            bad |= contract_epilogue_half<T, A, VEC, OUT_SEP, FOLD, NG>(P, a, h, rows, s0, ti, ts, b0, part, cacc);
       }
       if (bad) atomicOr(a.err, EB_INCONSISTENT);
     }
