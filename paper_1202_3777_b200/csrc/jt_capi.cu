@@ -891,6 +891,12 @@ static std::vector<int64_t> group_offsets(const jt_plan* p, const std::vector<in
   return out;
 }
 
+#ifndef CON_NCG_MID
+#define CON_NCG_MID 4  // case chunks per unit group for 8 <= nK < 32
+#endif
+#ifndef CON_NCG_SMALL
+#define CON_NCG_SMALL 1  // and for nK < 8 (a unit walks all case chunks)
+#endif
 static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram& hp, CPass& cp) {
   const jt_plan* p = st->plan;
   const int64_t B = st->B;
@@ -1036,7 +1042,7 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   cp.nBC = (int)((B + 32 * CVEC - 1) / (32 * CVEC));
   // a unit walks a share of the case chunks of its (i, row tile): all of them for
   // short sums (amortises the unit's setup), one per unit for long ones (parallelism)
-  cp.nCG = nK >= 32 ? cp.nBC : nK >= 8 ? std::min(4, cp.nBC) : 1;
+  cp.nCG = nK >= 32 ? cp.nBC : nK >= 8 ? std::min(CON_NCG_MID, cp.nBC) : std::min(CON_NCG_SMALL, cp.nBC);
   cp.nKS = 1;
   cp.kch = (int)nK;
   cp.n_units = (rowi ? 1 : nI) * cp.nT * cp.nCG;
