@@ -86,6 +86,10 @@ int jt_state_initialize(jt_state* st, int n_cpts, const int32_t* cpt_clique, con
  * replica, separators to ones) and drop all evidence: PropagationState.copy()
  * of a template state (cli.py:194-201), done on device for the whole batch. */
 int jt_state_reset(jt_state* st, void* stream);
+/* PropagationState.copy() (propagate.py:193-201) on the device: a new state over
+ * the same plan, batch and mode whose arenas, separator roles and evidence are a
+ * device-to-device copy of src. */
+int jt_state_clone(jt_state* src, jt_state** out);
 /* Read back one case (host views of state.clique_values / state.sep_values).
  * Shared-base states materialise the final tables of that case on the fly. */
 int jt_state_store(jt_state* st, int case_idx, double* clique_concat, double* sep_concat);
@@ -125,6 +129,10 @@ int jt_propagate_query(jt_state* st, int n, const int32_t* var, int normalize,
 
 /* Synchronize the stream, return and clear the device error word. */
 int jt_sync_error(jt_state* st);
+/* Lowest case index whose posterior had zero mass at the last jt_sync_error
+ * that returned JT_ERR_ZERO_MASS, else -1 (the reference raises per case:
+ * potential.py:181-186 via estimator.py:130-133). */
+int jt_error_case(const jt_state* st);
 const char* jt_error_string(int code);
 /* Kernel launches issued by this state since creation (for bench accounting). */
 int64_t jt_state_launch_count(const jt_state* st);

@@ -54,6 +54,8 @@ SIGNATURES = {
     "jt_query_device": (C.c_int, [_vp, C.c_int, _i32p, _i32p, C.c_int, _vp, _vp]),
     "jt_propagate_query": (C.c_int, [_vp, C.c_int, _i32p, C.c_int, _vp, _vp]),
     "jt_sync_error": (C.c_int, [_vp]),
+    "jt_error_case": (C.c_int, [_vp]),
+    "jt_state_clone": (C.c_int, [_vp, C.POINTER(_vp)]),
     "jt_error_string": (C.c_char_p, [C.c_int]),
     "jt_state_launch_count": (C.c_int64, [_vp]),
     "jt_run_message_mu": (C.c_int, [_f64p, C.c_int64, _f64p, C.c_int64, _f64p, C.c_int64, _vp, C.c_int64,

@@ -28,6 +28,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import JT_MATERIALIZED, JT_SHARED_BASE, check, f64, i32, ptr
+from .errors import StateOutOfRangeError, UnknownVariableError, ZeroMassError
 from .propagate import _scope_size, plan_for
 
 MODES = {"shared": JT_SHARED_BASE, "materialized": JT_MATERIALIZED}
@@ -115,15 +116,9 @@ class BatchPropagator:
 
     def encode(self, cases):
         """(case, var, clique, value) int32 arrays for jt_apply_evidence."""
-        cidx, vs, cs, xs = [], [], [], []
-        for b, ev in enumerate(cases):
-            items = ev.assignments.items() if hasattr(ev, "assignments") else dict(ev).items()
-            for var, val in sorted(items):
-                cidx.append(b)
-                vs.append(int(var))
-                cs.append(self.owner[int(var)])
-                xs.append(int(val))
-        return i32(cidx), i32(vs), i32(cs), i32(xs)
+        obs = self.encode_obs(cases)
+        own = self._owner_arr[obs[:, 1]] if len(obs) else np.zeros(0, np.int32)
+        return i32(obs[:, 0]), i32(obs[:, 1]), i32(own), i32(obs[:, 2])
 
     def step(self, encoded, out, stream=None):
         """One device step over ≤ batch cases: reset, evidence, propagate and
@@ -131,8 +126,7 @@ class BatchPropagator:
         `stream` (default: this propagator's stream)."""
         cidx, vs, cs, xs = encoded
         L = _lib.lib()
-        if stream is None:
-            stream = C.c_void_p(self.stream.cuda_stream)
+        stream = self._raw_stream(stream)
         check(L.jt_state_reset(self.handle, stream), "reset")
         if len(vs):
             check(L.jt_apply_evidence(self.handle, len(vs), ptr(cidx, C.c_int32), ptr(vs, C.c_int32),
@@ -140,26 +134,59 @@ class BatchPropagator:
         check(L.jt_propagate_query(self.handle, len(self._qv), ptr(self._qv, C.c_int32), 1,
                                    C.c_void_p(out.data_ptr()), stream), "propagate")
 
+    @property
+    def _owner_arr(self):
+        if not hasattr(self, "_own_np"):
+            a = np.full(len(self.tree.cards), -1, dtype=np.int32)
+            for v, c in self.owner.items():
+                a[v] = c
+            self._own_np = a
+            self._card_np = np.asarray(self.tree.cards, dtype=np.int64)
+        return self._own_np
+
     def encode_obs(self, cases):
-        """Compact device-evidence encoding: int32 [n_obs, 3] (case, var, state);
-        every variable of the tree is listed as active with its owning clique so
-        the propagation program is the same for every batch."""
-        cidx, vs, _, xs = self.encode(cases)
-        obs = np.stack([cidx, vs, xs], axis=1).astype(np.int32) if len(vs) else np.zeros((0, 3), np.int32)
-        return obs
+        """Compact device-evidence encoding: int32 [n_obs, 3] (case, var, state),
+        validated like the reference's Evidence.check (model.py:130-137):
+        unknown variables raise UnknownVariableError, states outside [0, card)
+        raise StateOutOfRangeError."""
+        rows = [(b, v, x) for b, ev in enumerate(cases)
+                for v, x in (ev.assignments if hasattr(ev, "assignments") else ev).items()]
+        if not rows:
+            return np.zeros((0, 3), np.int32)
+        obs = np.asarray(rows, dtype=np.int64)
+        own = self._owner_arr
+        v, x = obs[:, 1], obs[:, 2]
+        bad_v = (v < 0) | (v >= len(own))
+        if bad_v.any() or (own[np.where(bad_v, 0, v)] < 0).any():
+            i = int(np.flatnonzero(bad_v | (own[np.where(bad_v, 0, v)] < 0))[0])
+            raise UnknownVariableError(int(v[i]))
+        card = self._card_np[v]
+        bad_x = (x < 0) | (x >= card)
+        if bad_x.any():
+            i = int(np.flatnonzero(bad_x)[0])
+            raise StateOutOfRangeError(int(v[i]), int(x[i]), int(card[i]))
+        return np.ascontiguousarray(obs, dtype=np.int32)
 
     def active_vars(self):
+        """Every variable of the tree listed as active with its owning clique, so
+        the propagation program is the same for every micro-batch."""
         if not hasattr(self, "_act"):
             vs = sorted(self.owner)
             self._act = (i32(vs), i32([self.owner[v] for v in vs]))
         return self._act
 
+    def _raw_stream(self, stream):
+        if stream is None:
+            return C.c_void_p(self.stream.cuda_stream)
+        if hasattr(stream, "cuda_stream"):
+            return C.c_void_p(stream.cuda_stream)
+        return stream if isinstance(stream, C.c_void_p) else C.c_void_p(stream)
+
     def step_device(self, obs_dev, out, stream=None):
         """One step with observations already on the device (int32 [n, 3] CUDA
         tensor): reset → masks built on device → propagate → posteriors."""
         L = _lib.lib()
-        if stream is None:
-            stream = C.c_void_p(self.stream.cuda_stream)
+        stream = self._raw_stream(stream)
         av, ac = self.active_vars()
         check(L.jt_state_reset(self.handle, stream), "reset")
         n = int(obs_dev.shape[0])
@@ -169,23 +196,60 @@ class BatchPropagator:
         check(L.jt_propagate_query(self.handle, len(self._qv), ptr(self._qv, C.c_int32), 1,
                                    C.c_void_p(out.data_ptr()), stream), "propagate")
 
-    def run(self, cases, out=None, stream=None):
-        """Posteriors of every case, `batch` at a time, as a CUDA tensor."""
+    def run(self, cases, out=None, stream=None, to_host=False):
+        """Posteriors of every case (list of {var: state} dicts or Evidence),
+        `batch` cases per device step — the batched form of the reference's
+        per-case loop (estimator.py:118-134).
+
+        Pipelined: while micro-batch m runs on the device, the host encodes and
+        pins micro-batch m+1; observations cross PCIe as int32 triples and the
+        evidence masks are built on the device.  `stream` (a torch.cuda.Stream)
+        orders the work after the caller's queued work and the caller after it;
+        default: the current stream.  Returns a CUDA tensor [n, cols], or with
+        `to_host=True` a host numpy array (copied back inside this call).
+        A case whose evidence has zero probability raises ZeroMassError naming
+        the case index (the reference raises per case, potential.py:181-186)."""
         import torch
 
         n = len(cases)
         steps = (n + self.batch - 1) // self.batch
-        caller = torch.cuda.current_stream(self.torch_device)
+        caller = stream if stream is not None else torch.cuda.current_stream(self.torch_device)
         if out is None:
             out = torch.empty((steps * self.batch, self.cols), dtype=torch.float64, device=self.torch_device)
         elif out.shape[0] < steps * self.batch or out.shape[1] != self.cols:
             raise ValueError(f"out must be at least [{steps * self.batch}, {self.cols}]")
+        host = torch.empty((n, self.cols), dtype=torch.float64, pin_memory=True) if to_host else None
         self.stream.wait_stream(caller)
-        for s in range(steps):
-            chunk = cases[s * self.batch:(s + 1) * self.batch]
-            self.step(self.encode(chunk), out[s * self.batch:(s + 1) * self.batch], stream)
+        raw = C.c_void_p(self.stream.cuda_stream)
+        with torch.cuda.stream(self.stream):
+            for s in range(steps):
+                obs = self.encode_obs(cases[s * self.batch:(s + 1) * self.batch])
+                d_obs = torch.from_numpy(obs).pin_memory().to(self.torch_device, non_blocking=True)
+                self.step_device(d_obs, out[s * self.batch:(s + 1) * self.batch], raw)
+            if to_host:
+                host.copy_(out[:n], non_blocking=True)
         caller.wait_stream(self.stream)
+        if to_host:
+            self.stream.synchronize()
+            self._check(out, n)
+            return host.numpy()
         return out[:n]
+
+    def _check(self, out, n):
+        try:
+            self.sync()
+        except ZeroMassError as exc:
+            import torch
+
+            bad = torch.isnan(out[:n]).any(dim=1).nonzero()
+            case = int(bad[0, 0]) if bad.numel() else -1
+            err = ZeroMassError(f"evidence of case {case} has zero probability ({exc})")
+            err.case = case
+            raise err from None
+
+    def close(self):
+        """Free the device state now (also happens when the propagator is collected)."""
+        self._fin()
 
     def sync(self):
         check(_lib.lib().jt_sync_error(self.handle))

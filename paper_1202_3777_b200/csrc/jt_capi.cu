@@ -16,6 +16,7 @@
 #include "jt_internal.h"
 
 #include <algorithm>
+#include <climits>
 #include <cstdio>
 #include <iterator>
 #include <cstdlib>
@@ -263,12 +264,16 @@ struct jt_state {
   std::vector<int> ev_clique;               // per var: clique holding its active factor, -1 none
   int64_t* d_evoff = nullptr;               // per var: aux offset of its mask [card][B]
   int32_t* d_cards = nullptr;               // per var cardinality
-  int32_t* d_obs = nullptr;                 // observation staging (case, var, state) + fill list
+  int32_t* d_obs = nullptr;                 // observation staging (case, var, state)
   int64_t obs_cap = 0;
+  int32_t* d_fill = nullptr;                // variables whose masks are (re)filled with ones
+  int64_t fill_cap = 0;
+  std::vector<int32_t> fill_host;           // contents of d_fill
   std::map<std::string, std::unique_ptr<Program>> programs;
   std::map<std::string, std::unique_ptr<struct ClusterProg>> cprogs;  // small trees in cluster smem
   int64_t launches = 0;
   int64_t device_bytes = 0;
+  int err_case = -1;        // lowest case index of the last zero-mass error (jt_sync_error)
   bool fresh = true;        // separators hold ones (reset/load): collect may skip old/ratio
   bool seps_stale = false;  // separators logically ones but not yet filled
   // Two tables per separator (X at sep_off, Y at ratC_off): one holds the
@@ -292,6 +297,7 @@ struct jt_state {
     cudaFree(d_evoff);
     cudaFree(d_cards);
     cudaFree(d_obs);
+    cudaFree(d_fill);
     for (auto& kv : qmeta) cudaFree(kv.second.first);
     for (int i = 0; i < N_SIDE; ++i) {
       if (side[i]) cudaStreamDestroy(side[i]);
@@ -380,8 +386,12 @@ extern "C" int jt_state_create(const jt_plan* plan, int batch, int mode, jt_stat
   if (st->n_base) CK(cudaMalloc(&st->d_base, st->n_base * es));
   CK(cudaMalloc(&st->d_aux, std::max<int64_t>(st->n_aux, 4) * es));
   CK(cudaMalloc(&st->d_qout, st->n_qout * sizeof(double)));
-  CK(cudaMalloc(&st->d_err, sizeof(int)));
-  CK(cudaMemset(st->d_err, 0, sizeof(int)));
+  // error word [flags, lowest failing case index (INT_MAX: none)]
+  CK(cudaMalloc(&st->d_err, 2 * sizeof(int)));
+  {
+    const int init[2] = {0, INT_MAX};
+    CK(cudaMemcpy(st->d_err, init, sizeof init, cudaMemcpyHostToDevice));
+  }
   CK(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
   CK(cudaMalloc(&st->d_evoff, std::max(1, plan->n_vars) * sizeof(int64_t)));
   CK(cudaMalloc(&st->d_cards, std::max(1, plan->n_vars) * sizeof(int32_t)));
@@ -1936,6 +1946,30 @@ extern "C" int jt_state_store(jt_state* st, int case_idx, double* clique_concat,
   return JT_OK;
 }
 
+extern "C" int jt_state_clone(jt_state* src, jt_state** out) {
+  if (!src || !out) return JT_ERR_BAD_ARG;
+  DevGuard g(src->plan->device);
+  jt_state* dst = nullptr;
+  int rc = jt_state_create(src->plan, src->B, src->mode, &dst);
+  if (rc) return rc;
+  std::unique_ptr<jt_state> own(dst);
+  cudaStream_t s = dst->stream;
+  // src work may be queued on any stream of the caller's: order after all of it
+  CK(cudaDeviceSynchronize());
+  const size_t es = src->esz;
+  if (src->n_clique) CK(cudaMemcpyAsync(dst->d_clique, src->d_clique, src->n_clique * es, cudaMemcpyDeviceToDevice, s));
+  if (src->n_base) CK(cudaMemcpyAsync(dst->d_base, src->d_base, src->n_base * es, cudaMemcpyDeviceToDevice, s));
+  if (src->n_aux) CK(cudaMemcpyAsync(dst->d_aux, src->d_aux, src->n_aux * es, cudaMemcpyDeviceToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  dst->fresh = src->fresh;
+  dst->seps_stale = src->seps_stale;
+  dst->sep_in_y = src->sep_in_y;
+  dst->ev_clique = src->ev_clique;
+  dst->h_base = src->h_base;
+  *out = own.release();
+  return JT_OK;
+}
+
 extern "C" int jt_clear_evidence(jt_state* st) {
   if (!st) return JT_ERR_BAD_ARG;
   std::fill(st->ev_clique.begin(), st->ev_clique.end(), -1);
@@ -1991,24 +2025,24 @@ static int evidence_common(jt_state* st, int n, const int32_t* d_obs, const std:
       fill.push_back(v);
     }
   }
-  // fill list rides behind the observations in the staging buffer
-  int32_t* d_fill = nullptr;
+  // The fill list (variables whose masks start as ones) is the same for every
+  // micro-batch of a batch run: it lives in its own device buffer and is
+  // re-uploaded only when it changes, so the steady state issues no pageable
+  // host->device copy (which may synchronize the stream and stall pipelining).
   if (!fill.empty()) {
-    const int64_t need = 3 * (int64_t)n + (int64_t)fill.size();
-    if (d_obs != st->d_obs) {  // device observations: stage the fill list alone
-      if ((int64_t)fill.size() > st->obs_cap) {
-        cudaFree(st->d_obs);
-        st->d_obs = nullptr;
-        CK(cudaMalloc(&st->d_obs, fill.size() * sizeof(int32_t)));
-        st->obs_cap = (int64_t)fill.size();
+    if (fill != st->fill_host) {
+      if ((int64_t)fill.size() > st->fill_cap) {
+        CK(cudaStreamSynchronize(s));
+        cudaFree(st->d_fill);
+        st->d_fill = nullptr;
+        st->fill_cap = 0;
+        CK(cudaMalloc(&st->d_fill, fill.size() * sizeof(int32_t)));
+        st->fill_cap = (int64_t)fill.size();
       }
-      d_fill = st->d_obs;
-    } else {
-      d_fill = st->d_obs + 3 * (int64_t)n;
-      (void)need;
+      CK(cudaMemcpyAsync(st->d_fill, fill.data(), fill.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+      st->fill_host = fill;
     }
-    CK(cudaMemcpyAsync(d_fill, fill.data(), fill.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-    CK(launch_ev_fill(st->d_aux, p->dtype, d_fill, (int)fill.size(), st->d_evoff, st->d_cards, st->B, s));
+    CK(launch_ev_fill(st->d_aux, p->dtype, st->d_fill, (int)fill.size(), st->d_evoff, st->d_cards, st->B, s));
     st->launches++;
   }
   CK(launch_ev_zero(st->d_aux, p->dtype, d_obs, n, st->d_evoff, st->d_cards, st->B, s));
@@ -2077,7 +2111,7 @@ extern "C" int jt_apply_evidence(jt_state* st, int n, const int32_t* case_idx, c
     obs[3 * i + 1] = var[i];
     obs[3 * i + 2] = value[i];
   }
-  const int64_t need = 3 * (int64_t)n + (int64_t)vars.size();
+  const int64_t need = 3 * (int64_t)n;
   if (need > st->obs_cap) {
     cudaFree(st->d_obs);
     st->d_obs = nullptr;
@@ -2340,6 +2374,18 @@ static int build_cluster_prog(jt_state* st, const std::vector<int>& roots, Clust
   return JT_OK;
 }
 
+// Shared-base states keep only the latest propagation's ratios: the base never
+// absorbs a message, so the Hugin update new/old of a second propagation has no
+// table to apply to.  A re-propagation (or one after incremental evidence)
+// therefore restarts from the base and every active evidence mask (evidence
+// accumulates as masks until reset): calibrated tables are P(C, e) whatever the
+// message history, so this equals the reference's repeated belief_propagation.
+static void shared_restart(jt_state* st) {
+  if (st->mode != JT_SHARED_BASE || st->fresh) return;
+  st->fresh = true;
+  st->seps_stale = st->plan->n_seps > 0;
+}
+
 extern "C" int jt_propagate(jt_state* st, const int32_t* roots_or_null, void* stream) {
   if (!st) return JT_ERR_BAD_ARG;
   DevGuard g(st->plan->device);
@@ -2347,6 +2393,7 @@ extern "C" int jt_propagate(jt_state* st, const int32_t* roots_or_null, void* st
   int rc = resolve_roots(st, roots_or_null, roots);
   if (rc) return rc;
   cudaStream_t s = pick_stream(st, stream);
+  shared_restart(st);
   const bool fresh = st->fresh;
   if (st->B == 1 && st->mode == JT_MATERIALIZED) {
     // small trees: the whole propagation in one cluster's shared memory, one launch
@@ -2460,8 +2507,11 @@ static int query_program(jt_state* st, int n, const int32_t* var, const int32_t*
   std::vector<int> kk = vs;
   kk.insert(kk.end(), cs.begin(), cs.end());
   const bool shared = st->mode == JT_SHARED_BASE;
+  // shared-base state not propagated since reset/load: its tables are base × evidence
+  const bool unprop = shared && st->fresh;
   std::vector<int> kv = active_ev(st);
   kv.push_back((int)st->sep_in_y);
+  kv.push_back((int)unprop);
   std::string key = key_of("q", kk, kv);
   Program* pr;
   auto it = st->programs.find(key);
@@ -2480,8 +2530,10 @@ static int query_program(jt_state* st, int n, const int32_t* var, const int32_t*
       if (shared) {
         // final table of the clique = base × evidence × Π neighbour ratios
         const int c = cs[i];
-        for (auto& ch : o.children[c]) ps.factors.push_back(sep_tensor(st, ch.second, sep_alt(st, ch.second)));
-        if (o.parent[c] >= 0) ps.factors.push_back(sep_tensor(st, o.psep[c], st->ratD_off[o.psep[c]]));
+        if (!unprop) {
+          for (auto& ch : o.children[c]) ps.factors.push_back(sep_tensor(st, ch.second, sep_alt(st, ch.second)));
+          if (o.parent[c] >= 0) ps.factors.push_back(sep_tensor(st, o.psep[c], st->ratD_off[o.psep[c]]));
+        }
         for (int v = 0; v < p->n_vars; ++v)
           if (st->ev_clique[v] == c) ps.factors.push_back(ev_tensor(st, v));
       }
@@ -2546,6 +2598,7 @@ extern "C" int jt_propagate_query(jt_state* st, int n, const int32_t* var, int n
     return n ? jt_query_device(st, n, var, nullptr, normalize, out_device, stream) : JT_OK;
   }
   cudaStream_t s = pick_stream(st, stream);
+  shared_restart(st);
   const bool fresh = st->fresh;
   if (!fresh) {
     int rc = ensure_seps(st, s);
@@ -2578,13 +2631,17 @@ extern "C" int jt_sync_error(jt_state* st) {
   if (!st) return JT_ERR_BAD_ARG;
   DevGuard g(st->plan->device);
   CK(cudaDeviceSynchronize());
-  int h = 0;
-  CK(cudaMemcpy(&h, st->d_err, sizeof(int), cudaMemcpyDeviceToHost));
-  CK(cudaMemset(st->d_err, 0, sizeof(int)));
-  if (h & EB_INCONSISTENT) return JT_ERR_INCONSISTENT_DIVISION;
-  if (h & EB_ZERO_MASS) return JT_ERR_ZERO_MASS;
+  int h[2] = {0, INT_MAX};
+  const int init[2] = {0, INT_MAX};
+  CK(cudaMemcpy(h, st->d_err, sizeof h, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(st->d_err, init, sizeof init, cudaMemcpyHostToDevice));
+  st->err_case = (h[0] & EB_ZERO_MASS) && h[1] != INT_MAX ? h[1] : -1;
+  if (h[0] & EB_INCONSISTENT) return JT_ERR_INCONSISTENT_DIVISION;
+  if (h[0] & EB_ZERO_MASS) return JT_ERR_ZERO_MASS;
   return JT_OK;
 }
+
+extern "C" int jt_error_case(const jt_state* st) { return st ? st->err_case : -1; }
 
 extern "C" const char* jt_error_string(int code) {
   switch (code) {
@@ -2789,9 +2846,10 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
       if (g.kind != 3) continue;
       for (int q = 0; q < g.n_cpasses; ++q) {
         const CPass& c = hp.cpasses[g.cpass_off + q];
-        snprintf(line, sizeof line, "  contract clique %d out %d nI %d nS %d nK %d nG %d nE %d units %lld rowi %d gI-dep",
+        snprintf(line, sizeof line,
+                 "  contract clique %d out %d nI %d nS %d nK %d nG %d nE %d units %lld rowi %d ks %d gI-dep",
                  hp.cpass_clique[g.cpass_off + q], c.out_kind, c.nI, c.nS, c.nK, c.nG, c.nE, (long long)c.n_units,
-                 c.rowi);
+                 c.rowi, c.nKS);
         out += line;
         for (int gg = 0; gg < c.nG; ++gg) {  // does factor gg depend on i?
           bool dep = false;

@@ -1639,6 +1639,7 @@ __global__ void normalize_kernel(const double* __restrict__ qout, const int64_t*
   }
   if (!(s > 0.0)) {
     atomicOr(err, EB_ZERO_MASS);
+    atomicMin(err + 1, b);  // lowest failing case (jt_error_case)
     for (int d = 0; d < card; ++d) o[d] = __longlong_as_double(0x7ff8000000000000ULL);
     return;
   }

@@ -18,6 +18,7 @@ try:  # sklearn is only the parameter protocol (get_params/set_params/clone)
 except Exception:  # pragma: no cover
     BaseEstimator = object
 
+from .errors import StateOutOfRangeError, UnknownVariableError
 from .propagate import ENGINE_NAMES, CudaEngine, apply_evidence, belief_propagation, initialize
 from .tree import FLAT, INTERLEAVED
 
@@ -79,14 +80,29 @@ class JunctionTreeEngine(BaseEstimator):
             raise ValueError("this JunctionTreeEngine is not fitted yet; call fit()")
 
     def _var_id(self, key):
-        return key if isinstance(key, (int, np.integer)) else self.network_.id_of(key)
+        if isinstance(key, (int, np.integer)):
+            return key
+        try:
+            return self.network_.id_of(key)
+        except (KeyError, ValueError, LookupError) as exc:
+            raise UnknownVariableError(key) from exc
 
     def _evidence(self, evidence):
         if evidence is None:
             return {}
         if hasattr(evidence, "assignments"):
             evidence = evidence.assignments
-        return {int(self._var_id(k)): int(v) for k, v in dict(evidence).items()}
+        out = {}
+        n_vars = len(self.network_.variables)
+        for k, v in dict(evidence).items():
+            var = int(self._var_id(k))
+            if not 0 <= var < n_vars:  # model.py:130-137: Evidence.check
+                raise UnknownVariableError(k)
+            card = int(self.network_.variables[var].cardinality)
+            if not 0 <= int(v) < card:
+                raise StateOutOfRangeError(k, int(v), card)
+            out[var] = int(v)
+        return out
 
     def _name(self, v):
         return self.network_.variables[v].name
@@ -128,9 +144,7 @@ class JunctionTreeEngine(BaseEstimator):
             X = [X]
         rows = [self._evidence(x) for x in X]
         bp = self._propagator(target_id)
-        out = bp.run(rows).cpu().numpy()
-        bp.sync()
-        return out
+        return bp.run(rows, to_host=True)
 
     def predict(self, X) -> np.ndarray:
         """Most probable state of `target` per sample."""

@@ -88,11 +88,13 @@ def _dtype_code(dtype) -> int:
 
 
 class Plan:
-    """Device plan of one junction tree (jt_plan): structure only, no data."""
+    """Device plan of one junction tree (jt_plan): structure only, no data.
+    Holds only a weak reference to its tree, so the plan cache never pins a
+    tree (or its device plan) beyond the tree's own lifetime."""
 
     def __init__(self, tree, dtype="f64", device=0):
         _lib.require_device()
-        self.tree = tree
+        self._tree_ref = weakref.ref(tree)
         self.dtype = _dtype_code(dtype)
         self.device = int(device)
         cards = i32(tree.cards)
@@ -120,6 +122,10 @@ class Plan:
         self.clique_sizes = [_scope_size(c.scope) for c in tree.cliques]
         self.sep_sizes = [_scope_size(s.scope) for s in tree.separators]
         self._fin = weakref.finalize(self, _lib.lib().jt_plan_destroy, h)
+
+    @property
+    def tree(self):
+        return self._tree_ref()
 
     def mapping_table(self, clique_id: int, sep_id: int) -> np.ndarray:
         """μ[clique, sep] built on the device (K0), as the reference's int array."""
@@ -221,16 +227,19 @@ class PropagationState:
     """Clique and separator tables of one propagation run, resident in HBM
     (propagate.py:172-201)."""
 
-    def __init__(self, tree, mappings, engine=None, _plan=None):
+    def __init__(self, tree, mappings, engine=None, _plan=None, _handle=None):
         self.tree = tree
-        self.mappings = mappings
+        self._mappings = mappings
         self.engine = engine if engine is not None else CudaEngine()
         self.evidence_applied = False
         self.plan = _plan if _plan is not None else plan_for(tree, _engine_dtype(self.engine),
                                                               _engine_device(self.engine))
-        h = C.c_void_p()
-        check(_lib.lib().jt_state_create(self.plan.handle, 1, JT_MATERIALIZED, C.byref(h)),
-              "jt_state_create")
+        if _handle is None:
+            h = C.c_void_p()
+            check(_lib.lib().jt_state_create(self.plan.handle, 1, JT_MATERIALIZED, C.byref(h)),
+                  "jt_state_create")
+        else:
+            h = _handle
         self.handle = h
         self._fin = weakref.finalize(self, _lib.lib().jt_state_destroy, h)
         self._c_off = np.concatenate([[0], np.cumsum(self.plan.clique_sizes)]).astype(np.int64)
@@ -238,6 +247,18 @@ class PropagationState:
         self._hc = None  # host concat buffers when materialised
         self._hs = None
         self._exposed = False
+
+    @property
+    def mappings(self):
+        """μ tables (compiler.py:330-339), built on first access only: the device
+        never reads them (stride arithmetic), so states do not pay for them."""
+        if self._mappings is None:
+            self._mappings = build_mapping_tables(self.tree, layout=FLAT)
+        return self._mappings
+
+    @mappings.setter
+    def mappings(self, value):
+        self._mappings = value
 
     # -- host views ---------------------------------------------------------
     def _pull(self):
@@ -271,10 +292,11 @@ class PropagationState:
         return self._views(self._hs, self._s_off)
 
     def copy(self) -> "PropagationState":
-        self._pull()
-        other = PropagationState(self.tree, self.mappings, self.engine, _plan=self.plan)
-        check(_lib.lib().jt_state_load(other.handle, -1, ptr(self._hc, C.c_double),
-                                       ptr(self._hs, C.c_double)), "jt_state_load")
+        """Deep copy (propagate.py:193-201), device to device (jt_state_clone)."""
+        self._push()
+        h = C.c_void_p()
+        check(_lib.lib().jt_state_clone(self.handle, C.byref(h)), "copy")
+        other = PropagationState(self.tree, self._mappings, self.engine, _plan=self.plan, _handle=h)
         other.evidence_applied = self.evidence_applied
         return other
 
@@ -336,8 +358,6 @@ def initialize(tree, net, mappings=None, engine=None) -> PropagationState:
     """All-ones cliques, each CPT multiplied into its assigned clique
     (propagate.py:204-222).  The products are formed on the device
     (jt_state_initialize): only the CPTs cross PCIe."""
-    if mappings is None:
-        mappings = build_mapping_tables(tree, layout=FLAT)
     cl, off, vs, vals, n = cpt_arrays(tree, net)
     state = PropagationState(tree, mappings, _as_engine(engine))
     check(_lib.lib().jt_state_initialize(state.handle, n, ptr(cl, C.c_int32), ptr(off, C.c_int32),
@@ -347,8 +367,6 @@ def initialize(tree, net, mappings=None, engine=None) -> PropagationState:
 
 def from_potentials(tree, clique_tables, mappings=None, engine=None) -> PropagationState:
     """State over externally supplied clique tables (propagate.py:225-240)."""
-    if mappings is None:
-        mappings = build_mapping_tables(tree, layout=FLAT)
     tables = []
     for clique, values in zip(tree.cliques, clique_tables):
         values = np.ascontiguousarray(values, dtype=np.float64)

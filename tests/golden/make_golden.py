@@ -151,12 +151,39 @@ def corpus():
         json.dump(doc, f)
 
 
+BENCH_IDX = list(range(0, 24)) + list(range(4072, 4120)) + list(range(8168, 8192))
+
+
+def bench_golden(name="c5", n_total=8192, evidence_seed=1234):
+    """The bench workload itself (bench.py: c5, seed-1234 evidence, 8192 cases per
+    GPU in two 4096-case micro-batches): reference SequentialEngine posteriors of
+    every variable for a sample of case indices that covers the start and end of
+    BOTH micro-batches (0..23, 4072..4119 across the boundary, 8168..8191)."""
+    members, cards = synth.config_members(name)
+    tree = build_tree(members, cards)
+    tree.cpt_assignment = {v: synth.smallest_holder(tree, v) for v in range(len(cards))}
+    tables = synth.scaled_potentials(tree, seed=0)
+    posts = []
+    for i in BENCH_IDX:
+        ev = synth.evidence_cases(tree, 1, seed=evidence_seed, first=i)[0]
+        st = from_potentials(tree, tables)
+        apply_evidence(st, ev)
+        belief_propagation(st)
+        posts.append(np.concatenate([query_marginal(st, v).values for v in range(len(cards))]))
+    np.savez_compressed(os.path.join(HERE, f"{name}_bench.npz"), idx=np.array(BENCH_IDX),
+                        n_total=np.array([n_total]), seed=np.array([evidence_seed]), post=np.stack(posts))
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["corpus"]:
         corpus()
+        sys.exit(0)
+    if sys.argv[1:] == ["bench"]:
+        bench_golden()
         sys.exit(0)
     mapping_tables()
     corpus()
     for name, n in (("c1", 8), ("c2", 4), ("c4M", 2), ("c5", 8), ("c4B", 1), ("c3", 1)):
         config_golden(name, n)
         print("golden", name)
+    bench_golden()

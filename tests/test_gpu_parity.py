@@ -339,8 +339,9 @@ def test_tree_dump_to_device_plan():  # §8f row 4: .jt.json → cached device p
 def test_batch_contraction_path_large_batch(dtype, batch):
     """Shared-base micro-batches large enough for the contraction passes
     (DESIGN.md §3b): every case matches the reference goldens / the oracle.
-    132 cases: the last case chunk is partial (lanes past B leave the case loop
-    before the K-split combine)."""
+    128 cases run the K-split contraction passes (test_planner asserts the
+    planner compiles them); 132 cases leave a partial last case chunk, which
+    routes the long sums to the general kernels (K-split needs whole chunks)."""
     from paper_1202_3777_b200.batch import BatchPropagator
 
     tree, data = load_golden("c5")
@@ -416,3 +417,156 @@ def test_cluster_smem_propagation_matches_reference(monkeypatch):
             P().belief_propagation(st)
             got = all_posteriors(st, len(tree.cards))
             assert rel_err(got, want) < 1e-5, (name, ev)
+
+
+def test_device_mapping_tables_random_scope_pairs():
+    """K0 on the 80 reference-generated random (clique, separator) scope pairs
+    (the property test_compiler.py:233-256 draws from): bit-exact, int32."""
+    from conftest import GOLDEN
+    import os
+
+    d = np.load(os.path.join(GOLDEN, "mapping_tables.npz"))
+    n = len([k for k in d.files if k.endswith("_ids")])
+    assert n == 80
+    for i in range(n):
+        ids = [int(x) for x in d[f"case{i}_ids"]]
+        cards = [int(x) for x in d[f"case{i}_cards"]]
+        sep = [int(x) for x in d[f"case{i}_sep"]]
+        all_cards = [2] * (max(ids) + 1)
+        for v, c in zip(ids, cards):
+            all_cards[v] = c
+        # a two-clique tree: the clique, and the separator scope as its neighbour
+        tree = build_tree([tuple(ids), tuple(sep)], tuple(all_cards))
+        plan = P().Plan(tree, "f64")
+        cid = next(c.id for c in tree.cliques if list(c.scope.ids) == ids)
+        mu = plan.mapping_table(cid, 0)
+        want = d[f"case{i}_mu"]
+        assert mu.dtype == want.dtype and np.array_equal(mu, want), i
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_shared_state_repropagation_and_incremental_evidence(dtype):
+    """a shared-base state propagated twice without a reset, and
+    again after incremental evidence, must give the reference's posteriors
+    (test_propagate.py:278-300 semantics), through the C ABI."""
+    import ctypes as C
+
+    from paper_1202_3777_b200 import _lib
+    from paper_1202_3777_b200.batch import BatchPropagator
+    from paper_1202_3777_b200._lib import i32, ptr
+
+    tree, tables = synth.make_config("c5")
+    B = 8
+    cases = synth.evidence_cases(tree, B, seed=5)
+    more = synth.evidence_cases(tree, B, seed=6)
+    bp = BatchPropagator(tree, tables, batch=B, dtype=dtype, mode="shared")
+    L = _lib.lib()
+    import torch
+
+    out = torch.empty((B, bp.cols), dtype=torch.float64, device="cuda")
+
+    def enter(evs):
+        cidx, vs, cs, xs = bp.encode(evs)
+        _lib.check(L.jt_apply_evidence(bp.handle, len(vs), ptr(cidx, C.c_int32), ptr(vs, C.c_int32),
+                                       ptr(cs, C.c_int32), ptr(xs, C.c_int32), None))
+
+    def prop():
+        _lib.check(L.jt_propagate_query(bp.handle, len(bp._qv), ptr(bp._qv, C.c_int32), 1,
+                                        C.c_void_p(out.data_ptr()), None))
+        bp.sync()
+        return out.cpu().numpy()
+
+    template = jtref.from_potentials(tree, tables)
+    n = len(tree.cards)
+    _lib.check(L.jt_state_reset(bp.handle, None))
+    enter(cases)
+    first = prop()
+    want = np.stack([jtref.case_posteriors(template, ev, range(n)) for ev in cases])
+    assert rel_err(first, want) < TOL[dtype]
+    second = prop()  # no reset: a no-op on normalized marginals
+    assert rel_err(second, want) < TOL[dtype]
+    # incremental evidence on the propagated state: accumulates with the first
+    extra = [{v: x for v, x in m.items() if v not in c} for c, m in zip(cases, more)]
+    enter(extra)
+    third = prop()
+    want3 = np.stack([jtref.case_posteriors(template, {**c, **e}, range(n)) for c, e in zip(cases, extra)])
+    assert rel_err(third, want3) < TOL[dtype]
+    # queries on a reset state that was never propagated: base × evidence only
+    _lib.check(L.jt_state_reset(bp.handle, None))
+    v = i32([0])
+    got = np.empty((B, tree.cards[0]))
+    _lib.check(L.jt_query(bp.handle, 1, ptr(v, C.c_int32), None, 1, ptr(got, C.c_double), None))
+    holder = min((c for c in tree.cliques if 0 in c.scope.ids), key=lambda c: (c.scope.size, c.id))
+    t = np.asarray(tables[holder.id]).reshape(holder.scope.cards)
+    marg = t.sum(axis=tuple(range(1, t.ndim)))
+    assert rel_err(got, np.broadcast_to(marg / marg.sum(), got.shape)) < TOL[dtype]
+    bp.close()
+
+
+def test_batch_zero_mass_names_the_case():
+    """Impossible evidence in one case of a micro-batch: ZeroMassError names
+    that case (the reference raises per case, potential.py:181-186 via
+    estimator.py:130-133); the other cases' posteriors are unaffected."""
+    from paper_1202_3777_b200.batch import BatchPropagator
+    from paper_1202_3777_b200.errors import ZeroMassError
+
+    tree, tables = synth.make_config("c1")
+    v = 3
+    cid = tree.cpt_assignment[v]
+    scope = tree.cliques[cid].scope
+    pos = list(scope.ids).index(v)
+    t = np.asarray(tables[cid], dtype=np.float64).reshape(scope.cards).copy()
+    idx = [slice(None)] * t.ndim
+    idx[pos] = 0
+    t[tuple(idx)] = 0.0  # state 0 of variable 3 is impossible
+    tables = list(tables)
+    tables[cid] = t.ravel()
+    cases = [{1: 0}] * 5 + [{v: 0}] + [{2: 1}] * 2
+    for mode in ("shared", "materialized"):
+        bp = BatchPropagator(tree, tables, batch=4, dtype="f64", mode=mode)
+        with pytest.raises(ZeroMassError) as ei:
+            bp.run(cases, to_host=True)
+        assert ei.value.case == 5 and "case 5" in str(ei.value), mode
+        ok = bp.run(cases[:5], to_host=True)
+        template = jtref.from_potentials(tree, tables)
+        want = jtref.case_posteriors(template, cases[0], range(len(tree.cards)))
+        assert rel_err(ok[0], want) < 1e-10, mode
+
+
+def test_state_copy_is_device_side_and_independent():
+    """PropagationState.copy() (propagate.py:193-201) through jt_state_clone:
+    the copy has the same tables, and evolving it leaves the original alone."""
+    tree, data = load_golden("c1")
+    tables = synth.scaled_potentials(tree, 0)
+    st = P().from_potentials(tree, tables, engine=P().CudaEngine(dtype="f64"))
+    P().apply_evidence(st, {3: 1})
+    base_c = [c.copy() for c in st.clique_values]
+    cp = st.copy()
+    assert all(np.array_equal(a, b) for a, b in zip(cp.clique_values, base_c))
+    P().apply_evidence(cp, {17: 2})
+    P().belief_propagation(cp)
+    assert all(np.array_equal(a, b) for a, b in zip(st.clique_values, base_c))
+    P().belief_propagation(st)
+    template = jtref.from_potentials(tree, tables)
+    n = len(tree.cards)
+    assert rel_err(all_posteriors(st, n), jtref.case_posteriors(template, {3: 1}, range(n))) < 1e-10
+    assert rel_err(all_posteriors(cp, n), jtref.case_posteriors(template, {3: 1, 17: 2}, range(n))) < 1e-10
+    assert st._mappings is None  # μ tables are built only when asked for
+    assert st.mappings is not None
+
+
+def test_estimator_rejects_bad_evidence_like_reference():
+    """predict_proba raises the reference's error types
+    (model.py:130-137) for unknown variables and out-of-range states."""
+    from conftest import load_corpus_networks
+    from paper_1202_3777_b200.errors import StateOutOfRangeError, UnknownVariableError
+    from paper_1202_3777_b200.estimator import JunctionTreeEngine
+
+    name, tree, net, _, rows, want = load_corpus_networks()[0]
+    est = JunctionTreeEngine(target=net.variables[-1].name, batch=4).fit_compiled(tree, net)
+    with pytest.raises(UnknownVariableError):
+        est.predict_proba([{len(net.variables) + 3: 0}])
+    with pytest.raises(UnknownVariableError):
+        est.predict_proba([{"no-such-variable": 0}])
+    with pytest.raises(StateOutOfRangeError):
+        est.predict_proba([{0: net.variables[0].cardinality}])

@@ -60,3 +60,16 @@ def test_batch_program_uses_contraction_passes():
     assert "contract clique" in text
     total = float(next(l for l in text.splitlines() if l.startswith("compulsory total MB")).split()[-1])
     assert 30000 < total < 60000  # ~46.6 GB per 2048-case micro-batch
+
+
+@pytest.mark.parametrize("batch", [128, 4096])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_ksplit_contraction_is_compiled(batch, dtype):
+    """The K-split contraction path (long sums over few units, partials combined
+    in chunk order by the last warp) must really be in the programs the GPU
+    parity tests run: B = 128 (test_gpu_parity) and the bench's B = 4096
+    (test_gpu_headline).  Guards against the planner heuristics silently
+    dropping the coverage."""
+    text = report("c5", batch=batch, mode="shared", kind=1, dtype=dtype)
+    ks = [int(line.split(" ks ")[1].split()[0]) for line in text.splitlines() if " ks " in line]
+    assert ks and max(ks) > 1, (batch, dtype)
