@@ -2802,6 +2802,14 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
         else if (ps.out_kind != OUT_NONE) bytes += tsize(ps.out) * st.esz * 3;
         const double csz = (double)plan->csize[ps.clique] * (ps.src_arena == A_BASE ? 1.0 : (double)st.B);
         if (ps.scope.empty()) bytes += csz * st.esz * (ps.write ? 2 : 1);
+        if (getenv("JT_DEBUG_SPECS")) {
+          double fb = 0.0;
+          for (auto& f : ps.factors) fb += tsize(f) * st.esz;
+          snprintf(line, sizeof line, "  spec w%zu clique %d src %d out %d nf %zu factors MB %.1f out MB %.1f\n", w,
+                   ps.clique, ps.src_arena, ps.out_kind, ps.factors.size(), fb / 1e6,
+                   ps.out_kind != OUT_NONE ? tsize(ps.out) * st.esz / 1e6 : 0.0);
+          out += line;
+        }
       }
       tot += bytes;
       snprintf(line, sizeof line, "compulsory wave %zu MB %.1f\n", w, bytes / 1e6);
