@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstdio>
 #include <iterator>
 #include <cstdlib>
@@ -273,7 +274,19 @@ struct jt_state {
   std::map<std::string, std::unique_ptr<struct ClusterProg>> cprogs;  // small trees in cluster smem
   int64_t launches = 0;
   int64_t device_bytes = 0;
+  int* d_qexp = nullptr;    // per-query exponents of unnormalized queries
+  int64_t qexp_cap = 0;
   int err_case = -1;        // lowest case index of the last zero-mass error (jt_sync_error)
+  // Power-of-two prescaling (exact: only exponents move).  Every table is stored
+  // as exact * 2^e: pre_e per clique is chosen at load/initialize so each clique
+  // sums to about the size of its parent separator (root: 1) -- the balance the
+  // reference's own generator lacks (uniform(0.1,1) tables reach 2e107 on a
+  // Pigs-shaped tree), so fp32 states neither overflow nor
+  // underflow on unscaled inputs.  e_c / e_s track the current exponent of every
+  // clique / separator table through messages and propagations (host integers:
+  // the scaling is data-independent per state); host views and unnormalized
+  // queries (P(e), propagate.py:363-377) undo it exactly.
+  std::vector<int> pre_e, e_c, e_s;
   bool fresh = true;        // separators hold ones (reset/load): collect may skip old/ratio
   bool seps_stale = false;  // separators logically ones but not yet filled
   // Two tables per separator (X at sep_off, Y at ratC_off): one holds the
@@ -298,6 +311,7 @@ struct jt_state {
     cudaFree(d_cards);
     cudaFree(d_obs);
     cudaFree(d_fill);
+    cudaFree(d_qexp);
     for (auto& kv : qmeta) cudaFree(kv.second.first);
     for (int i = 0; i < N_SIDE; ++i) {
       if (side[i]) cudaStreamDestroy(side[i]);
@@ -367,6 +381,54 @@ static void layout_state(jt_state* st) {
   }
   st->n_qout = std::max<int64_t>(qo, 1);
   st->ev_clique.assign(plan->n_vars, -1);
+  st->pre_e.assign(plan->n_cliques, 0);
+  st->e_c.assign(plan->n_cliques, 0);
+  st->e_s.assign(plan->n_seps, 0);
+}
+
+// Exponent that brings a clique table summing to `sum` to about `target`.
+static int balance_exp(double sum, double target) {
+  if (!(sum > 0.0) || !std::isfinite(sum)) return 0;
+  const double e = std::round(std::log2(target / sum));
+  return (int)std::max(-900.0, std::min(900.0, e));
+}
+
+// pre_e from the clique tables (host, fp64, clique-id order at `at(c)`): each
+// clique scaled to sum to its BFS-parent separator's size, roots to 1
+// (SURVEY Appendix A balance, as powers of two).
+template <class F>
+static void choose_prescale(jt_state* st, F at) {
+  const jt_plan* p = st->plan;
+  std::vector<int64_t> target(p->n_cliques, 1);
+  std::vector<char> seen(p->n_cliques, 0);
+  std::vector<int> q(p->roots.begin(), p->roots.end());
+  for (int r : p->roots) seen[r] = 1;
+  for (size_t h = 0; h < q.size(); ++h)
+    for (auto& nb : p->nbrs[q[h]])
+      if (!seen[nb.first]) {
+        seen[nb.first] = 1;
+        target[nb.first] = p->ssize[nb.second];
+        q.push_back(nb.first);
+      }
+  for (int c = 0; c < p->n_cliques; ++c) {
+    const double* v = at(c);
+    double sum = 0.0;
+    for (int64_t i = 0; i < p->csize[c]; ++i) sum += v[i];
+    st->pre_e[c] = balance_exp(sum, (double)target[c]);
+  }
+}
+
+// exponent of the joint Π φ_c / Π φ_s: every table of a calibrated state
+static int joint_exp(const jt_state* st) {
+  int64_t e = 0;
+  for (int x : st->e_c) e += x;
+  for (int x : st->e_s) e -= x;
+  return (int)e;
+}
+
+static void set_all_exp(jt_state* st, int e) {
+  std::fill(st->e_c.begin(), st->e_c.end(), e);
+  std::fill(st->e_s.begin(), st->e_s.end(), e);
 }
 
 extern "C" int jt_state_create(const jt_plan* plan, int batch, int mode, jt_state** out) {
@@ -901,6 +963,11 @@ static std::vector<int64_t> group_offsets(const jt_plan* p, const std::vector<in
   return out;
 }
 
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
 #ifndef CON_NCG_MID
 #define CON_NCG_MID 4  // case chunks per unit group for 8 <= nK < 32
 #endif
@@ -1049,10 +1116,20 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   cp.rowi = rowi ? 1 : 0;
   const int trows = rowi ? 1 : TMC;  // rowi: one i per unit
   cp.nT = rowi ? (int)((nI + trows - 1) / trows) : (int)((nS + trows - 1) / trows);
-  cp.nBC = (int)((B + 32 * CVEC - 1) / (32 * CVEC));
+  {
+    const int cvec = st->esz == 4 ? 4 : 2;  // case lanes per vector of the kernels
+    cp.nBC = (int)((B + 32 * cvec - 1) / (32 * cvec));
+  }
   // a unit walks a share of the case chunks of its (i, row tile): all of them for
   // short sums (amortises the unit's setup), one per unit for long ones (parallelism)
-  cp.nCG = nK >= 32 ? cp.nBC : nK >= 8 ? std::min(CON_NCG_MID, cp.nBC) : std::min(CON_NCG_SMALL, cp.nBC);
+  {
+    static const int ncg_small = env_int("JT_NCG_SMALL", CON_NCG_SMALL);
+    static const int ncg_mid = env_int("JT_NCG_MID", CON_NCG_MID);
+    static const int ncg_long = env_int("JT_NCG_LONG", 1 << 30);
+    cp.nCG = nK >= 32 ? std::min(ncg_long, cp.nBC) : nK >= 8 ? std::min(ncg_mid, cp.nBC) : std::min(ncg_small, cp.nBC);
+    static const int cmaj = env_int("JT_CMAJ", 0);  // bit 0: rowi passes, bit 1: tile passes
+    cp.cmaj = (cmaj >> (rowi ? 0 : 1)) & 1;
+  }
   cp.nKS = 1;
   cp.kch = (int)nK;
   cp.n_units = (rowi ? 1 : nI) * cp.nT * cp.nCG;
@@ -1250,6 +1327,35 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
         lg.grid = (int)std::min<int64_t>((lg.n_items + NT / 32 - 1) / (NT / 32), (int64_t)occ * st->num_sms);
       items.insert(items.end(), g.second.begin(), g.second.end());
       rt.groups.push_back(lg);
+    }
+    // JT_SPLIT_CPASS=1 (diagnostic): one launch per contraction pass, so an ncu
+    // launch list attributes time and DRAM bytes to single passes
+    if (getenv("JT_SPLIT_CPASS")) {
+      std::vector<CPass> cps2[4 * NGK];
+      std::vector<int> cpc2[4 * NGK];
+      for (int key = 0; key < 4 * NGK; ++key) {
+        cps2[key].swap(cps[key]);
+        cpc2[key].swap(cpc[key]);
+      }
+      for (int key = 0; key < 4 * NGK; ++key)
+        for (size_t q = 0; q < cps2[key].size(); ++q) {
+          const int fold = (key / NGK) & 1;
+          LaunchGrp cg;
+          cg.kind = 3;
+          cg.lm = fold;
+          cg.m = (key / NGK) >> 1;
+          cg.vec = key % NGK;
+          cg.cpass_off = (int64_t)hp.cpasses.size();
+          CPass cp = cps2[key][q];
+          cp.unit0 = 0;
+          cg.n_units = cp.n_units;
+          cg.n_cpasses = 1;
+          hp.cpasses.push_back(cp);
+          hp.cpass_clique.push_back(cpc2[key][q]);
+          const int occ = occ_override ? occ_override : contract_max_ctas_per_sm(st->plan->dtype, fold, cg.m, cg.vec);
+          cg.grid = (int)std::min<int64_t>((cg.n_units + NT / 32 - 1) / (NT / 32), (int64_t)occ * st->num_sms);
+          rt.groups.push_back(cg);
+        }
     }
     for (int key = 0; key < 4 * NGK; ++key) {
       const int fold = (key / NGK) & 1;
@@ -1767,12 +1873,21 @@ extern "C" int jt_state_load(jt_state* st, int case_idx, const double* clique_co
   const int64_t B = st->B;
   if ((rc = ensure_seps(st, s))) return rc;
   st->fresh = (case_idx < 0 && !sep_concat) || (st->fresh && !sep_concat);
+  if (clique_concat && case_idx < 0) {
+    // new base tables: fresh prescale exponents; separators (ones or given) unscaled
+    std::vector<int64_t> co(p->n_cliques + 1, 0);
+    for (int c = 0; c < p->n_cliques; ++c) co[c + 1] = co[c] + p->csize[c];
+    choose_prescale(st, [&](int c) { return clique_concat + co[c]; });
+    st->e_c = st->pre_e;
+    std::fill(st->e_s.begin(), st->e_s.end(), 0);
+  }
   if (clique_concat && case_idx < 0 && shared) {
-    // host copy of the base for contraction passes; programs built on the old base are stale
+    // host copy of the (prescaled) base for contraction passes; programs built on the old base are stale
     st->h_base.assign(st->n_base, 1.0);
     int64_t o = 0;
     for (int c = 0; c < p->n_cliques; ++c) {
-      std::copy(clique_concat + o, clique_concat + o + p->csize[c], st->h_base.begin() + st->boff[c]);
+      for (int64_t i = 0; i < p->csize[c]; ++i)
+        st->h_base[st->boff[c] + i] = std::ldexp(clique_concat[o + i], st->pre_e[c]);
       o += p->csize[c];
     }
     st->programs.clear();
@@ -1784,11 +1899,11 @@ extern "C" int jt_state_load(jt_state* st, int case_idx, const double* clique_co
       const int64_t nc = p->csize[c];
       if (case_idx < 0) {
         char* dst = (char*)st->d_base + st->boff[c] * st->esz;
-        CK(launch_convert_d2t(p->dtype, st->d_stage + o, dst, nc, 1, 1, s));
+        CK(launch_convert_d2t(p->dtype, st->d_stage + o, dst, nc, 1, 1, s, st->pre_e[c]));
       }
       if (!shared) {
         char* dst = (char*)st->d_clique + (st->coff[c] + (case_idx < 0 ? 0 : case_idx)) * st->esz;
-        CK(launch_convert_d2t(p->dtype, st->d_stage + o, dst, nc, B, case_idx < 0 ? B : 1, s));
+        CK(launch_convert_d2t(p->dtype, st->d_stage + o, dst, nc, B, case_idx < 0 ? B : 1, s, st->e_c[c]));
       }
       o += nc;
     }
@@ -1802,7 +1917,7 @@ extern "C" int jt_state_load(jt_state* st, int case_idx, const double* clique_co
     const int64_t ns = p->ssize[sp];
     char* dst = (char*)st->d_aux + (sep_cur(st, sp) + (case_idx < 0 ? 0 : case_idx)) * st->esz;
     if (sep_concat) {
-      CK(launch_convert_d2t(p->dtype, st->d_stage + o, dst, ns, B, case_idx < 0 ? B : 1, s));
+      CK(launch_convert_d2t(p->dtype, st->d_stage + o, dst, ns, B, case_idx < 0 ? B : 1, s, st->e_s[sp]));
     } else if (case_idx < 0) {
       CK(launch_fill(p->dtype, dst, ns * B, 1.0, s));
     }
@@ -1896,13 +2011,23 @@ extern "C" int jt_state_initialize(jt_state* st, int n_cpts, const int32_t* cpt_
     return e == cudaErrorMemoryAllocation ? JT_ERR_OOM : JT_ERR_CUDA;
   }
   st->launches++;
-  if (st->mode == JT_SHARED_BASE) {  // host copy of the new base (contraction passes)
+  {
+    // prescale the new base (power-of-two balance, see jt_state) from its clique sums
     std::vector<char> raw(st->n_base * st->esz);
     CK(cudaMemcpy(raw.data(), st->d_base, raw.size(), cudaMemcpyDeviceToHost));
-    st->h_base.resize(st->n_base);
+    std::vector<double> hb(st->n_base);
     for (int64_t i = 0; i < st->n_base; ++i)
-      st->h_base[i] = st->esz == 8 ? ((const double*)raw.data())[i] : (double)((const float*)raw.data())[i];
-    st->programs.clear();
+      hb[i] = st->esz == 8 ? ((const double*)raw.data())[i] : (double)((const float*)raw.data())[i];
+    choose_prescale(st, [&](int c) { return hb.data() + st->boff[c]; });
+    for (int c = 0; c < p->n_cliques; ++c) {
+      CK(launch_scale_pow2(p->dtype, (char*)st->d_base + st->boff[c] * st->esz, p->csize[c], st->pre_e[c], s));
+      for (int64_t i = 0; i < p->csize[c]; ++i) hb[st->boff[c] + i] = std::ldexp(hb[st->boff[c] + i], st->pre_e[c]);
+    }
+    CK(cudaStreamSynchronize(s));
+    if (st->mode == JT_SHARED_BASE) {  // host copy of the new base (contraction passes)
+      st->h_base.swap(hb);
+      st->programs.clear();
+    }
   }
   // every case starts from the new base tables; separators ones, no evidence
   rc = jt_state_reset(st, nullptr);
@@ -1927,7 +2052,7 @@ extern "C" int jt_state_store(jt_state* st, int case_idx, double* clique_concat,
     int64_t o = 0;
     for (int c = 0; c < p->n_cliques; ++c) {
       const char* src = (const char*)st->d_clique + (st->coff[c] + case_idx) * st->esz;
-      CK(launch_convert_t2d(p->dtype, src, B, st->d_stage + o, p->csize[c], s));
+      CK(launch_convert_t2d(p->dtype, src, B, st->d_stage + o, p->csize[c], s, st->e_c[c]));
       o += p->csize[c];
     }
     CK(cudaMemcpyAsync(clique_concat, st->d_stage, tot_c * 8, cudaMemcpyDeviceToHost, s));
@@ -1937,7 +2062,7 @@ extern "C" int jt_state_store(jt_state* st, int case_idx, double* clique_concat,
     int64_t o = 0;
     for (int sp = 0; sp < p->n_seps; ++sp) {
       const char* src = (const char*)st->d_aux + (sep_cur(st, sp) + case_idx) * st->esz;
-      CK(launch_convert_t2d(p->dtype, src, B, st->d_stage + o, p->ssize[sp], s));
+      CK(launch_convert_t2d(p->dtype, src, B, st->d_stage + o, p->ssize[sp], s, st->e_s[sp]));
       o += p->ssize[sp];
     }
     CK(cudaMemcpyAsync(sep_concat, st->d_stage, tot_s * 8, cudaMemcpyDeviceToHost, s));
@@ -1966,6 +2091,9 @@ extern "C" int jt_state_clone(jt_state* src, jt_state** out) {
   dst->sep_in_y = src->sep_in_y;
   dst->ev_clique = src->ev_clique;
   dst->h_base = src->h_base;
+  dst->pre_e = src->pre_e;
+  dst->e_c = src->e_c;
+  dst->e_s = src->e_s;
   *out = own.release();
   return JT_OK;
 }
@@ -1985,6 +2113,8 @@ extern "C" int jt_state_reset(jt_state* st, void* stream) {
   // separators back to ones: deferred — a fresh propagation never reads them
   st->seps_stale = p->n_seps > 0;
   st->fresh = true;
+  st->e_c = st->pre_e;
+  std::fill(st->e_s.begin(), st->e_s.end(), 0);
   if (st->mode == JT_SHARED_BASE) return JT_OK;
   Program* pr;
   auto it = st->programs.find("reset");
@@ -2148,6 +2278,12 @@ extern "C" int jt_message(jt_state* st, int src, int tgt, int sep, void* stream)
   int rc0 = ensure_seps(st, s);
   if (rc0) return rc0;
   st->fresh = false;
+  // exponents (jt_state): new sep = star of src; tgt *= new/old
+  {
+    const int es_old = st->e_s[sep];
+    st->e_s[sep] = st->e_c[src];
+    st->e_c[tgt] += st->e_c[src] - es_old;
+  }
   const std::string mkey = key_of("msg", {src, tgt, sep, (int)st->sep_in_y});
   Program* pr;
   auto it = st->programs.find(mkey);
@@ -2384,6 +2520,8 @@ static void shared_restart(jt_state* st) {
   if (st->mode != JT_SHARED_BASE || st->fresh) return;
   st->fresh = true;
   st->seps_stale = st->plan->n_seps > 0;
+  st->e_c = st->pre_e;
+  std::fill(st->e_s.begin(), st->e_s.end(), 0);
 }
 
 extern "C" int jt_propagate(jt_state* st, const int32_t* roots_or_null, void* stream) {
@@ -2407,6 +2545,7 @@ extern "C" int jt_propagate(jt_state* st, const int32_t* roots_or_null, void* st
     ClusterProg* cp = cit->second.get();
     if (cp->ok) {
       if ((rc = ensure_seps(st, s))) return rc;
+      set_all_exp(st, joint_exp(st));
       ClusterArgs a;
       a.clique = st->d_clique;
       a.aux = st->d_aux;
@@ -2442,6 +2581,7 @@ extern "C" int jt_propagate(jt_state* st, const int32_t* roots_or_null, void* st
   }
   rc = run_program(st, pr, s);
   if (rc) return rc;
+  set_all_exp(st, joint_exp(st));  // calibrated: every table is a marginal of the joint
   if (fresh) st->sep_in_y = !st->sep_in_y;
   st->fresh = false;
   st->seps_stale = false;
@@ -2459,7 +2599,7 @@ static int smallest_holder(const jt_plan* p, int v) {
 // raw marginals are already in qout; normalize into out_device [B][Σcard].
 // Per-variable-list metadata is uploaded once and cached, so this is async.
 static int finish_query(jt_state* st, int n, const int32_t* var, int normalize, double* out_device,
-                        cudaStream_t s, int* total_cols_out) {
+                        cudaStream_t s, int* total_cols_out, const std::vector<int>& exps) {
   const jt_plan* p = st->plan;
   std::vector<int> vs(var, var + n);
   const std::string key = key_of("qm", vs);
@@ -2485,13 +2625,30 @@ static int finish_query(jt_state* st, int n, const int32_t* var, int normalize, 
   const int32_t* dqc = reinterpret_cast<const int32_t*>(dqo + n);
   const int32_t* dqcol = dqc + n;
   const int cols = it->second.second;
-  CK(launch_normalize(st->d_qout, dqo, dqc, dqcol, n, st->B, cols, normalize, out_device, st->d_err, s));
+  // stored tables are exact * 2^e: unnormalized results undo it (one exponent, or per query)
+  const int* d_qexp = nullptr;
+  int exp_all = exps.empty() ? 0 : exps[0];
+  if (!normalize && std::any_of(exps.begin(), exps.end(), [&](int e) { return e != exp_all; })) {
+    if ((int64_t)exps.size() > st->qexp_cap) {
+      CK(cudaStreamSynchronize(s));
+      cudaFree(st->d_qexp);
+      st->d_qexp = nullptr;
+      st->qexp_cap = 0;
+      CK(cudaMalloc(&st->d_qexp, exps.size() * sizeof(int)));
+      st->qexp_cap = (int64_t)exps.size();
+    }
+    CK(cudaMemcpyAsync(st->d_qexp, exps.data(), exps.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+    d_qexp = st->d_qexp;
+  }
+  CK(launch_normalize(st->d_qout, dqo, dqc, dqcol, n, st->B, cols, normalize, out_device, st->d_err, d_qexp,
+                      exp_all, s));
   st->launches++;
   if (total_cols_out) *total_cols_out = cols;
   return JT_OK;
 }
 
-static int query_program(jt_state* st, int n, const int32_t* var, const int32_t* clique, cudaStream_t s) {
+static int query_program(jt_state* st, int n, const int32_t* var, const int32_t* clique, cudaStream_t s,
+                         std::vector<int>& exps) {
   const jt_plan* p = st->plan;
   std::vector<int> vs, cs;
   for (int i = 0; i < n; ++i) {
@@ -2503,6 +2660,7 @@ static int query_program(jt_state* st, int n, const int32_t* var, const int32_t*
     if (!std::binary_search(p->cvars[c].begin(), p->cvars[c].end(), v)) return JT_ERR_BAD_ARG;
     vs.push_back(v);
     cs.push_back(c);
+    exps.push_back(st->e_c[c]);
   }
   std::vector<int> kk = vs;
   kk.insert(kk.end(), cs.begin(), cs.end());
@@ -2551,9 +2709,10 @@ extern "C" int jt_query_device(jt_state* st, int n, const int32_t* var, const in
   if (n == 0) return JT_OK;
   DevGuard g(st->plan->device);
   cudaStream_t s = pick_stream(st, stream);
-  int rc = query_program(st, n, var, clique, s);
+  std::vector<int> exps;
+  int rc = query_program(st, n, var, clique, s, exps);
   if (rc) return rc;
-  return finish_query(st, n, var, normalize, out_device, s, nullptr);
+  return finish_query(st, n, var, normalize, out_device, s, nullptr, exps);
 }
 
 extern "C" int jt_query(jt_state* st, int n, const int32_t* var, const int32_t* clique, int normalize,
@@ -2621,10 +2780,11 @@ extern "C" int jt_propagate_query(jt_state* st, int n, const int32_t* var, int n
   }
   int rc = run_program(st, pr, s);
   if (rc) return rc;
+  set_all_exp(st, joint_exp(st));
   if (fresh) st->sep_in_y = !st->sep_in_y;
   st->fresh = false;
   st->seps_stale = false;
-  return n ? finish_query(st, n, var, normalize, out_device, s, nullptr) : JT_OK;
+  return n ? finish_query(st, n, var, normalize, out_device, s, nullptr, std::vector<int>(n, st->e_c[0])) : JT_OK;
 }
 
 extern "C" int jt_sync_error(jt_state* st) {

@@ -113,6 +113,8 @@ struct CPass {
   int64_t n_units;
   int nI, nS, nK, nG, nE, nT, nBC;
   int nCG;                  // case-chunk groups: a unit walks chunks cg, cg + nCG, ...
+  int cmaj;                 // 1: units enumerate the case-chunk group outermost (concurrent warps
+                            //    share one case chunk of every i: i-reused factor rows stay in L2)
   int rowi;                 // 1: nS == 1, units are TMC consecutive i (W layout [nI][nK])
   int nKS;                  // > 1: K split into nKS chunks of kch (units also index the chunk);
   int kch;                  //   partial sums combined in chunk order by the last warp of a group
@@ -209,11 +211,14 @@ cudaError_t launch_wave_own(int dtype, int vec, int lm, int m, const WaveArgs& a
 int wave_own_max_ctas_per_sm(int dtype, int vec);
 cudaError_t launch_normalize(const double* qout, const int64_t* q_off, const int32_t* q_card,
                              const int32_t* q_col, int nq, int B, int total_cols,
-                             int normalize, double* post, int* err, cudaStream_t s);
+                             int normalize, double* post, int* err, const int* q_exp, int exp_all,
+                             cudaStream_t s);
+// exp2: arena values are stored scaled by 2^exp2 (power-of-two prescaling)
 cudaError_t launch_convert_d2t(int dtype, const double* src, void* dst, int64_t n,
-                               int64_t dst_stride, int64_t bcount, cudaStream_t s);
+                               int64_t dst_stride, int64_t bcount, cudaStream_t s, int exp2 = 0);
 cudaError_t launch_convert_t2d(int dtype, const void* src, int64_t src_stride,
-                               double* dst, int64_t n, cudaStream_t s);
+                               double* dst, int64_t n, cudaStream_t s, int exp2 = 0);
+cudaError_t launch_scale_pow2(int dtype, void* p, int64_t n, int exp2, cudaStream_t s);
 cudaError_t launch_fill(int dtype, void* dst, int64_t n, double v, cudaStream_t s);
 cudaError_t launch_ev_fill(void* aux, int dtype, const int32_t* vars, int nv, const int64_t* var_off,
                            const int32_t* cards, int B, cudaStream_t s);

@@ -1163,10 +1163,22 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
     const CPass* __restrict__ P = a.passes + pi;
     const int nT = P->nT, nCG = P->nCG, nKS = P->nKS;
     // unit = (i, t, ks, cg), case chunk fastest: concurrent warps share factor rows
-    const int cg = (int)(ul % nCG);
-    const int ks = (int)((ul / nCG) % nKS);
-    const int t = (int)((ul / ((int64_t)nCG * nKS)) % nT);
-    const int64_t i = ul / ((int64_t)nCG * nKS * nT);
+    // (cmaj: case chunk slowest)
+    int cg, ks, t;
+    int64_t i;
+    if (P->cmaj) {
+      const int64_t per = (int64_t)P->nI * nT * nKS;
+      cg = (int)(ul / per);
+      const int64_t r = ul - (int64_t)cg * per;
+      ks = (int)(r % nKS);
+      t = (int)((r / nKS) % nT);
+      i = r / ((int64_t)nKS * nT);
+    } else {
+      cg = (int)(ul % nCG);
+      ks = (int)((ul / nCG) % nKS);
+      t = (int)((ul / ((int64_t)nCG * nKS)) % nT);
+      i = ul / ((int64_t)nCG * nKS * nT);
+    }
     const int nS = P->nS, nE = P->nE;
     const int kb = ks * P->kch;                      // this unit's k range [kb, kb + nK)
     const int nK = min(P->nK - kb, P->kch);
@@ -1375,8 +1387,8 @@ __global__ void __launch_bounds__(NT, FOLD ? ROWI_MINB_F : ROWI_MINB_NF) contrac
     }
     const CPass* __restrict__ P = a.passes + pi;
     const int nCG = P->nCG;
-    const int cg = (int)(ul % nCG);
-    const int64_t i = ul / nCG;
+    const int cg = P->cmaj ? (int)(ul / P->nI) : (int)(ul % nCG);
+    const int64_t i = P->cmaj ? ul % P->nI : ul / nCG;
     const int nK = P->nK, nG = P->nG, nE = P->nE;
     const int tw = nG + nE + 1;
     const int32_t* __restrict__ tir = a.tab + P->ti_off + i * tw;
@@ -1620,10 +1632,12 @@ int wave_max_ctas_per_sm(int dtype, int vec, int kv) { return kv == 2 ? occ_kv<2
 // ---- posteriors: raw marginals [var][card][B] -> normalized [B][Σcard] ----
 // normalize (potential.py:181-186): total <= 0 raises ZeroMassError; here the
 // case's row is NaN-filled and the zero-mass bit is set.
+// q_exp (nullable: exp_all for every query): the queried tables are stored
+// scaled by 2^q_exp (power-of-two prescaling); unnormalized results undo it.
 __global__ void normalize_kernel(const double* __restrict__ qout, const int64_t* __restrict__ q_off,
                                  const int32_t* __restrict__ q_card, const int32_t* __restrict__ q_col,
                                  int nq, int B, int total_cols, int normalize,
-                                 double* __restrict__ post, int* err) {
+                                 double* __restrict__ post, int* err, const int* __restrict__ q_exp, int exp_all) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)nq * B) return;
   const int i = (int)(idx / B);
@@ -1634,7 +1648,8 @@ __global__ void normalize_kernel(const double* __restrict__ qout, const int64_t*
   double s = 0.0;
   for (int d = 0; d < card; ++d) s += q[(int64_t)d * B + b];
   if (!normalize) {
-    for (int d = 0; d < card; ++d) o[d] = q[(int64_t)d * B + b];
+    const int ex = q_exp ? q_exp[i] : exp_all;
+    for (int d = 0; d < card; ++d) o[d] = ldexp(q[(int64_t)d * B + b], -ex);
     return;
   }
   if (!(s > 0.0)) {
@@ -1648,28 +1663,36 @@ __global__ void normalize_kernel(const double* __restrict__ qout, const int64_t*
 
 cudaError_t launch_normalize(const double* qout, const int64_t* q_off, const int32_t* q_card,
                              const int32_t* q_col, int nq, int B, int total_cols, int normalize,
-                             double* post, int* err, cudaStream_t s) {
+                             double* post, int* err, const int* q_exp, int exp_all, cudaStream_t s) {
   const int64_t n = (int64_t)nq * B;
   if (n == 0) return cudaSuccess;
   normalize_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(qout, q_off, q_card, q_col, nq, B,
-                                                               total_cols, normalize, post, err);
+                                                               total_cols, normalize, post, err, q_exp, exp_all);
   return cudaGetLastError();
 }
 
 // ---- host<->arena conversion (f64 staging <-> storage type, batch lanes) ----
+// exp2: stored = value * 2^exp2 (power-of-two prescaling, exact: ldexp only
+// moves the exponent)
 template <typename T>
 __global__ void d2t_kernel(const double* __restrict__ src, T* __restrict__ dst, int64_t n,
-                           int64_t stride, int64_t bcount) {
+                           int64_t stride, int64_t bcount, int exp2) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n * bcount) return;
   const int64_t e = idx / bcount, l = idx - (idx / bcount) * bcount;
-  dst[e * stride + l] = (T)src[e];
+  dst[e * stride + l] = (T)(exp2 ? ldexp(src[e], exp2) : src[e]);
 }
 
 template <typename T>
-__global__ void t2d_kernel(const T* __restrict__ src, int64_t stride, double* __restrict__ dst, int64_t n) {
+__global__ void t2d_kernel(const T* __restrict__ src, int64_t stride, double* __restrict__ dst, int64_t n, int exp2) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx < n) dst[idx] = (double)src[idx * stride];
+  if (idx < n) dst[idx] = exp2 ? ldexp((double)src[idx * stride], -exp2) : (double)src[idx * stride];
+}
+
+template <typename T>
+__global__ void scale_pow2_kernel(T* p, int64_t n, int exp2) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx < n) p[idx] = (T)ldexp((double)p[idx], exp2);
 }
 
 template <typename T>
@@ -1679,21 +1702,29 @@ __global__ void fill_kernel(T* dst, int64_t n, double v) {
 }
 
 cudaError_t launch_convert_d2t(int dtype, const double* src, void* dst, int64_t n, int64_t stride,
-                               int64_t bcount, cudaStream_t s) {
+                               int64_t bcount, cudaStream_t s, int exp2) {
   const int64_t tot = n * bcount;
   if (tot == 0) return cudaSuccess;
   const unsigned g = (unsigned)((tot + 255) / 256);
-  if (dtype == 0) d2t_kernel<float><<<g, 256, 0, s>>>(src, (float*)dst, n, stride, bcount);
-  else d2t_kernel<double><<<g, 256, 0, s>>>(src, (double*)dst, n, stride, bcount);
+  if (dtype == 0) d2t_kernel<float><<<g, 256, 0, s>>>(src, (float*)dst, n, stride, bcount, exp2);
+  else d2t_kernel<double><<<g, 256, 0, s>>>(src, (double*)dst, n, stride, bcount, exp2);
   return cudaGetLastError();
 }
 
 cudaError_t launch_convert_t2d(int dtype, const void* src, int64_t stride, double* dst, int64_t n,
-                               cudaStream_t s) {
+                               cudaStream_t s, int exp2) {
   if (n == 0) return cudaSuccess;
   const unsigned g = (unsigned)((n + 255) / 256);
-  if (dtype == 0) t2d_kernel<float><<<g, 256, 0, s>>>((const float*)src, stride, dst, n);
-  else t2d_kernel<double><<<g, 256, 0, s>>>((const double*)src, stride, dst, n);
+  if (dtype == 0) t2d_kernel<float><<<g, 256, 0, s>>>((const float*)src, stride, dst, n, exp2);
+  else t2d_kernel<double><<<g, 256, 0, s>>>((const double*)src, stride, dst, n, exp2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale_pow2(int dtype, void* p, int64_t n, int exp2, cudaStream_t s) {
+  if (n == 0 || exp2 == 0) return cudaSuccess;
+  const unsigned g = (unsigned)((n + 255) / 256);
+  if (dtype == 0) scale_pow2_kernel<float><<<g, 256, 0, s>>>((float*)p, n, exp2);
+  else scale_pow2_kernel<double><<<g, 256, 0, s>>>((double*)p, n, exp2);
   return cudaGetLastError();
 }
 

@@ -151,6 +151,31 @@ def corpus():
         json.dump(doc, f)
 
 
+def unscaled_golden(name="c2", n_cases=3, evidence_seed=77):
+    """The reference generator's own potentials, NOT rescaled: uniform(0.1, 1)
+    per clique in id order (synth.py:105-107, default_rng(0)).  On the
+    Pigs-shaped c2 tree these reach ~1e107 after propagation:
+    far outside fp32.  Reference posteriors and unnormalized masses P(e)
+    (query_marginal(..., normalize_result=False).total(), propagate.py:363-377)."""
+    members, cards = synth.config_members(name)
+    tree = build_tree(members, cards)
+    tree.cpt_assignment = {v: synth.smallest_holder(tree, v) for v in range(len(cards))}
+    rng = np.random.default_rng(0)
+    tables = [rng.uniform(0.1, 1.0, size=c.scope.size) for c in tree.cliques]
+    out = {}
+    cases = [dict()] + synth.evidence_cases(tree, n_cases, seed=evidence_seed)
+    for i, ev in enumerate(cases):
+        st = from_potentials(tree, tables)
+        if ev:
+            apply_evidence(st, ev)
+        belief_propagation(st)
+        out[f"post{i}"] = np.concatenate([query_marginal(st, v).values for v in range(len(cards))])
+        out[f"mass{i}"] = np.array([query_marginal(st, v, normalize_result=False).total() for v in (0, 5, 17)])
+        out[f"ev{i}"] = np.array(sorted(ev.items()), dtype=np.int64).reshape(-1, 2)
+        out[f"maxabs{i}"] = np.array([max(float(c.max()) for c in st.clique_values)])
+    np.savez_compressed(os.path.join(HERE, f"{name}_unscaled.npz"), **out)
+
+
 BENCH_IDX = list(range(0, 24)) + list(range(4072, 4120)) + list(range(8168, 8192))
 
 
@@ -181,9 +206,13 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["bench"]:
         bench_golden()
         sys.exit(0)
+    if sys.argv[1:] == ["unscaled"]:
+        unscaled_golden()
+        sys.exit(0)
     mapping_tables()
     corpus()
     for name, n in (("c1", 8), ("c2", 4), ("c4M", 2), ("c5", 8), ("c4B", 1), ("c3", 1)):
         config_golden(name, n)
         print("golden", name)
     bench_golden()
+    unscaled_golden()

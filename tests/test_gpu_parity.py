@@ -570,3 +570,60 @@ def test_estimator_rejects_bad_evidence_like_reference():
         est.predict_proba([{"no-such-variable": 0}])
     with pytest.raises(StateOutOfRangeError):
         est.predict_proba([{0: net.variables[0].cardinality}])
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_unscaled_generator_potentials_and_evidence_probability(dtype):
+    """Row f2: the reference generator's own potentials, not
+    rescaled (uniform(0.1, 1), synth.py:105-107), on the Pigs-shaped c2 tree
+    reach ~1e107 -- beyond fp32.  The power-of-two prescaling
+    (jt_state: exact, tracked per table) keeps the fp32 state in range, and
+    unnormalized queries restore P(e) (propagate.py:363-377,
+    test_propagate.py:318-326).  Posteriors and P(e) vs the reference at
+    1e-5 (fp32) / 1e-10 (fp64); host views are the exact (unscaled) tables."""
+    import os
+
+    from conftest import GOLDEN
+
+    tree, _ = load_golden("c2")
+    rng = np.random.default_rng(0)
+    tables = [rng.uniform(0.1, 1.0, size=c.scope.size) for c in tree.cliques]
+    g = np.load(os.path.join(GOLDEN, "c2_unscaled.npz"))
+    n = len(tree.cards)
+    for i in range(4):
+        ev = {int(v): int(x) for v, x in g[f"ev{i}"]}
+        st = P().from_potentials(tree, tables, engine=P().CudaEngine(dtype=dtype))
+        if ev:
+            P().apply_evidence(st, ev)
+        P().belief_propagation(st)
+        assert rel_err(all_posteriors(st, n), g[f"post{i}"]) < TOL[dtype], (dtype, i)
+        mass = np.array([P().query_marginal(st, v, normalize_result=False).total() for v in (0, 5, 17)])
+        assert rel_err(mass, g[f"mass{i}"]) < TOL[dtype], (dtype, i, mass, g[f"mass{i}"])
+        top = max(float(np.max(c)) for c in st.clique_values)
+        assert rel_err(top, g[f"maxabs{i}"][0]) < TOL[dtype], (dtype, i)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_unscaled_munin_shaped_tree_stays_finite(dtype):
+    """On the Munin-shaped c4M tree the reference's own fp64 path overflows to
+    inf/NaN with unscaled generator potentials.  Posteriors are
+    invariant under per-clique rescaling, so the oracle on the same tables
+    rescaled per Appendix A is the reference answer; the device gets the raw
+    tables in both precisions."""
+    tree, _ = load_golden("c4M")
+    rng = np.random.default_rng(3)
+    raw = [rng.uniform(0.1, 1.0, size=c.scope.size) for c in tree.cliques]
+    parent = synth.bfs_parents(tree)
+    scaled = []
+    for c, t in zip(tree.cliques, raw):
+        target = 1.0 if parent[c.id] == -1 else float(tree.separators[parent[c.id][1]].scope.size)
+        scaled.append(t * (target / t.sum()))
+    n = len(tree.cards)
+    ev = synth.evidence_cases(tree, 1, seed=11)[0]
+    want = jtref.case_posteriors(jtref.from_potentials(tree, scaled), ev, range(n))
+    st = P().from_potentials(tree, raw, engine=P().CudaEngine(dtype=dtype))
+    P().apply_evidence(st, ev)
+    P().belief_propagation(st)
+    got = all_posteriors(st, n)
+    assert np.all(np.isfinite(got))
+    assert rel_err(got, want) < TOL[dtype]
