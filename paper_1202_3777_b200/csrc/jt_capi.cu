@@ -200,6 +200,11 @@ struct Program {
   void* d_w = nullptr;
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t gstream = nullptr;
+  // persistent single-launch program (small single trees, jt_tiny.cu)
+  int tiny = 0, tiny_grid = 0, n_twaves = 0;
+  TPass* d_tpass = nullptr;
+  TinyWave* d_twaves = nullptr;
+  unsigned* d_bar = nullptr;
   int runs = 0;
   int64_t n_launches = 0;  // kernel launches per run
   ~Program() {
@@ -215,6 +220,9 @@ struct Program {
     cudaFree(d_cpass);
     cudaFree(d_ctab);
     cudaFree(d_w);
+    cudaFree(d_tpass);
+    cudaFree(d_twaves);
+    cudaFree(d_bar);
   }
 };
 
@@ -598,7 +606,7 @@ static std::vector<Dim> merge_dims(const std::vector<Dim>& in, int nf) {
 }
 
 static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pass_idx, BuiltPass& bp,
-                        bool allow_row = true, int kv = KV) {
+                        bool allow_row = true, int kv = KV, bool allow_own = true) {
   const int nf = (int)ps.factors.size();
   if (nf > MAXF) return JT_ERR_UNSUPPORTED;
   std::vector<Dim> dims = pass_dims(st, ps);
@@ -656,7 +664,7 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
     }
     // the thread-owned kernel is validated for one merged inner dimension only
     // (batched states: the case dim); multi-dim inner blocks take the general kernel
-    if (im.size() > 1) c.own_m = 0;
+    if (im.size() > 1 || !allow_own) c.own_m = 0;
     c.own = c.own_m > 0;
     c.BPI = c.own ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(TH / T, c.r_out));
     // several whole output groups per iteration when a group is smaller than an iteration
@@ -1134,6 +1142,28 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   cp.kch = (int)nK;
   cp.n_units = (rowi ? 1 : nI) * cp.nT * cp.nCG;
   int64_t min_units = (int64_t)st->num_sms * 8;
+  cp.igs = 1;
+  if (rowi && !I.empty() && !getenv("JT_NO_ROWG")) {
+    // i-groups: the innermost i variable's values share every factor that does not
+    // index it; group them into one warp unit when those shared factors dominate
+    const int v = I.back();
+    const int igs = p->cards[v];
+    double shared = 0.0, own = 0.0;
+    int gst[CMAXG] = {0};
+    for (int g = 0; g < nG; ++g) {
+      double n = (double)B;
+      for (int x : G[g]->vars) n *= p->cards[x];
+      gst[g] = (int)tensor_stride(p, *G[g], v, B);
+      (gst[g] == 0 ? shared : own) += n;
+    }
+    const int64_t units = (nI / igs) * (int64_t)cp.nCG;
+    if (igs >= 2 && igs <= 8 && nI % igs == 0 && shared > own && units >= min_units) {
+      cp.rowi = igs <= 4 ? 2 : 3;
+      cp.igs = igs;
+      for (int g = 0; g < nG; ++g) cp.gstride[g] = gst[g];
+      cp.n_units = units;
+    }
+  }
   // (the K-split combine is a warp collective: every lane must own cases, so B
   // must fill whole case chunks; otherwise the pass takes the general kernels)
   const int kvec = st->esz == 4 ? 4 : 2;
@@ -1259,8 +1289,8 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
     // contraction launch groups keyed by (fold, rowi, nG): fold = fp32 sums over > CKF
     // terms fold into fp64; nG is a compile-time parameter of the tile kernel
     constexpr int NGK = CMAXG + 1;
-    std::vector<CPass> cps[4 * NGK];
-    std::vector<int> cpc[4 * NGK];
+    std::vector<CPass> cps[8 * NGK];
+    std::vector<int> cpc[8 * NGK];
     for (auto& ps : w) {
       if (contract_eligible(st, ps)) {
         CPass cp;
@@ -1331,13 +1361,13 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
     // JT_SPLIT_CPASS=1 (diagnostic): one launch per contraction pass, so an ncu
     // launch list attributes time and DRAM bytes to single passes
     if (getenv("JT_SPLIT_CPASS")) {
-      std::vector<CPass> cps2[4 * NGK];
-      std::vector<int> cpc2[4 * NGK];
-      for (int key = 0; key < 4 * NGK; ++key) {
+      std::vector<CPass> cps2[8 * NGK];
+      std::vector<int> cpc2[8 * NGK];
+      for (int key = 0; key < 8 * NGK; ++key) {
         cps2[key].swap(cps[key]);
         cpc2[key].swap(cpc[key]);
       }
-      for (int key = 0; key < 4 * NGK; ++key)
+      for (int key = 0; key < 8 * NGK; ++key)
         for (size_t q = 0; q < cps2[key].size(); ++q) {
           const int fold = (key / NGK) & 1;
           LaunchGrp cg;
@@ -1357,7 +1387,7 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
           rt.groups.push_back(cg);
         }
     }
-    for (int key = 0; key < 4 * NGK; ++key) {
+    for (int key = 0; key < 8 * NGK; ++key) {
       const int fold = (key / NGK) & 1;
       if (cps[key].empty()) continue;
       LaunchGrp cg;
@@ -1393,6 +1423,97 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
   return JT_OK;
 }
 
+// Small single trees run as ONE persistent launch of tiny passes (jt_tiny.cu)
+// when every wave is small: their waves are latency-bound, so per-wave launches
+// and the general kernel's per-item epilogues dominate (c1 6 waves
+// in 50 us).
+#ifndef TINY_MAX_LOG2
+#define TINY_MAX_LOG2 22
+#endif
+static bool tiny_choice(const jt_state* st, const std::vector<std::vector<PassSpec>>& waves) {
+  if (st->B != 1 || st->mode != JT_MATERIALIZED || getenv("JT_NO_TINY")) return false;
+  static const int lg = env_int("JT_TINY_MAX_LOG2", TINY_MAX_LOG2);
+  int nw = 0;
+  for (auto& w : waves) {
+    if (w.empty()) continue;
+    ++nw;
+    int64_t el = 0;
+    for (auto& ps : w) {
+      const auto dd = pass_dims(st, ps);
+      int64_t n = 1;
+      for (auto& x : dd) n *= x.card;
+      el += n;
+    }
+    if (el > (int64_t(1) << lg)) return false;
+  }
+  return nw >= 3;
+}
+
+// Tiny passes of a program: per pass, the merged dims split into output dims
+// (those the output tensor indexes; every dim when there is no output) and row
+// dims; one thread per output entry, one warp when the row is long.
+static int build_tiny(const jt_state* st, const std::vector<std::vector<PassSpec>>& waves, std::vector<TPass>& tp,
+                      std::vector<TinyWave>& tw) {
+  auto fits = [](int64_t x) { return x >= INT32_MIN && x <= INT32_MAX; };
+  for (auto& w : waves) {
+    if (w.empty()) continue;
+    TinyWave wv{};
+    wv.pass0 = (int64_t)tp.size();
+    int64_t units = 0;
+    for (auto& ps : w) {
+      const int nf = (int)ps.factors.size();
+      if (nf > MAXF || (ps.write && !ps.scope.empty())) return JT_ERR_UNSUPPORTED;
+      const std::vector<Dim> dims = merge_dims(pass_dims(st, ps), nf);
+      const bool has_out = ps.out_kind != OUT_NONE;
+      TPass P;
+      std::memset(&P, 0, sizeof(P));
+      P.src_arena = ps.src_arena;
+      P.src_off = ps.src_arena == A_AUX ? ps.src_off : ps.src_arena == A_CLIQUE ? st->coff[ps.clique] : st->boff[ps.clique];
+      P.dst_off = ps.write ? st->coff[ps.clique] : -1;
+      P.nf = nf;
+      for (int f = 0; f < nf; ++f) P.fac_off[f] = ps.factors[f].off;
+      P.out_kind = ps.out_kind;
+      P.out_off = has_out ? ps.out.off : 0;
+      P.ratio_off = ps.ratio_off;
+      P.out2_off = ps.out2_off;
+      P.n_out = 1;
+      P.n_rest = 1;
+      for (const Dim& d : dims) {
+        if (!fits(d.src) || !fits(d.dst) || !fits(d.out) || d.card > INT32_MAX) return JT_ERR_UNSUPPORTED;
+        for (int f = 0; f < nf; ++f)
+          if (!fits(d.fac[f])) return JT_ERR_UNSUPPORTED;
+        if (!has_out || d.out != 0) {
+          if (P.nod == TD) return JT_ERR_UNSUPPORTED;
+          const int k = P.nod++;
+          P.ocard[k] = (int)d.card;
+          P.osrc[k] = (int)d.src;
+          P.odst[k] = (int)d.dst;
+          P.oout[k] = (int)d.out;
+          for (int f = 0; f < nf; ++f) P.ofac[f][k] = (int)d.fac[f];
+          P.n_out *= d.card;
+        } else {
+          if (P.nrd == TD) return JT_ERR_UNSUPPORTED;
+          const int k = P.nrd++;
+          P.rcard[k] = (int)d.card;
+          P.rsrc[k] = (int)d.src;
+          P.rdst[k] = (int)d.dst;
+          for (int f = 0; f < nf; ++f) P.rfac[f][k] = (int)d.fac[f];
+          P.n_rest *= d.card;
+        }
+      }
+      P.warp = P.n_rest >= 96 ? 1 : 0;
+      P.unit0 = units;
+      const int64_t nu = P.warp ? P.n_out * 32 : P.n_out;
+      units += (nu + 31) / 32 * 32;
+      tp.push_back(P);
+    }
+    wv.n_passes = (int)(tp.size() - wv.pass0);
+    wv.n_threads = units;
+    tw.push_back(wv);
+  }
+  return JT_OK;
+}
+
 static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>& waves,
                          std::unique_ptr<Program>& out) {
   HostProgram hp;
@@ -1403,6 +1524,27 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
   auto prog = std::make_unique<Program>();
   prog->waves = hp.waves;
   for (auto& w : hp.waves) prog->n_launches += (int64_t)w.groups.size();
+  if (tiny_choice(st, waves)) {
+    std::vector<TPass> tp;
+    std::vector<TinyWave> tw;
+    if (build_tiny(st, waves, tp, tw) == JT_OK && !tw.empty()) {
+      int occ = 1;
+      TinyArgs dummy{};
+      CK(launch_tiny(st->plan->dtype, dummy, 0, nullptr, &occ));
+      int64_t max_ctas = 1;
+      for (auto& w : tw) max_ctas = std::max<int64_t>(max_ctas, (w.n_threads + NT - 1) / NT);
+      prog->tiny = 1;
+      prog->tiny_grid = (int)std::min<int64_t>(max_ctas, (int64_t)occ * st->num_sms);
+      prog->n_twaves = (int)tw.size();
+      prog->n_launches = 1;
+      CK(cudaMalloc(&prog->d_tpass, tp.size() * sizeof(TPass)));
+      CK(cudaMemcpy(prog->d_tpass, tp.data(), tp.size() * sizeof(TPass), cudaMemcpyHostToDevice));
+      CK(cudaMalloc(&prog->d_twaves, tw.size() * sizeof(TinyWave)));
+      CK(cudaMemcpy(prog->d_twaves, tw.data(), tw.size() * sizeof(TinyWave), cudaMemcpyHostToDevice));
+      CK(cudaMalloc(&prog->d_bar, 2 * sizeof(unsigned)));
+      CK(cudaMemset(prog->d_bar, 0, 2 * sizeof(unsigned)));
+    }
+  }
   auto& passes = hp.passes;
   auto& items = hp.items;
   auto& blk = hp.blk;
@@ -1524,6 +1666,21 @@ static int launch_program_waves(jt_state* st, Program* pr, cudaStream_t s) {
 // replayed as a CUDA graph on that stream (launch-bound small trees).
 static int run_program(jt_state* st, Program* pr, cudaStream_t s) {
   pr->runs++;
+  if (pr->tiny) {
+    TinyArgs a{};
+    a.clique = st->d_clique;
+    a.base = st->d_base;
+    a.aux = st->d_aux;
+    a.qout = st->d_qout;
+    a.err = st->d_err;
+    a.passes = pr->d_tpass;
+    a.waves = pr->d_twaves;
+    a.n_waves = pr->n_twaves;
+    a.bar = pr->d_bar;
+    CK(launch_tiny(st->plan->dtype, a, pr->tiny_grid, s));
+    st->launches++;
+    return JT_OK;
+  }
   if (pr->waves.size() <= 1 || pr->runs < 2) return launch_program_waves(st, pr, s);
   if (pr->gexec && pr->gstream == s) {
     CK(cudaGraphLaunch(pr->gexec, s));
@@ -2944,6 +3101,18 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
   if (rc) return rc;
   std::string out;
   char line[512];
+  if (tiny_choice(&st, waves)) {
+    std::vector<TPass> tp;
+    std::vector<TinyWave> tw;
+    if (build_tiny(&st, waves, tp, tw) == JT_OK) {
+      int64_t warp_passes = 0, threads = 0;
+      for (auto& x : tp) warp_passes += x.warp;
+      for (auto& x : tw) threads += x.n_threads;
+      snprintf(line, sizeof line, "tiny persistent program: one launch, %zu waves, %zu passes (%lld warp-per-entry), "
+               "%lld threads over all waves\n", tw.size(), tp.size(), (long long)warp_passes, (long long)threads);
+      out += line;
+    }
+  }
   {
     // compulsory HBM traffic per wave: every factor tensor read once, outputs
     // written once (separator updates also read the old values and write ratios)
@@ -3015,9 +3184,9 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
       for (int q = 0; q < g.n_cpasses; ++q) {
         const CPass& c = hp.cpasses[g.cpass_off + q];
         snprintf(line, sizeof line,
-                 "  contract clique %d out %d nI %d nS %d nK %d nG %d nE %d units %lld rowi %d ks %d gI-dep",
+                 "  contract clique %d out %d nI %d nS %d nK %d nG %d nE %d units %lld rowi %d ks %d igs %d gI-dep",
                  hp.cpass_clique[g.cpass_off + q], c.out_kind, c.nI, c.nS, c.nK, c.nG, c.nE, (long long)c.n_units,
-                 c.rowi, c.nKS);
+                 c.rowi, c.nKS, c.igs);
         out += line;
         for (int gg = 0; gg < c.nG; ++gg) {  // does factor gg depend on i?
           bool dep = false;

@@ -115,7 +115,10 @@ struct CPass {
   int nCG;                  // case-chunk groups: a unit walks chunks cg, cg + nCG, ...
   int cmaj;                 // 1: units enumerate the case-chunk group outermost (concurrent warps
                             //    share one case chunk of every i: i-reused factor rows stay in L2)
-  int rowi;                 // 1: nS == 1, units are TMC consecutive i (W layout [nI][nK])
+  int rowi;                 // 1: nS == 1, one i per unit (W layout [nI][nK]); 2/3: i-groups (below)
+  int igs;                  // rowi 2/3: a unit is igs consecutive i (the innermost i variable) that
+  int gstride[CMAXG];       //   share every G factor with gstride 0 (loaded once per k); factor g
+                            //   of member q sits at + q * gstride[g]
   int nKS;                  // > 1: K split into nKS chunks of kch (units also index the chunk);
   int kch;                  //   partial sums combined in chunk order by the last warp of a group
   int64_t part_off, cnt_off;
@@ -199,6 +202,44 @@ struct InitTerm {
 cudaError_t launch_init(void* base, int dtype, const double* cpt, const InitClique* cl, int n_cliques,
                         const InitTerm* terms, const int64_t* vdesc, int64_t max_size, cudaStream_t s);
 cudaError_t launch_wave(int dtype, int vec, int kv, const WaveArgs& a, int grid, cudaStream_t s);
+// ---- persistent single-launch programs for small single trees (jt_tiny.cu) ----
+// A tiny pass is one sweep over one clique table seen as [output entries] x
+// [row]: one thread (or, for long rows, one warp) per output entry walks its
+// row with mixed-radix odometers -- every factor, source, destination and
+// output offset from stride arithmetic, no tables.  Rows are summed in a fixed
+// order, so results are deterministic.  Passes without output: one thread per
+// element.  All waves of a propagation run in ONE cooperative launch, separated
+// by grid barriers.
+constexpr int TD = 16;  // merged dims per side (output / row)
+struct TPass {
+  int64_t src_off, dst_off, out_off, ratio_off, out2_off;
+  int64_t fac_off[MAXF];
+  int64_t unit0;            // first thread of the pass in its wave (multiple of 32)
+  int64_t n_out, n_rest;    // output entries (elements, without output), row length
+  int src_arena, nf, out_kind, warp;
+  int nod, nrd;
+  int ocard[TD], rcard[TD];
+  int osrc[TD], odst[TD], oout[TD], rsrc[TD], rdst[TD];
+  int ofac[MAXF][TD], rfac[MAXF][TD];
+};
+struct TinyWave {
+  int64_t pass0;            // first TPass of the wave
+  int64_t n_threads;        // threads of the wave (sum of the passes' units)
+  int n_passes, pad;
+};
+struct TinyArgs {
+  void* clique;
+  const void* base;
+  void* aux;
+  double* qout;
+  int* err;
+  const TPass* passes;
+  const TinyWave* waves;
+  int n_waves;
+  unsigned* bar;            // [counter, generation]
+};
+// occ_out != nullptr: only report the kernel's CTAs per SM
+cudaError_t launch_tiny(int dtype, const TinyArgs& a, int grid, cudaStream_t s, int* occ_out = nullptr);
 int wave_max_ctas_per_sm(int dtype, int vec, int kv);
 cudaError_t launch_wave_row(int dtype, int vec, int lin, const WaveArgs& a, int grid, cudaStream_t s);
 int wave_row_max_ctas_per_sm(int dtype, int vec);

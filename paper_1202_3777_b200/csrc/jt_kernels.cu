@@ -479,9 +479,11 @@ __global__ void __launch_bounds__(NT) wave_own_kernel(const WaveArgs a) {
 #endif
 // KVT vectors per thread per iteration: 4 for large waves; 2 at three CTAs per
 // SM for small, latency-bound waves (more warps in flight, less work per step)
-template <typename T, int VEC, int KVT>
-__global__ void __launch_bounds__(NT, KVT == 2 ? WK2_MINB : 2) wave_kernel(const WaveArgs a) {
-  pdl_enter();
+// The general pass interpreter over one wave's items.  COH (persistent
+// program): tables change between the waves of one launch, so factor loads
+// take the coherent path instead of the read-only (non-coherent) cache.
+template <typename T, int VEC, int KVT, bool COH>
+__device__ __forceinline__ void wave_body(const WaveArgs& a) {
   constexpr int TH = NT * KVT * VEC;  // positions per CTA iteration
   __shared__ DevPass P;
   __shared__ double part2[NT];
@@ -602,9 +604,10 @@ __global__ void __launch_bounds__(NT, KVT == 2 ? WK2_MINB : 2) wave_kernel(const
               const T* p = fb + fo[k];
               T g[VEC];
               if (VEC == 1 || fv) {
-                load_vec_ro<T, VEC>(p, g);
+                if (COH) load_vec<T, VEC>(p, g);
+                else load_vec_ro<T, VEC>(p, g);
               } else {
-                const T x = __ldg(p);
+                const T x = COH ? *p : __ldg(p);
 #pragma unroll
                 for (int l = 0; l < VEC; ++l) g[l] = x;
               }
@@ -719,6 +722,12 @@ __global__ void __launch_bounds__(NT, KVT == 2 ? WK2_MINB : 2) wave_kernel(const
     }
     __syncthreads();
   }
+}
+
+template <typename T, int VEC, int KVT>
+__global__ void __launch_bounds__(NT, KVT == 2 ? WK2_MINB : 2) wave_kernel(const WaveArgs a) {
+  pdl_enter();
+  wave_body<T, VEC, KVT, false>(a);
 }
 
 // Row passes: every position of a unit reduces into ONE output entry (n_in <= 1:
@@ -1457,6 +1466,132 @@ __global__ void __launch_bounds__(NT, FOLD ? ROWI_MINB_F : ROWI_MINB_NF) contrac
   }
 }
 
+// Row-per-i passes over i-groups: igs consecutive i differ only in the
+// innermost i variable, which most factors (the large ones) do not index.  One
+// warp walks the whole group: per k the shared factor rows are loaded once and
+// reused by every member (each member multiplies in its own few small factors
+// and W entry), so the large rows stream from DRAM once instead of igs times
+// through L2.  IGM: compile-time bound of igs (registers for the accumulators).
+template <typename T, bool FOLD, int IGM>
+__global__ void __launch_bounds__(NT, 4) contract_rowg_kernel(const CArgs a) {
+  pdl_enter();
+  constexpr int VEC = CTraits<T>::VEC;
+  constexpr int KF = 16;
+  T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
+  const T* __restrict__ aux_c = aux;
+  const T* __restrict__ W = reinterpret_cast<const T*>(a.w);
+  const int lane = threadIdx.x & 31;
+  const int n_warps = gridDim.x * (NT / 32);
+  int pi = 0;
+  for (int64_t u = blockIdx.x * (NT / 32) + (threadIdx.x >> 5); u < a.n_units; u += n_warps) {
+    int64_t ul;
+    if (a.interleave) {
+      pi = (int)(u % a.n_passes);
+      ul = u / a.n_passes;
+    } else {
+      while (pi + 1 < a.n_passes && u >= a.passes[pi + 1].unit0) ++pi;
+      while (pi > 0 && u < a.passes[pi].unit0) --pi;
+      ul = u - a.passes[pi].unit0;
+    }
+    const CPass* __restrict__ P = a.passes + pi;
+    const int nCG = P->nCG, igs = P->igs;
+    const int64_t n_grp = P->nI / igs;
+    const int cg = P->cmaj ? (int)(ul / n_grp) : (int)(ul % nCG);
+    const int64_t i0 = (P->cmaj ? ul % n_grp : ul / nCG) * igs;
+    const int nK = P->nK, nG = P->nG, nE = P->nE;
+    const int tw = nG + nE + 1;
+    const int32_t* __restrict__ tir = a.tab + P->ti_off + i0 * tw;  // member q: + q * tw
+    const int32_t* __restrict__ tk = a.tab + P->tk_off;
+    const int32_t* __restrict__ ts = a.tab + P->ts_off;
+    const T* gq[CMAXG];
+    int gs[CMAXG];
+#pragma unroll
+    for (int g = 0; g < CMAXG; ++g) {
+      gq[g] = aux_c + (g < nG ? P->gfac_off[g] + __ldg(tir + g) : 0);
+      gs[g] = g < nG ? P->gstride[g] : 0;
+    }
+    const T* __restrict__ wrow = W + P->w_off + i0 * (int64_t)nK;  // member q: + q * nK
+    const int bstep = 32 * VEC * nCG;
+    for (int b0 = cg * 32 * VEC + lane * VEC; b0 < a.B; b0 += bstep) {
+      double acc[IGM][VEC];
+      T part[IGM][VEC];
+#pragma unroll
+      for (int q = 0; q < IGM; ++q)
+#pragma unroll
+        for (int l = 0; l < VEC; ++l) {
+          acc[q][l] = 0.0;
+          part[q][l] = (T)0;
+        }
+      int since = 0;
+      for (int k = 0; k < nK; ++k) {
+        T ps[VEC];  // product of the shared factor rows
+#pragma unroll
+        for (int l = 0; l < VEC; ++l) ps[l] = (T)1;
+#pragma unroll
+        for (int g = 0; g < CMAXG; ++g) {
+          if (g < nG && gs[g] == 0) {
+            T f[VEC];
+            load_vec_ro<T, VEC>(gq[g] + b0 + __ldg(tk + k * nG + g), f);
+#pragma unroll
+            for (int l = 0; l < VEC; ++l) ps[l] *= f[l];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < IGM; ++q) {
+          if (q < igs) {
+            T pv[VEC];
+#pragma unroll
+            for (int l = 0; l < VEC; ++l) pv[l] = ps[l];
+#pragma unroll
+            for (int g = 0; g < CMAXG; ++g) {
+              if (g < nG && gs[g] != 0) {
+                T f[VEC];
+                load_vec_ro<T, VEC>(gq[g] + (int64_t)q * gs[g] + b0 + __ldg(tk + k * nG + g), f);
+#pragma unroll
+                for (int l = 0; l < VEC; ++l) pv[l] *= f[l];
+              }
+            }
+            const T w = __ldg(wrow + (int64_t)q * nK + k);
+#pragma unroll
+            for (int l = 0; l < VEC; ++l) part[q][l] += w * pv[l];
+          }
+        }
+        if (FOLD && ++since == KF) {
+#pragma unroll
+          for (int q = 0; q < IGM; ++q)
+#pragma unroll
+            for (int l = 0; l < VEC; ++l) {
+              acc[q][l] += (double)part[q][l];
+              part[q][l] = (T)0;
+            }
+          since = 0;
+        }
+      }
+      bool bad = false;
+#pragma unroll
+      for (int q = 0; q < IGM; ++q) {
+        if (q >= igs) continue;
+        const int32_t* tq = tir + (int64_t)q * tw;
+        double v[VEC];
+#pragma unroll
+        for (int l = 0; l < VEC; ++l) v[l] = acc[q][l] + (double)part[q][l];
+        for (int e = 0; e < nE; ++e) {
+          T f[VEC];
+          load_vec_ro<T, VEC>(aux_c + P->efac_off[e] + __ldg(tq + nG + e) + __ldg(ts + e) + b0, f);
+#pragma unroll
+          for (int l = 0; l < VEC; ++l) v[l] *= (double)f[l];
+        }
+        const int64_t j = (int64_t)__ldg(tq + nG + nE) + __ldg(ts + nE) + b0;
+        T old[VEC] = {};
+        if (P->out_kind == OUT_SEP || P->out_kind == OUT_SEP_DFRESH) load_vec<T, VEC>(aux_c + P->out_off + j, old);
+        bad |= finalize_lanes<T, double, VEC>(P->out_kind, P->out_off, P->ratio_off, P->out2_off, j, v, old, aux,
+                                              a.qout);
+      }
+      if (bad) atomicOr(a.err, EB_INCONSISTENT);
+    }
+  }
+}
+
 template <typename T, bool FOLD, int NG>
 static size_t contract_smem() {
   return (FOLD ? CFOLD_SMEM : 0) + CRing<T, NG, FOLD>::BYTES;
@@ -1500,6 +1635,17 @@ static auto by_ng(int ng, F f) {
 
 cudaError_t launch_contract(int dtype, int fold, int rowi, int ng, const CArgs& a, int grid, cudaStream_t s) {
   if (grid <= 0 || a.n_units <= 0) return cudaSuccess;
+  if (rowi >= 2) {  // i-groups: IGM 4 (rowi 2) or 8 (rowi 3)
+    if (dtype == 0) {
+      if (fold)
+        return rowi == 2 ? launch_pdl(contract_rowg_kernel<float, true, 4>, grid, NT, 0, s, a)
+                         : launch_pdl(contract_rowg_kernel<float, true, 8>, grid, NT, 0, s, a);
+      return rowi == 2 ? launch_pdl(contract_rowg_kernel<float, false, 4>, grid, NT, 0, s, a)
+                       : launch_pdl(contract_rowg_kernel<float, false, 8>, grid, NT, 0, s, a);
+    }
+    return rowi == 2 ? launch_pdl(contract_rowg_kernel<double, false, 4>, grid, NT, 0, s, a)
+                     : launch_pdl(contract_rowg_kernel<double, false, 8>, grid, NT, 0, s, a);
+  }
   if (rowi) {
     if (dtype == 0)
       return fold ? launch_pdl(contract_rowi_kernel<float, true>, grid, NT, 0, s, a)
@@ -1515,6 +1661,18 @@ cudaError_t launch_contract(int dtype, int fold, int rowi, int ng, const CArgs& 
 
 int contract_max_ctas_per_sm(int dtype, int fold, int rowi, int ng) {
   int n = 0;
+  if (rowi >= 2) {
+    if (dtype == 0 && fold)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rowi == 2 ? contract_rowg_kernel<float, true, 4>
+                                                                  : contract_rowg_kernel<float, true, 8>, NT, 0);
+    else if (dtype == 0)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rowi == 2 ? contract_rowg_kernel<float, false, 4>
+                                                                  : contract_rowg_kernel<float, false, 8>, NT, 0);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rowi == 2 ? contract_rowg_kernel<double, false, 4>
+                                                                  : contract_rowg_kernel<double, false, 8>, NT, 0);
+    return n > 0 ? n : 1;
+  }
   if (rowi) {
     if (dtype == 0 && fold) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_rowi_kernel<float, true>, NT, 0);
     else if (dtype == 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_rowi_kernel<float, false>, NT, 0);

@@ -1,0 +1,211 @@
+// Persistent single-launch propagation for small single trees (sm_100a).
+//
+// Small junction trees (c1 12 cliques, c2 368, c4M 870) are
+// latency-bound: every wave moves a few KB to a few MB and the cost is the
+// chain of dependent steps, not bandwidth.  Here the whole collect+distribute
+// program is ONE cooperative launch; its waves are separated by a grid barrier
+// and every pass is a "tiny pass" (jt_internal.h): one thread per separator
+// entry walks the entry's row of the clique (Alg. 1 step 1, the row sum of
+// _pass_block, propagate.py:67) multiplying the pass's factors in on the fly
+// (children's ratios, parent ratio), writes the clique back when the pass owns
+// the write (propagate.py:74-75), and applies the Hugin update to its entry
+// (ratio = new/old, 0/0 = 0, nonzero/0 flagged; propagate.py:68-76).  Rows of
+// 96 or more entries are split over a warp (lane chunks in order + shuffle
+// tree: deterministic).  Every offset is stride arithmetic over merged
+// mixed-radix dims (potential.py:42-63) -- no index maps, no block tables.
+#include "jt_internal.h"
+
+namespace jt {
+
+__device__ __forceinline__ unsigned tiny_ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Grid-wide barrier: arrive counter + generation word; the last CTA to arrive
+// resets the counter and bumps the generation.  The fences order every table
+// write of a wave before any read of the next (all loads below are coherent:
+// tables change between the waves of the launch).
+__device__ __forceinline__ void tiny_grid_barrier(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned gen = tiny_ld_acquire(bar + 1);
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (tiny_ld_acquire(bar + 1) == gen) __nanosleep(8);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <typename T>
+__device__ __forceinline__ void tiny_finalize(const TPass& P, int64_t j, double star, T* aux, double* qout, int* err) {
+  if (P.out_kind == OUT_SEP_FRESH) {
+    aux[P.out_off + j] = (T)star;
+  } else if (P.out_kind == OUT_SEP_DFRESH) {
+    const double c = (double)aux[P.out_off + j];
+    aux[P.ratio_off + j] = (T)(c != 0.0 ? star : 0.0);
+    aux[(P.out2_off >= 0 ? P.out2_off : P.out_off) + j] = (T)(c * star);
+  } else if (P.out_kind == OUT_SEP) {
+    const double old = (double)aux[P.out_off + j];
+    if (old == 0.0 && star != 0.0) atomicOr(err, EB_INCONSISTENT);
+    aux[P.ratio_off + j] = (T)((old != 0.0) ? star / old : 0.0);
+    aux[(P.out2_off >= 0 ? P.out2_off : P.out_off) + j] = (T)star;
+  } else if (P.out_kind == OUT_RAW) {
+    qout[P.out_off + j] = star;
+  }
+}
+
+// Sum (and optionally write) positions [r0, r1) of output entry j's row.
+template <typename T>
+__device__ __forceinline__ double tiny_row(const TPass& P, const T* __restrict__ src, T* __restrict__ dst,
+                                           const T* __restrict__ aux, int64_t j, int64_t r0, int64_t r1,
+                                           int64_t* out_j) {
+  const int nf = P.nf;
+  // output entry digits -> base offsets
+  int64_t so = 0, dd = 0, oo = 0;
+  int64_t fo[MAXF];
+#pragma unroll
+  for (int f = 0; f < MAXF; ++f) fo[f] = 0;
+  {
+    int64_t x = j;
+    for (int d = P.nod - 1; d >= 0; --d) {
+      const int c = P.ocard[d];
+      const int64_t dig = x % c;
+      x /= c;
+      so += dig * P.osrc[d];
+      dd += dig * P.odst[d];
+      oo += dig * P.oout[d];
+#pragma unroll
+      for (int f = 0; f < MAXF; ++f)
+        if (f < nf) fo[f] += dig * P.ofac[f][d];
+    }
+  }
+  *out_j = oo;
+  if (r0 >= r1) return 0.0;
+  // row start digits (odometer state)
+  int dig[TD];
+  {
+    int64_t x = r0;
+    for (int d = P.nrd - 1; d >= 0; --d) {
+      const int c = P.rcard[d];
+      dig[d] = (int)(x % c);
+      x /= c;
+      so += (int64_t)dig[d] * P.rsrc[d];
+      dd += (int64_t)dig[d] * P.rdst[d];
+#pragma unroll
+      for (int f = 0; f < MAXF; ++f)
+        if (f < nf) fo[f] += (int64_t)dig[d] * P.rfac[f][d];
+    }
+  }
+  const bool wr = P.dst_off >= 0;
+  double acc = 0.0;
+  for (int64_t r = r0; r < r1; ++r) {
+    T v = src[so];
+#pragma unroll
+    for (int f = 0; f < MAXF; ++f)
+      if (f < nf) v *= reinterpret_cast<const T*>(aux)[P.fac_off[f] + fo[f]];
+    if (wr) dst[dd] = v;
+    acc += (double)v;
+    // odometer step over the row dims (last fastest)
+    for (int d = P.nrd - 1; d >= 0; --d) {
+      so += P.rsrc[d];
+      dd += P.rdst[d];
+#pragma unroll
+      for (int f = 0; f < MAXF; ++f)
+        if (f < nf) fo[f] += P.rfac[f][d];
+      if (++dig[d] < P.rcard[d]) break;
+      const int c = P.rcard[d];
+      so -= (int64_t)c * P.rsrc[d];
+      dd -= (int64_t)c * P.rdst[d];
+#pragma unroll
+      for (int f = 0; f < MAXF; ++f)
+        if (f < nf) fo[f] -= (int64_t)c * P.rfac[f][d];
+      dig[d] = 0;
+    }
+  }
+  return acc;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(NT) tiny_persist_kernel(const TinyArgs a) {
+  T* __restrict__ clique = reinterpret_cast<T*>(a.clique);
+  const T* __restrict__ base = reinterpret_cast<const T*>(a.base);
+  T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
+  const int64_t stride = (int64_t)gridDim.x * NT;
+  const int lane = threadIdx.x & 31;
+  for (int w = 0; w < a.n_waves; ++w) {
+    const TinyWave tw = a.waves[w];
+    const TPass* __restrict__ ps = a.passes + tw.pass0;
+    int p = 0;
+    for (int64_t t = (int64_t)blockIdx.x * NT + threadIdx.x; t < tw.n_threads; t += stride) {
+      // pass of thread t: last pass with unit0 <= t (t only grows: walk forward)
+      while (p + 1 < tw.n_passes && ps[p + 1].unit0 <= t) ++p;
+      if (p > 0 && ps[p].unit0 > t) {  // new grid-stride round never goes back, but be safe
+        int lo = 0, hi = p;
+        while (lo < hi) {
+          const int m = (lo + hi + 1) / 2;
+          if (ps[m].unit0 <= t) lo = m;
+          else hi = m - 1;
+        }
+        p = lo;
+      }
+      const TPass& P = ps[p];
+      const int64_t u = t - P.unit0;
+      const T* src = (P.src_arena == A_BASE ? base : P.src_arena == A_AUX ? aux : clique) + P.src_off;
+      T* dst = clique + (P.dst_off >= 0 ? P.dst_off : 0);
+      if (!P.warp) {
+        if (u >= P.n_out) continue;
+        int64_t oj;
+        const double s = tiny_row<T>(P, src, dst, aux, u, 0, P.n_rest, &oj);
+        if (P.out_kind != OUT_NONE) tiny_finalize<T>(P, oj, s, aux, a.qout, a.err);
+      } else {
+        // one warp per entry: lane chunks of the row in lane order, shuffle tree
+        const int64_t j = u >> 5;
+        const int64_t per = (P.n_rest + 31) / 32;
+        const int64_t r0 = (int64_t)lane * per;
+        const int64_t r1 = r0 + per < P.n_rest ? r0 + per : P.n_rest;
+        int64_t oj;
+        double s = tiny_row<T>(P, src, dst, aux, j, r0, r1, &oj);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0 && P.out_kind != OUT_NONE) tiny_finalize<T>(P, oj, s, aux, a.qout, a.err);
+      }
+    }
+    if (w + 1 < a.n_waves) tiny_grid_barrier(a.bar);
+  }
+}
+
+template <typename T>
+static cudaError_t launch_tiny_t(const TinyArgs& a, int grid, cudaStream_t s, int* occ_out) {
+  auto k = tiny_persist_kernel<T>;
+  if (occ_out) {
+    int n = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, NT, 0);
+    *occ_out = n > 0 ? n : 1;
+    return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, a);
+}
+
+cudaError_t launch_tiny(int dtype, const TinyArgs& a, int grid, cudaStream_t s, int* occ_out) {
+  return dtype == 0 ? launch_tiny_t<float>(a, grid, s, occ_out) : launch_tiny_t<double>(a, grid, s, occ_out);
+}
+
+}  // namespace jt
