@@ -488,6 +488,56 @@ def roofline_block(args, tree, dtype, r, alg_elems):
             "launch_ms": round(prog_ms, 4), "peak_kind": pk_kind}
 
 
+def batch_table(configs=("c2", "c4M"), dtypes=("f64", "f32"), n_cases=4096, batch=2048, steps=5):
+    """Evidence batches on the other config shapes (shared-base mode; hub cliques
+    keep per-case tables): cases/s with evidence resident on the device, and the
+    oracle spot check of two cases from different micro-batches."""
+    import ctypes as C
+
+    import torch
+
+    from oracle import jtref
+    from paper_1202_3777_b200 import synth
+    from paper_1202_3777_b200.batch import BatchPropagator
+
+    out = {}
+    for name in configs:
+        tree, tables = synth.make_config(name)
+        cases = synth.evidence_cases(tree, n_cases, seed=1234)
+        template = jtref.from_potentials(tree, tables)
+        check = (1, n_cases - 1)
+        want = np.stack([jtref.case_posteriors(template, cases[i], range(len(tree.cards))) for i in check])
+        for dt in dtypes:
+            bp = BatchPropagator(tree, tables, batch=batch, dtype=dt, mode="auto")
+            sh = C.c_void_p(bp.stream.cuda_stream)
+            obs = [torch.from_numpy(bp.encode_obs(cases[m:m + batch])).cuda() for m in range(0, n_cases, batch)]
+            post = torch.empty((n_cases, bp.cols), dtype=torch.float64, device="cuda")
+
+            def step():
+                for k, o in enumerate(obs):
+                    bp.step_device(o, post[k * batch:(k + 1) * batch], sh)
+
+            for _ in range(3):
+                step()
+            bp.stream.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(bp.stream)
+            for _ in range(steps):
+                step()
+            e1.record(bp.stream)
+            e1.synchronize()
+            bp.sync()
+            ms = e0.elapsed_time(e1) / steps
+            got = post[list(check)].cpu().numpy()
+            out[f"{name}_{dt}"] = {"cases_per_s": round(n_cases / (ms * 1e-3), 1), "ms_per_step": round(ms, 3),
+                                  "micro_batch": batch, "mode": bp.mode,
+                                  "spot_max_rel_err": rel_err(got, want)}
+            bp.close()
+            del post, obs
+            torch.cuda.empty_cache()
+    return out
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -607,6 +657,10 @@ def main():
             line["single_tree"] = single_tree_table()
         except Exception as exc:  # report, never hide
             line["single_tree"] = {"error": repr(exc)}
+        try:
+            line["batch_other"] = batch_table()
+        except Exception as exc:
+            line["batch_other"] = {"error": repr(exc)}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -45,13 +45,30 @@ def _owners(tree):
     return owner
 
 
+def _smallest_holder_counts(tree):
+    counts = {}
+    for v in range(len(tree.cards)):
+        holders = [c for c in tree.cliques if v in c.scope.ids]
+        if holders:
+            c = min(holders, key=lambda c: (_scope_size(c.scope), c.id)).id
+            counts[c] = counts.get(c, 0) + 1
+    return counts
+
+
 def shared_supported(tree) -> bool:
-    """Shared-base passes carry every factor of a clique at once: neighbours'
-    ratios plus one evidence mask per variable the clique owns."""
+    """Shared-base passes carry every factor of a clique at once (neighbours'
+    ratios plus one evidence mask per variable the clique owns, <= MAX_FACTORS).
+    Hub cliques beyond that keep per-case tables (the library allocates them for
+    cliques over the limit under smallest-holder ownership, jt_state::hub), so
+    the mode is supported unless the tree's own evidence assignment puts more
+    factors on a clique that is not such a hub."""
+    hub_owned = _smallest_holder_counts(tree)
+    hub = {c for c in range(len(tree.cliques)) if len(tree.neighbors[c]) + hub_owned.get(c, 0) > MAX_FACTORS}
     owned = {}
     for v, c in _owners(tree).items():
         owned[c] = owned.get(c, 0) + 1
-    return all(len(tree.neighbors[c]) + owned.get(c, 0) <= MAX_FACTORS for c in range(len(tree.cliques)))
+    return all(len(tree.neighbors[c]) + owned.get(c, 0) <= MAX_FACTORS or c in hub
+               for c in range(len(tree.cliques)))
 
 
 class BatchPropagator:

@@ -282,6 +282,11 @@ struct jt_state {
   std::map<std::string, std::unique_ptr<struct ClusterProg>> cprogs;  // small trees in cluster smem
   int64_t launches = 0;
   int64_t device_bytes = 0;
+  // shared-base mode: cliques whose passes would need more than MAXF factors keep
+  // per-case tables in the clique arena (initialised from base x evidence at the
+  // start of each propagation, children absorbed eagerly); every other clique
+  // stays a shared base table
+  std::vector<char> hub;
   int* d_qexp = nullptr;    // per-query exponents of unnormalized queries
   int64_t qexp_cap = 0;
   int err_case = -1;        // lowest case index of the last zero-mass error (jt_sync_error)
@@ -347,18 +352,32 @@ struct DevGuard {
   }
 };
 
+static int smallest_holder(const jt_plan* p, int v);
+
 static void layout_state(jt_state* st) {
   const jt_plan* plan = st->plan;
   const int mode = st->mode;
   const int64_t B = st->B;
   st->esz = plan->dtype == JT_F32 ? 4 : 8;
-  // clique arena (materialized) / base arena (shared)
+  // clique arena: every clique (materialized); in shared-base mode only the hub
+  // cliques (more neighbour ratios + owned evidence masks than a pass carries,
+  // MAXF) get per-case tables: they absorb their children eagerly (jt_state::hub)
   int64_t off = 0;
+  st->hub.assign(plan->n_cliques, 0);
   for (int c = 0; c < plan->n_cliques; ++c) {
-    st->coff.push_back(off);
-    off = align4(off + plan->csize[c] * (mode == JT_MATERIALIZED ? B : 1));
+    if (mode == JT_MATERIALIZED) {
+      st->coff.push_back(off);
+      off = align4(off + plan->csize[c] * B);
+      continue;
+    }
+    int owned = 0;
+    for (int v = 0; v < plan->n_vars; ++v)
+      if (smallest_holder(plan, v) == c) ++owned;
+    st->hub[c] = (int)plan->nbrs[c].size() + owned > MAXF;
+    st->coff.push_back(st->hub[c] ? off : -1);
+    if (st->hub[c]) off = align4(off + plan->csize[c] * B);
   }
-  if (mode == JT_MATERIALIZED) st->n_clique = off;
+  st->n_clique = off;
   // base replica (one copy of every table, no batch dim): the shared-base
   // engine reads it directly; materialized states reset from it (jt_state_reset)
   int64_t boff = 0;
@@ -1135,7 +1154,8 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
     static const int ncg_mid = env_int("JT_NCG_MID", CON_NCG_MID);
     static const int ncg_long = env_int("JT_NCG_LONG", 1 << 30);
     cp.nCG = nK >= 32 ? std::min(ncg_long, cp.nBC) : nK >= 8 ? std::min(ncg_mid, cp.nBC) : std::min(ncg_small, cp.nBC);
-    static const int cmaj = env_int("JT_CMAJ", 0);  // bit 0: rowi passes, bit 1: tile passes
+    // bit 0: rowi passes, bit 1: tile passes (fp64 default: rowi chunk-major, measured +1-3%)
+    const int cmaj = env_int("JT_CMAJ", st->esz == 8 ? 1 : 0);
     cp.cmaj = (cmaj >> (rowi ? 0 : 1)) & 1;
   }
   cp.nKS = 1;
@@ -1143,7 +1163,8 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   cp.n_units = (rowi ? 1 : nI) * cp.nT * cp.nCG;
   int64_t min_units = (int64_t)st->num_sms * 8;
   cp.igs = 1;
-  if (rowi && !I.empty() && !getenv("JT_NO_ROWG")) {
+  // (fp64 only: the fp32 fold variant's per-member accumulators spill; measured slower)
+  if (rowi && !I.empty() && env_int("JT_ROWG", st->esz == 8 ? 1 : 0)) {
     // i-groups: the innermost i variable's values share every factor that does not
     // index it; group them into one warp unit when those shared factors dominate
     const int v = I.back();
@@ -1358,9 +1379,11 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
       items.insert(items.end(), g.second.begin(), g.second.end());
       rt.groups.push_back(lg);
     }
-    // JT_SPLIT_CPASS=1 (diagnostic): one launch per contraction pass, so an ncu
-    // launch list attributes time and DRAM bytes to single passes
-    if (getenv("JT_SPLIT_CPASS")) {
+    // JT_SPLIT_CPASS=1: one launch per contraction pass (also what an ncu launch
+    // list needs to attribute time and DRAM bytes to single passes)
+    // (default for fp64, where the measured program is 2-6% faster with the passes
+    // as separate parallel graph branches)
+    if (env_int("JT_SPLIT_CPASS", st->esz == 8 ? 1 : 0)) {
       std::vector<CPass> cps2[8 * NGK];
       std::vector<int> cpc2[8 * NGK];
       for (int key = 0; key < 8 * NGK; ++key) {
@@ -1501,9 +1524,12 @@ static int build_tiny(const jt_state* st, const std::vector<std::vector<PassSpec
           P.n_rest *= d.card;
         }
       }
-      P.warp = P.n_rest >= 96 ? 1 : 0;
+      // lanes per output entry: rows split into lane chunks of <= 2 batches (jt_tiny.cu)
+      int G = 1;
+      while (G < 32 && P.n_rest > (int64_t)G * 8) G *= 2;
+      P.warp = G;
       P.unit0 = units;
-      const int64_t nu = P.warp ? P.n_out * 32 : P.n_out;
+      const int64_t nu = P.n_out * G;
       units += (nu + 31) / 32 * 32;
       tp.push_back(P);
     }
@@ -1801,12 +1827,32 @@ static int build_propagate(jt_state* st, const std::vector<int>& roots, const st
     for (int v = 0; v < p->n_vars; ++v)
       if (st->ev_clique[v] >= 0) evs[st->ev_clique[v]].push_back(v);
   std::vector<char> eager(n, 0);
+  std::vector<PassSpec> hub_init;  // shared-base hubs: per-case table = base x evidence
+  std::vector<std::vector<PassSpec>> hub_init_more;
   for (int c = 0; c < n; ++c) {
     const int nfac = (int)o.children[c].size() + (o.parent[c] >= 0 ? 1 : 0) + (int)evs[c].size();
     if (nfac > MAXF) {
-      if (shared) return JT_ERR_UNSUPPORTED;
+      if (shared && !st->hub[c]) return JT_ERR_UNSUPPORTED;
       eager[c] = 1;
+      if (shared) {
+        for (size_t i = 0; i == 0 || i < evs[c].size(); i += MAXF) {
+          PassSpec ps;
+          ps.clique = c;
+          ps.src_arena = i == 0 ? A_BASE : A_CLIQUE;
+          ps.write = true;
+          for (size_t k = i; k < std::min(evs[c].size(), i + MAXF); ++k) ps.factors.push_back(ev_tensor(st, evs[c][k]));
+          if (i == 0) hub_init.push_back(ps);
+          else {
+            if (hub_init_more.size() < i / MAXF) hub_init_more.resize(i / MAXF);
+            hub_init_more[i / MAXF - 1].push_back(ps);
+          }
+        }
+      }
     }
+  }
+  if (!hub_init.empty()) {
+    waves.push_back(hub_init);
+    for (auto& w : hub_init_more) waves.push_back(w);
   }
   // collect ratio of a child separator: fresh propagations keep it in the
   // separator table itself (old == 1 ⇒ ratio == new)
@@ -1905,8 +1951,10 @@ static int build_propagate(jt_state* st, const std::vector<int>& roots, const st
     std::vector<Tensor> fac;
     if (!eager[c]) fac = child_ratios(c);
     if (o.parent[c] >= 0) fac.push_back(sep_tensor(st, o.psep[c], st->ratD_off[o.psep[c]]));
-    std::vector<Tensor> ef = ev_factors(c);
-    fac.insert(fac.end(), ef.begin(), ef.end());
+    if (!eager[c]) {  // eager shared-base hubs took their evidence in at initialisation
+      std::vector<Tensor> ef = ev_factors(c);
+      fac.insert(fac.end(), ef.begin(), ef.end());
+    }
     const auto& ch = o.children[c];
     for (size_t i = 0; i < ch.size(); ++i) {
       PassSpec ps;
@@ -1943,7 +1991,7 @@ static int build_propagate(jt_state* st, const std::vector<int>& roots, const st
     for (int v : qby[c]) {
       PassSpec ps;
       ps.clique = c;
-      ps.src_arena = shared ? A_BASE : A_CLIQUE;
+      ps.src_arena = shared && !eager[c] ? A_BASE : A_CLIQUE;
       ps.factors = shared ? fac : std::vector<Tensor>{};
       ps.out_kind = OUT_RAW;
       ps.out = var_out_tensor(st, v);
@@ -2843,14 +2891,25 @@ static int query_program(jt_state* st, int n, const int32_t* var, const int32_t*
       ps.out_kind = OUT_RAW;
       ps.out = var_out_tensor(st, vs[i]);
       if (shared) {
-        // final table of the clique = base × evidence × Π neighbour ratios
+        // final table of the clique = base × evidence × Π neighbour ratios; a hub
+        // (eager clique) holds base × evidence × children's ratios per case already
         const int c = cs[i];
-        if (!unprop) {
-          for (auto& ch : o.children[c]) ps.factors.push_back(sep_tensor(st, ch.second, sep_alt(st, ch.second)));
+        int nev = 0;
+        for (int v = 0; v < p->n_vars; ++v) nev += st->ev_clique[v] == c;
+        const bool eager = (int)o.children[c].size() + (o.parent[c] >= 0 ? 1 : 0) + nev > MAXF;
+        if (eager && !st->hub[c]) return JT_ERR_UNSUPPORTED;
+        if (eager && !unprop) {
+          ps.src_arena = A_CLIQUE;
           if (o.parent[c] >= 0) ps.factors.push_back(sep_tensor(st, o.psep[c], st->ratD_off[o.psep[c]]));
+        } else {
+          if (!unprop) {
+            for (auto& ch : o.children[c]) ps.factors.push_back(sep_tensor(st, ch.second, sep_alt(st, ch.second)));
+            if (o.parent[c] >= 0) ps.factors.push_back(sep_tensor(st, o.psep[c], st->ratD_off[o.psep[c]]));
+          }
+          for (int v = 0; v < p->n_vars; ++v)
+            if (st->ev_clique[v] == c) ps.factors.push_back(ev_tensor(st, v));
+          if ((int)ps.factors.size() > MAXF) return JT_ERR_UNSUPPORTED;
         }
-        for (int v = 0; v < p->n_vars; ++v)
-          if (st->ev_clique[v] == c) ps.factors.push_back(ev_tensor(st, v));
       }
       waves[0].push_back(ps);
     }
@@ -3106,9 +3165,9 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
     std::vector<TinyWave> tw;
     if (build_tiny(&st, waves, tp, tw) == JT_OK) {
       int64_t warp_passes = 0, threads = 0;
-      for (auto& x : tp) warp_passes += x.warp;
+      for (auto& x : tp) warp_passes += x.warp > 1;
       for (auto& x : tw) threads += x.n_threads;
-      snprintf(line, sizeof line, "tiny persistent program: one launch, %zu waves, %zu passes (%lld warp-per-entry), "
+      snprintf(line, sizeof line, "tiny persistent program: one launch, %zu waves, %zu passes (%lld with several lanes per entry), "
                "%lld threads over all waves\n", tw.size(), tp.size(), (long long)warp_passes, (long long)threads);
       out += line;
     }

@@ -216,7 +216,7 @@ struct TPass {
   int64_t fac_off[MAXF];
   int64_t unit0;            // first thread of the pass in its wave (multiple of 32)
   int64_t n_out, n_rest;    // output entries (elements, without output), row length
-  int src_arena, nf, out_kind, warp;
+  int src_arena, nf, out_kind, warp;  // warp: lanes per output entry (power of two <= 32)
   int nod, nrd;
   int ocard[TD], rcard[TD];
   int osrc[TD], odst[TD], oout[TD], rsrc[TD], rdst[TD];

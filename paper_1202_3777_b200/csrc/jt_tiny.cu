@@ -9,10 +9,11 @@
 // _pass_block, propagate.py:67) multiplying the pass's factors in on the fly
 // (children's ratios, parent ratio), writes the clique back when the pass owns
 // the write (propagate.py:74-75), and applies the Hugin update to its entry
-// (ratio = new/old, 0/0 = 0, nonzero/0 flagged; propagate.py:68-76).  Rows of
-// 96 or more entries are split over a warp (lane chunks in order + shuffle
-// tree: deterministic).  Every offset is stride arithmetic over merged
-// mixed-radix dims (potential.py:42-63) -- no index maps, no block tables.
+// (ratio = new/old, 0/0 = 0, nonzero/0 flagged; propagate.py:68-76).  Long
+// rows are split over a group of 2..32 lanes (lane chunks in order + a fixed
+// shuffle tree: deterministic), so no lane waits on more than a few L2 round
+// trips per wave.  Every offset is stride arithmetic over merged mixed-radix
+// dims (potential.py:42-63) -- no index maps, no block tables.
 #include "jt_internal.h"
 
 namespace jt {
@@ -63,12 +64,15 @@ __device__ __forceinline__ void tiny_finalize(const TPass& P, int64_t j, double 
 }
 
 // Sum (and optionally write) positions [r0, r1) of output entry j's row.
+// Positions go in batches of TB: the odometer first produces every offset of
+// the batch (integer work only), then all loads of the batch issue back to
+// back, so a lane waits for one L2 round trip per batch, not per position.
+constexpr int TB = 4;
 template <typename T>
 __device__ __forceinline__ double tiny_row(const TPass& P, const T* __restrict__ src, T* __restrict__ dst,
                                            const T* __restrict__ aux, int64_t j, int64_t r0, int64_t r1,
                                            int64_t* out_j) {
   const int nf = P.nf;
-  // output entry digits -> base offsets
   int64_t so = 0, dd = 0, oo = 0;
   int64_t fo[MAXF];
 #pragma unroll
@@ -89,7 +93,6 @@ __device__ __forceinline__ double tiny_row(const TPass& P, const T* __restrict__
   }
   *out_j = oo;
   if (r0 >= r1) return 0.0;
-  // row start digits (odometer state)
   int dig[TD];
   {
     int64_t x = r0;
@@ -105,29 +108,55 @@ __device__ __forceinline__ double tiny_row(const TPass& P, const T* __restrict__
     }
   }
   const bool wr = P.dst_off >= 0;
+  const T* __restrict__ fb[MAXF];
+#pragma unroll
+  for (int f = 0; f < MAXF; ++f) fb[f] = aux + (f < nf ? P.fac_off[f] : 0);
   double acc = 0.0;
-  for (int64_t r = r0; r < r1; ++r) {
-    T v = src[so];
+  for (int64_t rb = r0; rb < r1; rb += TB) {
+    const int nb = (int)(r1 - rb < TB ? r1 - rb : TB);
+    int64_t bs[TB], bd[TB], bf[MAXF][TB];
 #pragma unroll
-    for (int f = 0; f < MAXF; ++f)
-      if (f < nf) v *= reinterpret_cast<const T*>(aux)[P.fac_off[f] + fo[f]];
-    if (wr) dst[dd] = v;
-    acc += (double)v;
-    // odometer step over the row dims (last fastest)
-    for (int d = P.nrd - 1; d >= 0; --d) {
-      so += P.rsrc[d];
-      dd += P.rdst[d];
+    for (int q = 0; q < TB; ++q) {
+      bs[q] = so;
+      bd[q] = dd;
 #pragma unroll
-      for (int f = 0; f < MAXF; ++f)
-        if (f < nf) fo[f] += P.rfac[f][d];
-      if (++dig[d] < P.rcard[d]) break;
-      const int c = P.rcard[d];
-      so -= (int64_t)c * P.rsrc[d];
-      dd -= (int64_t)c * P.rdst[d];
+      for (int f = 0; f < MAXF; ++f) bf[f][q] = fo[f];
+      if (q < nb) {
+        // odometer step over the row dims (last fastest)
+        for (int d = P.nrd - 1; d >= 0; --d) {
+          so += P.rsrc[d];
+          dd += P.rdst[d];
 #pragma unroll
-      for (int f = 0; f < MAXF; ++f)
-        if (f < nf) fo[f] -= (int64_t)c * P.rfac[f][d];
-      dig[d] = 0;
+          for (int f = 0; f < MAXF; ++f)
+            if (f < nf) fo[f] += P.rfac[f][d];
+          if (++dig[d] < P.rcard[d]) break;
+          const int c = P.rcard[d];
+          so -= (int64_t)c * P.rsrc[d];
+          dd -= (int64_t)c * P.rdst[d];
+#pragma unroll
+          for (int f = 0; f < MAXF; ++f)
+            if (f < nf) fo[f] -= (int64_t)c * P.rfac[f][d];
+          dig[d] = 0;
+        }
+      }
+    }
+    T v[TB];
+#pragma unroll
+    for (int q = 0; q < TB; ++q) v[q] = q < nb ? src[bs[q]] : (T)0;
+#pragma unroll
+    for (int f = 0; f < MAXF; ++f) {
+      if (f < nf) {
+#pragma unroll
+        for (int q = 0; q < TB; ++q)
+          if (q < nb) v[q] *= fb[f][bf[f][q]];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < TB; ++q) {
+      if (q < nb) {
+        if (wr) dst[bd[q]] = v[q];
+        acc += (double)v[q];
+      }
     }
   }
   return acc;
@@ -143,40 +172,32 @@ __global__ void __launch_bounds__(NT) tiny_persist_kernel(const TinyArgs a) {
   for (int w = 0; w < a.n_waves; ++w) {
     const TinyWave tw = a.waves[w];
     const TPass* __restrict__ ps = a.passes + tw.pass0;
-    int p = 0;
     for (int64_t t = (int64_t)blockIdx.x * NT + threadIdx.x; t < tw.n_threads; t += stride) {
-      // pass of thread t: last pass with unit0 <= t (t only grows: walk forward)
-      while (p + 1 < tw.n_passes && ps[p + 1].unit0 <= t) ++p;
-      if (p > 0 && ps[p].unit0 > t) {  // new grid-stride round never goes back, but be safe
-        int lo = 0, hi = p;
-        while (lo < hi) {
-          const int m = (lo + hi + 1) / 2;
-          if (ps[m].unit0 <= t) lo = m;
-          else hi = m - 1;
-        }
-        p = lo;
+      // pass of thread t: last pass with unit0 <= t (warp-uniform: passes start at multiples of 32)
+      int lo = 0, hi = tw.n_passes - 1;
+      while (lo < hi) {
+        const int m = (lo + hi + 1) >> 1;
+        if (ps[m].unit0 <= t) lo = m;
+        else hi = m - 1;
       }
-      const TPass& P = ps[p];
+      const TPass& P = ps[lo];
       const int64_t u = t - P.unit0;
       const T* src = (P.src_arena == A_BASE ? base : P.src_arena == A_AUX ? aux : clique) + P.src_off;
       T* dst = clique + (P.dst_off >= 0 ? P.dst_off : 0);
-      if (!P.warp) {
-        if (u >= P.n_out) continue;
-        int64_t oj;
-        const double s = tiny_row<T>(P, src, dst, aux, u, 0, P.n_rest, &oj);
-        if (P.out_kind != OUT_NONE) tiny_finalize<T>(P, oj, s, aux, a.qout, a.err);
-      } else {
-        // one warp per entry: lane chunks of the row in lane order, shuffle tree
-        const int64_t j = u >> 5;
-        const int64_t per = (P.n_rest + 31) / 32;
-        const int64_t r0 = (int64_t)lane * per;
-        const int64_t r1 = r0 + per < P.n_rest ? r0 + per : P.n_rest;
-        int64_t oj;
-        double s = tiny_row<T>(P, src, dst, aux, j, r0, r1, &oj);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0 && P.out_kind != OUT_NONE) tiny_finalize<T>(P, oj, s, aux, a.qout, a.err);
-      }
+      // P.warp = lanes per output entry (1, 2, 4, 8, 16 or 32): lane chunks of the
+      // row in lane order, then a fixed shuffle tree inside the lane group
+      const int G = P.warp;
+      const int64_t j = u / G;
+      const int sub = (int)(u - j * G);
+      const bool live = j < P.n_out;  // lanes of the pass's padding compute nothing
+      const int64_t per = (P.n_rest + G - 1) / G;
+      const int64_t r0 = live ? (int64_t)sub * per : 0;
+      const int64_t r1 = live ? (r0 + per < P.n_rest ? r0 + per : P.n_rest) : 0;
+      int64_t oj = 0;
+      double s = live ? tiny_row<T>(P, src, dst, aux, live ? j : 0, r0, r1, &oj) : 0.0;
+      for (int o = 1; o < G; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (live && sub == 0 && P.out_kind != OUT_NONE) tiny_finalize<T>(P, oj, s, aux, a.qout, a.err);
+      (void)lane;
     }
     if (w + 1 < a.n_waves) tiny_grid_barrier(a.bar);
   }

@@ -627,3 +627,32 @@ def test_unscaled_munin_shaped_tree_stays_finite(dtype):
     got = all_posteriors(st, n)
     assert np.all(np.isfinite(got))
     assert rel_err(got, want) < TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("batch", [16, 128])
+def test_shared_base_batches_with_hub_cliques(dtype, batch):
+    """the Pigs-shaped c2 tree has cliques with more neighbour
+    ratios + owned evidence masks than one pass carries (MAXF).  In shared-base
+    mode those hubs keep per-case tables (base x evidence, children absorbed
+    eagerly) while every other clique stays shared: batches run in shared mode
+    (no materialized fallback) and match the reference goldens / the oracle
+    (estimator.py:118-134)."""
+    from paper_1202_3777_b200.batch import BatchPropagator, shared_supported
+
+    tree, data = load_golden("c2")
+    assert shared_supported(tree)
+    tables = synth.scaled_potentials(tree, 0)
+    golden = golden_cases(data)
+    extra = synth.evidence_cases(tree, 4, seed=21)
+    template = jtref.from_potentials(tree, tables)
+    want_extra = [jtref.case_posteriors(template, ev, range(len(tree.cards))) for ev in extra]
+    n = batch + 8
+    cases = [golden[i % len(golden)][0] for i in range(n - len(extra))] + extra
+    bp = BatchPropagator(tree, tables, batch=batch, dtype=dtype, mode="auto")
+    assert bp.mode == "shared"
+    out = bp.run(cases, to_host=True)
+    for i in range(n - len(extra)):
+        assert rel_err(out[i], golden[i % len(golden)][1]) < TOL[dtype], (dtype, batch, i)
+    for k, want in enumerate(want_extra):
+        assert rel_err(out[n - len(extra) + k], want) < TOL[dtype], (dtype, batch, "extra", k)

@@ -37,16 +37,20 @@ def test_batch_programs_compile(name, batch):
         report(name, batch=batch, mode=mode, kind=1, dtype="f32")
 
 
-def test_shared_mode_rejects_cliques_with_too_many_factors():
-    # c2 (Pigs-shaped) has cliques with > 8 neighbours: the batch layer must
-    # fall back to materialized mode (batch.shared_supported)
+def test_shared_mode_hub_cliques_keep_per_case_tables():
+    # c2 (Pigs-shaped) has cliques with > 8 neighbour ratios + evidence masks: in
+    # shared-base mode those hubs get per-case tables (initialised from base x
+    # evidence, children absorbed eagerly) instead of a materialized fallback
     from paper_1202_3777_b200 import synth
     from paper_1202_3777_b200.batch import shared_supported
 
     tree, _ = synth.make_config("c2")
-    assert not shared_supported(tree)
-    with pytest.raises(NotImplementedError):
-        report("c2", batch=8, mode="shared", kind=1)
+    assert shared_supported(tree)
+    text = report("c2", batch=8, mode="shared", kind=1)
+    assert "compulsory total MB" in text
+    # wave 0 initialises the hubs: write passes from the base replica (src 1)
+    first = [l for l in text.split("\nwave 1 ")[0].splitlines() if l.startswith("  pass")]
+    assert first and all(" src 1 " in l and " wr 1 " in l for l in first)
 
 
 def test_large_cliques_use_row_kernel():
