@@ -201,7 +201,7 @@ struct Program {
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t gstream = nullptr;
   // persistent single-launch program (small single trees, jt_tiny.cu)
-  int tiny = 0, tiny_grid = 0, n_twaves = 0;
+  int tiny = 0, tiny_grid = 0, n_twaves = 0, tiny_nfm = MAXF;
   TPass* d_tpass = nullptr;
   TinyWave* d_twaves = nullptr;
   unsigned* d_bar = nullptr;
@@ -1077,7 +1077,9 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   // nS == 1 uses the row-per-i kernel
   const bool rowi = nS == 1;
   const int64_t nSp = rowi ? 1 : (nS + 7) & ~int64_t(7);  // W rows padded: two 4-vector loads per k
-  const int64_t w0 = (int64_t)hp.w.size();
+  // every pass's W starts 64-byte aligned: the tile kernel loads W rows as
+  // 16-byte vectors, and a preceding row-per-i pass leaves an arbitrary length
+  const int64_t w0 = ((int64_t)hp.w.size() + 7) & ~int64_t(7);
   hp.w.resize(w0 + nI * nK * nSp, 0.0);
   {
     // per clique position: contribution to i, k, s' linear indices (R: none)
@@ -1472,6 +1474,14 @@ static bool tiny_choice(const jt_state* st, const std::vector<std::vector<PassSp
   return nw >= 3;
 }
 
+// q = (umulhi(n, mul) + n) >> shr == n / d for 0 <= n < 2^31 (round-up method)
+static void fast_div(int64_t d, unsigned& mul, int& shr) {
+  int l = 0;
+  while ((int64_t(1) << l) < d) ++l;
+  mul = (unsigned)(((uint64_t(1) << 32) * ((uint64_t(1) << l) - (uint64_t)d)) / (uint64_t)d + 1);
+  shr = l;
+}
+
 // Tiny passes of a program: per pass, the merged dims split into output dims
 // (those the output tensor indexes; every dim when there is no output) and row
 // dims; one thread per output entry, one warp when the row is long.
@@ -1509,6 +1519,7 @@ static int build_tiny(const jt_state* st, const std::vector<std::vector<PassSpec
           if (P.nod == TD) return JT_ERR_UNSUPPORTED;
           const int k = P.nod++;
           P.ocard[k] = (int)d.card;
+          fast_div(d.card, P.omul[k], P.oshr[k]);
           P.osrc[k] = (int)d.src;
           P.odst[k] = (int)d.dst;
           P.oout[k] = (int)d.out;
@@ -1518,6 +1529,7 @@ static int build_tiny(const jt_state* st, const std::vector<std::vector<PassSpec
           if (P.nrd == TD) return JT_ERR_UNSUPPORTED;
           const int k = P.nrd++;
           P.rcard[k] = (int)d.card;
+          fast_div(d.card, P.rmul[k], P.rshr[k]);
           P.rsrc[k] = (int)d.src;
           P.rdst[k] = (int)d.dst;
           for (int f = 0; f < nf; ++f) P.rfac[f][k] = (int)d.fac[f];
@@ -1525,6 +1537,7 @@ static int build_tiny(const jt_state* st, const std::vector<std::vector<PassSpec
         }
       }
       // lanes per output entry: rows split into lane chunks of <= 2 batches (jt_tiny.cu)
+      if (P.n_out * 32 > INT32_MAX || P.n_rest > INT32_MAX) return JT_ERR_UNSUPPORTED;
       int G = 1;
       while (G < 32 && P.n_rest > (int64_t)G * 8) G *= 2;
       P.warp = G;
@@ -1554,9 +1567,11 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
     std::vector<TPass> tp;
     std::vector<TinyWave> tw;
     if (build_tiny(st, waves, tp, tw) == JT_OK && !tw.empty()) {
-      int occ = 1;
+      int occ = 1, nfm = 1;
+      for (auto& x : tp) nfm = std::max(nfm, x.nf);
       TinyArgs dummy{};
-      CK(launch_tiny(st->plan->dtype, dummy, 0, nullptr, &occ));
+      CK(launch_tiny(st->plan->dtype, nfm, dummy, 0, nullptr, &occ));
+      prog->tiny_nfm = nfm;
       int64_t max_ctas = 1;
       for (auto& w : tw) max_ctas = std::max<int64_t>(max_ctas, (w.n_threads + NT - 1) / NT);
       prog->tiny = 1;
@@ -1703,7 +1718,7 @@ static int run_program(jt_state* st, Program* pr, cudaStream_t s) {
     a.waves = pr->d_twaves;
     a.n_waves = pr->n_twaves;
     a.bar = pr->d_bar;
-    CK(launch_tiny(st->plan->dtype, a, pr->tiny_grid, s));
+    CK(launch_tiny(st->plan->dtype, pr->tiny_nfm, a, pr->tiny_grid, s));
     st->launches++;
     return JT_OK;
   }

@@ -219,6 +219,8 @@ struct TPass {
   int src_arena, nf, out_kind, warp;  // warp: lanes per output entry (power of two <= 32)
   int nod, nrd;
   int ocard[TD], rcard[TD];
+  unsigned omul[TD], rmul[TD];  // fast division by the cards: q = (umulhi(n, mul) + n) >> shr
+  int oshr[TD], rshr[TD];
   int osrc[TD], odst[TD], oout[TD], rsrc[TD], rdst[TD];
   int ofac[MAXF][TD], rfac[MAXF][TD];
 };
@@ -239,7 +241,8 @@ struct TinyArgs {
   unsigned* bar;            // [counter, generation]
 };
 // occ_out != nullptr: only report the kernel's CTAs per SM
-cudaError_t launch_tiny(int dtype, const TinyArgs& a, int grid, cudaStream_t s, int* occ_out = nullptr);
+// nfm: factor count bound of the program's passes (2, 4 or 8; template of the kernel)
+cudaError_t launch_tiny(int dtype, int nfm, const TinyArgs& a, int grid, cudaStream_t s, int* occ_out = nullptr);
 int wave_max_ctas_per_sm(int dtype, int vec, int kv);
 cudaError_t launch_wave_row(int dtype, int vec, int lin, const WaveArgs& a, int grid, cudaStream_t s);
 int wave_row_max_ctas_per_sm(int dtype, int vec);

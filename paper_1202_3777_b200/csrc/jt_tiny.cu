@@ -63,31 +63,35 @@ __device__ __forceinline__ void tiny_finalize(const TPass& P, int64_t j, double 
   }
 }
 
+// n / d and n % d for n < 2^31 by multiply-high with a host-built magic number
+__device__ __forceinline__ int tiny_div(int n, unsigned mul, int shr) {
+  return (int)((__umulhi((unsigned)n, mul) + (unsigned)n) >> shr);
+}
+
 // Sum (and optionally write) positions [r0, r1) of output entry j's row.
 // Positions go in batches of TB: the odometer first produces every offset of
-// the batch (integer work only), then all loads of the batch issue back to
-// back, so a lane waits for one L2 round trip per batch, not per position.
+// the batch (32-bit integer work only), then all loads of the batch issue back
+// to back, so a lane waits for one L2 round trip per batch, not per position.
 constexpr int TB = 4;
-template <typename T>
+template <typename T, int NFM>
 __device__ __forceinline__ double tiny_row(const TPass& P, const T* __restrict__ src, T* __restrict__ dst,
-                                           const T* __restrict__ aux, int64_t j, int64_t r0, int64_t r1,
-                                           int64_t* out_j) {
+                                           const T* __restrict__ aux, int j, int r0, int r1, int* out_j) {
   const int nf = P.nf;
-  int64_t so = 0, dd = 0, oo = 0;
-  int64_t fo[MAXF];
+  int so = 0, dd = 0, oo = 0;
+  int fo[NFM];
 #pragma unroll
-  for (int f = 0; f < MAXF; ++f) fo[f] = 0;
+  for (int f = 0; f < NFM; ++f) fo[f] = 0;
   {
-    int64_t x = j;
+    int x = j;
     for (int d = P.nod - 1; d >= 0; --d) {
-      const int c = P.ocard[d];
-      const int64_t dig = x % c;
-      x /= c;
+      const int q = tiny_div(x, P.omul[d], P.oshr[d]);
+      const int dig = x - q * P.ocard[d];
+      x = q;
       so += dig * P.osrc[d];
       dd += dig * P.odst[d];
       oo += dig * P.oout[d];
 #pragma unroll
-      for (int f = 0; f < MAXF; ++f)
+      for (int f = 0; f < NFM; ++f)
         if (f < nf) fo[f] += dig * P.ofac[f][d];
     }
   }
@@ -95,48 +99,66 @@ __device__ __forceinline__ double tiny_row(const TPass& P, const T* __restrict__
   if (r0 >= r1) return 0.0;
   int dig[TD];
   {
-    int64_t x = r0;
+    int x = r0;
     for (int d = P.nrd - 1; d >= 0; --d) {
-      const int c = P.rcard[d];
-      dig[d] = (int)(x % c);
-      x /= c;
-      so += (int64_t)dig[d] * P.rsrc[d];
-      dd += (int64_t)dig[d] * P.rdst[d];
+      const int q = tiny_div(x, P.rmul[d], P.rshr[d]);
+      dig[d] = x - q * P.rcard[d];
+      x = q;
+      so += dig[d] * P.rsrc[d];
+      dd += dig[d] * P.rdst[d];
 #pragma unroll
-      for (int f = 0; f < MAXF; ++f)
-        if (f < nf) fo[f] += (int64_t)dig[d] * P.rfac[f][d];
+      for (int f = 0; f < NFM; ++f)
+        if (f < nf) fo[f] += dig[d] * P.rfac[f][d];
     }
   }
   const bool wr = P.dst_off >= 0;
-  const T* __restrict__ fb[MAXF];
+  const T* __restrict__ fb[NFM];
 #pragma unroll
-  for (int f = 0; f < MAXF; ++f) fb[f] = aux + (f < nf ? P.fac_off[f] : 0);
+  for (int f = 0; f < NFM; ++f) fb[f] = aux + (f < nf ? P.fac_off[f] : 0);
+  const int nrd = P.nrd;
+  const int d0 = nrd - 1;  // innermost row dim: its step needs no carry most of the time
+  const int c0 = d0 >= 0 ? P.rcard[d0] : 1;
+  const int s0 = d0 >= 0 ? P.rsrc[d0] : 0, t0 = d0 >= 0 ? P.rdst[d0] : 0;
+  int f0[NFM];
+#pragma unroll
+  for (int f = 0; f < NFM; ++f) f0[f] = (d0 >= 0 && f < nf) ? P.rfac[f][d0] : 0;
   double acc = 0.0;
-  for (int64_t rb = r0; rb < r1; rb += TB) {
-    const int nb = (int)(r1 - rb < TB ? r1 - rb : TB);
-    int64_t bs[TB], bd[TB], bf[MAXF][TB];
+  for (int rb = r0; rb < r1; rb += TB) {
+    const int nb = r1 - rb < TB ? r1 - rb : TB;
+    int bs[TB], bd[TB], bf[NFM][TB];
 #pragma unroll
     for (int q = 0; q < TB; ++q) {
       bs[q] = so;
       bd[q] = dd;
 #pragma unroll
-      for (int f = 0; f < MAXF; ++f) bf[f][q] = fo[f];
-      if (q < nb) {
+      for (int f = 0; f < NFM; ++f) bf[f][q] = fo[f];
+      if (q < nb && d0 >= 0) {
         // odometer step over the row dims (last fastest)
-        for (int d = P.nrd - 1; d >= 0; --d) {
-          so += P.rsrc[d];
-          dd += P.rdst[d];
+        so += s0;
+        dd += t0;
 #pragma unroll
-          for (int f = 0; f < MAXF; ++f)
-            if (f < nf) fo[f] += P.rfac[f][d];
-          if (++dig[d] < P.rcard[d]) break;
-          const int c = P.rcard[d];
-          so -= (int64_t)c * P.rsrc[d];
-          dd -= (int64_t)c * P.rdst[d];
+        for (int f = 0; f < NFM; ++f) fo[f] += f0[f];
+        if (++dig[d0] == c0) {
+          so -= c0 * s0;
+          dd -= c0 * t0;
 #pragma unroll
-          for (int f = 0; f < MAXF; ++f)
-            if (f < nf) fo[f] -= (int64_t)c * P.rfac[f][d];
-          dig[d] = 0;
+          for (int f = 0; f < NFM; ++f) fo[f] -= c0 * f0[f];
+          dig[d0] = 0;
+          for (int d = d0 - 1; d >= 0; --d) {
+            so += P.rsrc[d];
+            dd += P.rdst[d];
+#pragma unroll
+            for (int f = 0; f < NFM; ++f)
+              if (f < nf) fo[f] += P.rfac[f][d];
+            if (++dig[d] < P.rcard[d]) break;
+            const int c = P.rcard[d];
+            so -= c * P.rsrc[d];
+            dd -= c * P.rdst[d];
+#pragma unroll
+            for (int f = 0; f < NFM; ++f)
+              if (f < nf) fo[f] -= c * P.rfac[f][d];
+            dig[d] = 0;
+          }
         }
       }
     }
@@ -144,7 +166,7 @@ __device__ __forceinline__ double tiny_row(const TPass& P, const T* __restrict__
 #pragma unroll
     for (int q = 0; q < TB; ++q) v[q] = q < nb ? src[bs[q]] : (T)0;
 #pragma unroll
-    for (int f = 0; f < MAXF; ++f) {
+    for (int f = 0; f < NFM; ++f) {
       if (f < nf) {
 #pragma unroll
         for (int q = 0; q < TB; ++q)
@@ -162,13 +184,12 @@ __device__ __forceinline__ double tiny_row(const TPass& P, const T* __restrict__
   return acc;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(NT) tiny_persist_kernel(const TinyArgs a) {
+template <typename T, int NFM>
+__global__ void __launch_bounds__(NT, 2) tiny_persist_kernel(const TinyArgs a) {
   T* __restrict__ clique = reinterpret_cast<T*>(a.clique);
   const T* __restrict__ base = reinterpret_cast<const T*>(a.base);
   T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
   const int64_t stride = (int64_t)gridDim.x * NT;
-  const int lane = threadIdx.x & 31;
   for (int w = 0; w < a.n_waves; ++w) {
     const TinyWave tw = a.waves[w];
     const TPass* __restrict__ ps = a.passes + tw.pass0;
@@ -181,31 +202,31 @@ __global__ void __launch_bounds__(NT) tiny_persist_kernel(const TinyArgs a) {
         else hi = m - 1;
       }
       const TPass& P = ps[lo];
-      const int64_t u = t - P.unit0;
+      const int u = (int)(t - P.unit0);
       const T* src = (P.src_arena == A_BASE ? base : P.src_arena == A_AUX ? aux : clique) + P.src_off;
       T* dst = clique + (P.dst_off >= 0 ? P.dst_off : 0);
       // P.warp = lanes per output entry (1, 2, 4, 8, 16 or 32): lane chunks of the
       // row in lane order, then a fixed shuffle tree inside the lane group
       const int G = P.warp;
-      const int64_t j = u / G;
-      const int sub = (int)(u - j * G);
+      const int j = u / G;
+      const int sub = u - j * G;
       const bool live = j < P.n_out;  // lanes of the pass's padding compute nothing
-      const int64_t per = (P.n_rest + G - 1) / G;
-      const int64_t r0 = live ? (int64_t)sub * per : 0;
-      const int64_t r1 = live ? (r0 + per < P.n_rest ? r0 + per : P.n_rest) : 0;
-      int64_t oj = 0;
-      double s = live ? tiny_row<T>(P, src, dst, aux, live ? j : 0, r0, r1, &oj) : 0.0;
+      const int nr = (int)P.n_rest;
+      const int per = (nr + G - 1) / G;
+      const int r0 = live ? sub * per : 0;
+      const int r1 = live ? (r0 + per < nr ? r0 + per : nr) : 0;
+      int oj = 0;
+      double s = live ? tiny_row<T, NFM>(P, src, dst, aux, j, r0, r1, &oj) : 0.0;
       for (int o = 1; o < G; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       if (live && sub == 0 && P.out_kind != OUT_NONE) tiny_finalize<T>(P, oj, s, aux, a.qout, a.err);
-      (void)lane;
     }
     if (w + 1 < a.n_waves) tiny_grid_barrier(a.bar);
   }
 }
 
-template <typename T>
+template <typename T, int NFM>
 static cudaError_t launch_tiny_t(const TinyArgs& a, int grid, cudaStream_t s, int* occ_out) {
-  auto k = tiny_persist_kernel<T>;
+  auto k = tiny_persist_kernel<T, NFM>;
   if (occ_out) {
     int n = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, NT, 0);
@@ -225,8 +246,15 @@ static cudaError_t launch_tiny_t(const TinyArgs& a, int grid, cudaStream_t s, in
   return cudaLaunchKernelEx(&cfg, k, a);
 }
 
-cudaError_t launch_tiny(int dtype, const TinyArgs& a, int grid, cudaStream_t s, int* occ_out) {
-  return dtype == 0 ? launch_tiny_t<float>(a, grid, s, occ_out) : launch_tiny_t<double>(a, grid, s, occ_out);
+template <typename T>
+static cudaError_t launch_tiny_nf(int nfm, const TinyArgs& a, int grid, cudaStream_t s, int* occ_out) {
+  if (nfm <= 2) return launch_tiny_t<T, 2>(a, grid, s, occ_out);
+  if (nfm <= 4) return launch_tiny_t<T, 4>(a, grid, s, occ_out);
+  return launch_tiny_t<T, MAXF>(a, grid, s, occ_out);
+}
+
+cudaError_t launch_tiny(int dtype, int nfm, const TinyArgs& a, int grid, cudaStream_t s, int* occ_out) {
+  return dtype == 0 ? launch_tiny_nf<float>(nfm, a, grid, s, occ_out) : launch_tiny_nf<double>(nfm, a, grid, s, occ_out);
 }
 
 }  // namespace jt
