@@ -202,6 +202,8 @@ struct Program {
   cudaStream_t gstream = nullptr;
   // persistent single-launch program (small single trees, jt_tiny.cu)
   int tiny = 0, tiny_grid = 0, n_twaves = 0, tiny_nfm = MAXF;
+  int tiny_waves_launch = 0;           // 1: one launch per wave (PDL) instead of one persistent launch
+  std::vector<int> tiny_wave_grid;     // per-wave grids of the per-wave launches
   TPass* d_tpass = nullptr;
   TinyWave* d_twaves = nullptr;
   unsigned* d_bar = nullptr;
@@ -336,6 +338,11 @@ struct jt_state {
 };
 
 static int64_t align4(int64_t x) { return (x + 3) & ~int64_t(3); }
+
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
 static int64_t sep_cur(const jt_state* st, int sp) { return st->sep_in_y ? st->ratC_off[sp] : st->sep_off[sp]; }
 static int64_t sep_alt(const jt_state* st, int sp) { return st->sep_in_y ? st->sep_off[sp] : st->ratC_off[sp]; }
 
@@ -683,7 +690,8 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
     }
     // the thread-owned kernel is validated for one merged inner dimension only
     // (batched states: the case dim); multi-dim inner blocks take the general kernel
-    if (im.size() > 1 || !allow_own) c.own_m = 0;
+    static const bool own_multi = env_int("JT_OWN_MULTI", 0) != 0;
+    if ((im.size() > 1 && !own_multi) || !allow_own) c.own_m = 0;
     c.own = c.own_m > 0;
     c.BPI = c.own ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(TH / T, c.r_out));
     // several whole output groups per iteration when a group is smaller than an iteration
@@ -710,6 +718,7 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
     if (c.own && has_out)
       nch = std::min<int64_t>(nch, ((int64_t)st->num_sms * 3 + c.n_out - 1) / c.n_out);
     if ((c.own || c.gpi > 1) && c.r_out * T <= per_item) nch = 1;  // whole groups per item instead
+    if (c.own && getenv("JT_OWN_NOCHUNK")) nch = 1;
     nch = std::max<int64_t>(1, std::min(nch, max_chunks));
     int64_t bpc = (c.r_out + nch - 1) / nch;
     bpc = (bpc + c.BPI - 1) / c.BPI * c.BPI;
@@ -781,7 +790,10 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
   d.kv = kv;
   d.own_m = best.own_m;
   d.flush_fac = 0;
-  if (best.own) {
+  // group-constant factors are multiplied into the group SUM at the flush, so a
+  // pass that also writes its clique table must take every factor per element
+  // (otherwise the written table misses them: wrong posteriors downstream)
+  if (best.own && !ps.write && !getenv("JT_OWN_NOFLUSH")) {
     for (int f = 0; f < nf; ++f) {
       bool constant = true;
       for (int i = 0; i < best.k; ++i)
@@ -988,11 +1000,6 @@ static std::vector<int64_t> group_offsets(const jt_plan* p, const std::vector<in
     out.swap(nx);
   }
   return out;
-}
-
-static int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v && *v ? atoi(v) : dflt;
 }
 
 #ifndef CON_NCG_MID
@@ -1329,7 +1336,9 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
       const int vec = small_wave ? wave_vec : pass_max_vec(st, ps);
       // single trees, small (latency-bound) waves or scalar passes: the general kernel
       // at 2 vectors per thread, 3 CTAs per SM (more warps in flight)
-      int rc = compile_pass(st, ps, vec, local, bp, !small_wave, st->B == 1 && (small_wave || vec == 1) ? 2 : KV);
+      static const bool no_row = getenv("JT_NO_ROW") != nullptr, no_own = getenv("JT_NO_OWN") != nullptr;
+      int rc = compile_pass(st, ps, vec, local, bp, !small_wave && !no_row,
+                            st->B == 1 && (small_wave || vec == 1) ? 2 : KV, !no_own);
       if (rc != JT_OK) return rc;
       bp.d.blk_off = (int64_t)blk.size();
       bp.d.blk32_off = (int64_t)hp.blk32.size();
@@ -1350,7 +1359,7 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
       if (bp.d.own) {
         const bool allf = bp.d.fac_vec == ((1u << bp.d.nf) - 1u);
         const bool full_vec = vec == (st->esz == 4 ? 4 : 2);
-        const int lm = full_vec && allf ? (bp.d.src_vec ? 2 : 1) : 0;
+        const int lm = full_vec && allf && !getenv("JT_OWN_LM0") ? (bp.d.src_vec ? 2 : 1) : 0;
         if (lm == 0 && bp.d.own_m != 1) return JT_ERR_UNSUPPORTED;
         key = {1, vec, lm, bp.d.own_m};
       }
@@ -1456,7 +1465,9 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
 #define TINY_MAX_LOG2 22
 #endif
 static bool tiny_choice(const jt_state* st, const std::vector<std::vector<PassSpec>>& waves) {
-  if (st->B != 1 || st->mode != JT_MATERIALIZED || getenv("JT_NO_TINY")) return false;
+  // opt-in (JT_TINY=1: one persistent launch, 2: one launch per wave): measured
+  // not faster than the graph-replayed wave program on c1/c2/c4M (profiles/README.md r2)
+  if (st->B != 1 || st->mode != JT_MATERIALIZED || env_int("JT_TINY", 0) == 0) return false;
   static const int lg = env_int("JT_TINY_MAX_LOG2", TINY_MAX_LOG2);
   int nw = 0;
   for (auto& w : waves) {
@@ -1578,6 +1589,14 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
       prog->tiny_grid = (int)std::min<int64_t>(max_ctas, (int64_t)occ * st->num_sms);
       prog->n_twaves = (int)tw.size();
       prog->n_launches = 1;
+      // JT_TINY=2: one PDL-chained launch per wave (graph-replayed) instead of one
+      // cooperative launch with grid barriers
+      prog->tiny_waves_launch = env_int("JT_TINY", 0) == 2;
+      if (prog->tiny_waves_launch) {
+        prog->n_launches = (int64_t)tw.size();
+        for (auto& w : tw)
+          prog->tiny_wave_grid.push_back((int)std::min<int64_t>((w.n_threads + NT - 1) / NT, (int64_t)occ * st->num_sms));
+      }
       CK(cudaMalloc(&prog->d_tpass, tp.size() * sizeof(TPass)));
       CK(cudaMemcpy(prog->d_tpass, tp.data(), tp.size() * sizeof(TPass), cudaMemcpyHostToDevice));
       CK(cudaMalloc(&prog->d_twaves, tw.size() * sizeof(TinyWave)));
@@ -1678,6 +1697,23 @@ static int ensure_side(jt_state* st) {
 }
 
 static int launch_program_waves(jt_state* st, Program* pr, cudaStream_t s) {
+  if (pr->tiny && pr->tiny_waves_launch) {
+    TinyArgs a{};
+    a.clique = st->d_clique;
+    a.base = st->d_base;
+    a.aux = st->d_aux;
+    a.qout = st->d_qout;
+    a.err = st->d_err;
+    a.passes = pr->d_tpass;
+    a.waves = pr->d_twaves;
+    a.n_waves = pr->n_twaves;
+    a.bar = pr->d_bar;
+    for (int w = 0; w < pr->n_twaves; ++w) {
+      CK(launch_tiny_wave(st->plan->dtype, pr->tiny_nfm, a, w, pr->tiny_wave_grid[w], s));
+      st->launches++;
+    }
+    return JT_OK;
+  }
   for (auto& w : pr->waves) {
     const int ng = (int)w.groups.size();
     if (ng == 1) {
@@ -1707,7 +1743,9 @@ static int launch_program_waves(jt_state* st, Program* pr, cudaStream_t s) {
 // replayed as a CUDA graph on that stream (launch-bound small trees).
 static int run_program(jt_state* st, Program* pr, cudaStream_t s) {
   pr->runs++;
-  if (pr->tiny) {
+  if (pr->tiny && pr->tiny_waves_launch) {
+    // per-wave launches: captured into a graph from the second run on (below)
+  } else if (pr->tiny) {
     TinyArgs a{};
     a.clique = st->d_clique;
     a.base = st->d_base;

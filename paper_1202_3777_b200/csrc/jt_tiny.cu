@@ -185,12 +185,12 @@ __device__ __forceinline__ double tiny_row(const TPass& P, const T* __restrict__
 }
 
 template <typename T, int NFM>
-__global__ void __launch_bounds__(NT, 2) tiny_persist_kernel(const TinyArgs a) {
+__device__ __forceinline__ void tiny_wave(const TinyArgs& a, int w) {
   T* __restrict__ clique = reinterpret_cast<T*>(a.clique);
   const T* __restrict__ base = reinterpret_cast<const T*>(a.base);
   T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
   const int64_t stride = (int64_t)gridDim.x * NT;
-  for (int w = 0; w < a.n_waves; ++w) {
+  {
     const TinyWave tw = a.waves[w];
     const TPass* __restrict__ ps = a.passes + tw.pass0;
     for (int64_t t = (int64_t)blockIdx.x * NT + threadIdx.x; t < tw.n_threads; t += stride) {
@@ -220,8 +220,25 @@ __global__ void __launch_bounds__(NT, 2) tiny_persist_kernel(const TinyArgs a) {
       for (int o = 1; o < G; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       if (live && sub == 0 && P.out_kind != OUT_NONE) tiny_finalize<T>(P, oj, s, aux, a.qout, a.err);
     }
+  }
+}
+
+// every wave in one cooperative launch, grid barriers between waves
+template <typename T, int NFM>
+__global__ void __launch_bounds__(NT, 2) tiny_persist_kernel(const TinyArgs a) {
+  for (int w = 0; w < a.n_waves; ++w) {
+    tiny_wave<T, NFM>(a, w);
     if (w + 1 < a.n_waves) tiny_grid_barrier(a.bar);
   }
+}
+
+// one wave per launch (programmatic dependent launch chains the waves; the
+// program is replayed as a CUDA graph)
+template <typename T, int NFM>
+__global__ void __launch_bounds__(NT, 2) tiny_wave_kernel(const TinyArgs a, int w) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  tiny_wave<T, NFM>(a, w);
 }
 
 template <typename T, int NFM>
@@ -244,6 +261,31 @@ static cudaError_t launch_tiny_t(const TinyArgs& a, int grid, cudaStream_t s, in
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, k, a);
+}
+
+template <typename T, int NFM>
+static cudaError_t launch_tiny_wave_t(const TinyArgs& a, int w, int grid, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NT);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, tiny_wave_kernel<T, NFM>, a, w);
+}
+
+template <typename T>
+static cudaError_t launch_tiny_wave_nf(int nfm, const TinyArgs& a, int w, int grid, cudaStream_t s) {
+  if (nfm <= 2) return launch_tiny_wave_t<T, 2>(a, w, grid, s);
+  if (nfm <= 4) return launch_tiny_wave_t<T, 4>(a, w, grid, s);
+  return launch_tiny_wave_t<T, MAXF>(a, w, grid, s);
+}
+
+cudaError_t launch_tiny_wave(int dtype, int nfm, const TinyArgs& a, int w, int grid, cudaStream_t s) {
+  return dtype == 0 ? launch_tiny_wave_nf<float>(nfm, a, w, grid, s) : launch_tiny_wave_nf<double>(nfm, a, w, grid, s);
 }
 
 template <typename T>
