@@ -202,7 +202,8 @@ struct Program {
   cudaStream_t gstream = nullptr;
   // persistent single-launch program (small single trees, jt_tiny.cu)
   int tiny = 0, tiny_grid = 0, n_twaves = 0, tiny_nfm = MAXF;
-  int tiny_waves_launch = 0;           // 1: one launch per wave (PDL) instead of one persistent launch
+  int tiny_waves_launch = 0;           // 1: per-wave launches (PDL), tiny kernel on the waves flagged below
+  std::vector<char> tiny_w;            // per (non-empty) wave: run as a tiny-pass launch
   std::vector<int> tiny_wave_grid;     // per-wave grids of the per-wave launches
   TPass* d_tpass = nullptr;
   TinyWave* d_twaves = nullptr;
@@ -1457,19 +1458,30 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
   return JT_OK;
 }
 
-// Small single trees run as ONE persistent launch of tiny passes (jt_tiny.cu)
-// when every wave is small: their waves are latency-bound, so per-wave launches
-// and the general kernel's per-item epilogues dominate (c1 6 waves
-// in 50 us).
+// Small waves of single trees run as tiny-pass launches (jt_tiny.cu): their
+// work is a few thousand entries, latency-bound, and the general kernel's
+// per-item block tables and smem epilogues dominate.  JT_TINY=2 (default):
+// per wave, a tiny launch when the wave touches at most 2^JT_TINY_WAVE_LOG2
+// elements, else the general launch groups (PDL chains every launch, the
+// program is graph-replayed); JT_TINY=1: the whole program as ONE cooperative
+// launch with grid barriers (every wave small); JT_TINY=0: off.
 #ifndef TINY_MAX_LOG2
 #define TINY_MAX_LOG2 22
 #endif
-static bool tiny_choice(const jt_state* st, const std::vector<std::vector<PassSpec>>& waves) {
-  // opt-in (JT_TINY=1: one persistent launch, 2: one launch per wave): measured
-  // not faster than the graph-replayed wave program on c1/c2/c4M (profiles/README.md r2)
-  if (st->B != 1 || st->mode != JT_MATERIALIZED || env_int("JT_TINY", 0) == 0) return false;
+#ifndef TINY_WAVE_LOG2
+#define TINY_WAVE_LOG2 17
+#endif
+static int tiny_mode() { return env_int("JT_TINY", 2); }
+
+static bool tiny_choice(const jt_state* st, const std::vector<std::vector<PassSpec>>& waves,
+                        std::vector<char>& per_wave) {
+  per_wave.clear();
+  const int mode = tiny_mode();
+  if (st->B != 1 || st->mode != JT_MATERIALIZED || mode == 0) return false;
   static const int lg = env_int("JT_TINY_MAX_LOG2", TINY_MAX_LOG2);
-  int nw = 0;
+  static const int lgw = env_int("JT_TINY_WAVE_LOG2", TINY_WAVE_LOG2);
+  int nw = 0, ntiny = 0;
+  bool all_small = true;
   for (auto& w : waves) {
     if (w.empty()) continue;
     ++nw;
@@ -1480,9 +1492,13 @@ static bool tiny_choice(const jt_state* st, const std::vector<std::vector<PassSp
       for (auto& x : dd) n *= x.card;
       el += n;
     }
-    if (el > (int64_t(1) << lg)) return false;
+    all_small = all_small && el <= (int64_t(1) << lg);
+    const bool t = mode == 1 || el <= (int64_t(1) << lgw);
+    per_wave.push_back(t ? 1 : 0);
+    ntiny += t;
   }
-  return nw >= 3;
+  if (mode == 1) return all_small && nw >= 3;
+  return ntiny > 0 && nw >= 2;
 }
 
 // q = (umulhi(n, mul) + n) >> shr == n / d for 0 <= n < 2^31 (round-up method)
@@ -1574,7 +1590,8 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
   auto prog = std::make_unique<Program>();
   prog->waves = hp.waves;
   for (auto& w : hp.waves) prog->n_launches += (int64_t)w.groups.size();
-  if (tiny_choice(st, waves)) {
+  std::vector<char> tiny_w;
+  if (tiny_choice(st, waves, tiny_w)) {
     std::vector<TPass> tp;
     std::vector<TinyWave> tw;
     if (build_tiny(st, waves, tp, tw) == JT_OK && !tw.empty()) {
@@ -1589,13 +1606,15 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
       prog->tiny_grid = (int)std::min<int64_t>(max_ctas, (int64_t)occ * st->num_sms);
       prog->n_twaves = (int)tw.size();
       prog->n_launches = 1;
-      // JT_TINY=2: one PDL-chained launch per wave (graph-replayed) instead of one
-      // cooperative launch with grid barriers
-      prog->tiny_waves_launch = env_int("JT_TINY", 0) == 2;
+      prog->tiny_waves_launch = tiny_mode() == 2;
       if (prog->tiny_waves_launch) {
-        prog->n_launches = (int64_t)tw.size();
-        for (auto& w : tw)
-          prog->tiny_wave_grid.push_back((int)std::min<int64_t>((w.n_threads + NT - 1) / NT, (int64_t)occ * st->num_sms));
+        prog->tiny_w = tiny_w;
+        prog->n_launches = 0;
+        for (size_t w = 0; w < tw.size(); ++w) {
+          prog->tiny_wave_grid.push_back(
+              (int)std::min<int64_t>((tw[w].n_threads + NT - 1) / NT, (int64_t)occ * st->num_sms));
+          prog->n_launches += tiny_w[w] ? 1 : (int64_t)hp.waves[w].groups.size();
+        }
       }
       CK(cudaMalloc(&prog->d_tpass, tp.size() * sizeof(TPass)));
       CK(cudaMemcpy(prog->d_tpass, tp.data(), tp.size() * sizeof(TPass), cudaMemcpyHostToDevice));
@@ -1697,8 +1716,9 @@ static int ensure_side(jt_state* st) {
 }
 
 static int launch_program_waves(jt_state* st, Program* pr, cudaStream_t s) {
+  TinyArgs ta{};
   if (pr->tiny && pr->tiny_waves_launch) {
-    TinyArgs a{};
+    TinyArgs& a = ta;
     a.clique = st->d_clique;
     a.base = st->d_base;
     a.aux = st->d_aux;
@@ -1708,13 +1728,15 @@ static int launch_program_waves(jt_state* st, Program* pr, cudaStream_t s) {
     a.waves = pr->d_twaves;
     a.n_waves = pr->n_twaves;
     a.bar = pr->d_bar;
-    for (int w = 0; w < pr->n_twaves; ++w) {
-      CK(launch_tiny_wave(st->plan->dtype, pr->tiny_nfm, a, w, pr->tiny_wave_grid[w], s));
-      st->launches++;
-    }
-    return JT_OK;
   }
+  int wi = -1;
   for (auto& w : pr->waves) {
+    ++wi;
+    if (pr->tiny && pr->tiny_waves_launch && pr->tiny_w[wi]) {
+      CK(launch_tiny_wave(st->plan->dtype, pr->tiny_nfm, ta, wi, pr->tiny_wave_grid[wi], s));
+      st->launches++;
+      continue;
+    }
     const int ng = (int)w.groups.size();
     if (ng == 1) {
       int rc = launch_group(st, pr, w, w.groups[0], s);
@@ -3213,15 +3235,19 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
   if (rc) return rc;
   std::string out;
   char line[512];
-  if (tiny_choice(&st, waves)) {
+  std::vector<char> tiny_w;
+  if (tiny_choice(&st, waves, tiny_w)) {
     std::vector<TPass> tp;
     std::vector<TinyWave> tw;
     if (build_tiny(&st, waves, tp, tw) == JT_OK) {
       int64_t warp_passes = 0, threads = 0;
       for (auto& x : tp) warp_passes += x.warp > 1;
       for (auto& x : tw) threads += x.n_threads;
-      snprintf(line, sizeof line, "tiny persistent program: one launch, %zu waves, %zu passes (%lld with several lanes per entry), "
-               "%lld threads over all waves\n", tw.size(), tp.size(), (long long)warp_passes, (long long)threads);
+      int64_t nt = 0;
+      for (char x : tiny_w) nt += x;
+      snprintf(line, sizeof line, "tiny passes (mode %d): %lld of %zu waves, %zu passes (%lld with several lanes per "
+               "entry), %lld threads over all waves\n", tiny_mode(), (long long)nt, tw.size(), tp.size(),
+               (long long)warp_passes, (long long)threads);
       out += line;
     }
   }
