@@ -206,6 +206,7 @@ struct Program {
   std::vector<char> tiny_w;            // per (non-empty) wave: run as a tiny-pass launch
   std::vector<int> tiny_wave_grid;     // per-wave grids of the per-wave launches
   TPass* d_tpass = nullptr;
+  int64_t* d_unit0 = nullptr;
   TinyWave* d_twaves = nullptr;
   unsigned* d_bar = nullptr;
   int runs = 0;
@@ -224,6 +225,7 @@ struct Program {
     cudaFree(d_ctab);
     cudaFree(d_w);
     cudaFree(d_tpass);
+    cudaFree(d_unit0);
     cudaFree(d_twaves);
     cudaFree(d_bar);
   }
@@ -1616,6 +1618,10 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
           prog->n_launches += tiny_w[w] ? 1 : (int64_t)hp.waves[w].groups.size();
         }
       }
+      std::vector<int64_t> u0;
+      for (auto& x : tp) u0.push_back(x.unit0);
+      CK(cudaMalloc(&prog->d_unit0, u0.size() * sizeof(int64_t)));
+      CK(cudaMemcpy(prog->d_unit0, u0.data(), u0.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
       CK(cudaMalloc(&prog->d_tpass, tp.size() * sizeof(TPass)));
       CK(cudaMemcpy(prog->d_tpass, tp.data(), tp.size() * sizeof(TPass), cudaMemcpyHostToDevice));
       CK(cudaMalloc(&prog->d_twaves, tw.size() * sizeof(TinyWave)));
@@ -1725,6 +1731,7 @@ static int launch_program_waves(jt_state* st, Program* pr, cudaStream_t s) {
     a.qout = st->d_qout;
     a.err = st->d_err;
     a.passes = pr->d_tpass;
+    a.unit0s = pr->d_unit0;
     a.waves = pr->d_twaves;
     a.n_waves = pr->n_twaves;
     a.bar = pr->d_bar;
@@ -1775,6 +1782,7 @@ static int run_program(jt_state* st, Program* pr, cudaStream_t s) {
     a.qout = st->d_qout;
     a.err = st->d_err;
     a.passes = pr->d_tpass;
+    a.unit0s = pr->d_unit0;
     a.waves = pr->d_twaves;
     a.n_waves = pr->n_twaves;
     a.bar = pr->d_bar;

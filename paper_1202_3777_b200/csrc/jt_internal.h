@@ -236,6 +236,7 @@ struct TinyArgs {
   double* qout;
   int* err;
   const TPass* passes;
+  const int64_t* unit0s;    // TPass::unit0 of every pass, compact (binary search)
   const TinyWave* waves;
   int n_waves;
   unsigned* bar;            // [counter, generation]

@@ -68,60 +68,72 @@ __device__ __forceinline__ int tiny_div(int n, unsigned mul, int shr) {
   return (int)((__umulhi((unsigned)n, mul) + (unsigned)n) >> shr);
 }
 
-// Sum (and optionally write) positions [r0, r1) of output entry j's row.
-// Positions go in batches of TB: the odometer first produces every offset of
-// the batch (32-bit integer work only), then all loads of the batch issue back
-// to back, so a lane waits for one L2 round trip per batch, not per position.
+// Row walk state of one lane: base offsets of its output entry plus the
+// odometer at its first row position.
+template <int NFM>
+struct TRow {
+  int so, dd, oo;
+  int fo[NFM];
+  int dig[TD];
+};
+
+// Decompose output entry j and row position r0 (program constants only: runs
+// before the wait on the previous wave).
+template <int NFM>
+__device__ __forceinline__ void tiny_prep(const TPass& P, int j, int r0, TRow<NFM>& R) {
+  const int nf = P.nf;
+  R.so = R.dd = R.oo = 0;
+#pragma unroll
+  for (int f = 0; f < NFM; ++f) R.fo[f] = 0;
+  int x = j;
+  for (int d = P.nod - 1; d >= 0; --d) {
+    const int q = tiny_div(x, P.omul[d], P.oshr[d]);
+    const int dig = x - q * P.ocard[d];
+    x = q;
+    R.so += dig * P.osrc[d];
+    R.dd += dig * P.odst[d];
+    R.oo += dig * P.oout[d];
+#pragma unroll
+    for (int f = 0; f < NFM; ++f)
+      if (f < nf) R.fo[f] += dig * P.ofac[f][d];
+  }
+  x = r0;
+  for (int d = P.nrd - 1; d >= 0; --d) {
+    const int q = tiny_div(x, P.rmul[d], P.rshr[d]);
+    R.dig[d] = x - q * P.rcard[d];
+    x = q;
+    R.so += R.dig[d] * P.rsrc[d];
+    R.dd += R.dig[d] * P.rdst[d];
+#pragma unroll
+    for (int f = 0; f < NFM; ++f)
+      if (f < nf) R.fo[f] += R.dig[d] * P.rfac[f][d];
+  }
+}
+
+// Sum (and optionally write) positions [r0, r1) of the row.  Positions go in
+// batches of TB: the odometer first produces every offset of the batch (32-bit
+// integer work only), then all loads of the batch issue back to back, so a lane
+// waits for one L2 round trip per batch, not per position.
 constexpr int TB = 4;
 template <typename T, int NFM>
-__device__ __forceinline__ double tiny_row(const TPass& P, const T* __restrict__ src, T* __restrict__ dst,
-                                           const T* __restrict__ aux, int j, int r0, int r1, int* out_j) {
+__device__ __forceinline__ double tiny_exec(const TPass& P, const T* __restrict__ src, T* __restrict__ dst,
+                                            const T* __restrict__ aux, TRow<NFM>& R, int r0, int r1) {
   const int nf = P.nf;
-  int so = 0, dd = 0, oo = 0;
-  int fo[NFM];
-#pragma unroll
-  for (int f = 0; f < NFM; ++f) fo[f] = 0;
-  {
-    int x = j;
-    for (int d = P.nod - 1; d >= 0; --d) {
-      const int q = tiny_div(x, P.omul[d], P.oshr[d]);
-      const int dig = x - q * P.ocard[d];
-      x = q;
-      so += dig * P.osrc[d];
-      dd += dig * P.odst[d];
-      oo += dig * P.oout[d];
-#pragma unroll
-      for (int f = 0; f < NFM; ++f)
-        if (f < nf) fo[f] += dig * P.ofac[f][d];
-    }
-  }
-  *out_j = oo;
   if (r0 >= r1) return 0.0;
-  int dig[TD];
-  {
-    int x = r0;
-    for (int d = P.nrd - 1; d >= 0; --d) {
-      const int q = tiny_div(x, P.rmul[d], P.rshr[d]);
-      dig[d] = x - q * P.rcard[d];
-      x = q;
-      so += dig[d] * P.rsrc[d];
-      dd += dig[d] * P.rdst[d];
-#pragma unroll
-      for (int f = 0; f < NFM; ++f)
-        if (f < nf) fo[f] += dig[d] * P.rfac[f][d];
-    }
-  }
   const bool wr = P.dst_off >= 0;
   const T* __restrict__ fb[NFM];
 #pragma unroll
   for (int f = 0; f < NFM; ++f) fb[f] = aux + (f < nf ? P.fac_off[f] : 0);
-  const int nrd = P.nrd;
-  const int d0 = nrd - 1;  // innermost row dim: its step needs no carry most of the time
+  const int d0 = P.nrd - 1;  // innermost row dim: its step needs no carry most of the time
   const int c0 = d0 >= 0 ? P.rcard[d0] : 1;
   const int s0 = d0 >= 0 ? P.rsrc[d0] : 0, t0 = d0 >= 0 ? P.rdst[d0] : 0;
   int f0[NFM];
 #pragma unroll
   for (int f = 0; f < NFM; ++f) f0[f] = (d0 >= 0 && f < nf) ? P.rfac[f][d0] : 0;
+  int so = R.so, dd = R.dd;
+  int fo[NFM];
+#pragma unroll
+  for (int f = 0; f < NFM; ++f) fo[f] = R.fo[f];
   double acc = 0.0;
   for (int rb = r0; rb < r1; rb += TB) {
     const int nb = r1 - rb < TB ? r1 - rb : TB;
@@ -138,26 +150,26 @@ __device__ __forceinline__ double tiny_row(const TPass& P, const T* __restrict__
         dd += t0;
 #pragma unroll
         for (int f = 0; f < NFM; ++f) fo[f] += f0[f];
-        if (++dig[d0] == c0) {
+        if (++R.dig[d0] == c0) {
           so -= c0 * s0;
           dd -= c0 * t0;
 #pragma unroll
           for (int f = 0; f < NFM; ++f) fo[f] -= c0 * f0[f];
-          dig[d0] = 0;
+          R.dig[d0] = 0;
           for (int d = d0 - 1; d >= 0; --d) {
             so += P.rsrc[d];
             dd += P.rdst[d];
 #pragma unroll
             for (int f = 0; f < NFM; ++f)
               if (f < nf) fo[f] += P.rfac[f][d];
-            if (++dig[d] < P.rcard[d]) break;
+            if (++R.dig[d] < P.rcard[d]) break;
             const int c = P.rcard[d];
             so -= c * P.rsrc[d];
             dd -= c * P.rdst[d];
 #pragma unroll
             for (int f = 0; f < NFM; ++f)
               if (f < nf) fo[f] -= c * P.rfac[f][d];
-            dig[d] = 0;
+            R.dig[d] = 0;
           }
         }
       }
@@ -184,42 +196,55 @@ __device__ __forceinline__ double tiny_row(const TPass& P, const T* __restrict__
   return acc;
 }
 
-template <typename T, int NFM>
+// One wave: every thread finds its pass (binary search over the wave's compact
+// unit0 list), decomposes its entry and row start, and -- with PDL -- only then
+// waits for the previous wave: descriptor reads and index math overlap the
+// previous kernel's tail.
+template <typename T, int NFM, bool PDL>
 __device__ __forceinline__ void tiny_wave(const TinyArgs& a, int w) {
   T* __restrict__ clique = reinterpret_cast<T*>(a.clique);
   const T* __restrict__ base = reinterpret_cast<const T*>(a.base);
   T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
   const int64_t stride = (int64_t)gridDim.x * NT;
-  {
-    const TinyWave tw = a.waves[w];
-    const TPass* __restrict__ ps = a.passes + tw.pass0;
-    for (int64_t t = (int64_t)blockIdx.x * NT + threadIdx.x; t < tw.n_threads; t += stride) {
-      // pass of thread t: last pass with unit0 <= t (warp-uniform: passes start at multiples of 32)
-      int lo = 0, hi = tw.n_passes - 1;
+  const TinyWave tw = a.waves[w];
+  const TPass* __restrict__ ps = a.passes + tw.pass0;
+  const int64_t* __restrict__ u0 = a.unit0s + tw.pass0;
+  bool waited = !PDL;
+  for (int64_t t = (int64_t)blockIdx.x * NT + threadIdx.x; t < tw.n_threads || !waited; t += stride) {
+    const bool in = t < tw.n_threads;
+    int lo = 0;
+    if (in) {
+      int hi = tw.n_passes - 1;
       while (lo < hi) {
         const int m = (lo + hi + 1) >> 1;
-        if (ps[m].unit0 <= t) lo = m;
+        if (__ldg(u0 + m) <= t) lo = m;
         else hi = m - 1;
       }
-      const TPass& P = ps[lo];
-      const int u = (int)(t - P.unit0);
-      const T* src = (P.src_arena == A_BASE ? base : P.src_arena == A_AUX ? aux : clique) + P.src_off;
-      T* dst = clique + (P.dst_off >= 0 ? P.dst_off : 0);
-      // P.warp = lanes per output entry (1, 2, 4, 8, 16 or 32): lane chunks of the
-      // row in lane order, then a fixed shuffle tree inside the lane group
-      const int G = P.warp;
-      const int j = u / G;
-      const int sub = u - j * G;
-      const bool live = j < P.n_out;  // lanes of the pass's padding compute nothing
-      const int nr = (int)P.n_rest;
-      const int per = (nr + G - 1) / G;
-      const int r0 = live ? sub * per : 0;
-      const int r1 = live ? (r0 + per < nr ? r0 + per : nr) : 0;
-      int oj = 0;
-      double s = live ? tiny_row<T, NFM>(P, src, dst, aux, j, r0, r1, &oj) : 0.0;
-      for (int o = 1; o < G; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (live && sub == 0 && P.out_kind != OUT_NONE) tiny_finalize<T>(P, oj, s, aux, a.qout, a.err);
     }
+    const TPass& P = ps[lo];
+    const int u = in ? (int)(t - __ldg(u0 + lo)) : 0;
+    // P.warp = lanes per output entry (1, 2, 4, 8, 16 or 32): lane chunks of the
+    // row in lane order, then a fixed shuffle tree inside the lane group
+    const int G = in ? P.warp : 1;
+    const int j = u / G;
+    const int sub = u - j * G;
+    const bool live = in && j < P.n_out;  // lanes of the pass's padding compute nothing
+    const int nr = live ? (int)P.n_rest : 0;
+    const int per = (nr + G - 1) / G;
+    const int r0 = live ? sub * per : 0;
+    const int r1 = live ? (r0 + per < nr ? r0 + per : nr) : 0;
+    TRow<NFM> R;
+    if (live) tiny_prep<NFM>(P, j, r0, R);
+    if (!waited) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      waited = true;
+    }
+    if (!in) break;
+    const T* src = (P.src_arena == A_BASE ? base : P.src_arena == A_AUX ? aux : clique) + P.src_off;
+    T* dst = clique + (P.dst_off >= 0 ? P.dst_off : 0);
+    double s = live ? tiny_exec<T, NFM>(P, src, dst, aux, R, r0, r1) : 0.0;
+    for (int o = 1; o < G; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (live && sub == 0 && P.out_kind != OUT_NONE) tiny_finalize<T>(P, R.oo, s, aux, a.qout, a.err);
   }
 }
 
@@ -227,7 +252,7 @@ __device__ __forceinline__ void tiny_wave(const TinyArgs& a, int w) {
 template <typename T, int NFM>
 __global__ void __launch_bounds__(NT, 2) tiny_persist_kernel(const TinyArgs a) {
   for (int w = 0; w < a.n_waves; ++w) {
-    tiny_wave<T, NFM>(a, w);
+    tiny_wave<T, NFM, false>(a, w);
     if (w + 1 < a.n_waves) tiny_grid_barrier(a.bar);
   }
 }
@@ -236,9 +261,8 @@ __global__ void __launch_bounds__(NT, 2) tiny_persist_kernel(const TinyArgs a) {
 // program is replayed as a CUDA graph)
 template <typename T, int NFM>
 __global__ void __launch_bounds__(NT, 2) tiny_wave_kernel(const TinyArgs a, int w) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  tiny_wave<T, NFM>(a, w);
+  tiny_wave<T, NFM, true>(a, w);
 }
 
 template <typename T, int NFM>
