@@ -1471,7 +1471,7 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
 #define TINY_MAX_LOG2 22
 #endif
 #ifndef TINY_WAVE_LOG2
-#define TINY_WAVE_LOG2 17
+#define TINY_WAVE_LOG2 18
 #endif
 static int tiny_mode() { return env_int("JT_TINY", 2); }
 
@@ -1685,6 +1685,8 @@ static int launch_group(jt_state* st, const Program* pr, const WaveRt& w, const 
     c.partials = pr->d_part;
     c.counters = pr->d_cnt;
     c.interleave = g.interleave;
+    static const int stream_epi = env_int("JT_EPI_CS", 1);
+    c.stream_epi = stream_epi;
     CK(launch_contract(st->plan->dtype, g.lm, g.m, g.vec, c, g.grid, s));
     st->launches++;
     return JT_OK;

@@ -139,6 +139,8 @@ struct CArgs {
   int B;
   double* partials;         // K-split partial sums
   int* counters;            // K-split arrival counters (reset by the last warp)
+  int stream_epi;           // 1: epilogue inputs (E factors, old separators) load and outputs store
+                            //    with evict-first hints: the streams do not flush reused factor rows
   int interleave;           // 1: every pass has n_units / n_passes units and unit u belongs to
                             // pass u % n_passes (passes reading the same tensors run side by side)
 };

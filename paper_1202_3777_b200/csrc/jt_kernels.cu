@@ -64,6 +64,16 @@ __device__ __forceinline__ void store_vec(T* p, const T (&v)[VEC]) {
   *reinterpret_cast<V*>(p) = x;
 }
 
+template <typename T, int VEC>
+__device__ __forceinline__ void store_vec_cs(T* p, const T (&v)[VEC]) {
+  using V = typename VecT<T, VEC>::type;
+  V x;
+  T* xs = reinterpret_cast<T*>(&x);
+#pragma unroll
+  for (int l = 0; l < VEC; ++l) xs[l] = v[l];
+  __stcs(reinterpret_cast<V*>(p), x);
+}
+
 // Programmatic dependent launch: wave kernels are launched with the
 // programmatic-serialization attribute, so a kernel's CTAs may be scheduled
 // while the previous wave drains; every such kernel waits for the previous
@@ -1005,7 +1015,7 @@ int wave_row_max_ctas_per_sm(int dtype, int vec) {
 template <typename T, typename A, int VEC>
 __device__ __forceinline__ bool finalize_lanes(int kind, int64_t out_off, int64_t ratio_off, int64_t out2_off,
                                                int64_t j, const A (&star)[VEC], const T (&old)[VEC], T* aux,
-                                               double* qout) {
+                                               double* qout, bool cs = false) {
   if (kind == OUT_RAW) {
 #pragma unroll
     for (int l = 0; l < VEC; ++l) qout[out_off + j + l] = (double)star[l];
@@ -1015,7 +1025,8 @@ __device__ __forceinline__ bool finalize_lanes(int kind, int64_t out_off, int64_
   if (kind == OUT_SEP_FRESH) {
 #pragma unroll
     for (int l = 0; l < VEC; ++l) nw[l] = (T)star[l];
-    store_vec<T, VEC>(aux + out_off + j, nw);
+    if (cs) store_vec_cs<T, VEC>(aux + out_off + j, nw);
+    else store_vec<T, VEC>(aux + out_off + j, nw);
     return false;
   }
   T rt[VEC];
@@ -1032,8 +1043,13 @@ __device__ __forceinline__ bool finalize_lanes(int kind, int64_t out_off, int64_
       nw[l] = (T)star[l];
     }
   }
-  store_vec<T, VEC>(aux + ratio_off + j, rt);
-  store_vec<T, VEC>(aux + (out2_off >= 0 ? out2_off : out_off) + j, nw);
+  if (cs) {
+    store_vec_cs<T, VEC>(aux + ratio_off + j, rt);
+    store_vec_cs<T, VEC>(aux + (out2_off >= 0 ? out2_off : out_off) + j, nw);
+  } else {
+    store_vec<T, VEC>(aux + ratio_off + j, rt);
+    store_vec<T, VEC>(aux + (out2_off >= 0 ? out2_off : out_off) + j, nw);
+  }
   return bad;
 }
 
@@ -1119,7 +1135,7 @@ __device__ __forceinline__ bool contract_epilogue_half(const CPass* __restrict__
       }
     }
     bad |= finalize_lanes<T, A, VEC>(KIND, P->out_off, P->ratio_off, P->out2_off, (int64_t)jo[r] + b0, v, old[r], aux,
-                                     a.qout);
+                                     a.qout, a.stream_epi != 0);
   }
   return bad;
 }
@@ -1451,16 +1467,22 @@ __global__ void __launch_bounds__(NT, FOLD ? ROWI_MINB_F : ROWI_MINB_NF) contrac
       double v[VEC];
 #pragma unroll
       for (int l = 0; l < VEC; ++l) v[l] = acc[l] + (double)part[l];
+      const bool cs = a.stream_epi != 0;
       for (int e = 0; e < nE; ++e) {
         T f[VEC];
-        load_vec_ro<T, VEC>(aux_c + P->efac_off[e] + __ldg(tir + nG + e) + __ldg(ts + e) + b0, f);
+        const T* ep = aux_c + P->efac_off[e] + __ldg(tir + nG + e) + __ldg(ts + e) + b0;
+        if (cs) load_vec_cs<T, VEC>(ep, f);
+        else load_vec_ro<T, VEC>(ep, f);
 #pragma unroll
         for (int l = 0; l < VEC; ++l) v[l] *= (double)f[l];
       }
       const int64_t j = (int64_t)__ldg(tir + nG + nE) + __ldg(ts + nE) + b0;
       T old[VEC] = {};
-      if (P->out_kind == OUT_SEP || P->out_kind == OUT_SEP_DFRESH) load_vec<T, VEC>(aux_c + P->out_off + j, old);
-      if (finalize_lanes<T, double, VEC>(P->out_kind, P->out_off, P->ratio_off, P->out2_off, j, v, old, aux, a.qout))
+      if (P->out_kind == OUT_SEP || P->out_kind == OUT_SEP_DFRESH) {
+        if (cs) load_vec_cs<T, VEC>(aux_c + P->out_off + j, old);
+        else load_vec<T, VEC>(aux_c + P->out_off + j, old);
+      }
+      if (finalize_lanes<T, double, VEC>(P->out_kind, P->out_off, P->ratio_off, P->out2_off, j, v, old, aux, a.qout, cs))
         atomicOr(a.err, EB_INCONSISTENT);
     }
   }
@@ -1575,17 +1597,23 @@ __global__ void __launch_bounds__(NT, 4) contract_rowg_kernel(const CArgs a) {
         double v[VEC];
 #pragma unroll
         for (int l = 0; l < VEC; ++l) v[l] = acc[q][l] + (double)part[q][l];
+        const bool cs = a.stream_epi != 0;
         for (int e = 0; e < nE; ++e) {
           T f[VEC];
-          load_vec_ro<T, VEC>(aux_c + P->efac_off[e] + __ldg(tq + nG + e) + __ldg(ts + e) + b0, f);
+          const T* ep = aux_c + P->efac_off[e] + __ldg(tq + nG + e) + __ldg(ts + e) + b0;
+          if (cs) load_vec_cs<T, VEC>(ep, f);
+          else load_vec_ro<T, VEC>(ep, f);
 #pragma unroll
           for (int l = 0; l < VEC; ++l) v[l] *= (double)f[l];
         }
         const int64_t j = (int64_t)__ldg(tq + nG + nE) + __ldg(ts + nE) + b0;
         T old[VEC] = {};
-        if (P->out_kind == OUT_SEP || P->out_kind == OUT_SEP_DFRESH) load_vec<T, VEC>(aux_c + P->out_off + j, old);
+        if (P->out_kind == OUT_SEP || P->out_kind == OUT_SEP_DFRESH) {
+          if (cs) load_vec_cs<T, VEC>(aux_c + P->out_off + j, old);
+          else load_vec<T, VEC>(aux_c + P->out_off + j, old);
+        }
         bad |= finalize_lanes<T, double, VEC>(P->out_kind, P->out_off, P->ratio_off, P->out2_off, j, v, old, aux,
-                                              a.qout);
+                                              a.qout, cs);
       }
       if (bad) atomicOr(a.err, EB_INCONSISTENT);
     }
