@@ -1011,7 +1011,8 @@ static std::vector<int64_t> group_offsets(const jt_plan* p, const std::vector<in
 #ifndef CON_NCG_SMALL
 #define CON_NCG_SMALL 1  // and for nK < 8 (a unit walks all case chunks)
 #endif
-static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram& hp, CPass& cp) {
+static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram& hp, CPass& cp,
+                            const PassSpec* ps_b = nullptr) {
   const jt_plan* p = st->plan;
   const int64_t B = st->B;
   const auto& C = p->cvars[ps.clique];
@@ -1031,6 +1032,18 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   std::set_difference(s.begin(), s.end(), U.begin(), U.end(), std::back_inserter(S));
   std::set_difference(U.begin(), U.end(), s.begin(), s.end(), std::back_inserter(K));
   const int nG = (int)G.size(), nE = (int)E.size();
+  // second output: same scope, same G factors (hence same I, K', W); its own E factors
+  std::vector<const Tensor*> Eb;
+  if (ps_b) {
+    std::vector<const Tensor*> Gb;
+    for (auto& f : ps_b->factors) (subset(f.vars, s) ? Eb : Gb).push_back(&f);
+    if (ps_b->out.vars != s || ps_b->clique != ps.clique || Gb.size() != G.size() || (int)Eb.size() > MAXF)
+      return JT_ERR_UNSUPPORTED;
+    for (size_t g = 0; g < G.size(); ++g)
+      if (Gb[g]->off != G[g]->off || Gb[g]->vars != G[g]->vars) return JT_ERR_UNSUPPORTED;
+    if (!std::includes(U.begin(), U.end(), s.begin(), s.end())) return JT_ERR_UNSUPPORTED;  // row-per-i only
+  }
+  const int nEb = (int)Eb.size();
   // enumeration order of i (any order works: every i-dependent offset comes from
   // the per-i table): the variables that index the largest factor tensors vary
   // slowest, so consecutive i (consecutive warps) re-read the same factor rows
@@ -1068,6 +1081,16 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
     eI[e] = group_offsets(p, I, strides(I, *E[e]));
     eS[e] = group_offsets(p, S, strides(S, *E[e]));
   }
+  std::vector<std::vector<int64_t>> ebI(nEb), ebS(nEb);
+  for (int e = 0; e < nEb; ++e) {
+    ebI[e] = group_offsets(p, I, strides(I, *Eb[e]));
+    ebS[e] = group_offsets(p, S, strides(S, *Eb[e]));
+  }
+  std::vector<int64_t> obI, obS;
+  if (ps_b) {
+    obI = group_offsets(p, I, strides(I, ps_b->out));
+    obS = group_offsets(p, S, strides(S, ps_b->out));
+  }
   const std::vector<int64_t> oI = group_offsets(p, I, strides(I, ps.out));
   const std::vector<int64_t> oS = group_offsets(p, S, strides(S, ps.out));
   const int64_t nI = (int64_t)oI.size(), nS = (int64_t)oS.size();
@@ -1083,6 +1106,9 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   for (int e = 0; e < nE; ++e)
     if (!fits(eI[e]) || !fits(eS[e])) return JT_ERR_UNSUPPORTED;
   if (!fits(oI) || !fits(oS)) return JT_ERR_UNSUPPORTED;
+  for (int e = 0; e < nEb; ++e)
+    if (!fits(ebI[e]) || !fits(ebS[e])) return JT_ERR_UNSUPPORTED;
+  if (ps_b && (!fits(obI) || !fits(obS))) return JT_ERR_UNSUPPORTED;
   // W[i][k][s'] = Σ_R base: walk the clique once, odometer over its variables
   // nS == 1 uses the row-per-i kernel
   const bool rowi = nS == 1;
@@ -1138,6 +1164,10 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
     for (int g = 0; g < nG; ++g) hp.ctab.push_back((int32_t)gI[g][i]);
     for (int e = 0; e < nE; ++e) hp.ctab.push_back((int32_t)eI[e][i]);
     hp.ctab.push_back((int32_t)oI[i]);
+    if (ps_b) {
+      for (int e = 0; e < nEb; ++e) hp.ctab.push_back((int32_t)ebI[e][i]);
+      hp.ctab.push_back((int32_t)obI[i]);
+    }
   }
   cp.tk_off = (int64_t)hp.ctab.size();
   for (int64_t k = 0; k < nK; ++k)
@@ -1146,6 +1176,10 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   for (int64_t x = 0; x < nS; ++x) {
     for (int e = 0; e < nE; ++e) hp.ctab.push_back((int32_t)eS[e][x]);
     hp.ctab.push_back((int32_t)oS[x]);
+    if (ps_b) {
+      for (int e = 0; e < nEb; ++e) hp.ctab.push_back((int32_t)ebS[e][x]);
+      hp.ctab.push_back((int32_t)obS[x]);
+    }
   }
   cp.nI = (int)nI;
   cp.nS = (int)nS;
@@ -1231,6 +1265,18 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   cp.out2_off = ps.out2_off;
   for (int g = 0; g < nG; ++g) cp.gfac_off[g] = G[g]->off;
   for (int e = 0; e < nE; ++e) cp.efac_off[e] = E[e]->off;
+  cp.out_kind_b = OUT_NONE;
+  if (ps_b) {
+    cp.igs = 1;  // the paired epilogue lives in the plain row-per-i kernel
+    cp.rowi = 1;
+    cp.n_units = cp.nT * cp.nCG;
+    cp.out_kind_b = ps_b->out_kind;
+    cp.nE_b = nEb;
+    cp.out_off_b = ps_b->out.off;
+    cp.ratio_off_b = ps_b->ratio_off;
+    cp.out2_off_b = ps_b->out2_off;
+    for (int e = 0; e < nEb; ++e) cp.efac_off_b[e] = Eb[e]->off;
+  }
   return JT_OK;
 }
 
@@ -1291,6 +1337,24 @@ static int validate_waves(const jt_state* st, const std::vector<std::vector<Pass
   return JT_OK;
 }
 
+// Sibling passes of one wave that may share a K-sum (compile_contract with a
+// second output): same clique, same output scope, both contraction passes.
+static std::vector<int> pair_specs(const jt_state* st, const std::vector<PassSpec>& w) {
+  std::vector<int> partner(w.size(), -1);
+  if (!env_int("JT_PAIR", 1)) return partner;
+  for (size_t a = 0; a < w.size(); ++a) {
+    if (partner[a] >= 0 || !contract_eligible(st, w[a]) || w[a].out_kind == OUT_RAW) continue;
+    for (size_t b = a + 1; b < w.size(); ++b) {
+      if (partner[b] >= 0 || !contract_eligible(st, w[b]) || w[b].out_kind == OUT_RAW) continue;
+      if (w[b].clique != w[a].clique || w[b].out.vars != w[a].out.vars) continue;
+      partner[a] = (int)b;
+      partner[b] = (int)a;
+      break;
+    }
+  }
+  return partner;
+}
+
 static int compile_program(const jt_state* st, const std::vector<std::vector<PassSpec>>& waves, HostProgram& hp,
                            int occ_override = 0) {
   auto& passes = hp.passes;
@@ -1324,10 +1388,26 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
     constexpr int NGK = CMAXG + 1;
     std::vector<CPass> cps[8 * NGK];
     std::vector<int> cpc[8 * NGK];
-    for (auto& ps : w) {
+    // row-per-i siblings sharing a K-sum (same clique, output scope and G factors,
+    // e.g. distribute messages to children over equal separators) become ONE pass
+    // with two epilogues: the shared factor rows stream once
+    std::vector<int> partner = pair_specs(st, w);
+    for (size_t wi = 0; wi < w.size(); ++wi) {
+      const PassSpec& ps = w[wi];
+      if (partner[wi] >= 0 && partner[wi] < (int)wi) continue;  // compiled with its partner
       if (contract_eligible(st, ps)) {
         CPass cp;
-        if (compile_contract(st, ps, hp, cp) == JT_OK) {
+        bool paired = false;
+        if (partner[wi] >= 0) {
+          const size_t n_w = hp.w.size(), n_t = hp.ctab.size();
+          paired = compile_contract(st, ps, hp, cp, &w[partner[wi]]) == JT_OK;
+          if (!paired) {  // fall back to two separate passes
+            hp.w.resize(n_w);
+            hp.ctab.resize(n_t);
+            partner[partner[wi]] = -1;
+          }
+        }
+        if (paired || compile_contract(st, ps, hp, cp) == JT_OK) {
           const int key = ((st->esz == 4 && cp.nK > CKF ? 1 : 0) + 2 * cp.rowi) * NGK + (cp.rowi ? 0 : cp.nG);
           cps[key].push_back(cp);
           cpc[key].push_back(ps.clique);
@@ -3267,6 +3347,22 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
     double tot = 0.0;
     for (size_t w = 0; w < waves.size(); ++w) {
       double bytes = 0.0;
+      // paired row-per-i siblings read their shared (K-sum) factors once
+      const std::vector<int> partner = pair_specs(&st, waves[w]);
+      for (size_t a = 0; a < waves[w].size(); ++a) {
+        const int b = partner[a];
+        if (b < 0 || b < (int)a) continue;
+        const auto& A = waves[w][a];
+        for (auto& f : waves[w][b].factors) {
+          if (std::includes(A.out.vars.begin(), A.out.vars.end(), f.vars.begin(), f.vars.end())) continue;
+          bool shared = false;
+          for (auto& g : A.factors) shared = shared || (g.off == f.off && g.vars == f.vars);
+          if (!shared) continue;
+          double n = f.batch ? (double)st.B : 1.0;
+          for (int v : f.vars) n *= plan->cards[v];
+          bytes -= n * st.esz;
+        }
+      }
       for (auto& ps : waves[w]) {
         auto tsize = [&](const Tensor& t) {
           double n = t.batch ? (double)st.B : 1.0;

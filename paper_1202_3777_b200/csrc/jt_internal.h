@@ -126,6 +126,14 @@ struct CPass {
   int64_t out_off, ratio_off, out2_off;
   int64_t gfac_off[MAXF];   // aux offsets of the G factors
   int64_t efac_off[MAXF];   // aux offsets of the E factors
+  // second output (row-per-i passes): a sibling pass of the same clique with the
+  // same output scope and the same K-sum (G factors) -- e.g. the distribute
+  // messages to two children over equal separators -- shares the sum; only its
+  // epilogue factors and output differ.  out_kind_b == OUT_NONE: no second output.
+  // ti rows then hold [G, E, out, E_b, out_b]; ts rows [E, out, E_b, out_b].
+  int out_kind_b, nE_b;
+  int64_t out_off_b, ratio_off_b, out2_off_b;
+  int64_t efac_off_b[MAXF];
 };
 struct CArgs {
   const void* w;

@@ -1415,7 +1415,8 @@ __global__ void __launch_bounds__(NT, FOLD ? ROWI_MINB_F : ROWI_MINB_NF) contrac
     const int cg = P->cmaj ? (int)(ul / P->nI) : (int)(ul % nCG);
     const int64_t i = P->cmaj ? ul % P->nI : ul / nCG;
     const int nK = P->nK, nG = P->nG, nE = P->nE;
-    const int tw = nG + nE + 1;
+    const bool two = P->out_kind_b != OUT_NONE;  // paired sibling output (same K-sum)
+    const int tw = nG + nE + 1 + (two ? P->nE_b + 1 : 0);
     const int32_t* __restrict__ tir = a.tab + P->ti_off + i * tw;
     const int32_t* __restrict__ tk = a.tab + P->tk_off;
     const int32_t* __restrict__ ts = a.tab + P->ts_off;
@@ -1464,9 +1465,9 @@ __global__ void __launch_bounds__(NT, FOLD ? ROWI_MINB_F : ROWI_MINB_NF) contrac
           since = 0;
         }
       }
-      double v[VEC];
+      double vsum[VEC], v[VEC];
 #pragma unroll
-      for (int l = 0; l < VEC; ++l) v[l] = acc[l] + (double)part[l];
+      for (int l = 0; l < VEC; ++l) v[l] = vsum[l] = acc[l] + (double)part[l];
       const bool cs = a.stream_epi != 0;
       for (int e = 0; e < nE; ++e) {
         T f[VEC];
@@ -1482,8 +1483,32 @@ __global__ void __launch_bounds__(NT, FOLD ? ROWI_MINB_F : ROWI_MINB_NF) contrac
         if (cs) load_vec_cs<T, VEC>(aux_c + P->out_off + j, old);
         else load_vec<T, VEC>(aux_c + P->out_off + j, old);
       }
-      if (finalize_lanes<T, double, VEC>(P->out_kind, P->out_off, P->ratio_off, P->out2_off, j, v, old, aux, a.qout, cs))
-        atomicOr(a.err, EB_INCONSISTENT);
+      bool bad = finalize_lanes<T, double, VEC>(P->out_kind, P->out_off, P->ratio_off, P->out2_off, j, v, old, aux,
+                                                a.qout, cs);
+      if (two) {
+        const int32_t* tb = tir + nG + nE + 1;  // [E_b..., out_b] of this i
+        const int32_t* sb = ts + nE + 1;        // [E_b..., out_b] of the (single) s' row
+        const int nEb = P->nE_b;
+#pragma unroll
+        for (int l = 0; l < VEC; ++l) v[l] = vsum[l];
+        for (int e = 0; e < nEb; ++e) {
+          T f[VEC];
+          const T* ep = aux_c + P->efac_off_b[e] + __ldg(tb + e) + __ldg(sb + e) + b0;
+          if (cs) load_vec_cs<T, VEC>(ep, f);
+          else load_vec_ro<T, VEC>(ep, f);
+#pragma unroll
+          for (int l = 0; l < VEC; ++l) v[l] *= (double)f[l];
+        }
+        const int64_t jb = (int64_t)__ldg(tb + nEb) + __ldg(sb + nEb) + b0;
+        T oldb[VEC] = {};
+        if (P->out_kind_b == OUT_SEP || P->out_kind_b == OUT_SEP_DFRESH) {
+          if (cs) load_vec_cs<T, VEC>(aux_c + P->out_off_b + jb, oldb);
+          else load_vec<T, VEC>(aux_c + P->out_off_b + jb, oldb);
+        }
+        bad |= finalize_lanes<T, double, VEC>(P->out_kind_b, P->out_off_b, P->ratio_off_b, P->out2_off_b, jb, v, oldb,
+                                              aux, a.qout, cs);
+      }
+      if (bad) atomicOr(a.err, EB_INCONSISTENT);
     }
   }
 }
