@@ -3352,16 +3352,23 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
       for (size_t a = 0; a < waves[w].size(); ++a) {
         const int b = partner[a];
         if (b < 0 || b < (int)a) continue;
+        // a tensor the paired pass reads for both outputs (a shared factor, or one
+        // output's old separator that is the other's factor) comes from DRAM once
         const auto& A = waves[w][a];
-        for (auto& f : waves[w][b].factors) {
-          if (std::includes(A.out.vars.begin(), A.out.vars.end(), f.vars.begin(), f.vars.end())) continue;
-          bool shared = false;
-          for (auto& g : A.factors) shared = shared || (g.off == f.off && g.vars == f.vars);
-          if (!shared) continue;
-          double n = f.batch ? (double)st.B : 1.0;
-          for (int v : f.vars) n *= plan->cards[v];
-          bytes -= n * st.esz;
+        const auto& Bp = waves[w][b];
+        auto nbytes = [&](const Tensor& t) {
+          double n = t.batch ? (double)st.B : 1.0;
+          for (int v : t.vars) n *= plan->cards[v];
+          return n * st.esz;
+        };
+        auto same = [](const Tensor& x, const Tensor& y) { return x.off == y.off && x.vars == y.vars; };
+        for (auto& f : Bp.factors) {
+          bool dup = same(f, A.out);
+          for (auto& g : A.factors) dup = dup || same(g, f);
+          if (dup) bytes -= nbytes(f);
         }
+        for (auto& g : A.factors)
+          if (same(g, Bp.out)) bytes -= nbytes(g);
       }
       for (auto& ps : waves[w]) {
         auto tsize = [&](const Tensor& t) {
