@@ -1386,8 +1386,12 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
 #ifndef ROWI_MINB_F
 #define ROWI_MINB_F 4
 #endif
+#ifndef ROWI_MINB_D
+#define ROWI_MINB_D 8
+#endif
 template <typename T, bool FOLD>
-__global__ void __launch_bounds__(NT, FOLD ? ROWI_MINB_F : ROWI_MINB_NF) contract_rowi_kernel(const CArgs a) {
+__global__ void __launch_bounds__(NT, FOLD ? ROWI_MINB_F : sizeof(T) == 8 ? ROWI_MINB_D : ROWI_MINB_NF)
+    contract_rowi_kernel(const CArgs a) {
   pdl_enter();
   // one i per warp unit (few registers: three or four CTAs per SM), KU values
   // of k in flight, each with its nG factor-row vectors
@@ -1519,8 +1523,11 @@ __global__ void __launch_bounds__(NT, FOLD ? ROWI_MINB_F : ROWI_MINB_NF) contrac
 // reused by every member (each member multiplies in its own few small factors
 // and W entry), so the large rows stream from DRAM once instead of igs times
 // through L2.  IGM: compile-time bound of igs (registers for the accumulators).
+#ifndef ROWG_MINB
+#define ROWG_MINB 4
+#endif
 template <typename T, bool FOLD, int IGM>
-__global__ void __launch_bounds__(NT, 4) contract_rowg_kernel(const CArgs a) {
+__global__ void __launch_bounds__(NT, ROWG_MINB) contract_rowg_kernel(const CArgs a) {
   pdl_enter();
   constexpr int VEC = CTraits<T>::VEC;
   constexpr int KF = 16;
