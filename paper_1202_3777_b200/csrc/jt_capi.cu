@@ -1209,8 +1209,9 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   cp.n_units = (rowi ? 1 : nI) * cp.nT * cp.nCG;
   int64_t min_units = (int64_t)st->num_sms * 8;
   cp.igs = 1;
-  // (fp64 only: the fp32 fold variant's per-member accumulators spill; measured slower)
-  if (rowi && !I.empty() && env_int("JT_ROWG", st->esz == 8 ? 1 : 0)) {
+  // (opt-in, JT_ROWG=1: measured slower than plain row-per-i once paired passes and
+  // evict-first epilogue streams cut the re-reads it was built against)
+  if (rowi && !I.empty() && env_int("JT_ROWG", 0)) {
     // i-groups: the innermost i variable's values share every factor that does not
     // index it; group them into one warp unit when those shared factors dominate
     const int v = I.back();
@@ -1224,7 +1225,8 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
       (gst[g] == 0 ? shared : own) += n;
     }
     const int64_t units = (nI / igs) * (int64_t)cp.nCG;
-    if (igs >= 2 && igs <= 8 && nI % igs == 0 && shared > own && units >= min_units) {
+    static const int igs_max = env_int("JT_ROWG_MAX", 8);
+    if (igs >= 2 && igs <= igs_max && nI % igs == 0 && shared > own && units >= min_units) {
       cp.rowi = igs <= 4 ? 2 : 3;
       cp.igs = igs;
       for (int g = 0; g < nG; ++g) cp.gstride[g] = gst[g];
