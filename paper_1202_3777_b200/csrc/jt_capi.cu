@@ -1200,8 +1200,8 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
     static const int ncg_mid = env_int("JT_NCG_MID", CON_NCG_MID);
     static const int ncg_long = env_int("JT_NCG_LONG", 1 << 30);
     cp.nCG = nK >= 32 ? std::min(ncg_long, cp.nBC) : nK >= 8 ? std::min(ncg_mid, cp.nBC) : std::min(ncg_small, cp.nBC);
-    // bit 0: rowi passes, bit 1: tile passes (fp64 default: rowi chunk-major, measured +1-3%)
-    const int cmaj = env_int("JT_CMAJ", st->esz == 8 ? 1 : 0);
+    // bit 0: rowi passes, bit 1: tile passes (default: rowi chunk-major, measured +2-6%)
+    const int cmaj = env_int("JT_CMAJ", 1);
     cp.cmaj = (cmaj >> (rowi ? 0 : 1)) & 1;
   }
   cp.nKS = 1;
@@ -1477,9 +1477,9 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
     }
     // JT_SPLIT_CPASS=1: one launch per contraction pass (also what an ncu launch
     // list needs to attribute time and DRAM bytes to single passes)
-    // (default for fp64, where the measured program is 2-6% faster with the passes
+    // (default: the measured program is 2-8% faster with the passes
     // as separate parallel graph branches)
-    if (env_int("JT_SPLIT_CPASS", st->esz == 8 ? 1 : 0)) {
+    if (env_int("JT_SPLIT_CPASS", 1)) {
       std::vector<CPass> cps2[8 * NGK];
       std::vector<int> cpc2[8 * NGK];
       for (int key = 0; key < 8 * NGK; ++key) {
