@@ -231,22 +231,6 @@ struct Program {
   }
 };
 
-// Whole-propagation program for a small tree held in one cluster's shared memory
-// (jt_cluster.cu).  ok == false: the tree does not fit / the device cannot run it.
-struct ClusterProg {
-  bool ok = false;
-  int n_ranks = 0, smem = 0, n_levels = 0, table_elems = 0;
-  ClusterSeg* d_segs = nullptr;
-  int* d_seg_begin = nullptr;
-  int* d_blob = nullptr;
-  ClusterLevel* d_levels = nullptr;
-  ~ClusterProg() {
-    cudaFree(d_segs);
-    cudaFree(d_seg_begin);
-    cudaFree(d_blob);
-    cudaFree(d_levels);
-  }
-};
 
 // ------------------------------------------------------------------ state --
 struct jt_state {
@@ -284,7 +268,6 @@ struct jt_state {
   int64_t fill_cap = 0;
   std::vector<int32_t> fill_host;           // contents of d_fill
   std::map<std::string, std::unique_ptr<Program>> programs;
-  std::map<std::string, std::unique_ptr<struct ClusterProg>> cprogs;  // small trees in cluster smem
   int64_t launches = 0;
   int64_t device_bytes = 0;
   // shared-base mode: cliques whose passes would need more than MAXF factors keep
@@ -317,7 +300,6 @@ struct jt_state {
   std::vector<double> h_base;
   ~jt_state() {
     programs.clear();
-    cprogs.clear();
     cudaFree(d_clique);
     cudaFree(d_base);
     cudaFree(d_aux);
@@ -2693,194 +2675,6 @@ static int resolve_roots(const jt_state* st, const int32_t* roots_or_null, std::
   return JT_OK;
 }
 
-// Build the cluster program of a single-tree (B == 1, materialized) propagation:
-// bin-pack every clique, separator and ratio table onto the fewest cluster
-// ranks whose shared memory holds them, then list the levels (collect by
-// height, distribute by depth) with their messages and target cliques.
-static int build_cluster_prog(jt_state* st, const std::vector<int>& roots, ClusterProg& cp) {
-  const jt_plan* p = st->plan;
-  cp.ok = false;
-  // opt-in (JT_CLUSTER=1): correct (the GPU suite passes with it) but still slower
-  // than the graph-replayed wave program — see profiles/README.md r05
-  if (st->B != 1 || st->mode != JT_MATERIALIZED || !getenv("JT_CLUSTER")) return JT_OK;
-  int optin = 0;
-  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device);
-  const int64_t cap = (int64_t)(optin - 2048) / st->esz;  // elements per rank
-  if (cap <= 0) return JT_OK;
-  // tables: cliques, separators, ratio scratch (one per separator)
-  struct Tab { int64_t size; int kind, id; int rank = -1; int64_t off = 0; };
-  std::vector<Tab> tabs;
-  for (int c = 0; c < p->n_cliques; ++c) tabs.push_back({p->csize[c], 0, c});
-  for (int sp = 0; sp < p->n_seps; ++sp) tabs.push_back({p->ssize[sp], 1, sp});
-  for (int sp = 0; sp < p->n_seps; ++sp) tabs.push_back({p->ssize[sp], 2, sp});
-  for (auto& t : tabs)
-    if (align4(t.size) > cap) return JT_OK;
-  std::vector<int> order(tabs.size());
-  std::iota(order.begin(), order.end(), 0);
-  std::sort(order.begin(), order.end(), [&](int a, int b) { return tabs[a].size > tabs[b].size; });
-  int n_ranks = 0;
-  for (int nr = 1; nr <= CL_MAX_RANKS && !n_ranks; nr *= 2) {  // fewest ranks that hold everything
-    std::vector<int64_t> used(nr, 0);
-    bool fit = true;
-    for (int i : order) {
-      int best = -1;
-      for (int r = 0; r < nr; ++r)
-        if (used[r] + align4(tabs[i].size) <= cap && (best < 0 || used[r] < used[best])) best = r;
-      if (best < 0) {
-        fit = false;
-        break;
-      }
-      tabs[i].rank = best;
-      tabs[i].off = used[best];
-      used[best] += align4(tabs[i].size);
-    }
-    if (fit) n_ranks = nr;
-  }
-  if (!n_ranks) return JT_OK;
-  auto tab_of = [&](int kind, int id) -> const Tab& {
-    return tabs[(kind == 0 ? 0 : kind == 1 ? p->n_cliques : p->n_cliques + p->n_seps) + id];
-  };
-  int64_t table_elems = 0;
-  for (auto& t : tabs) table_elems = std::max<int64_t>(table_elems, t.off + align4(t.size));
-  // segments (HBM <-> shared memory copies), grouped by rank
-  std::vector<ClusterSeg> segs;
-  std::vector<int> seg_begin(n_ranks + 1, 0);
-  for (int r = 0; r < n_ranks; ++r) {
-    seg_begin[r] = (int)segs.size();
-    for (auto& t : tabs) {
-      if (t.kind == 2 || t.rank != r) continue;
-      ClusterSeg g;
-      g.rank = t.rank;
-      g.lofs = (int)t.off;
-      g.len = (int)t.size;
-      g.arena = t.kind == 0 ? A_CLIQUE : A_AUX;
-      g.gofs = t.kind == 0 ? st->coff[t.id] : sep_cur(st, t.id);
-      segs.push_back(g);
-    }
-  }
-  seg_begin[n_ranks] = (int)segs.size();
-  Orient o = orient(p, roots);
-  std::vector<int> blob;
-  std::vector<ClusterLevel> levels;
-  int max_blob = 0;
-  auto strides_of = [&](const std::vector<int>& vars) {
-    std::vector<int64_t> st_(vars.size(), 1);
-    for (int i = (int)vars.size() - 2; i >= 0; --i) st_[i] = st_[i + 1] * p->cards[vars[i + 1]];
-    return st_;
-  };
-  // one level: (src, tgt, sep) messages -> message records, target records
-  auto add_level = [&](const std::vector<std::array<int, 3>>& lm) -> bool {
-    if (lm.empty()) return true;
-    ClusterLevel L{};
-    L.blob_off = (int64_t)blob.size();
-    L.n_msgs = (int)lm.size();
-    std::vector<int> lb((size_t)L.n_msgs * CL_MREC, 0);
-    std::map<int, std::vector<int>> into;  // target clique -> message ordinals
-    for (int mi = 0; mi < L.n_msgs; ++mi) {
-      const int src = lm[mi][0], sp = lm[mi][2];
-      const auto& cv = p->cvars[src];
-      const auto& sv = p->svars[sp];
-      if ((int)cv.size() > CL_MAXD) return false;
-      const auto cst = strides_of(cv);
-      int* M = lb.data() + (size_t)mi * CL_MREC;
-      const Tab &ts = tab_of(0, src), &tsep = tab_of(1, sp), &trat = tab_of(2, sp);
-      M[0] = ts.rank; M[1] = (int)ts.off; M[2] = tsep.rank; M[3] = (int)tsep.off;
-      M[4] = trat.rank; M[5] = (int)trat.off;
-      M[6] = (int)(p->csize[src] / std::max<int64_t>(1, p->ssize[sp]));
-      int nsd = 0, nrd = 0;
-      for (int v : sv) {
-        const int pos = (int)(std::lower_bound(cv.begin(), cv.end(), v) - cv.begin());
-        M[11 + nsd] = p->cards[v];
-        M[11 + CL_MAXD + nsd] = (int)cst[pos];
-        ++nsd;
-      }
-      for (size_t i = 0; i < cv.size(); ++i)
-        if (!std::binary_search(sv.begin(), sv.end(), cv[i])) {
-          M[11 + 2 * CL_MAXD + nrd] = p->cards[cv[i]];
-          M[11 + 3 * CL_MAXD + nrd] = (int)cst[i];
-          ++nrd;
-        }
-      M[7] = nsd;
-      M[8] = nrd;
-      const bool lng = M[6] > 32;
-      M[9] = (int)L.n_short;
-      M[10] = (int)L.n_long;
-      (lng ? L.n_long : L.n_short) += p->ssize[sp];
-      into[lm[mi][1]].push_back(mi);
-    }
-    L.n_tgts = (int)into.size();
-    const size_t toff_at = lb.size();
-    lb.resize(lb.size() + L.n_tgts, 0);
-    int ti = 0;
-    for (auto& kv : into) {
-      const int t = kv.first;
-      const auto& tv = p->cvars[t];
-      const int nd = (int)tv.size(), nin = (int)kv.second.size();
-      if (nd > CL_MAXD || nin > CL_MAXIN) return false;
-      lb[toff_at + ti++] = (int)lb.size();
-      const Tab& tt = tab_of(0, t);
-      lb.push_back(tt.rank);
-      lb.push_back((int)tt.off);
-      lb.push_back((int)p->csize[t]);
-      lb.push_back(nd);
-      lb.push_back(nin);
-      lb.push_back((int)L.n_elem_chunks);
-      for (int d = 0; d < nd; ++d) lb.push_back(p->cards[tv[d]]);
-      for (int k = 0; k < nin; ++k) {
-        const int mi = kv.second[k];
-        const int sp = lm[mi][2];
-        const Tab& trat = tab_of(2, sp);
-        lb.push_back(trat.rank);
-        lb.push_back((int)trat.off);
-        const auto& sv = p->svars[sp];
-        const auto sst = strides_of(sv);
-        for (int d = 0; d < nd; ++d) {
-          auto it = std::lower_bound(sv.begin(), sv.end(), tv[d]);
-          lb.push_back((it != sv.end() && *it == tv[d]) ? (int)sst[it - sv.begin()] : 0);
-        }
-      }
-      L.n_elem_chunks += (p->csize[t] + CL_CHUNK - 1) / CL_CHUNK;
-    }
-    while (lb.size() % 4) lb.push_back(0);  // int4 staging
-    L.blob_len = (int)lb.size();
-    max_blob = std::max(max_blob, L.blob_len);
-    blob.insert(blob.end(), lb.begin(), lb.end());
-    levels.push_back(L);
-    return true;
-  };
-  for (int h = 0; h <= o.max_height; ++h) {  // collect: children of height h send to their parents
-    std::vector<std::array<int, 3>> lm;
-    for (int c = 0; c < p->n_cliques; ++c)
-      if (o.height[c] == h && o.parent[c] >= 0) lm.push_back({c, o.parent[c], o.psep[c]});
-    if (!add_level(lm)) return JT_OK;
-  }
-  for (int d = 0; d <= o.max_depth; ++d) {  // distribute: depth d sends to its children
-    std::vector<std::array<int, 3>> lm;
-    for (int c = 0; c < p->n_cliques; ++c)
-      if (o.depth[c] == d)
-        for (auto& ch : o.children[c]) lm.push_back({c, ch.first, ch.second});
-    if (!add_level(lm)) return JT_OK;
-  }
-  (void)max_blob;
-  const int64_t smem = align4(table_elems) * st->esz;
-  cp.smem = (int)smem;
-  cp.table_elems = (int)align4(table_elems);
-  if (cluster_prop_supported(p->dtype, n_ranks, cp.smem) <= 0) return JT_OK;
-  cp.n_ranks = n_ranks;
-  auto up = [&](auto** dptr, const auto& vec) -> int {
-    using E = typename std::decay_t<decltype(vec)>::value_type;
-    CK(cudaMalloc((void**)dptr, std::max<size_t>(vec.size(), 1) * sizeof(E)));
-    if (!vec.empty()) CK(cudaMemcpy(*dptr, vec.data(), vec.size() * sizeof(E), cudaMemcpyHostToDevice));
-    return JT_OK;
-  };
-  int rc;
-  if ((rc = up(&cp.d_segs, segs)) || (rc = up(&cp.d_seg_begin, seg_begin)) || (rc = up(&cp.d_blob, blob)) ||
-      (rc = up(&cp.d_levels, levels)))
-    return rc;
-  cp.n_levels = (int)levels.size();
-  cp.ok = true;
-  return JT_OK;
-}
 
 // Shared-base states keep only the latest propagation's ratios: the base never
 // absorbs a message, so the Hugin update new/old of a second propagation has no
@@ -2905,36 +2699,6 @@ extern "C" int jt_propagate(jt_state* st, const int32_t* roots_or_null, void* st
   cudaStream_t s = pick_stream(st, stream);
   shared_restart(st);
   const bool fresh = st->fresh;
-  if (st->B == 1 && st->mode == JT_MATERIALIZED) {
-    // small trees: the whole propagation in one cluster's shared memory, one launch
-    const std::string ckey = key_of("cl", roots, {(int)st->sep_in_y});
-    auto cit = st->cprogs.find(ckey);
-    if (cit == st->cprogs.end()) {
-      auto cpn = std::make_unique<ClusterProg>();
-      if ((rc = build_cluster_prog(st, roots, *cpn))) return rc;
-      cit = st->cprogs.emplace(ckey, std::move(cpn)).first;
-    }
-    ClusterProg* cp = cit->second.get();
-    if (cp->ok) {
-      if ((rc = ensure_seps(st, s))) return rc;
-      set_all_exp(st, joint_exp(st));
-      ClusterArgs a;
-      a.clique = st->d_clique;
-      a.aux = st->d_aux;
-      a.err = st->d_err;
-      a.segs = cp->d_segs;
-      a.seg_begin = cp->d_seg_begin;
-      a.blob = cp->d_blob;
-      a.levels = cp->d_levels;
-      a.n_levels = cp->n_levels;
-      a.table_elems = cp->table_elems;
-      CK(launch_cluster_prop(st->plan->dtype, a, cp->n_ranks, cp->smem, s));
-      st->launches++;
-      st->fresh = false;
-      st->seps_stale = false;
-      return JT_OK;
-    }
-  }
   if (!fresh && (rc = ensure_seps(st, s))) return rc;
   std::vector<int> tag{(int)fresh, (int)st->sep_in_y};
   std::vector<int> kv = active_ev(st);

@@ -157,46 +157,6 @@ constexpr int CKF = 16;     // fp32 contraction sums longer than this fold into 
 cudaError_t launch_contract(int dtype, int fold, int rowi, int ng, const CArgs& a, int grid, cudaStream_t s);
 int contract_max_ctas_per_sm(int dtype, int fold, int rowi, int ng);
 
-// ---- small trees in cluster shared memory (jt_cluster.cu) ----
-constexpr int CL_MAX_RANKS = 16;  // CTAs per cluster (non-portable above 8)
-constexpr int CL_MAXD = 12;       // dims per clique
-constexpr int CL_MAXIN = 16;      // messages into one target in one level
-constexpr int CL_CHUNK = 16;      // target elements per thread item
-constexpr int CL_THREADS = 256;
-// Per-level descriptor blob (int32), staged into shared memory at the start of
-// the level.  Message records are CL_MREC ints:
-//   [0] src_rank [1] src_off [2] sep_rank [3] sep_off [4] rat_rank [5] rat_off
-//   [6] L (row length) [7] nsd [8] nrd [9] short0 [10] long0
-//   [11 + d] sd_card, [11 + CL_MAXD + d] sd_stride, [11 + 2 CL_MAXD + d] rd_card,
-//   [11 + 3 CL_MAXD + d] rd_stride
-// Target records follow (offsets in a table after the messages):
-//   rank off size nd nin chunk0 card[nd] then per incoming message:
-//   rat_rank rat_off sstride[nd]
-constexpr int CL_MREC = 11 + 4 * CL_MAXD;
-struct ClusterSeg {               // a table's home: (rank, local offset) <-> HBM copy
-  int rank, lofs, len, arena;
-  int64_t gofs;
-};
-struct ClusterLevel {
-  int64_t blob_off;               // int offset of the level's blob
-  int blob_len;                   // ints
-  int n_msgs, n_tgts;             // message records, then n_tgts target-record offsets, then records
-  int64_t n_short, n_long, n_elem_chunks;
-};
-struct ClusterArgs {
-  void* clique;
-  void* aux;
-  int* err;
-  const ClusterSeg* segs;         // sorted by rank
-  const int* seg_begin;           // [n_ranks + 1]
-  const int* blob;
-  const ClusterLevel* levels;
-  int n_levels;
-  int table_elems;                // shared-memory elements of the largest rank's tables
-};
-cudaError_t launch_cluster_prop(int dtype, const ClusterArgs& a, int n_ranks, int smem_bytes, cudaStream_t s);
-int cluster_prop_supported(int dtype, int n_ranks, int smem_bytes);
-
 // device initialize: one entry per clique, one term per CPT, 3 int64 per CPT variable
 // (clique stride, card, CPT stride)
 struct InitClique {

@@ -403,20 +403,24 @@ def test_batch_from_networks_with_components():
             assert rel_err(got, want) < 1e-10, (name, mode)
 
 
-def test_cluster_smem_propagation_matches_reference(monkeypatch):
-    """Opt-in whole-tree-in-cluster-shared-memory propagation (JT_CLUSTER=1):
-    same posteriors and final tables as the reference on c1 and c2."""
-    monkeypatch.setenv("JT_CLUSTER", "1")
-    for name in ("c1", "c2"):
-        tree, data = load_golden(name)
-        tables = synth.scaled_potentials(tree, 0)
-        for ev, want in golden_cases(data)[:3]:
-            st = P().from_potentials(tree, tables, engine=P().CudaEngine(dtype="f32"))
-            if ev:
-                P().apply_evidence(st, ev)
-            P().belief_propagation(st)
-            got = all_posteriors(st, len(tree.cards))
-            assert rel_err(got, want) < 1e-5, (name, ev)
+def test_tiny_wave_launch_modes_match_reference(monkeypatch):
+    """Small single trees run their small waves as tiny-pass launches (JT_TINY=2,
+    default), or the whole program as one cooperative launch with grid barriers
+    (JT_TINY=1), or the general kernels only (JT_TINY=0): the same posteriors as
+    the reference in every mode, fp32 and fp64, on c1, c2 and c4M."""
+    for mode in ("1", "2", "0"):
+        monkeypatch.setenv("JT_TINY", mode)
+        for name in ("c1", "c2", "c4M"):
+            tree, data = load_golden(name)
+            tables = synth.scaled_potentials(tree, 0)
+            for dtype in ("f32", "f64"):
+                for ev, want in golden_cases(data)[:2]:
+                    st = P().from_potentials(tree, tables, engine=P().CudaEngine(dtype=dtype))
+                    if ev:
+                        P().apply_evidence(st, ev)
+                    P().belief_propagation(st)
+                    got = all_posteriors(st, len(tree.cards))
+                    assert rel_err(got, want) < TOL[dtype], (mode, name, dtype, ev)
 
 
 def test_device_mapping_tables_random_scope_pairs():
