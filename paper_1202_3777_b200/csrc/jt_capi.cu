@@ -1250,9 +1250,12 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   for (int g = 0; g < nG; ++g) cp.gfac_off[g] = G[g]->off;
   for (int e = 0; e < nE; ++e) cp.efac_off[e] = E[e]->off;
   cp.out_kind_b = OUT_NONE;
+  // long K sums on the row-per-i kernel: several k in flight per lane (rowi code 4)
+  static const int longk = env_int("JT_ROWI_LONGK", 16);
+  if (cp.rowi == 1 && longk > 0 && nK >= longk) cp.rowi = 4;
   if (ps_b) {
     cp.igs = 1;  // the paired epilogue lives in the plain row-per-i kernel
-    cp.rowi = 1;
+    cp.rowi = cp.rowi == 4 ? 4 : 1;
     cp.n_units = cp.nT * cp.nCG;
     cp.out_kind_b = ps_b->out_kind;
     cp.nE_b = nEb;
@@ -1370,8 +1373,8 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
     // contraction launch groups keyed by (fold, rowi, nG): fold = fp32 sums over > CKF
     // terms fold into fp64; nG is a compile-time parameter of the tile kernel
     constexpr int NGK = CMAXG + 1;
-    std::vector<CPass> cps[8 * NGK];
-    std::vector<int> cpc[8 * NGK];
+    std::vector<CPass> cps[10 * NGK];
+    std::vector<int> cpc[10 * NGK];
     // row-per-i siblings sharing a K-sum (same clique, output scope and G factors,
     // e.g. distribute messages to children over equal separators) become ONE pass
     // with two epilogues: the shared factor rows stream once
@@ -1462,13 +1465,13 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
     // (default: the measured program is 2-8% faster with the passes
     // as separate parallel graph branches)
     if (env_int("JT_SPLIT_CPASS", 1)) {
-      std::vector<CPass> cps2[8 * NGK];
-      std::vector<int> cpc2[8 * NGK];
-      for (int key = 0; key < 8 * NGK; ++key) {
+      std::vector<CPass> cps2[10 * NGK];
+      std::vector<int> cpc2[10 * NGK];
+      for (int key = 0; key < 10 * NGK; ++key) {
         cps2[key].swap(cps[key]);
         cpc2[key].swap(cpc[key]);
       }
-      for (int key = 0; key < 8 * NGK; ++key)
+      for (int key = 0; key < 10 * NGK; ++key)
         for (size_t q = 0; q < cps2[key].size(); ++q) {
           const int fold = (key / NGK) & 1;
           LaunchGrp cg;
@@ -1488,7 +1491,7 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
           rt.groups.push_back(cg);
         }
     }
-    for (int key = 0; key < 8 * NGK; ++key) {
+    for (int key = 0; key < 10 * NGK; ++key) {
       const int fold = (key / NGK) & 1;
       if (cps[key].empty()) continue;
       LaunchGrp cg;

@@ -1389,14 +1389,23 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
 #ifndef ROWI_MINB_D
 #define ROWI_MINB_D 8
 #endif
-template <typename T, bool FOLD>
-__global__ void __launch_bounds__(NT, FOLD ? ROWI_MINB_F : sizeof(T) == 8 ? ROWI_MINB_D : ROWI_MINB_NF)
+// LONGK: passes with long K sums (nK >= 16) keep ROWI_KU_L values of k in flight
+// per lane (their loads would otherwise chain one memory latency per k) at a
+// larger register budget
+#ifndef ROWI_KU_L
+#define ROWI_KU_L 4
+#endif
+#ifndef ROWI_MINB_L
+#define ROWI_MINB_L 4
+#endif
+template <typename T, bool FOLD, bool LONGK = false>
+__global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F : sizeof(T) == 8 ? ROWI_MINB_D : ROWI_MINB_NF)
     contract_rowi_kernel(const CArgs a) {
   pdl_enter();
   // one i per warp unit (few registers: three or four CTAs per SM), KU values
   // of k in flight, each with its nG factor-row vectors
   constexpr int VEC = CTraits<T>::VEC;
-  constexpr int KU = FOLD ? ROWI_KU_F : ROWI_KU_NF;
+  constexpr int KU = LONGK ? ROWI_KU_L : FOLD ? ROWI_KU_F : ROWI_KU_NF;
   constexpr int KF = 16;
   T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
   const T* __restrict__ aux_c = aux;
@@ -1695,7 +1704,7 @@ static auto by_ng(int ng, F f) {
 
 cudaError_t launch_contract(int dtype, int fold, int rowi, int ng, const CArgs& a, int grid, cudaStream_t s) {
   if (grid <= 0 || a.n_units <= 0) return cudaSuccess;
-  if (rowi >= 2) {  // i-groups: IGM 4 (rowi 2) or 8 (rowi 3)
+  if (rowi == 2 || rowi == 3) {  // i-groups: IGM 4 (rowi 2) or 8 (rowi 3)
     if (dtype == 0) {
       if (fold)
         return rowi == 2 ? launch_pdl(contract_rowg_kernel<float, true, 4>, grid, NT, 0, s, a)
@@ -1708,9 +1717,12 @@ cudaError_t launch_contract(int dtype, int fold, int rowi, int ng, const CArgs& 
   }
   if (rowi) {
     if (dtype == 0)
-      return fold ? launch_pdl(contract_rowi_kernel<float, true>, grid, NT, 0, s, a)
-                  : launch_pdl(contract_rowi_kernel<float, false>, grid, NT, 0, s, a);
-    return launch_pdl(contract_rowi_kernel<double, false>, grid, NT, 0, s, a);
+      return rowi == 4 ? (fold ? launch_pdl(contract_rowi_kernel<float, true, true>, grid, NT, 0, s, a)
+                               : launch_pdl(contract_rowi_kernel<float, false, true>, grid, NT, 0, s, a))
+             : fold ? launch_pdl(contract_rowi_kernel<float, true>, grid, NT, 0, s, a)
+                    : launch_pdl(contract_rowi_kernel<float, false>, grid, NT, 0, s, a);
+    return rowi == 4 ? launch_pdl(contract_rowi_kernel<double, false, true>, grid, NT, 0, s, a)
+                     : launch_pdl(contract_rowi_kernel<double, false>, grid, NT, 0, s, a);
   }
   if (dtype == 0 && fold)
     return by_ng<float, true>(ng, [&](auto c) { return launch_contract_t<float, true, decltype(c)::value>(a, grid, s); });
@@ -1721,7 +1733,7 @@ cudaError_t launch_contract(int dtype, int fold, int rowi, int ng, const CArgs& 
 
 int contract_max_ctas_per_sm(int dtype, int fold, int rowi, int ng) {
   int n = 0;
-  if (rowi >= 2) {
+  if (rowi == 2 || rowi == 3) {
     if (dtype == 0 && fold)
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rowi == 2 ? contract_rowg_kernel<float, true, 4>
                                                                   : contract_rowg_kernel<float, true, 8>, NT, 0);
@@ -1734,9 +1746,16 @@ int contract_max_ctas_per_sm(int dtype, int fold, int rowi, int ng) {
     return n > 0 ? n : 1;
   }
   if (rowi) {
-    if (dtype == 0 && fold) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_rowi_kernel<float, true>, NT, 0);
-    else if (dtype == 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_rowi_kernel<float, false>, NT, 0);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, contract_rowi_kernel<double, false>, NT, 0);
+    const bool lk = rowi == 4;
+    if (dtype == 0 && fold)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lk ? contract_rowi_kernel<float, true, true>
+                                                           : contract_rowi_kernel<float, true>, NT, 0);
+    else if (dtype == 0)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lk ? contract_rowi_kernel<float, false, true>
+                                                           : contract_rowi_kernel<float, false>, NT, 0);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lk ? contract_rowi_kernel<double, false, true>
+                                                           : contract_rowi_kernel<double, false>, NT, 0);
     return n > 0 ? n : 1;
   }
   if (dtype == 0 && fold) return by_ng<float, true>(ng, [&](auto c) { return occ_contract_t<float, true, decltype(c)::value>(); });
