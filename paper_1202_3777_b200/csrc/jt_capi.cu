@@ -1250,8 +1250,9 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   for (int g = 0; g < nG; ++g) cp.gfac_off[g] = G[g]->off;
   for (int e = 0; e < nE; ++e) cp.efac_off[e] = E[e]->off;
   cp.out_kind_b = OUT_NONE;
-  // long K sums on the row-per-i kernel: several k in flight per lane (rowi code 4)
-  static const int longk = env_int("JT_ROWI_LONGK", 16);
+  // long K sums on the row-per-i kernel: several k in flight per lane (rowi code 4);
+  // fp64 only (fp32 long sums fold, at two k per step already; measured -2% with it)
+  const int longk = env_int("JT_ROWI_LONGK", st->esz == 8 ? 16 : 0);
   if (cp.rowi == 1 && longk > 0 && nK >= longk) cp.rowi = 4;
   if (ps_b) {
     cp.igs = 1;  // the paired epilogue lives in the plain row-per-i kernel
