@@ -1236,8 +1236,14 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
     cp.cnt_off = hp.n_cnt;
     hp.n_cnt += groups;
   }
-  // too few units to fill the GPU (e.g. a posterior over a long factor row):
-  // the chunked thread-owned/general passes parallelise over the clique instead
+  // too few units: first split the case chunks finer (more units of fewer chunks,
+  // e.g. leaf messages with short sums over a few thousand separator rows)
+  while (cp.nKS == 1 && cp.n_units < min_units && cp.nCG < cp.nBC) {
+    cp.nCG = std::min(cp.nBC, cp.nCG * 2);
+    cp.n_units = (rowi ? 1 : nI) * cp.nT * cp.nCG;
+  }
+  // still too few (e.g. a posterior over a long factor row): the chunked
+  // thread-owned/general passes parallelise over the clique instead
   if (cp.n_units < min_units) {
     hp.w.resize(w0);
     hp.ctab.resize(cp.ti_off);
