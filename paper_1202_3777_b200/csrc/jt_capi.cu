@@ -1350,15 +1350,17 @@ static std::vector<int> pair_specs(const jt_state* st, const std::vector<PassSpe
 }
 
 static int compile_program(const jt_state* st, const std::vector<std::vector<PassSpec>>& waves, HostProgram& hp,
-                           int occ_override = 0) {
+                           int occ_override = 0, const std::vector<std::vector<char>>* skip = nullptr) {
   auto& passes = hp.passes;
   auto& items = hp.items;
   auto& blk = hp.blk;
   auto& bins = hp.bins;
   int64_t& n_part = hp.n_part;
   int64_t& n_cnt = hp.n_cnt;
-  for (auto& w : waves) {
+  for (size_t wix = 0; wix < waves.size(); ++wix) {
+    const auto& w = waves[wix];
     if (w.empty()) continue;
+    auto skipped = [&](size_t q) { return skip && !(*skip)[wix].empty() && (*skip)[wix][q]; };
     WaveRt rt;
     rt.pass_base = (int64_t)passes.size();
     rt.item_base = (int64_t)items.size();
@@ -1388,6 +1390,7 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
     std::vector<int> partner = pair_specs(st, w);
     for (size_t wi = 0; wi < w.size(); ++wi) {
       const PassSpec& ps = w[wi];
+      if (skipped(wi)) continue;  // a tiny pass (jt_tiny.cu)
       if (partner[wi] >= 0 && partner[wi] < (int)wi) continue;  // compiled with its partner
       if (contract_eligible(st, ps)) {
         CPass cp;
@@ -1547,33 +1550,58 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
 #ifndef TINY_WAVE_LOG2
 #define TINY_WAVE_LOG2 18
 #endif
+#ifndef TINY_ROW_MAX
+#define TINY_ROW_MAX 0
+#endif
 static int tiny_mode() { return env_int("JT_TINY", 2); }
 
-static bool tiny_choice(const jt_state* st, const std::vector<std::vector<PassSpec>>& waves,
-                        std::vector<char>& per_wave) {
-  per_wave.clear();
+// Row shape of a pass as a tiny pass: output entries x row length (merged dims).
+static void tiny_shape(const jt_state* st, const PassSpec& ps, int64_t& n_out, int64_t& n_rest) {
+  const std::vector<Dim> dims = merge_dims(pass_dims(st, ps), (int)ps.factors.size());
+  n_out = n_rest = 1;
+  for (const Dim& d : dims) ((ps.out_kind == OUT_NONE || d.out != 0) ? n_out : n_rest) *= d.card;
+}
+
+// Per wave and pass: run as a tiny pass?  Mode 2: every pass of a wave touching
+// at most 2^JT_TINY_WAVE_LOG2 elements, and (JT_TINY_ROW_MAX > 0) any pass whose
+// rows are at most that long; mode 1: all passes when every wave is small.
+static bool tiny_masks(const jt_state* st, const std::vector<std::vector<PassSpec>>& waves,
+                       std::vector<std::vector<char>>& mask) {
+  mask.assign(waves.size(), {});
   const int mode = tiny_mode();
   if (st->B != 1 || st->mode != JT_MATERIALIZED || mode == 0) return false;
   static const int lg = env_int("JT_TINY_MAX_LOG2", TINY_MAX_LOG2);
   static const int lgw = env_int("JT_TINY_WAVE_LOG2", TINY_WAVE_LOG2);
+  static const int row_max = env_int("JT_TINY_ROW_MAX", TINY_ROW_MAX);
   int nw = 0, ntiny = 0;
   bool all_small = true;
-  for (auto& w : waves) {
+  for (size_t wi = 0; wi < waves.size(); ++wi) {
+    const auto& w = waves[wi];
+    mask[wi].assign(w.size(), 0);
     if (w.empty()) continue;
     ++nw;
     int64_t el = 0;
-    for (auto& ps : w) {
-      const auto dd = pass_dims(st, ps);
-      int64_t n = 1;
-      for (auto& x : dd) n *= x.card;
-      el += n;
+    std::vector<int64_t> rows(w.size());
+    for (size_t q = 0; q < w.size(); ++q) {
+      int64_t no, nr;
+      tiny_shape(st, w[q], no, nr);
+      el += no * nr;
+      rows[q] = nr;
     }
     all_small = all_small && el <= (int64_t(1) << lg);
-    const bool t = mode == 1 || el <= (int64_t(1) << lgw);
-    per_wave.push_back(t ? 1 : 0);
-    ntiny += t;
+    for (size_t q = 0; q < w.size(); ++q) {
+      const bool t = mode == 1 || el <= (int64_t(1) << lgw) || (row_max > 0 && rows[q] <= row_max);
+      mask[wi][q] = t ? 1 : 0;
+      ntiny += t;
+    }
   }
-  if (mode == 1) return all_small && nw >= 3;
+  if (mode == 1) {
+    if (!(all_small && nw >= 3)) {
+      for (auto& m : mask) std::fill(m.begin(), m.end(), 0);
+      return false;
+    }
+    return true;
+  }
   return ntiny > 0 && nw >= 2;
 }
 
@@ -1588,15 +1616,18 @@ static void fast_div(int64_t d, unsigned& mul, int& shr) {
 // Tiny passes of a program: per pass, the merged dims split into output dims
 // (those the output tensor indexes; every dim when there is no output) and row
 // dims; one thread per output entry, one warp when the row is long.
-static int build_tiny(const jt_state* st, const std::vector<std::vector<PassSpec>>& waves, std::vector<TPass>& tp,
-                      std::vector<TinyWave>& tw) {
+static int build_tiny(const jt_state* st, const std::vector<std::vector<PassSpec>>& waves,
+                      const std::vector<std::vector<char>>& mask, std::vector<TPass>& tp, std::vector<TinyWave>& tw) {
   auto fits = [](int64_t x) { return x >= INT32_MIN && x <= INT32_MAX; };
-  for (auto& w : waves) {
+  for (size_t wi = 0; wi < waves.size(); ++wi) {
+    const auto& w = waves[wi];
     if (w.empty()) continue;
     TinyWave wv{};
     wv.pass0 = (int64_t)tp.size();
     int64_t units = 0;
-    for (auto& ps : w) {
+    for (size_t q = 0; q < w.size(); ++q) {
+      if (!mask[wi][q]) continue;
+      const PassSpec& ps = w[q];
       const int nf = (int)ps.factors.size();
       if (nf > MAXF || (ps.write && !ps.scope.empty())) return JT_ERR_UNSUPPORTED;
       const std::vector<Dim> dims = merge_dims(pass_dims(st, ps), nf);
@@ -1661,16 +1692,22 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
   HostProgram hp;
   int rc0 = validate_waves(st, waves);
   if (rc0) return rc0;
-  rc0 = compile_program(st, waves, hp);
+  std::vector<std::vector<char>> tmask;
+  std::vector<TPass> tp;
+  std::vector<TinyWave> tw;
+  bool tiny = tiny_masks(st, waves, tmask);
+  if (tiny && (build_tiny(st, waves, tmask, tp, tw) != JT_OK || tp.empty())) {
+    tiny = false;
+    tp.clear();
+    tw.clear();
+  }
+  rc0 = compile_program(st, waves, hp, 0, tiny ? &tmask : nullptr);
   if (rc0) return rc0;
   auto prog = std::make_unique<Program>();
   prog->waves = hp.waves;
   for (auto& w : hp.waves) prog->n_launches += (int64_t)w.groups.size();
-  std::vector<char> tiny_w;
-  if (tiny_choice(st, waves, tiny_w)) {
-    std::vector<TPass> tp;
-    std::vector<TinyWave> tw;
-    if (build_tiny(st, waves, tp, tw) == JT_OK && !tw.empty()) {
+  if (tiny) {
+    {
       int occ = 1, nfm = 1;
       for (auto& x : tp) nfm = std::max(nfm, x.nf);
       TinyArgs dummy{};
@@ -1684,12 +1721,12 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
       prog->n_launches = 1;
       prog->tiny_waves_launch = tiny_mode() == 2;
       if (prog->tiny_waves_launch) {
-        prog->tiny_w = tiny_w;
         prog->n_launches = 0;
         for (size_t w = 0; w < tw.size(); ++w) {
           prog->tiny_wave_grid.push_back(
               (int)std::min<int64_t>((tw[w].n_threads + NT - 1) / NT, (int64_t)occ * st->num_sms));
-          prog->n_launches += tiny_w[w] ? 1 : (int64_t)hp.waves[w].groups.size();
+          prog->tiny_w.push_back(tw[w].n_passes > 0 ? 1 : 0);
+          prog->n_launches += (tw[w].n_passes > 0 ? 1 : 0) + (int64_t)hp.waves[w].groups.size();
         }
       }
       std::vector<int64_t> u0;
@@ -1815,14 +1852,18 @@ static int launch_program_waves(jt_state* st, Program* pr, cudaStream_t s) {
   int wi = -1;
   for (auto& w : pr->waves) {
     ++wi;
-    if (pr->tiny && pr->tiny_waves_launch && pr->tiny_w[wi]) {
-      CK(launch_tiny_wave(st->plan->dtype, pr->tiny_nfm, ta, wi, pr->tiny_wave_grid[wi], s));
+    // the wave's tiny passes run as one more (independent) launch group
+    const bool has_tiny = pr->tiny && pr->tiny_waves_launch && pr->tiny_w[wi];
+    const int ng = (int)w.groups.size() + (has_tiny ? 1 : 0);
+    auto launch_gi = [&](int gi, cudaStream_t gs) -> int {
+      if (gi < (int)w.groups.size()) return launch_group(st, pr, w, w.groups[gi], gs);
+      CK(launch_tiny_wave(st->plan->dtype, pr->tiny_nfm, ta, wi, pr->tiny_wave_grid[wi], gs));
       st->launches++;
-      continue;
-    }
-    const int ng = (int)w.groups.size();
+      return JT_OK;
+    };
+    if (ng == 0) continue;
     if (ng == 1) {
-      int rc = launch_group(st, pr, w, w.groups[0], s);
+      int rc = launch_gi(0, s);
       if (rc) return rc;
       continue;
     }
@@ -1834,7 +1875,7 @@ static int launch_program_waves(jt_state* st, Program* pr, cudaStream_t s) {
     for (int i = 0; i < nside; ++i) CK(cudaStreamWaitEvent(st->side[i], st->ev_fork, 0));
     for (int gi = 0; gi < ng; ++gi) {
       cudaStream_t gs = gi == 0 ? s : st->side[(gi - 1) % jt_state::N_SIDE];
-      if ((rc = launch_group(st, pr, w, w.groups[gi], gs))) return rc;
+      if ((rc = launch_gi(gi, gs))) return rc;
     }
     for (int i = 0; i < nside; ++i) {
       CK(cudaEventRecord(st->ev_join[i], st->side[i]));
@@ -3097,20 +3138,22 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
   rc = validate_waves(&st, waves);
   if (rc) return rc;
   HostProgram hp;
-  rc = compile_program(&st, waves, hp, occ > 0 ? occ : 2);
+  std::vector<std::vector<char>> tmask;
+  std::vector<TPass> tp;
+  std::vector<TinyWave> tw;
+  bool tiny = tiny_masks(&st, waves, tmask);
+  if (tiny && (build_tiny(&st, waves, tmask, tp, tw) != JT_OK || tp.empty())) tiny = false;
+  rc = compile_program(&st, waves, hp, occ > 0 ? occ : 2, tiny ? &tmask : nullptr);
   if (rc) return rc;
   std::string out;
   char line[512];
-  std::vector<char> tiny_w;
-  if (tiny_choice(&st, waves, tiny_w)) {
-    std::vector<TPass> tp;
-    std::vector<TinyWave> tw;
-    if (build_tiny(&st, waves, tp, tw) == JT_OK) {
+  if (tiny) {
+    {
       int64_t warp_passes = 0, threads = 0;
       for (auto& x : tp) warp_passes += x.warp > 1;
       for (auto& x : tw) threads += x.n_threads;
       int64_t nt = 0;
-      for (char x : tiny_w) nt += x;
+      for (auto& x : tw) nt += x.n_passes > 0;
       snprintf(line, sizeof line, "tiny passes (mode %d): %lld of %zu waves, %zu passes (%lld with several lanes per "
                "entry), %lld threads over all waves\n", tiny_mode(), (long long)nt, tw.size(), tp.size(),
                (long long)warp_passes, (long long)threads);
