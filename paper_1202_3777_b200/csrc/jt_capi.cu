@@ -1154,15 +1154,6 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   cp.tk_off = (int64_t)hp.ctab.size();
   for (int64_t k = 0; k < nK; ++k)
     for (int g = 0; g < nG; ++g) hp.ctab.push_back((int32_t)gK[g][k]);
-  // linear k-offsets (the usual case: K' is one variable, or its variables merge)
-  cp.klin = env_int("JT_KLIN", 1) ? 1 : 0;
-  for (int g = 0; g < nG && cp.klin; ++g) {
-    const int64_t st1 = nK > 1 ? gK[g][1] : 0;
-    if (st1 > INT32_MAX) cp.klin = 0;
-    for (int64_t k = 0; k < nK && cp.klin; ++k)
-      if (gK[g][k] != k * st1) cp.klin = 0;
-    if (cp.klin) cp.kstride[g] = (int)st1;
-  }
   cp.ts_off = (int64_t)hp.ctab.size();
   for (int64_t x = 0; x < nS; ++x) {
     for (int e = 0; e < nE; ++e) hp.ctab.push_back((int32_t)eS[e][x]);

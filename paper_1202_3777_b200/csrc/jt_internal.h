@@ -131,8 +131,6 @@ struct CPass {
   // messages to two children over equal separators -- shares the sum; only its
   // epilogue factors and output differ.  out_kind_b == OUT_NONE: no second output.
   // ti rows then hold [G, E, out, E_b, out_b]; ts rows [E, out, E_b, out_b].
-  int klin;                 // 1: every G factor's k-offset is k * kstride[g] (K' one variable,
-  int kstride[CMAXG];       //    or mergeable): no per-k table lookups
   int out_kind_b, nE_b;
   int64_t out_off_b, ratio_off_b, out2_off_b;
   int64_t efac_off_b[MAXF];

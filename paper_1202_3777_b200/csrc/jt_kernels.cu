@@ -1219,18 +1219,10 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
     const T* gq[NG > 0 ? NG : 1];  // factor g at (i, k = kb, case 0)
 #pragma unroll
     for (int g = 0; g < NG; ++g) gq[g] = aux_c + P->gfac_off[g] + __ldg(ti + g);
-    const bool klin = P->klin != 0;
-    int kst[NG > 0 ? NG : 1];
-#pragma unroll
-    for (int g = 0; g < NG; ++g) {
-      kst[g] = P->kstride[g];
-      if (klin) gq[g] += (int64_t)kb * kst[g];  // k below is relative to kb (the K-split chunk)
-    }
     for (int b0 = cg * 32 * VEC + lane * VEC; b0 < a.B; b0 += bstep) {
       auto issue = [&](int k, unsigned char* sp) {
 #pragma unroll
-        for (int g = 0; g < NG; ++g)
-          cp_async16(sp + g * 512, gq[g] + b0 + (klin ? k * kst[g] : __ldg(tk + k * NG + g)));
+        for (int g = 0; g < NG; ++g) cp_async16(sp + g * 512, gq[g] + b0 + __ldg(tk + k * NG + g));
       };
       if (NG > 0) {
 #pragma unroll
@@ -1444,10 +1436,6 @@ __global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F :
     const T* gq[CMAXG];
 #pragma unroll
     for (int g = 0; g < CMAXG; ++g) gq[g] = aux_c + (g < nG ? P->gfac_off[g] + __ldg(tir + g) : 0);
-    const bool klin = P->klin != 0;
-    int kst[CMAXG];
-#pragma unroll
-    for (int g = 0; g < CMAXG; ++g) kst[g] = g < nG ? P->kstride[g] : 0;
     const T* __restrict__ wrow = W + P->w_off + i * (int64_t)nK;
     const int bstep = 32 * VEC * nCG;
     for (int b0 = cg * 32 * VEC + lane * VEC; b0 < a.B; b0 += bstep) {
@@ -1470,7 +1458,7 @@ __global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F :
           for (int g = 0; g < CMAXG; ++g) {
             if (g < nG) {
               T f[VEC];
-              load_vec_ro<T, VEC>(gq[g] + b0 + (klin ? kq * kst[g] : __ldg(tk + kq * nG + g)), f);
+              load_vec_ro<T, VEC>(gq[g] + b0 + __ldg(tk + kq * nG + g), f);
 #pragma unroll
               for (int l = 0; l < VEC; ++l) pv[q][l] *= f[l];
             }
