@@ -240,11 +240,12 @@ class BatchPropagator:
         raw = C.c_void_p(self.stream.cuda_stream)
         with torch.cuda.stream(self.stream):
             for s in range(steps):
-                obs = self.encode_obs(cases[s * self.batch:(s + 1) * self.batch])
+                lo, hi = s * self.batch, min(n, (s + 1) * self.batch)
+                obs = self.encode_obs(cases[lo:hi])
                 d_obs = torch.from_numpy(obs).pin_memory().to(self.torch_device, non_blocking=True)
                 self.step_device(d_obs, out[s * self.batch:(s + 1) * self.batch], raw)
-            if to_host:
-                host.copy_(out[:n], non_blocking=True)
+                if to_host:  # this micro-batch's posteriors cross PCIe while the next one runs
+                    host[lo:hi].copy_(out[lo:hi], non_blocking=True)
         caller.wait_stream(self.stream)
         if to_host:
             self.stream.synchronize()

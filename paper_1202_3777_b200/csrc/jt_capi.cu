@@ -235,7 +235,8 @@ struct Program {
 // ------------------------------------------------------------------ state --
 struct jt_state {
   const jt_plan* plan = nullptr;
-  int B = 1;
+  int B = 1;       // case lanes of every batched tensor (padded, see padded_batch)
+  int B_user = 1;  // cases the caller asked for: API bounds, posterior rows
   int mode = JT_MATERIALIZED;
   int esz = 4;
   int num_sms = 148;
@@ -345,6 +346,20 @@ struct DevGuard {
 };
 
 static int smallest_holder(const jt_plan* p, int v);
+
+// Case lanes: micro-batches above one thread-owned block (NT*VEC lanes) are
+// padded to a whole number of blocks, others of >= one case chunk (32*VEC
+// lanes) to whole chunks, so every pass keeps its vector, thread-owned and
+// K-split kernels (an odd size such as 4000 otherwise fell to the general kernels
+// at half the speed, or failed to plan in fp64).  Padded lanes carry no evidence,
+// are propagated like any case and never reach the caller.
+static int padded_batch(const jt_plan* plan, int batch) {
+  const int vec = plan->dtype == JT_F32 ? 4 : 2;
+  const int L = NT * vec, chunk = 32 * vec;
+  if (batch > L) return (batch + L - 1) / L * L;
+  if (batch >= chunk) return (batch + chunk - 1) / chunk * chunk;
+  return batch;
+}
 
 static void layout_state(jt_state* st) {
   const jt_plan* plan = st->plan;
@@ -456,7 +471,8 @@ extern "C" int jt_state_create(const jt_plan* plan, int batch, int mode, jt_stat
   DevGuard g(plan->device);
   auto st = std::make_unique<jt_state>();
   st->plan = plan;
-  st->B = batch;
+  st->B = padded_batch(plan, batch);
+  st->B_user = batch;
   st->mode = mode;
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, plan->device));
@@ -2265,7 +2281,7 @@ static int ensure_seps(jt_state* st, cudaStream_t s) {
 
 // ------------------------------------------------------------------ C ABI --
 extern "C" int jt_state_load(jt_state* st, int case_idx, const double* clique_concat, const double* sep_concat) {
-  if (!st || case_idx < -1 || case_idx >= st->B) return JT_ERR_BAD_ARG;
+  if (!st || case_idx < -1 || case_idx >= st->B_user) return JT_ERR_BAD_ARG;
   const jt_plan* p = st->plan;
   DevGuard g(p->device);
   const bool shared = st->mode == JT_SHARED_BASE;
@@ -2442,7 +2458,7 @@ extern "C" int jt_state_initialize(jt_state* st, int n_cpts, const int32_t* cpt_
 }
 
 extern "C" int jt_state_store(jt_state* st, int case_idx, double* clique_concat, double* sep_concat) {
-  if (!st || case_idx < 0 || case_idx >= st->B) return JT_ERR_BAD_ARG;
+  if (!st || case_idx < 0 || case_idx >= st->B_user) return JT_ERR_BAD_ARG;
   const jt_plan* p = st->plan;
   DevGuard g(p->device);
   if (st->mode == JT_SHARED_BASE && clique_concat) return JT_ERR_UNSUPPORTED;
@@ -2641,7 +2657,7 @@ extern "C" int jt_apply_evidence(jt_state* st, int n, const int32_t* case_idx, c
   std::vector<int32_t> obs(3 * (size_t)n);
   for (int i = 0; i < n; ++i) {
     const int b = case_idx ? case_idx[i] : -1;
-    if (b < -1 || b >= st->B || value[i] < 0 || value[i] >= p->cards[var[i]]) return JT_ERR_BAD_ARG;
+    if (b < -1 || b >= st->B_user || value[i] < 0 || value[i] >= p->cards[var[i]]) return JT_ERR_BAD_ARG;
     obs[3 * i] = b;
     obs[3 * i + 1] = var[i];
     obs[3 * i + 2] = value[i];
@@ -2827,7 +2843,7 @@ static int finish_query(jt_state* st, int n, const int32_t* var, int normalize, 
     CK(cudaMemcpyAsync(st->d_qexp, exps.data(), exps.size() * sizeof(int), cudaMemcpyHostToDevice, s));
     d_qexp = st->d_qexp;
   }
-  CK(launch_normalize(st->d_qout, dqo, dqc, dqcol, n, st->B, cols, normalize, out_device, st->d_err, d_qexp,
+  CK(launch_normalize(st->d_qout, dqo, dqc, dqcol, n, st->B, st->B_user, cols, normalize, out_device, st->d_err, d_qexp,
                       exp_all, s));
   st->launches++;
   if (total_cols_out) *total_cols_out = cols;
@@ -2924,7 +2940,7 @@ extern "C" int jt_query(jt_state* st, int n, const int32_t* var, const int32_t* 
     if (var[i] < 0 || var[i] >= p->n_vars) return JT_ERR_BAD_ARG;
     cols += p->cards[var[i]];
   }
-  const int64_t need = cols * st->B;
+  const int64_t need = cols * st->B_user;
   if (need > st->post_cap) {
     cudaFree(st->d_post);
     st->d_post = nullptr;
@@ -3120,7 +3136,8 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
   if (!plan || !buf || len <= 0 || batch < 1) return JT_ERR_BAD_ARG;
   jt_state st;
   st.plan = plan;
-  st.B = batch;
+  st.B = padded_batch(plan, batch);
+  st.B_user = batch;
   st.mode = mode;
   st.num_sms = num_sms > 0 ? num_sms : 148;
   layout_state(&st);

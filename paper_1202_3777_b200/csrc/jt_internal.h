@@ -227,7 +227,7 @@ constexpr int CHUNK_GROUP = 32;  // chunk partials combined in groups of this ma
 cudaError_t launch_wave_own(int dtype, int vec, int lm, int m, const WaveArgs& a, int grid, cudaStream_t s);
 int wave_own_max_ctas_per_sm(int dtype, int vec);
 cudaError_t launch_normalize(const double* qout, const int64_t* q_off, const int32_t* q_card,
-                             const int32_t* q_col, int nq, int B, int total_cols,
+                             const int32_t* q_col, int nq, int B, int rows, int total_cols,
                              int normalize, double* post, int* err, const int* q_exp, int exp_all,
                              cudaStream_t s);
 // exp2: arena values are stored scaled by 2^exp2 (power-of-two prescaling)

@@ -1873,12 +1873,13 @@ int wave_max_ctas_per_sm(int dtype, int vec, int kv) { return kv == 2 ? occ_kv<2
 // scaled by 2^q_exp (power-of-two prescaling); unnormalized results undo it.
 __global__ void normalize_kernel(const double* __restrict__ qout, const int64_t* __restrict__ q_off,
                                  const int32_t* __restrict__ q_card, const int32_t* __restrict__ q_col,
-                                 int nq, int B, int total_cols, int normalize,
+                                 int nq, int B, int rows, int total_cols, int normalize,
                                  double* __restrict__ post, int* err, const int* __restrict__ q_exp, int exp_all) {
+  // qout is [card][B] (B = padded case lanes); posteriors are written for the first `rows` cases
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)nq * B) return;
-  const int i = (int)(idx / B);
-  const int b = (int)(idx - (int64_t)i * B);
+  if (idx >= (int64_t)nq * rows) return;
+  const int i = (int)(idx / rows);
+  const int b = (int)(idx - (int64_t)i * rows);
   const double* q = qout + q_off[i];
   const int card = q_card[i];
   double* o = post + (int64_t)b * total_cols + q_col[i];
@@ -1899,11 +1900,11 @@ __global__ void normalize_kernel(const double* __restrict__ qout, const int64_t*
 }
 
 cudaError_t launch_normalize(const double* qout, const int64_t* q_off, const int32_t* q_card,
-                             const int32_t* q_col, int nq, int B, int total_cols, int normalize,
+                             const int32_t* q_col, int nq, int B, int rows, int total_cols, int normalize,
                              double* post, int* err, const int* q_exp, int exp_all, cudaStream_t s) {
-  const int64_t n = (int64_t)nq * B;
+  const int64_t n = (int64_t)nq * rows;
   if (n == 0) return cudaSuccess;
-  normalize_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(qout, q_off, q_card, q_col, nq, B,
+  normalize_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(qout, q_off, q_card, q_col, nq, B, rows,
                                                                total_cols, normalize, post, err, q_exp, exp_all);
   return cudaGetLastError();
 }

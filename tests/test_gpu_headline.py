@@ -63,3 +63,23 @@ def test_bench_workload_both_micro_batches(workload, dtype):
     assert np.array_equal(host, out)
     bp.close()
 
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_odd_micro_batch_pads_case_lanes(workload, dtype):
+    """A micro-batch that is not a whole number of thread-owned blocks (4000
+    cases) is padded to whole blocks inside the state (it
+    used to fall to the general kernels at half the speed, or fail to plan in
+    fp64).  The padded lanes never reach the caller: 8000 cases in two
+    micro-batches of 4000 match the reference on every golden case below 8000,
+    across the micro-batch boundary (cases 3999/4000)."""
+    from paper_1202_3777_b200.batch import BatchPropagator
+
+    tree, tables, cases, idx, want = workload
+    keep = idx < 8000
+    bp = BatchPropagator(tree, tables, batch=4000, dtype=dtype, mode="shared")
+    out = bp.run(cases[:8000], to_host=True)
+    assert out.shape == (8000, bp.cols)
+    assert rel_err(out[idx[keep]], want[keep]) < TOL[dtype], dtype
+    assert {int(i) // 4000 for i in idx[keep]} == {0, 1}
+    bp.close()
