@@ -202,6 +202,7 @@ struct Program {
   cudaStream_t gstream = nullptr;
   // persistent single-launch program (small single trees, jt_tiny.cu)
   int tiny = 0, tiny_grid = 0, n_twaves = 0, tiny_nfm = MAXF;
+  int tiny_cluster = 0;                // > 0: the whole program in one cluster of this many CTAs
   int tiny_waves_launch = 0;           // 1: per-wave launches (PDL), tiny kernel on the waves flagged below
   std::vector<char> tiny_w;            // per (non-empty) wave: run as a tiny-pass launch
   std::vector<int> tiny_wave_grid;     // per-wave grids of the per-wave launches
@@ -1736,6 +1737,22 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
       prog->n_twaves = (int)tw.size();
       prog->n_launches = 1;
       prog->tiny_waves_launch = tiny_mode() == 2;
+      // every wave all tiny and within one cluster's threads: one cluster launch
+      {
+        static const int cmax = env_int("JT_TINY_CLUSTER", 16);
+        bool all_tiny = tiny_mode() == 2 && cmax > 0;
+        int64_t max_thr = 0;
+        for (size_t w = 0; w < tw.size() && all_tiny; ++w) {
+          all_tiny = hp.waves[w].groups.empty();
+          max_thr = std::max(max_thr, tw[w].n_threads);
+        }
+        static const int rounds = env_int("JT_TINY_CLUSTER_ROUNDS", 1);  // grid-stride rounds per wave
+        if (all_tiny && max_thr <= (int64_t)cmax * NT * rounds) {
+          prog->tiny_cluster = (int)std::min<int64_t>(cmax, std::max<int64_t>(1, (max_thr + NT - 1) / NT));
+          prog->tiny_waves_launch = 0;
+          prog->n_launches = 1;
+        }
+      }
       if (prog->tiny_waves_launch) {
         prog->n_launches = 0;
         for (size_t w = 0; w < tw.size(); ++w) {
@@ -1907,6 +1924,21 @@ static int run_program(jt_state* st, Program* pr, cudaStream_t s) {
   pr->runs++;
   if (pr->tiny && pr->tiny_waves_launch) {
     // per-wave launches: captured into a graph from the second run on (below)
+  } else if (pr->tiny && pr->tiny_cluster) {
+    TinyArgs a{};
+    a.clique = st->d_clique;
+    a.base = st->d_base;
+    a.aux = st->d_aux;
+    a.qout = st->d_qout;
+    a.err = st->d_err;
+    a.passes = pr->d_tpass;
+    a.unit0s = pr->d_unit0;
+    a.waves = pr->d_twaves;
+    a.n_waves = pr->n_twaves;
+    a.bar = pr->d_bar;
+    CK(launch_tiny_cluster(st->plan->dtype, pr->tiny_nfm, a, pr->tiny_cluster, s));
+    st->launches++;
+    return JT_OK;
   } else if (pr->tiny) {
     TinyArgs a{};
     a.clique = st->d_clique;

@@ -214,6 +214,8 @@ struct TinyArgs {
 // occ_out != nullptr: only report the kernel's CTAs per SM
 // nfm: factor count bound of the program's passes (2, 4 or 8; template of the kernel)
 cudaError_t launch_tiny(int dtype, int nfm, const TinyArgs& a, int grid, cudaStream_t s, int* occ_out = nullptr);
+// the whole tiny program in one thread-block cluster of `grid` (<= 16) CTAs
+cudaError_t launch_tiny_cluster(int dtype, int nfm, const TinyArgs& a, int grid, cudaStream_t s);
 // one wave of a tiny program as its own launch (PDL-chained, graph-replayable)
 cudaError_t launch_tiny_wave(int dtype, int nfm, const TinyArgs& a, int w, int grid, cudaStream_t s);
 int wave_max_ctas_per_sm(int dtype, int vec, int kv);

@@ -265,6 +265,56 @@ __global__ void __launch_bounds__(NT, 2) tiny_wave_kernel(const TinyArgs a, int 
   tiny_wave<T, NFM, true>(a, w);
 }
 
+// The whole program in ONE thread-block cluster (<= 16 CTAs): waves separated
+// by the hardware cluster barrier (release/acquire at cluster scope orders the
+// global-memory tables between waves) -- for trees whose every wave fits a
+// cluster's threads, where a grid barrier or a launch per wave costs more than
+// the wave itself.
+template <typename T, int NFM>
+__global__ void __launch_bounds__(NT, 1) tiny_cluster_kernel(const TinyArgs a) {
+  for (int w = 0; w < a.n_waves; ++w) {
+    tiny_wave<T, NFM, false>(a, w);
+    if (w + 1 < a.n_waves) {
+      __syncthreads();
+      asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+      asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    }
+  }
+}
+
+template <typename T, int NFM>
+static cudaError_t launch_tiny_cluster_t(const TinyArgs& a, int grid, cudaStream_t s) {
+  auto k = tiny_cluster_kernel<T, NFM>;
+  if (grid > 8) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NT);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = grid;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, a);
+}
+
+template <typename T>
+static cudaError_t launch_tiny_cluster_nf(int nfm, const TinyArgs& a, int grid, cudaStream_t s) {
+  if (nfm <= 2) return launch_tiny_cluster_t<T, 2>(a, grid, s);
+  if (nfm <= 4) return launch_tiny_cluster_t<T, 4>(a, grid, s);
+  return launch_tiny_cluster_t<T, MAXF>(a, grid, s);
+}
+
+cudaError_t launch_tiny_cluster(int dtype, int nfm, const TinyArgs& a, int grid, cudaStream_t s) {
+  return dtype == 0 ? launch_tiny_cluster_nf<float>(nfm, a, grid, s)
+                    : launch_tiny_cluster_nf<double>(nfm, a, grid, s);
+}
+
 template <typename T, int NFM>
 static cudaError_t launch_tiny_t(const TinyArgs& a, int grid, cudaStream_t s, int* occ_out) {
   auto k = tiny_persist_kernel<T, NFM>;
