@@ -1739,7 +1739,10 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
       prog->tiny_waves_launch = tiny_mode() == 2;
       // every wave all tiny and within one cluster's threads: one cluster launch
       {
-        static const int cmax = env_int("JT_TINY_CLUSTER", 16);
+        // (opt-in, JT_TINY_CLUSTER=<ctas>: measured slower than per-wave launches on c1,
+        // 39 vs 29 us -- fewer threads per wave lengthen each wave more than the
+        // cluster barrier saves)
+        static const int cmax = env_int("JT_TINY_CLUSTER", 0);
         bool all_tiny = tiny_mode() == 2 && cmax > 0;
         int64_t max_thr = 0;
         for (size_t w = 0; w < tw.size() && all_tiny; ++w) {
