@@ -1389,6 +1389,9 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
 #ifndef ROWI_MINB_D
 #define ROWI_MINB_D 8
 #endif
+#ifndef ROWI_PREFETCH_E
+#define ROWI_PREFETCH_E 0
+#endif
 // LONGK: passes with long K sums (nK >= 16) keep ROWI_KU_L values of k in flight
 // per lane (their loads would otherwise chain one memory latency per k) at a
 // larger register budget
@@ -1445,6 +1448,15 @@ __global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F :
       T part[VEC];
 #pragma unroll
       for (int l = 0; l < VEC; ++l) part[l] = (T)0;
+#if ROWI_PREFETCH_E
+      // short sums: the first epilogue factor and the old separator values do not
+      // depend on the K-sum -- issue them before it (one memory round trip per unit)
+      T e0[VEC] = {}, o0[VEC] = {};
+      const bool pre = !LONGK && !FOLD && nE >= 1;
+      const bool pre_old = !LONGK && !FOLD && (P->out_kind == OUT_SEP || P->out_kind == OUT_SEP_DFRESH);
+      if (pre) load_vec_cs<T, VEC>(aux_c + P->efac_off[0] + __ldg(tir + nG) + __ldg(ts) + b0, e0);
+      if (pre_old) load_vec_cs<T, VEC>(aux_c + P->out_off + __ldg(tir + nG + nE) + __ldg(ts + nE) + b0, o0);
+#endif
       int since = 0;
       for (int k = 0; k < nK; k += KU) {
         T pv[KU][VEC];
@@ -1484,14 +1496,28 @@ __global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F :
       const bool cs = a.stream_epi != 0;
       for (int e = 0; e < nE; ++e) {
         T f[VEC];
-        const T* ep = aux_c + P->efac_off[e] + __ldg(tir + nG + e) + __ldg(ts + e) + b0;
-        if (cs) load_vec_cs<T, VEC>(ep, f);
-        else load_vec_ro<T, VEC>(ep, f);
+#if ROWI_PREFETCH_E
+        if (e == 0 && pre) {
+#pragma unroll
+          for (int l = 0; l < VEC; ++l) f[l] = e0[l];
+        } else
+#endif
+        {
+          const T* ep = aux_c + P->efac_off[e] + __ldg(tir + nG + e) + __ldg(ts + e) + b0;
+          if (cs) load_vec_cs<T, VEC>(ep, f);
+          else load_vec_ro<T, VEC>(ep, f);
+        }
 #pragma unroll
         for (int l = 0; l < VEC; ++l) v[l] *= (double)f[l];
       }
       const int64_t j = (int64_t)__ldg(tir + nG + nE) + __ldg(ts + nE) + b0;
       T old[VEC] = {};
+#if ROWI_PREFETCH_E
+      if (pre_old) {
+#pragma unroll
+        for (int l = 0; l < VEC; ++l) old[l] = o0[l];
+      } else
+#endif
       if (P->out_kind == OUT_SEP || P->out_kind == OUT_SEP_DFRESH) {
         if (cs) load_vec_cs<T, VEC>(aux_c + P->out_off + j, old);
         else load_vec<T, VEC>(aux_c + P->out_off + j, old);
