@@ -711,7 +711,9 @@ static int compile_pass(const jt_state* st, const PassSpec& ps, int vec, int pas
       c.BPI = 1;
     }
     // chunking: ~8 items per SM slot for big passes, >= 2 iterations per item otherwise
-    const int64_t per_item = std::max<int64_t>(2 * TH, total / (int64_t)(st->num_sms * 8));
+    static const int ips = env_int("JT_ITEMS_PER_SM", 8);
+    static const int min_it = env_int("JT_MIN_ITERS", 2);
+    const int64_t per_item = std::max<int64_t>((int64_t)min_it * TH, total / (int64_t)(st->num_sms * ips));
     const int64_t desired = std::max<int64_t>(1, (total + per_item - 1) / per_item);
     const int64_t max_chunks = (c.r_out + c.BPI - 1) / c.BPI;
     int64_t nch = has_out ? (desired + c.n_out - 1) / c.n_out : desired;
