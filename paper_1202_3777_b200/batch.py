@@ -166,11 +166,15 @@ class BatchPropagator:
         validated like the reference's Evidence.check (model.py:130-137):
         unknown variables raise UnknownVariableError, states outside [0, card)
         raise StateOutOfRangeError."""
-        rows = [(b, v, x) for b, ev in enumerate(cases)
-                for v, x in (ev.assignments if hasattr(ev, "assignments") else ev).items()]
-        if not rows:
+        evs = [ev.assignments if hasattr(ev, "assignments") else ev for ev in cases]
+        counts = [len(ev) for ev in evs]
+        n = sum(counts)
+        if not n:
             return np.zeros((0, 3), np.int32)
-        obs = np.asarray(rows, dtype=np.int64)
+        obs = np.empty((n, 3), dtype=np.int64)
+        obs[:, 0] = np.repeat(np.arange(len(evs), dtype=np.int64), counts)
+        obs[:, 1] = np.fromiter((v for ev in evs for v in ev), dtype=np.int64, count=n)
+        obs[:, 2] = np.fromiter((x for ev in evs for x in ev.values()), dtype=np.int64, count=n)
         own = self._owner_arr
         v, x = obs[:, 1], obs[:, 2]
         bad_v = (v < 0) | (v >= len(own))

@@ -25,7 +25,8 @@ def report(*a, **k):
 def test_single_tree_program_compiles(name, dtype, kind):
     text = report(name, batch=1, mode="materialized", kind=kind, dtype=dtype)
     assert "compulsory total MB" in text and "\nwave 0" in text
-    assert "pass clique" in text
+    # small waves of single trees run as tiny passes (jt_tiny.cu), the rest as general passes
+    assert "pass clique" in text or text.startswith("tiny passes")
 
 
 @pytest.mark.parametrize("name", ["c1", "c5", "c4B"])
@@ -77,3 +78,12 @@ def test_ksplit_contraction_is_compiled(batch, dtype):
     text = report("c5", batch=batch, mode="shared", kind=1, dtype=dtype)
     ks = [int(line.split(" ks ")[1].split()[0]) for line in text.splitlines() if " ks " in line]
     assert ks and max(ks) > 1, (batch, dtype)
+
+
+def test_small_single_trees_use_tiny_passes():
+    """Single trees: waves touching at most 2^18 elements run as tiny passes
+    (one launch per wave, PDL-chained); c1 entirely, c3 (16.8M-entry cliques) never."""
+    c1 = report("c1", batch=1, mode="materialized", kind=0, dtype="f32")
+    assert c1.startswith("tiny passes (mode 2): 7 of 7 waves")
+    c3 = report("c3", batch=1, mode="materialized", kind=0, dtype="f32")
+    assert not c3.startswith("tiny passes")
