@@ -177,6 +177,7 @@ struct LaunchGrp {  // one kernel launch of a wave
   int n_cpasses = 0;
   int64_t n_units = 0;
   int interleave = 0;  // CArgs::interleave
+  int rp_idx = -1;     // >= 0: single row-per-i pass launched with its tables in the parameters
 };
 
 struct WaveRt {
@@ -201,6 +202,7 @@ struct Program {
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t gstream = nullptr;
   // persistent single-launch program (small single trees, jt_tiny.cu)
+  std::vector<RowiParam> rparams;  // per single row-per-i launch (LaunchGrp::rp_idx)
   int tiny = 0, tiny_grid = 0, n_twaves = 0, tiny_nfm = MAXF;
   int tiny_cluster = 0;                // > 0: the whole program in one cluster of this many CTAs
   int tiny_waves_launch = 0;           // 1: per-wave launches (PDL), tiny kernel on the waves flagged below
@@ -983,6 +985,7 @@ struct HostProgram {
   std::vector<int32_t> ctab;
   std::vector<double> w;
   std::vector<int> cpass_clique;
+  std::vector<RowiParam> rparams;
 };
 
 // ----------------------------------------------------- contraction passes --
@@ -1516,6 +1519,17 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
           cg.n_units = cp.n_units;
           cg.n_cpasses = 1;
           hp.cpasses.push_back(cp);
+          // row-per-i pass: descriptor and tables in the kernel parameters (constant bank)
+          const int tsw = cp.nE + 1 + (cp.out_kind_b != OUT_NONE ? cp.nE_b + 1 : 0);
+          if ((cp.rowi == 1 || cp.rowi == 4) && cp.nK * cp.nG <= RP_TK && tsw <= RP_TS && env_int("JT_ROWI_PARAM", 1)) {
+            RowiParam rp;
+            std::memset(&rp, 0, sizeof(rp));
+            rp.cp = cp;
+            for (int x = 0; x < cp.nK * cp.nG; ++x) rp.tk[x] = hp.ctab[cp.tk_off + x];
+            for (int x = 0; x < tsw; ++x) rp.ts[x] = hp.ctab[cp.ts_off + x];
+            cg.rp_idx = (int)hp.rparams.size();
+            hp.rparams.push_back(rp);
+          }
           hp.cpass_clique.push_back(cpc2[key][q]);
           const int occ = occ_override ? occ_override : contract_max_ctas_per_sm(st->plan->dtype, fold, cg.m, cg.vec);
           cg.grid = (int)std::min<int64_t>((cg.n_units + NT / 32 - 1) / (NT / 32), (int64_t)occ * st->num_sms);
@@ -1726,6 +1740,7 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
   if (rc0) return rc0;
   auto prog = std::make_unique<Program>();
   prog->waves = hp.waves;
+  prog->rparams = hp.rparams;
   for (auto& w : hp.waves) prog->n_launches += (int64_t)w.groups.size();
   if (tiny) {
     {
@@ -1838,7 +1853,10 @@ static int launch_group(jt_state* st, const Program* pr, const WaveRt& w, const 
     c.interleave = g.interleave;
     static const int stream_epi = env_int("JT_EPI_CS", 1);
     c.stream_epi = stream_epi;
-    CK(launch_contract(st->plan->dtype, g.lm, g.m, g.vec, c, g.grid, s));
+    if (g.rp_idx >= 0)
+      CK(launch_contract_rowi_param(st->plan->dtype, g.lm, g.m == 4, c, pr->rparams[g.rp_idx], g.grid, s));
+    else
+      CK(launch_contract(st->plan->dtype, g.lm, g.m, g.vec, c, g.grid, s));
     st->launches++;
     return JT_OK;
   }

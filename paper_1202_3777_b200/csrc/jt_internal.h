@@ -155,6 +155,18 @@ struct CArgs {
 constexpr int CKF = 16;     // fp32 contraction sums longer than this fold into fp64
 // ng: factors per k (0..CMAXG) of every pass of the launch (compile-time in the kernel; ignored for rowi)
 cudaError_t launch_contract(int dtype, int fold, int rowi, int ng, const CArgs& a, int grid, cudaStream_t s);
+// A single row-per-i pass with its descriptor and k-table carried in the kernel
+// parameters (__grid_constant__): the per-k, warp-uniform table lookups come from
+// the constant bank instead of competing with the factor streams for L1.
+constexpr int RP_TK = 448;  // ints of the k-table (nK x nG)
+constexpr int RP_TS = 24;   // ints of the s'-row table (nS == 1: E, out, E_b, out_b)
+struct RowiParam {
+  CPass cp;
+  int32_t tk[RP_TK];
+  int32_t ts[RP_TS];
+};
+cudaError_t launch_contract_rowi_param(int dtype, int fold, int longk, const CArgs& a, const RowiParam& rp, int grid,
+                                       cudaStream_t s);
 int contract_max_ctas_per_sm(int dtype, int fold, int rowi, int ng);
 
 // device initialize: one entry per clique, one term per CPT, 3 int64 per CPT variable

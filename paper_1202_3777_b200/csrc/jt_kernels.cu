@@ -1401,10 +1401,9 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
 #ifndef ROWI_MINB_L
 #define ROWI_MINB_L 4
 #endif
-template <typename T, bool FOLD, bool LONGK = false>
-__global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F : sizeof(T) == 8 ? ROWI_MINB_D : ROWI_MINB_NF)
-    contract_rowi_kernel(const CArgs a) {
-  pdl_enter();
+template <typename T, bool FOLD, bool LONGK, bool PRM>
+__device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restrict__ P0, const int32_t* __restrict__ tk0,
+                                          const int32_t* __restrict__ ts0) {
   // one i per warp unit (few registers: three or four CTAs per SM), KU values
   // of k in flight, each with its nG factor-row vectors
   constexpr int VEC = CTraits<T>::VEC;
@@ -1418,7 +1417,9 @@ __global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F :
   int pi = 0;
   for (int64_t u = blockIdx.x * (NT / 32) + (threadIdx.x >> 5); u < a.n_units; u += n_warps) {
     int64_t ul;
-    if (a.interleave) {
+    if (PRM) {
+      ul = u;  // one pass per launch, starting at unit 0
+    } else if (a.interleave) {
       pi = (int)(u % a.n_passes);
       ul = u / a.n_passes;
     } else {
@@ -1426,7 +1427,7 @@ __global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F :
       while (pi > 0 && u < a.passes[pi].unit0) --pi;
       ul = u - a.passes[pi].unit0;
     }
-    const CPass* __restrict__ P = a.passes + pi;
+    const CPass* __restrict__ P = PRM ? P0 : a.passes + pi;
     const int nCG = P->nCG;
     const int cg = P->cmaj ? (int)(ul / P->nI) : (int)(ul % nCG);
     const int64_t i = P->cmaj ? ul % P->nI : ul / nCG;
@@ -1434,8 +1435,8 @@ __global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F :
     const bool two = P->out_kind_b != OUT_NONE;  // paired sibling output (same K-sum)
     const int tw = nG + nE + 1 + (two ? P->nE_b + 1 : 0);
     const int32_t* __restrict__ tir = a.tab + P->ti_off + i * tw;
-    const int32_t* __restrict__ tk = a.tab + P->tk_off;
-    const int32_t* __restrict__ ts = a.tab + P->ts_off;
+    const int32_t* __restrict__ tk = PRM ? tk0 : a.tab + P->tk_off;
+    const int32_t* __restrict__ ts = PRM ? ts0 : a.tab + P->ts_off;
     const T* gq[CMAXG];
 #pragma unroll
     for (int g = 0; g < CMAXG; ++g) gq[g] = aux_c + (g < nG ? P->gfac_off[g] + __ldg(tir + g) : 0);
@@ -1455,7 +1456,7 @@ __global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F :
       const bool pre = !LONGK && !FOLD && nE >= 1;
       const bool pre_old = !LONGK && !FOLD && (P->out_kind == OUT_SEP || P->out_kind == OUT_SEP_DFRESH);
       if (pre) load_vec_cs<T, VEC>(aux_c + P->efac_off[0] + __ldg(tir + nG) + __ldg(ts) + b0, e0);
-      if (pre_old) load_vec_cs<T, VEC>(aux_c + P->out_off + __ldg(tir + nG + nE) + __ldg(ts + nE) + b0, o0);
+      if (pre_old) load_vec_cs<T, VEC>(aux_c + P->out_off + __ldg(tir + nG + nE) + TSV(nE) + b0, o0);
 #endif
       int since = 0;
       for (int k = 0; k < nK; k += KU) {
@@ -1470,7 +1471,7 @@ __global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F :
           for (int g = 0; g < CMAXG; ++g) {
             if (g < nG) {
               T f[VEC];
-              load_vec_ro<T, VEC>(gq[g] + b0 + __ldg(tk + kq * nG + g), f);
+              load_vec_ro<T, VEC>(gq[g] + b0 + (PRM ? tk[kq * nG + g] : __ldg(tk + kq * nG + g)), f);
 #pragma unroll
               for (int l = 0; l < VEC; ++l) pv[q][l] *= f[l];
             }
@@ -1490,6 +1491,8 @@ __global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F :
           since = 0;
         }
       }
+#define TSV(x) (PRM ? ts[(x)] : __ldg(ts + (x)))
+#define SBV(x) (PRM ? sb[(x)] : __ldg(sb + (x)))
       double vsum[VEC], v[VEC];
 #pragma unroll
       for (int l = 0; l < VEC; ++l) v[l] = vsum[l] = acc[l] + (double)part[l];
@@ -1503,14 +1506,14 @@ __global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F :
         } else
 #endif
         {
-          const T* ep = aux_c + P->efac_off[e] + __ldg(tir + nG + e) + __ldg(ts + e) + b0;
+          const T* ep = aux_c + P->efac_off[e] + __ldg(tir + nG + e) + TSV(e) + b0;
           if (cs) load_vec_cs<T, VEC>(ep, f);
           else load_vec_ro<T, VEC>(ep, f);
         }
 #pragma unroll
         for (int l = 0; l < VEC; ++l) v[l] *= (double)f[l];
       }
-      const int64_t j = (int64_t)__ldg(tir + nG + nE) + __ldg(ts + nE) + b0;
+      const int64_t j = (int64_t)__ldg(tir + nG + nE) + TSV(nE) + b0;
       T old[VEC] = {};
 #if ROWI_PREFETCH_E
       if (pre_old) {
@@ -1532,13 +1535,13 @@ __global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F :
         for (int l = 0; l < VEC; ++l) v[l] = vsum[l];
         for (int e = 0; e < nEb; ++e) {
           T f[VEC];
-          const T* ep = aux_c + P->efac_off_b[e] + __ldg(tb + e) + __ldg(sb + e) + b0;
+          const T* ep = aux_c + P->efac_off_b[e] + __ldg(tb + e) + SBV(e) + b0;
           if (cs) load_vec_cs<T, VEC>(ep, f);
           else load_vec_ro<T, VEC>(ep, f);
 #pragma unroll
           for (int l = 0; l < VEC; ++l) v[l] *= (double)f[l];
         }
-        const int64_t jb = (int64_t)__ldg(tb + nEb) + __ldg(sb + nEb) + b0;
+        const int64_t jb = (int64_t)__ldg(tb + nEb) + SBV(nEb) + b0;
         T oldb[VEC] = {};
         if (P->out_kind_b == OUT_SEP || P->out_kind_b == OUT_SEP_DFRESH) {
           if (cs) load_vec_cs<T, VEC>(aux_c + P->out_off_b + jb, oldb);
@@ -1548,8 +1551,38 @@ __global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F :
                                               aux, a.qout, cs);
       }
       if (bad) atomicOr(a.err, EB_INCONSISTENT);
+#undef TSV
+#undef SBV
     }
   }
+}
+
+template <typename T, bool FOLD, bool LONGK = false>
+__global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F : sizeof(T) == 8 ? ROWI_MINB_D : ROWI_MINB_NF)
+    contract_rowi_kernel(const CArgs a) {
+  pdl_enter();
+  rowi_body<T, FOLD, LONGK, false>(a, nullptr, nullptr, nullptr);
+}
+
+template <typename T, bool FOLD, bool LONGK>
+__global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F : sizeof(T) == 8 ? ROWI_MINB_D : ROWI_MINB_NF)
+    contract_rowi_p_kernel(const CArgs a, const __grid_constant__ RowiParam rp) {
+  pdl_enter();
+  rowi_body<T, FOLD, LONGK, true>(a, &rp.cp, rp.tk, rp.ts);
+}
+
+cudaError_t launch_contract_rowi_param(int dtype, int fold, int longk, const CArgs& a, const RowiParam& rp, int grid,
+                                       cudaStream_t s) {
+  if (grid <= 0 || a.n_units <= 0) return cudaSuccess;
+  if (dtype == 0) {
+    if (fold)
+      return longk ? launch_pdl(contract_rowi_p_kernel<float, true, true>, grid, NT, 0, s, a, rp)
+                   : launch_pdl(contract_rowi_p_kernel<float, true, false>, grid, NT, 0, s, a, rp);
+    return longk ? launch_pdl(contract_rowi_p_kernel<float, false, true>, grid, NT, 0, s, a, rp)
+                 : launch_pdl(contract_rowi_p_kernel<float, false, false>, grid, NT, 0, s, a, rp);
+  }
+  return longk ? launch_pdl(contract_rowi_p_kernel<double, false, true>, grid, NT, 0, s, a, rp)
+               : launch_pdl(contract_rowi_p_kernel<double, false, false>, grid, NT, 0, s, a, rp);
 }
 
 // Row-per-i passes over i-groups: igs consecutive i differ only in the
