@@ -178,6 +178,7 @@ struct LaunchGrp {  // one kernel launch of a wave
   int64_t n_units = 0;
   int interleave = 0;  // CArgs::interleave
   int rp_idx = -1;     // >= 0: single row-per-i pass launched with its tables in the parameters
+  int tp_idx = -1;     // >= 0: single tile pass launched with its tables in the parameters
 };
 
 struct WaveRt {
@@ -203,6 +204,7 @@ struct Program {
   cudaStream_t gstream = nullptr;
   // persistent single-launch program (small single trees, jt_tiny.cu)
   std::vector<RowiParam> rparams;  // per single row-per-i launch (LaunchGrp::rp_idx)
+  std::vector<TileParam> tparams;  // per single tile launch (LaunchGrp::tp_idx)
   int tiny = 0, tiny_grid = 0, n_twaves = 0, tiny_nfm = MAXF;
   int tiny_cluster = 0;                // > 0: the whole program in one cluster of this many CTAs
   int tiny_waves_launch = 0;           // 1: per-wave launches (PDL), tiny kernel on the waves flagged below
@@ -986,6 +988,7 @@ struct HostProgram {
   std::vector<double> w;
   std::vector<int> cpass_clique;
   std::vector<RowiParam> rparams;
+  std::vector<TileParam> tparams;
 };
 
 // ----------------------------------------------------- contraction passes --
@@ -1530,6 +1533,16 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
             cg.rp_idx = (int)hp.rparams.size();
             hp.rparams.push_back(rp);
           }
+          const int64_t tsn = (int64_t)cp.nS * (cp.nE + 1);
+          if (cp.rowi == 0 && cp.nK * cp.nG <= RP_TK && tsn <= TP_TS && env_int("JT_TILE_PARAM", 1)) {
+            TileParam tpm;
+            std::memset(&tpm, 0, sizeof(tpm));
+            tpm.cp = cp;
+            for (int x = 0; x < cp.nK * cp.nG; ++x) tpm.tk[x] = hp.ctab[cp.tk_off + x];
+            for (int64_t x = 0; x < tsn; ++x) tpm.ts[x] = hp.ctab[cp.ts_off + x];
+            cg.tp_idx = (int)hp.tparams.size();
+            hp.tparams.push_back(tpm);
+          }
           hp.cpass_clique.push_back(cpc2[key][q]);
           const int occ = occ_override ? occ_override : contract_max_ctas_per_sm(st->plan->dtype, fold, cg.m, cg.vec);
           cg.grid = (int)std::min<int64_t>((cg.n_units + NT / 32 - 1) / (NT / 32), (int64_t)occ * st->num_sms);
@@ -1741,6 +1754,7 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
   auto prog = std::make_unique<Program>();
   prog->waves = hp.waves;
   prog->rparams = hp.rparams;
+  prog->tparams = hp.tparams;
   for (auto& w : hp.waves) prog->n_launches += (int64_t)w.groups.size();
   if (tiny) {
     {
@@ -1855,6 +1869,8 @@ static int launch_group(jt_state* st, const Program* pr, const WaveRt& w, const 
     c.stream_epi = stream_epi;
     if (g.rp_idx >= 0)
       CK(launch_contract_rowi_param(st->plan->dtype, g.lm, g.m == 4, c, pr->rparams[g.rp_idx], g.grid, s));
+    else if (g.tp_idx >= 0)
+      CK(launch_contract_tile_param(st->plan->dtype, g.lm, g.vec, c, pr->tparams[g.tp_idx], g.grid, s));
     else
       CK(launch_contract(st->plan->dtype, g.lm, g.m, g.vec, c, g.grid, s));
     st->launches++;

@@ -167,6 +167,14 @@ struct RowiParam {
 };
 cudaError_t launch_contract_rowi_param(int dtype, int fold, int longk, const CArgs& a, const RowiParam& rp, int grid,
                                        cudaStream_t s);
+constexpr int TP_TS = 1024;  // ints of the s'-row table of a tile pass (nS x (nE + 1))
+struct TileParam {
+  CPass cp;
+  int32_t tk[RP_TK];
+  int32_t ts[TP_TS];
+};
+cudaError_t launch_contract_tile_param(int dtype, int fold, int ng, const CArgs& a, const TileParam& tp, int grid,
+                                       cudaStream_t s);
 int contract_max_ctas_per_sm(int dtype, int fold, int rowi, int ng);
 
 // device initialize: one entry per clique, one term per CPT, 3 int64 per CPT variable

@@ -1097,7 +1097,7 @@ __device__ __forceinline__ void con_epi_load(const T* p, T (&v)[VEC]) {
 // Epilogue of one half tile (TMC/2 rows) for one output kind: the rows' old
 // separator values are loaded before any store (stores would otherwise order
 // the loads behind them); returns "nonzero / 0 seen".
-template <typename T, typename A, int VEC, int KIND, bool FOLD, int NG>
+template <typename T, typename A, int VEC, int KIND, bool FOLD, int NG, bool PRM = false>
 __device__ __forceinline__ bool contract_epilogue_half(const CPass* __restrict__ P, const CArgs& a, int h, int rows,
                                                        int s0, const int32_t* __restrict__ ti,
                                                        const int32_t* __restrict__ ts, int b0,
@@ -1108,7 +1108,10 @@ __device__ __forceinline__ bool contract_epilogue_half(const CPass* __restrict__
   int jo[TMC / 2];
   const int jb = __ldg(ti + NG + nE);
 #pragma unroll
-  for (int r = 0; r < TMC / 2; ++r) jo[r] = h + r < rows ? jb + __ldg(ts + (int64_t)(s0 + h + r) * (nE + 1) + nE) : 0;
+  for (int r = 0; r < TMC / 2; ++r) {
+    const int32_t* q = ts + (int64_t)(s0 + h + r) * (nE + 1) + nE;
+    jo[r] = h + r < rows ? jb + (PRM ? *q : __ldg(q)) : 0;
+  }
   T old[TMC / 2][VEC];
 #pragma unroll
   for (int r = 0; r < TMC / 2; ++r) {
@@ -1129,7 +1132,7 @@ __device__ __forceinline__ bool contract_epilogue_half(const CPass* __restrict__
       const int32_t* tsr = ts + (int64_t)(s0 + h + r) * (nE + 1);
       for (int e = 0; e < nE; ++e) {
         T f[VEC];
-        con_epi_load<T, VEC>(aux_c + P->efac_off[e] + __ldg(ti + NG + e) + __ldg(tsr + e) + b0, f);
+        con_epi_load<T, VEC>(aux_c + P->efac_off[e] + __ldg(ti + NG + e) + (PRM ? tsr[e] : __ldg(tsr + e)) + b0, f);
 #pragma unroll
         for (int l = 0; l < VEC; ++l) v[l] *= (A)f[l];
       }
@@ -1157,9 +1160,9 @@ __device__ __forceinline__ bool contract_epilogue_half(const CPass* __restrict__
 #ifndef CON_WPF
 #define CON_WPF 1
 #endif
-template <typename T, bool FOLD, int NG>
-__global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
-  pdl_enter();
+template <typename T, bool FOLD, int NG, bool PRM>
+__device__ __forceinline__ void tile_body(const CArgs& a, const CPass* __restrict__ P0, const int32_t* __restrict__ tk0,
+                                          const int32_t* __restrict__ ts0) {
   constexpr int VEC = CTraits<T>::VEC;
   constexpr int WV = sizeof(T) == 4 ? 4 : 2;  // W row loaded as TMC / WV vectors
   using R = CRing<T, NG, FOLD>;
@@ -1177,7 +1180,9 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
   int pi = 0;
   for (int64_t u = blockIdx.x * (NT / 32) + (threadIdx.x >> 5); u < a.n_units; u += n_warps) {
     int64_t ul;
-    if (a.interleave) {
+    if (PRM) {
+      ul = u;  // one pass per launch, starting at unit 0
+    } else if (a.interleave) {
       pi = (int)(u % a.n_passes);
       ul = u / a.n_passes;
     } else {
@@ -1185,7 +1190,7 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
       while (pi > 0 && u < a.passes[pi].unit0) --pi;
       ul = u - a.passes[pi].unit0;
     }
-    const CPass* __restrict__ P = a.passes + pi;
+    const CPass* __restrict__ P = PRM ? P0 : a.passes + pi;
     const int nT = P->nT, nCG = P->nCG, nKS = P->nKS;
     // unit = (i, t, ks, cg), case chunk fastest: concurrent warps share factor rows
     // (cmaj: case chunk slowest)
@@ -1213,8 +1218,8 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
     const int s0 = t * TMC;
     const int rows = min(TMC, nS - s0);
     const int32_t* __restrict__ ti = a.tab + P->ti_off + i * (NG + nE + 1);
-    const int32_t* __restrict__ tk = a.tab + P->tk_off + (int64_t)kb * NG;
-    const int32_t* __restrict__ ts = a.tab + P->ts_off;
+    const int32_t* __restrict__ tk = (PRM ? tk0 : a.tab + P->tk_off) + (int64_t)kb * NG;
+    const int32_t* __restrict__ ts = PRM ? ts0 : a.tab + P->ts_off;
     const T* __restrict__ wrow = W + P->w_off + (i * (int64_t)nKall + kb) * nSp + s0;
     const T* gq[NG > 0 ? NG : 1];  // factor g at (i, k = kb, case 0)
 #pragma unroll
@@ -1222,7 +1227,7 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
     for (int b0 = cg * 32 * VEC + lane * VEC; b0 < a.B; b0 += bstep) {
       auto issue = [&](int k, unsigned char* sp) {
 #pragma unroll
-        for (int g = 0; g < NG; ++g) cp_async16(sp + g * 512, gq[g] + b0 + __ldg(tk + k * NG + g));
+        for (int g = 0; g < NG; ++g) cp_async16(sp + g * 512, gq[g] + b0 + (PRM ? tk[k * NG + g] : __ldg(tk + k * NG + g)));
       };
       if (NG > 0) {
 #pragma unroll
@@ -1344,26 +1349,39 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
         case OUT_SEP_FRESH:
 #pragma unroll
           for (int h = 0; h < TMC; h += TMC / 2)
-            contract_epilogue_half<T, A, VEC, OUT_SEP_FRESH, FOLD, NG>(P, a, h, rows, s0, ti, ts, b0, part, cacc);
+            contract_epilogue_half<T, A, VEC, OUT_SEP_FRESH, FOLD, NG, PRM>(P, a, h, rows, s0, ti, ts, b0, part, cacc);
           break;
         case OUT_RAW:
 #pragma unroll
           for (int h = 0; h < TMC; h += TMC / 2)
-            contract_epilogue_half<T, A, VEC, OUT_RAW, FOLD, NG>(P, a, h, rows, s0, ti, ts, b0, part, cacc);
+            contract_epilogue_half<T, A, VEC, OUT_RAW, FOLD, NG, PRM>(P, a, h, rows, s0, ti, ts, b0, part, cacc);
           break;
         case OUT_SEP_DFRESH:
 #pragma unroll
           for (int h = 0; h < TMC; h += TMC / 2)
-            contract_epilogue_half<T, A, VEC, OUT_SEP_DFRESH, FOLD, NG>(P, a, h, rows, s0, ti, ts, b0, part, cacc);
+            contract_epilogue_half<T, A, VEC, OUT_SEP_DFRESH, FOLD, NG, PRM>(P, a, h, rows, s0, ti, ts, b0, part, cacc);
           break;
         default:
 #pragma unroll
           for (int h = 0; h < TMC; h += TMC / 2)
-            bad |= contract_epilogue_half<T, A, VEC, OUT_SEP, FOLD, NG>(P, a, h, rows, s0, ti, ts, b0, part, cacc);
+            bad |= contract_epilogue_half<T, A, VEC, OUT_SEP, FOLD, NG, PRM>(P, a, h, rows, s0, ti, ts, b0, part, cacc);
       }
       if (bad) atomicOr(a.err, EB_INCONSISTENT);
     }
   }
+}
+
+template <typename T, bool FOLD, int NG>
+__global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
+  pdl_enter();
+  tile_body<T, FOLD, NG, false>(a, nullptr, nullptr, nullptr);
+}
+
+// one tile pass per launch, its descriptor and k / s' tables in the kernel parameters
+template <typename T, bool FOLD, int NG>
+__global__ void __launch_bounds__(NT, CON_MINB) contract_p_kernel(const CArgs a, const __grid_constant__ TileParam tp) {
+  pdl_enter();
+  tile_body<T, FOLD, NG, true>(a, &tp.cp, tp.tk, tp.ts);
 }
 
 // Row-per-i contraction passes (nS == 1: every output variable is also a factor
@@ -1388,9 +1406,6 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_kernel(const CArgs a) {
 #endif
 #ifndef ROWI_MINB_D
 #define ROWI_MINB_D 8
-#endif
-#ifndef ROWI_PREFETCH_E
-#define ROWI_PREFETCH_E 0
 #endif
 // LONGK: passes with long K sums (nK >= 16) keep ROWI_KU_L values of k in flight
 // per lane (their loads would otherwise chain one memory latency per k) at a
@@ -1449,15 +1464,6 @@ __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restric
       T part[VEC];
 #pragma unroll
       for (int l = 0; l < VEC; ++l) part[l] = (T)0;
-#if ROWI_PREFETCH_E
-      // short sums: the first epilogue factor and the old separator values do not
-      // depend on the K-sum -- issue them before it (one memory round trip per unit)
-      T e0[VEC] = {}, o0[VEC] = {};
-      const bool pre = !LONGK && !FOLD && nE >= 1;
-      const bool pre_old = !LONGK && !FOLD && (P->out_kind == OUT_SEP || P->out_kind == OUT_SEP_DFRESH);
-      if (pre) load_vec_cs<T, VEC>(aux_c + P->efac_off[0] + __ldg(tir + nG) + __ldg(ts) + b0, e0);
-      if (pre_old) load_vec_cs<T, VEC>(aux_c + P->out_off + __ldg(tir + nG + nE) + TSV(nE) + b0, o0);
-#endif
       int since = 0;
       for (int k = 0; k < nK; k += KU) {
         T pv[KU][VEC];
@@ -1499,12 +1505,6 @@ __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restric
       const bool cs = a.stream_epi != 0;
       for (int e = 0; e < nE; ++e) {
         T f[VEC];
-#if ROWI_PREFETCH_E
-        if (e == 0 && pre) {
-#pragma unroll
-          for (int l = 0; l < VEC; ++l) f[l] = e0[l];
-        } else
-#endif
         {
           const T* ep = aux_c + P->efac_off[e] + __ldg(tir + nG + e) + TSV(e) + b0;
           if (cs) load_vec_cs<T, VEC>(ep, f);
@@ -1515,12 +1515,6 @@ __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restric
       }
       const int64_t j = (int64_t)__ldg(tir + nG + nE) + TSV(nE) + b0;
       T old[VEC] = {};
-#if ROWI_PREFETCH_E
-      if (pre_old) {
-#pragma unroll
-        for (int l = 0; l < VEC; ++l) old[l] = o0[l];
-      } else
-#endif
       if (P->out_kind == OUT_SEP || P->out_kind == OUT_SEP_DFRESH) {
         if (cs) load_vec_cs<T, VEC>(aux_c + P->out_off + j, old);
         else load_vec<T, VEC>(aux_c + P->out_off + j, old);
@@ -1759,6 +1753,28 @@ static auto by_ng(int ng, F f) {
     case 3: return f(std::integral_constant<int, 3>());
     default: return f(std::integral_constant<int, 4>());
   }
+}
+
+template <typename T, bool FOLD, int NG>
+static cudaError_t launch_contract_p_t(const CArgs& a, const TileParam& tp, int grid, cudaStream_t s) {
+  static bool done = false;
+  if (!done) {
+    cudaError_t e = cudaFuncSetAttribute(contract_p_kernel<T, FOLD, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)contract_smem<T, FOLD, NG>());
+    if (e != cudaSuccess) return e;
+    done = true;
+  }
+  return launch_pdl(contract_p_kernel<T, FOLD, NG>, grid, NT, contract_smem<T, FOLD, NG>(), s, a, tp);
+}
+
+cudaError_t launch_contract_tile_param(int dtype, int fold, int ng, const CArgs& a, const TileParam& tp, int grid,
+                                       cudaStream_t s) {
+  if (grid <= 0 || a.n_units <= 0) return cudaSuccess;
+  if (dtype == 0 && fold)
+    return by_ng<float, true>(ng, [&](auto c) { return launch_contract_p_t<float, true, decltype(c)::value>(a, tp, grid, s); });
+  if (dtype == 0)
+    return by_ng<float, false>(ng, [&](auto c) { return launch_contract_p_t<float, false, decltype(c)::value>(a, tp, grid, s); });
+  return by_ng<double, false>(ng, [&](auto c) { return launch_contract_p_t<double, false, decltype(c)::value>(a, tp, grid, s); });
 }
 
 cudaError_t launch_contract(int dtype, int fold, int rowi, int ng, const CArgs& a, int grid, cudaStream_t s) {
