@@ -1782,8 +1782,8 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
           all_tiny = hp.waves[w].groups.empty();
           max_thr = std::max(max_thr, tw[w].n_threads);
         }
-        static const int rounds = env_int("JT_TINY_CLUSTER_ROUNDS", 1);  // grid-stride rounds per wave
-        if (all_tiny && max_thr <= (int64_t)cmax * NT * rounds) {
+        // one unit per thread: every wave must fit the cluster's threads
+        if (all_tiny && max_thr <= (int64_t)cmax * NT) {
           prog->tiny_cluster = (int)std::min<int64_t>(cmax, std::max<int64_t>(1, (max_thr + NT - 1) / NT));
           prog->tiny_waves_launch = 0;
           prog->n_launches = 1;

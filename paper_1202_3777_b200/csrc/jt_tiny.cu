@@ -203,54 +203,81 @@ __device__ __forceinline__ double tiny_exec(const TPass& P, const T* __restrict_
 // unit0 list), decomposes its entry and row start, and -- with PDL -- only then
 // waits for the previous wave: descriptor reads and index math overlap the
 // previous kernel's tail.
-template <typename T, int NFM, bool PDL>
-__device__ __forceinline__ void tiny_wave(const TinyArgs& a, int w) {
-  T* __restrict__ clique = reinterpret_cast<T*>(a.clique);
-  const T* __restrict__ base = reinterpret_cast<const T*>(a.base);
-  T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
-  const int64_t stride = (int64_t)gridDim.x * NT;
+// One lane's unit of a wave: its pass, output entry, row chunk and the row
+// walk's start state -- all from program constants (descriptor reads and index
+// math), so it can be prepared before the previous wave's writes are visible.
+template <int NFM>
+struct TinyLane {
+  const TPass* P;
+  int G, sub, r0, r1;
+  bool in, live;
+  TRow<NFM> R;
+};
+
+template <int NFM>
+__device__ __forceinline__ void tiny_lane_prep(const TinyArgs& a, int w, int64_t t, TinyLane<NFM>& L) {
   const TinyWave tw = a.waves[w];
   const TPass* __restrict__ ps = a.passes + tw.pass0;
   const int64_t* __restrict__ u0 = a.unit0s + tw.pass0;
-  bool waited = !PDL;
-  for (int64_t t = (int64_t)blockIdx.x * NT + threadIdx.x; t < tw.n_threads || !waited; t += stride) {
-    const bool in = t < tw.n_threads;
-    int lo = 0;
-    if (in) {
-      int hi = tw.n_passes - 1;
-      while (lo < hi) {
-        const int m = (lo + hi + 1) >> 1;
-        if (__ldg(u0 + m) <= t) lo = m;
-        else hi = m - 1;
-      }
+  L.in = t < tw.n_threads;
+  int lo = 0;
+  if (L.in) {
+    int hi = tw.n_passes - 1;
+    while (lo < hi) {
+      const int m = (lo + hi + 1) >> 1;
+      if (__ldg(u0 + m) <= t) lo = m;
+      else hi = m - 1;
     }
-    const TPass& P = ps[lo];
-    const int u = in ? (int)(t - __ldg(u0 + lo)) : 0;
-    // P.warp = lanes per output entry (1, 2, 4, 8, 16 or 32): lane chunks of the
-    // row in lane order, then a fixed shuffle tree inside the lane group
-    const int G = in ? P.warp : 1;
-    const int j = u / G;
-    const int sub = u - j * G;
-    const bool live = in && j < P.n_out;  // lanes of the pass's padding compute nothing
-    const int nr = live ? (int)P.n_rest : 0;
-    const int per = (nr + G - 1) / G;
-    const int r0 = live ? sub * per : 0;
-    const int r1 = live ? (r0 + per < nr ? r0 + per : nr) : 0;
-    TRow<NFM> R;
-    if (live) tiny_prep<NFM>(P, j, r0, R);
+  }
+  L.P = ps + lo;
+  const TPass& P = *L.P;
+  const int u = L.in ? (int)(t - __ldg(u0 + lo)) : 0;
+  // P.warp = lanes per output entry (1, 2, 4, 8, 16 or 32): lane chunks of the
+  // row in lane order, then a fixed shuffle tree inside the lane group
+  L.G = L.in ? P.warp : 1;
+  const int j = u / L.G;
+  L.sub = u - j * L.G;
+  L.live = L.in && j < P.n_out;  // lanes of the pass's padding compute nothing
+  const int nr = L.live ? (int)P.n_rest : 0;
+  const int per = (nr + L.G - 1) / L.G;
+  L.r0 = L.live ? L.sub * per : 0;
+  L.r1 = L.live ? (L.r0 + per < nr ? L.r0 + per : nr) : 0;
+  if (L.live) tiny_prep<NFM>(P, j, L.r0, L.R);
+}
+
+// The data part: row loads, the lane-group shuffle tree, the Hugin update.
+template <typename T, int NFM>
+__device__ __forceinline__ void tiny_lane_exec(const TinyArgs& a, TinyLane<NFM>& L) {
+  T* __restrict__ clique = reinterpret_cast<T*>(a.clique);
+  const T* __restrict__ base = reinterpret_cast<const T*>(a.base);
+  T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
+  const TPass& P = *L.P;
+  const T* src = (P.src_arena == A_BASE ? base : P.src_arena == A_AUX ? aux : clique) + P.src_off;
+  T* dst = clique + (P.dst_off >= 0 ? P.dst_off : 0);
+  const bool fin = L.live && L.sub == 0 && P.out_kind != OUT_NONE;
+  T oldv = (T)0;
+  if (fin && (P.out_kind == OUT_SEP || P.out_kind == OUT_SEP_DFRESH)) oldv = aux[P.out_off + L.R.oo];
+  double s = L.live ? tiny_exec<T, NFM>(P, src, dst, aux, L.R, L.r0, L.r1) : 0.0;
+  for (int o = 1; o < L.G; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (fin) tiny_finalize<T>(P, L.R.oo, s, aux, a.qout, a.err, oldv);
+}
+
+// One wave, grid-stride over its units; with PDL the first unit is prepared
+// before the wait on the previous wave, overlapping that kernel's tail.
+template <typename T, int NFM, bool PDL>
+__device__ __forceinline__ void tiny_wave(const TinyArgs& a, int w) {
+  const int64_t stride = (int64_t)gridDim.x * NT;
+  const int64_t n = a.waves[w].n_threads;
+  bool waited = !PDL;
+  for (int64_t t = (int64_t)blockIdx.x * NT + threadIdx.x; t < n || !waited; t += stride) {
+    TinyLane<NFM> L;
+    tiny_lane_prep<NFM>(a, w, t, L);
     if (!waited) {
       asm volatile("griddepcontrol.wait;" ::: "memory");
       waited = true;
     }
-    if (!in) break;
-    const T* src = (P.src_arena == A_BASE ? base : P.src_arena == A_AUX ? aux : clique) + P.src_off;
-    T* dst = clique + (P.dst_off >= 0 ? P.dst_off : 0);
-    const bool fin = live && sub == 0 && P.out_kind != OUT_NONE;
-    T oldv = (T)0;
-    if (fin && (P.out_kind == OUT_SEP || P.out_kind == OUT_SEP_DFRESH)) oldv = aux[P.out_off + R.oo];
-    double s = live ? tiny_exec<T, NFM>(P, src, dst, aux, R, r0, r1) : 0.0;
-    for (int o = 1; o < G; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (fin) tiny_finalize<T>(P, R.oo, s, aux, a.qout, a.err, oldv);
+    if (!L.in) break;
+    tiny_lane_exec<T, NFM>(a, L);
   }
 }
 
@@ -278,10 +305,15 @@ __global__ void __launch_bounds__(NT, 2) tiny_wave_kernel(const TinyArgs a, int 
 // the wave itself.
 template <typename T, int NFM>
 __global__ void __launch_bounds__(NT, 1) tiny_cluster_kernel(const TinyArgs a) {
+  // every wave fits the cluster's threads (one unit per thread): the next
+  // wave's unit is prepared while this wave's stores drain, before the barrier
+  const int64_t t = (int64_t)blockIdx.x * NT + threadIdx.x;
+  TinyLane<NFM> L;
+  tiny_lane_prep<NFM>(a, 0, t, L);
   for (int w = 0; w < a.n_waves; ++w) {
-    tiny_wave<T, NFM, false>(a, w);
+    if (L.in) tiny_lane_exec<T, NFM>(a, L);
     if (w + 1 < a.n_waves) {
-      __syncthreads();
+      tiny_lane_prep<NFM>(a, w + 1, t, L);
       asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
       asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
     }
