@@ -1444,8 +1444,15 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
       // single trees, small (latency-bound) waves or scalar passes: the general kernel
       // at 2 vectors per thread, 3 CTAs per SM (more warps in flight)
       static const bool no_row = getenv("JT_NO_ROW") != nullptr, no_own = getenv("JT_NO_OWN") != nullptr;
-      int rc = compile_pass(st, ps, vec, local, bp, !small_wave && !no_row,
-                            st->B == 1 && (small_wave || vec == 1) ? 2 : KV, !no_own);
+      // single trees: 2 vectors per thread (3 CTAs/SM, more warps in flight) unless the pass
+      // streams a clique above 2^23 elements from HBM (c3), where 4 per thread measure better
+      // (c4B 0.73 -> 0.66 ms, c5 0.32 -> 0.30 ms fp32; c3 keeps 0.24)
+      static const int single_kv = env_int("JT_SINGLE_KV", 0);  // > 0: forced for every single-tree pass
+      int64_t pass_el = 1;
+      for (auto& x : pass_dims(st, ps)) pass_el *= x.card;
+      const int kv = st->B == 1 && single_kv > 0 ? single_kv
+                   : st->B == 1 && (small_wave || vec == 1 || pass_el <= (int64_t(1) << 23)) ? 2 : KV;
+      int rc = compile_pass(st, ps, vec, local, bp, !small_wave && !no_row, kv, !no_own);
       if (rc != JT_OK) return rc;
       bp.d.blk_off = (int64_t)blk.size();
       bp.d.blk32_off = (int64_t)hp.blk32.size();
