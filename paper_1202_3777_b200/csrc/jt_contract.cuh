@@ -1,4 +1,7 @@
-// Contraction kernels of the shared-base batch path, sm_100a.
+// Contraction kernels of the shared-base batch path, sm_100a:
+// templates only.  The launchers live in jt_contract_{tile,tilep,rowi}.cu so the
+// instantiations compile in parallel.
+#pragma once
 #include "jt_internal.h"
 #include "jt_device.cuh"
 #include <algorithm>
@@ -565,19 +568,6 @@ __global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F :
   rowi_body<T, FOLD, LONGK, true>(a, &rp.cp, rp.tk, rp.ts);
 }
 
-cudaError_t launch_contract_rowi_param(int dtype, int fold, int longk, const CArgs& a, const RowiParam& rp, int grid,
-                                       cudaStream_t s) {
-  if (grid <= 0 || a.n_units <= 0) return cudaSuccess;
-  if (dtype == 0) {
-    if (fold)
-      return longk ? launch_pdl(contract_rowi_p_kernel<float, true, true>, grid, NT, 0, s, a, rp)
-                   : launch_pdl(contract_rowi_p_kernel<float, true, false>, grid, NT, 0, s, a, rp);
-    return longk ? launch_pdl(contract_rowi_p_kernel<float, false, true>, grid, NT, 0, s, a, rp)
-                 : launch_pdl(contract_rowi_p_kernel<float, false, false>, grid, NT, 0, s, a, rp);
-  }
-  return longk ? launch_pdl(contract_rowi_p_kernel<double, false, true>, grid, NT, 0, s, a, rp)
-               : launch_pdl(contract_rowi_p_kernel<double, false, false>, grid, NT, 0, s, a, rp);
-}
 
 // Row-per-i passes over i-groups: igs consecutive i differ only in the
 // innermost i variable, which most factors (the large ones) do not index.  One
@@ -767,76 +757,8 @@ static cudaError_t launch_contract_p_t(const CArgs& a, const TileParam& tp, int 
   return launch_pdl(contract_p_kernel<T, FOLD, NG>, grid, NT, contract_smem<T, FOLD, NG>(), s, a, tp);
 }
 
-cudaError_t launch_contract_tile_param(int dtype, int fold, int ng, const CArgs& a, const TileParam& tp, int grid,
-                                       cudaStream_t s) {
-  if (grid <= 0 || a.n_units <= 0) return cudaSuccess;
-  if (dtype == 0 && fold)
-    return by_ng<float, true>(ng, [&](auto c) { return launch_contract_p_t<float, true, decltype(c)::value>(a, tp, grid, s); });
-  if (dtype == 0)
-    return by_ng<float, false>(ng, [&](auto c) { return launch_contract_p_t<float, false, decltype(c)::value>(a, tp, grid, s); });
-  return by_ng<double, false>(ng, [&](auto c) { return launch_contract_p_t<double, false, decltype(c)::value>(a, tp, grid, s); });
-}
 
-cudaError_t launch_contract(int dtype, int fold, int rowi, int ng, const CArgs& a, int grid, cudaStream_t s) {
-  if (grid <= 0 || a.n_units <= 0) return cudaSuccess;
-  if (rowi == 2 || rowi == 3) {  // i-groups: IGM 4 (rowi 2) or 8 (rowi 3)
-    if (dtype == 0) {
-      if (fold)
-        return rowi == 2 ? launch_pdl(contract_rowg_kernel<float, true, 4>, grid, NT, 0, s, a)
-                         : launch_pdl(contract_rowg_kernel<float, true, 8>, grid, NT, 0, s, a);
-      return rowi == 2 ? launch_pdl(contract_rowg_kernel<float, false, 4>, grid, NT, 0, s, a)
-                       : launch_pdl(contract_rowg_kernel<float, false, 8>, grid, NT, 0, s, a);
-    }
-    return rowi == 2 ? launch_pdl(contract_rowg_kernel<double, false, 4>, grid, NT, 0, s, a)
-                     : launch_pdl(contract_rowg_kernel<double, false, 8>, grid, NT, 0, s, a);
-  }
-  if (rowi) {
-    if (dtype == 0)
-      return rowi == 4 ? (fold ? launch_pdl(contract_rowi_kernel<float, true, true>, grid, NT, 0, s, a)
-                               : launch_pdl(contract_rowi_kernel<float, false, true>, grid, NT, 0, s, a))
-             : fold ? launch_pdl(contract_rowi_kernel<float, true>, grid, NT, 0, s, a)
-                    : launch_pdl(contract_rowi_kernel<float, false>, grid, NT, 0, s, a);
-    return rowi == 4 ? launch_pdl(contract_rowi_kernel<double, false, true>, grid, NT, 0, s, a)
-                     : launch_pdl(contract_rowi_kernel<double, false>, grid, NT, 0, s, a);
-  }
-  if (dtype == 0 && fold)
-    return by_ng<float, true>(ng, [&](auto c) { return launch_contract_t<float, true, decltype(c)::value>(a, grid, s); });
-  if (dtype == 0)
-    return by_ng<float, false>(ng, [&](auto c) { return launch_contract_t<float, false, decltype(c)::value>(a, grid, s); });
-  return by_ng<double, false>(ng, [&](auto c) { return launch_contract_t<double, false, decltype(c)::value>(a, grid, s); });
-}
 
-int contract_max_ctas_per_sm(int dtype, int fold, int rowi, int ng) {
-  int n = 0;
-  if (rowi == 2 || rowi == 3) {
-    if (dtype == 0 && fold)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rowi == 2 ? contract_rowg_kernel<float, true, 4>
-                                                                  : contract_rowg_kernel<float, true, 8>, NT, 0);
-    else if (dtype == 0)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rowi == 2 ? contract_rowg_kernel<float, false, 4>
-                                                                  : contract_rowg_kernel<float, false, 8>, NT, 0);
-    else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rowi == 2 ? contract_rowg_kernel<double, false, 4>
-                                                                  : contract_rowg_kernel<double, false, 8>, NT, 0);
-    return n > 0 ? n : 1;
-  }
-  if (rowi) {
-    const bool lk = rowi == 4;
-    if (dtype == 0 && fold)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lk ? contract_rowi_kernel<float, true, true>
-                                                           : contract_rowi_kernel<float, true>, NT, 0);
-    else if (dtype == 0)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lk ? contract_rowi_kernel<float, false, true>
-                                                           : contract_rowi_kernel<float, false>, NT, 0);
-    else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lk ? contract_rowi_kernel<double, false, true>
-                                                           : contract_rowi_kernel<double, false>, NT, 0);
-    return n > 0 ? n : 1;
-  }
-  if (dtype == 0 && fold) return by_ng<float, true>(ng, [&](auto c) { return occ_contract_t<float, true, decltype(c)::value>(); });
-  if (dtype == 0) return by_ng<float, false>(ng, [&](auto c) { return occ_contract_t<float, false, decltype(c)::value>(); });
-  return by_ng<double, false>(ng, [&](auto c) { return occ_contract_t<double, false, decltype(c)::value>(); });
-}
 
 
 }  // namespace jt
