@@ -162,6 +162,7 @@ struct PassSpec {
   Tensor out;
   int64_t ratio_off = -1;
   int64_t out2_off = -1;
+  int64_t x_off = -1;       // >= 0: this (paired) pass also writes its clique's product X here
 };
 
 struct LaunchGrp {  // one kernel launch of a wave
@@ -178,6 +179,7 @@ struct LaunchGrp {  // one kernel launch of a wave
   int64_t n_units = 0;
   int interleave = 0;  // CArgs::interleave
   int rp_idx = -1;     // >= 0: single row-per-i pass launched with its tables in the parameters
+  int xw = 0;          // 1: that pass writes the clique product X (rowi_p kernel with XW)
   int tp_idx = -1;     // >= 0: single tile pass launched with its tables in the parameters
 };
 
@@ -1283,6 +1285,7 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   for (int g = 0; g < nG; ++g) cp.gfac_off[g] = G[g]->off;
   for (int e = 0; e < nE; ++e) cp.efac_off[e] = E[e]->off;
   cp.out_kind_b = OUT_NONE;
+  cp.x_off = -1;
   // long K sums on the row-per-i kernel: several k in flight per lane (rowi code 4);
   // fp64 only (fp32 long sums fold, at two k per step already; measured -2% with it)
   const int longk = env_int("JT_ROWI_LONGK", st->esz == 8 ? 16 : 0);
@@ -1297,6 +1300,12 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
     cp.ratio_off_b = ps_b->ratio_off;
     cp.out2_off_b = ps_b->out2_off;
     for (int e = 0; e < nEb; ++e) cp.efac_off_b[e] = Eb[e]->off;
+    cp.x_off = ps.x_off;
+  }
+  if (ps.x_off >= 0 && (!ps_b || cp.rowi != 1 || cp.out_kind != OUT_SEP_DFRESH)) {
+    hp.w.resize(w0);
+    hp.ctab.resize(cp.ti_off);
+    return JT_ERR_UNSUPPORTED;  // X is written by the paired short-K row-per-i epilogue only
   }
   return JT_OK;
 }
@@ -1425,12 +1434,14 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
         if (partner[wi] >= 0) {
           const size_t n_w = hp.w.size(), n_t = hp.ctab.size();
           paired = compile_contract(st, ps, hp, cp, &w[partner[wi]]) == JT_OK;
+          if (!paired && ps.x_off >= 0) return JT_ERR_UNSUPPORTED;  // caller rebuilds without X
           if (!paired) {  // fall back to two separate passes
             hp.w.resize(n_w);
             hp.ctab.resize(n_t);
             partner[partner[wi]] = -1;
           }
         }
+        if (!paired && ps.x_off >= 0) return JT_ERR_UNSUPPORTED;
         if (paired || compile_contract(st, ps, hp, cp) == JT_OK) {
           const int key = ((st->esz == 4 && cp.nK > CKF ? 1 : 0) + 2 * cp.rowi) * NGK + (cp.rowi ? 0 : cp.nG);
           cps[key].push_back(cp);
@@ -1531,13 +1542,17 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
           hp.cpasses.push_back(cp);
           // row-per-i pass: descriptor and tables in the kernel parameters (constant bank)
           const int tsw = cp.nE + 1 + (cp.out_kind_b != OUT_NONE ? cp.nE_b + 1 : 0);
-          if ((cp.rowi == 1 || cp.rowi == 4) && cp.nK * cp.nG <= RP_TK && tsw <= RP_TS && env_int("JT_ROWI_PARAM", 1)) {
+          if (cp.x_off >= 0 && !((cp.rowi == 1) && cp.nK * cp.nG <= RP_TK && tsw <= RP_TS))
+            return JT_ERR_UNSUPPORTED;  // X needs the parameter-space row-per-i kernel
+          if ((cp.rowi == 1 || cp.rowi == 4) && cp.nK * cp.nG <= RP_TK && tsw <= RP_TS &&
+              (env_int("JT_ROWI_PARAM", 1) || cp.x_off >= 0)) {
             RowiParam rp;
             std::memset(&rp, 0, sizeof(rp));
             rp.cp = cp;
             for (int x = 0; x < cp.nK * cp.nG; ++x) rp.tk[x] = hp.ctab[cp.tk_off + x];
             for (int x = 0; x < tsw; ++x) rp.ts[x] = hp.ctab[cp.ts_off + x];
             cg.rp_idx = (int)hp.rparams.size();
+            cg.xw = cp.x_off >= 0 ? 1 : 0;
             hp.rparams.push_back(rp);
           }
           const int64_t tsn = (int64_t)cp.nS * (cp.nE + 1);
@@ -1559,6 +1574,8 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
     for (int key = 0; key < 10 * NGK; ++key) {
       const int fold = (key / NGK) & 1;
       if (cps[key].empty()) continue;
+      for (auto& x : cps[key])
+        if (x.x_off >= 0) return JT_ERR_UNSUPPORTED;  // X needs one pass per launch
       LaunchGrp cg;
       cg.kind = 3;
       cg.lm = fold;
@@ -1875,7 +1892,7 @@ static int launch_group(jt_state* st, const Program* pr, const WaveRt& w, const 
     static const int stream_epi = env_int("JT_EPI_CS", 1);
     c.stream_epi = stream_epi;
     if (g.rp_idx >= 0)
-      CK(launch_contract_rowi_param(st->plan->dtype, g.lm, g.m == 4, c, pr->rparams[g.rp_idx], g.grid, s));
+      CK(launch_contract_rowi_param(st->plan->dtype, g.lm, g.m == 4, c, pr->rparams[g.rp_idx], g.grid, s, g.xw != 0));
     else if (g.tp_idx >= 0)
       CK(launch_contract_tile_param(st->plan->dtype, g.lm, g.vec, c, pr->tparams[g.tp_idx], g.grid, s));
     else
@@ -2112,7 +2129,7 @@ static Orient orient(const jt_plan* p, const std::vector<int>& roots) {
 // written once in distribute.  Cliques with more factors than a pass carries
 // absorb their children's ratios eagerly (in-place) during collect instead.
 static int build_propagate(jt_state* st, const std::vector<int>& roots, const std::vector<int>& qvars,
-                           std::vector<std::vector<PassSpec>>& waves, bool fresh = false) {
+                           std::vector<std::vector<PassSpec>>& waves, bool fresh = false, bool hub_x = false) {
   const jt_plan* p = st->plan;
   const bool shared = st->mode == JT_SHARED_BASE;
   const int src_arena = shared ? A_BASE : A_CLIQUE;
@@ -2241,9 +2258,12 @@ static int build_propagate(jt_state* st, const std::vector<int>& roots, const st
     qby[best].push_back(v);
   }
   // ---- distribute: by depth, root first ----
-  std::vector<std::vector<PassSpec>> dw(o.max_depth + 3);
+  // dwx[d]: passes of depth d that read a clique product X written at depth d
+  std::vector<std::vector<PassSpec>> dw(o.max_depth + 3), dwx(o.max_depth + 3);
+  std::vector<char> x_used(o.max_depth + 3, 0);
   for (int c = 0; c < n; ++c) {
     const int d = o.depth[c];
+    const size_t dw0 = dw[d].size();
     std::vector<Tensor> fac;
     if (!eager[c]) fac = child_ratios(c);
     if (o.parent[c] >= 0) fac.push_back(sep_tensor(st, o.psep[c], st->ratD_off[o.psep[c]]));
@@ -2294,6 +2314,67 @@ static int build_propagate(jt_state* st, const std::vector<int>& roots, const st
       // materialized: queries read the final table, after its writer
       dw[shared ? d : d + 2].push_back(ps);
     }
+    // Clique product X (shared-base, fresh): when two children share a separator
+    // scope S, their paired pass reads every factor over S anyway; it also writes
+    // X = Π{factors of c over S} (into the per-program message scratch), and the
+    // clique's other passes that multiply all of those factors read X instead,
+    // one sub-wave later (c5's hub: its other two distribute passes read one
+    // tensor instead of three 140000-entry separators).
+    if (hub_x && shared && fresh && !eager[c] && !x_used[d] && dw[d].size() > dw0) {
+      std::map<std::vector<int>, int> by_scope;
+      for (auto& chp : ch) by_scope[p->svars[chp.second]]++;
+      const std::vector<int>* S = nullptr;
+      for (auto& kv : by_scope)
+        if (kv.second >= 2 && (!S || kv.first.size() > S->size())) S = &kv.first;
+      std::vector<Tensor> fin;
+      if (S)
+        for (auto& t : fac)
+          if (std::includes(S->begin(), S->end(), t.vars.begin(), t.vars.end())) fin.push_back(t);
+      if (S && fin.size() >= 2) {
+        auto has = [](const std::vector<Tensor>& fs, const Tensor& t) {
+          for (auto& f : fs)
+            if (f.off == t.off && f.vars == t.vars) return true;
+          return false;
+        };
+        int writer = -1, consumers = 0;
+        for (size_t q = dw0; q < dw[d].size(); ++q) {
+          PassSpec& ps = dw[d][q];
+          if (ps.clique != c || !ps.scope.empty()) continue;
+          if (ps.out.vars == *S) {
+            if (writer < 0 && ps.out_kind == OUT_SEP_DFRESH) writer = (int)q;
+            continue;
+          }
+          bool all = true;
+          for (auto& t : fin) all = all && has(ps.factors, t);
+          consumers += all;
+        }
+        if (writer >= 0 && consumers > 0) {
+          int s_id = -1;
+          for (auto& chp : ch)
+            if (p->svars[chp.second] == *S) s_id = chp.second;
+          Tensor X = sep_tensor(st, s_id, st->msg_ratio_off);
+          dw[d][writer].x_off = st->msg_ratio_off;
+          std::vector<PassSpec> keep;
+          for (size_t q = dw0; q < dw[d].size(); ++q) {
+            PassSpec ps = dw[d][q];
+            bool all = ps.clique == c && ps.scope.empty() && ps.out.vars != *S;
+            for (auto& t : fin) all = all && has(ps.factors, t);
+            if (!all) {
+              keep.push_back(ps);
+              continue;
+            }
+            std::vector<Tensor> f2{X};
+            for (auto& t : ps.factors)
+              if (!has(fin, t)) f2.push_back(t);
+            ps.factors = f2;
+            dwx[d].push_back(ps);
+          }
+          dw[d].resize(dw0);
+          dw[d].insert(dw[d].end(), keep.begin(), keep.end());
+          x_used[d] = 1;
+        }
+      }
+    }
   }
   for (int sp = 0; sp < p->n_seps; ++sp) {
     if (qsep[sp].empty()) continue;
@@ -2311,7 +2392,10 @@ static int build_propagate(jt_state* st, const std::vector<int>& roots, const st
       dw[o.depth[par] + 1].push_back(ps);
     }
   }
-  for (auto& w : dw) waves.push_back(w);
+  for (size_t d = 0; d < dw.size(); ++d) {
+    waves.push_back(dw[d]);
+    if (!dwx[d].empty()) waves.push_back(dwx[d]);
+  }
   return JT_OK;
 }
 
@@ -3067,9 +3151,14 @@ extern "C" int jt_propagate_query(jt_state* st, int n, const int32_t* var, int n
     pr = it->second.get();
   } else {
     std::vector<std::vector<PassSpec>> waves;
-    int rc = build_propagate(st, p->roots, vs, waves, fresh);
+    int rc = build_propagate(st, p->roots, vs, waves, fresh, env_int("JT_HUBX", 1) != 0);
     if (rc) return rc;
     rc = get_program(st, key, waves, &pr);
+    if (rc == JT_ERR_UNSUPPORTED) {  // the clique product could not be placed: plain program
+      waves.clear();
+      if ((rc = build_propagate(st, p->roots, vs, waves, fresh, false))) return rc;
+      rc = get_program(st, key, waves, &pr);
+    }
     if (rc) return rc;
   }
   int rc = run_program(st, pr, s);
@@ -3230,10 +3319,17 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
     }
   }
   std::vector<std::vector<PassSpec>> waves;
-  int rc = build_propagate(&st, plan->roots, qv, waves, kind >= 1);
+  int rc = build_propagate(&st, plan->roots, qv, waves, kind >= 1, env_int("JT_HUBX", 1) != 0);
   if (rc) return rc;
   rc = validate_waves(&st, waves);
   if (rc) return rc;
+  {
+    HostProgram probe;
+    if (compile_program(&st, waves, probe, occ > 0 ? occ : 2) == JT_ERR_UNSUPPORTED) {
+      waves.clear();  // as the runtime does: the clique product could not be placed
+      if ((rc = build_propagate(&st, plan->roots, qv, waves, kind >= 1, false))) return rc;
+    }
+  }
   HostProgram hp;
   std::vector<std::vector<char>> tmask;
   std::vector<TPass> tp;
@@ -3298,6 +3394,7 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
         else if (ps.out_kind != OUT_NONE) bytes += tsize(ps.out) * st.esz * 3;
         const double csz = (double)plan->csize[ps.clique] * (ps.src_arena == A_BASE ? 1.0 : (double)st.B);
         if (ps.scope.empty()) bytes += csz * st.esz * (ps.write ? 2 : 1);
+        if (ps.x_off >= 0) bytes += tsize(ps.out) * st.esz;  // the clique product X
         if (getenv("JT_DEBUG_SPECS")) {
           double fb = 0.0;
           for (auto& f : ps.factors) fb += tsize(f) * st.esz;

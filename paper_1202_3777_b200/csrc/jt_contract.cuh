@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_p_kernel(const CArgs a,
 #ifndef ROWI_MINB_L
 #define ROWI_MINB_L 4
 #endif
-template <typename T, bool FOLD, bool LONGK, bool PRM>
+template <typename T, bool FOLD, bool LONGK, bool PRM, bool XW = false>
 __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restrict__ P0, const int32_t* __restrict__ tk0,
                                           const int32_t* __restrict__ ts0) {
   // one i per warp unit (few registers: three or four CTAs per SM), KU values
@@ -506,6 +506,9 @@ __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restric
 #pragma unroll
       for (int l = 0; l < VEC; ++l) v[l] = vsum[l] = acc[l] + (double)part[l];
       const bool cs = a.stream_epi != 0;
+      double xp[XW ? VEC : 1];  // XW: product of the E factors (times old below) -> X
+#pragma unroll
+      for (int l = 0; l < (XW ? VEC : 1); ++l) xp[l] = 1.0;
       for (int e = 0; e < nE; ++e) {
         T f[VEC];
         {
@@ -514,13 +517,23 @@ __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restric
           else load_vec_ro<T, VEC>(ep, f);
         }
 #pragma unroll
-        for (int l = 0; l < VEC; ++l) v[l] *= (double)f[l];
+        for (int l = 0; l < VEC; ++l) {
+          v[l] *= (double)f[l];
+          if (XW) xp[l % (XW ? VEC : 1)] *= (double)f[l];
+        }
       }
       const int64_t j = (int64_t)__ldg(tir + nG + nE) + TSV(nE) + b0;
       T old[VEC] = {};
       if (P->out_kind == OUT_SEP || P->out_kind == OUT_SEP_DFRESH) {
         if (cs) load_vec_cs<T, VEC>(aux_c + P->out_off + j, old);
         else load_vec<T, VEC>(aux_c + P->out_off + j, old);
+      }
+      if (XW) {  // X = old * Π E (the product of every factor over the output scope)
+        T xv[VEC];
+#pragma unroll
+        for (int l = 0; l < VEC; ++l) xv[l] = (T)(xp[l % (XW ? VEC : 1)] * (double)old[l]);
+        if (cs) store_vec_cs<T, VEC>(aux + P->x_off + j, xv);
+        else store_vec<T, VEC>(aux + P->x_off + j, xv);
       }
       bool bad = finalize_lanes<T, double, VEC>(P->out_kind, P->out_off, P->ratio_off, P->out2_off, j, v, old, aux,
                                                 a.qout, cs);
@@ -561,11 +574,11 @@ __global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F :
   rowi_body<T, FOLD, LONGK, false>(a, nullptr, nullptr, nullptr);
 }
 
-template <typename T, bool FOLD, bool LONGK>
+template <typename T, bool FOLD, bool LONGK, bool XW = false>
 __global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F : sizeof(T) == 8 ? ROWI_MINB_D : ROWI_MINB_NF)
     contract_rowi_p_kernel(const CArgs a, const __grid_constant__ RowiParam rp) {
   pdl_enter();
-  rowi_body<T, FOLD, LONGK, true>(a, &rp.cp, rp.tk, rp.ts);
+  rowi_body<T, FOLD, LONGK, true, XW>(a, &rp.cp, rp.tk, rp.ts);
 }
 
 

@@ -8,8 +8,15 @@ cudaError_t launch_contract_tile(int dtype, int fold, int ng, const CArgs& a, in
 int contract_tile_max_ctas_per_sm(int dtype, int fold, int ng);
 
 cudaError_t launch_contract_rowi_param(int dtype, int fold, int longk, const CArgs& a, const RowiParam& rp, int grid,
-                                       cudaStream_t s) {
+                                       cudaStream_t s, bool xw) {
   if (grid <= 0 || a.n_units <= 0) return cudaSuccess;
+  if (xw) {  // paired short-K passes that also write the clique's product X
+    if (longk) return cudaErrorInvalidValue;
+    if (dtype == 0)
+      return fold ? launch_pdl(contract_rowi_p_kernel<float, true, false, true>, grid, NT, 0, s, a, rp)
+                  : launch_pdl(contract_rowi_p_kernel<float, false, false, true>, grid, NT, 0, s, a, rp);
+    return launch_pdl(contract_rowi_p_kernel<double, false, false, true>, grid, NT, 0, s, a, rp);
+  }
   if (dtype == 0) {
     if (fold)
       return longk ? launch_pdl(contract_rowi_p_kernel<float, true, true>, grid, NT, 0, s, a, rp)

@@ -131,6 +131,8 @@ struct CPass {
   // messages to two children over equal separators -- shares the sum; only its
   // epilogue factors and output differ.  out_kind_b == OUT_NONE: no second output.
   // ti rows then hold [G, E, out, E_b, out_b]; ts rows [E, out, E_b, out_b].
+  int64_t x_off;            // >= 0 (paired passes): also write X = old_a * Π E_a (the product of every
+                            // factor over the output scope) here, for the clique's other passes
   int out_kind_b, nE_b;
   int64_t out_off_b, ratio_off_b, out2_off_b;
   int64_t efac_off_b[MAXF];
@@ -166,7 +168,7 @@ struct RowiParam {
   int32_t ts[RP_TS];
 };
 cudaError_t launch_contract_rowi_param(int dtype, int fold, int longk, const CArgs& a, const RowiParam& rp, int grid,
-                                       cudaStream_t s);
+                                       cudaStream_t s, bool xw = false);
 constexpr int TP_TS = 1024;  // ints of the s'-row table of a tile pass (nS x (nE + 1))
 struct TileParam {
   CPass cp;
