@@ -87,3 +87,18 @@ def test_small_single_trees_use_tiny_passes():
     assert c1.startswith("tiny passes (mode 2): 7 of 7 waves")
     c3 = report("c3", batch=1, mode="materialized", kind=0, dtype="f32")
     assert not c3.startswith("tiny passes")
+
+
+def test_batch_program_pairs_siblings_and_shares_the_hub_product(monkeypatch):
+    """c5's hub clique 2 sends distribute messages to two children over the same
+    140000-entry separator: the planner pairs them into ONE row-per-i pass with
+    two epilogues; in fp64 that pass also writes the clique product X and the
+    hub's two other distribute passes read it (one sub-wave later), which the
+    compulsory-bytes accounting reflects."""
+    f64 = report("c5", batch=4096, mode="shared", kind=1, dtype="f64")
+    paired = [l for l in f64.splitlines() if l.startswith("  contract clique 2 out 4 nI 140000")]
+    assert len(paired) == 1, paired  # two DFRESH passes -> one paired pass
+    total = lambda t: float(next(l for l in t.splitlines() if l.startswith("compulsory total MB")).split()[-1])
+    monkeypatch.setenv("JT_HUBX", "0")
+    f64_nox = report("c5", batch=4096, mode="shared", kind=1, dtype="f64")
+    assert total(f64) < total(f64_nox) - 10000  # ~13.8 GB fewer per 4096-case micro-batch
