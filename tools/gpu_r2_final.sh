@@ -7,6 +7,6 @@ set -u
 TAG=${1:-r2c}
 bash tools/gpu_r2.sh $TAG
 bash tools/gpu_single_list.sh $TAG "c3 c4B c5" f32
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:contract_rowi_kernel -s 7 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:contract_rowi -s 7 -c 1 \
   -o gpurun_out/full_${TAG}_paired -f python tools/prof_run.py --config c5 --dtype f64 --batch 4096 --reps 0 \
   > gpurun_out/full_${TAG}_paired.log 2>&1; echo "full rc=$?"
