@@ -1568,7 +1568,10 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
             hp.tparams.push_back(tpm);
           }
           hp.cpass_clique.push_back(cpc2[key][q]);
-          const int occ = occ_override ? occ_override : contract_max_ctas_per_sm(st->plan->dtype, fold, cg.m, cg.vec);
+          const int occ = occ_override ? occ_override
+                          : cg.rp_idx >= 0
+                              ? contract_rowi_param_max_ctas(st->plan->dtype, fold, cg.m == 4, cp.nG, cg.xw != 0)
+                              : contract_max_ctas_per_sm(st->plan->dtype, fold, cg.m, cg.vec);
           cg.grid = (int)std::min<int64_t>((cg.n_units + NT / 32 - 1) / (NT / 32), (int64_t)occ * st->num_sms);
           rt.groups.push_back(cg);
         }

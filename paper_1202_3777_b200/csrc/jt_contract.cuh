@@ -419,7 +419,9 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_p_kernel(const CArgs a,
 #ifndef ROWI_MINB_L
 #define ROWI_MINB_L 4
 #endif
-template <typename T, bool FOLD, bool LONGK, bool PRM, bool XW = false>
+// NGC: the pass's factor count when fixed at compile time (1..3; 0 = read from
+// the descriptor, loops bounded by CMAXG and predicated per factor)
+template <typename T, bool FOLD, bool LONGK, bool PRM, bool XW = false, int NGC = 0>
 __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restrict__ P0, const int32_t* __restrict__ tk0,
                                           const int32_t* __restrict__ ts0) {
   // one i per warp unit (few registers: three or four CTAs per SM), KU values
@@ -449,15 +451,16 @@ __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restric
     const int nCG = P->nCG;
     const int cg = P->cmaj ? (int)(ul / P->nI) : (int)(ul % nCG);
     const int64_t i = P->cmaj ? ul % P->nI : ul / nCG;
-    const int nK = P->nK, nG = P->nG, nE = P->nE;
+    constexpr int GM = NGC ? NGC : CMAXG;
+    const int nK = P->nK, nG = NGC ? NGC : P->nG, nE = P->nE;
     const bool two = P->out_kind_b != OUT_NONE;  // paired sibling output (same K-sum)
     const int tw = nG + nE + 1 + (two ? P->nE_b + 1 : 0);
     const int32_t* __restrict__ tir = a.tab + P->ti_off + i * tw;
     const int32_t* __restrict__ tk = PRM ? tk0 : a.tab + P->tk_off;
     const int32_t* __restrict__ ts = PRM ? ts0 : a.tab + P->ts_off;
-    const T* gq[CMAXG];
+    const T* gq[GM];
 #pragma unroll
-    for (int g = 0; g < CMAXG; ++g) gq[g] = aux_c + (g < nG ? P->gfac_off[g] + __ldg(tir + g) : 0);
+    for (int g = 0; g < GM; ++g) gq[g] = aux_c + (g < nG ? P->gfac_off[g] + __ldg(tir + g) : 0);
     const T* __restrict__ wrow = W + P->w_off + i * (int64_t)nK;
     const int bstep = 32 * VEC * nCG;
     for (int b0 = cg * 32 * VEC + lane * VEC; b0 < a.B; b0 += bstep) {
@@ -477,8 +480,8 @@ __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restric
 #pragma unroll
           for (int l = 0; l < VEC; ++l) pv[q][l] = (T)1;
 #pragma unroll
-          for (int g = 0; g < CMAXG; ++g) {
-            if (g < nG) {
+          for (int g = 0; g < GM; ++g) {
+            if (NGC || g < nG) {
               T f[VEC];
               load_vec_ro<T, VEC>(gq[g] + b0 + (PRM ? tk[kq * nG + g] : __ldg(tk + kq * nG + g)), f);
 #pragma unroll
@@ -574,11 +577,11 @@ __global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F :
   rowi_body<T, FOLD, LONGK, false>(a, nullptr, nullptr, nullptr);
 }
 
-template <typename T, bool FOLD, bool LONGK, bool XW = false>
+template <typename T, bool FOLD, bool LONGK, bool XW = false, int NGC = 0>
 __global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F : sizeof(T) == 8 ? ROWI_MINB_D : ROWI_MINB_NF)
     contract_rowi_p_kernel(const CArgs a, const __grid_constant__ RowiParam rp) {
   pdl_enter();
-  rowi_body<T, FOLD, LONGK, true, XW>(a, &rp.cp, rp.tk, rp.ts);
+  rowi_body<T, FOLD, LONGK, true, XW, NGC>(a, &rp.cp, rp.tk, rp.ts);
 }
 
 

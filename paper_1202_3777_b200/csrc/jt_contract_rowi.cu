@@ -1,5 +1,7 @@
 // Row-per-i contraction launchers (plain, long-K, i-grouped, parameter-space) and the
 // contraction dispatchers.
+#include <cstdlib>
+
 #include "jt_contract.cuh"
 
 namespace jt {
@@ -7,25 +9,32 @@ namespace jt {
 cudaError_t launch_contract_tile(int dtype, int fold, int ng, const CArgs& a, int grid, cudaStream_t s);
 int contract_tile_max_ctas_per_sm(int dtype, int fold, int ng);
 
+cudaError_t launch_contract_rowi_param_float(int fold, int longk, int ng, const CArgs& a, const RowiParam& rp, int grid,
+                                            cudaStream_t s, bool xw);
+cudaError_t launch_contract_rowi_param_double(int fold, int longk, int ng, const CArgs& a, const RowiParam& rp, int grid,
+                                             cudaStream_t s, bool xw);
+int contract_rowi_param_max_ctas_float(int fold, int longk, int ng, bool xw);
+int contract_rowi_param_max_ctas_double(int fold, int longk, int ng, bool xw);
+
+// JT_ROWI_NGC=0: the descriptor-driven kernel for every factor count (A/B switch)
+static int rowi_ngc(int ng) {
+  static const int on = getenv("JT_ROWI_NGC") ? atoi(getenv("JT_ROWI_NGC")) : 1;
+  return on ? ng : 0;
+}
+
+// xw: paired short-K passes that also write the clique's product X
 cudaError_t launch_contract_rowi_param(int dtype, int fold, int longk, const CArgs& a, const RowiParam& rp, int grid,
                                        cudaStream_t s, bool xw) {
   if (grid <= 0 || a.n_units <= 0) return cudaSuccess;
-  if (xw) {  // paired short-K passes that also write the clique's product X
-    if (longk) return cudaErrorInvalidValue;
-    if (dtype == 0)
-      return fold ? launch_pdl(contract_rowi_p_kernel<float, true, false, true>, grid, NT, 0, s, a, rp)
-                  : launch_pdl(contract_rowi_p_kernel<float, false, false, true>, grid, NT, 0, s, a, rp);
-    return launch_pdl(contract_rowi_p_kernel<double, false, false, true>, grid, NT, 0, s, a, rp);
-  }
-  if (dtype == 0) {
-    if (fold)
-      return longk ? launch_pdl(contract_rowi_p_kernel<float, true, true>, grid, NT, 0, s, a, rp)
-                   : launch_pdl(contract_rowi_p_kernel<float, true, false>, grid, NT, 0, s, a, rp);
-    return longk ? launch_pdl(contract_rowi_p_kernel<float, false, true>, grid, NT, 0, s, a, rp)
-                 : launch_pdl(contract_rowi_p_kernel<float, false, false>, grid, NT, 0, s, a, rp);
-  }
-  return longk ? launch_pdl(contract_rowi_p_kernel<double, false, true>, grid, NT, 0, s, a, rp)
-               : launch_pdl(contract_rowi_p_kernel<double, false, false>, grid, NT, 0, s, a, rp);
+  const int ng = rowi_ngc(rp.cp.nG);
+  return dtype == 0 ? launch_contract_rowi_param_float(fold, longk, ng, a, rp, grid, s, xw)
+                    : launch_contract_rowi_param_double(fold, longk, ng, a, rp, grid, s, xw);
+}
+
+int contract_rowi_param_max_ctas(int dtype, int fold, int longk, int ng, bool xw) {
+  ng = rowi_ngc(ng);
+  return dtype == 0 ? contract_rowi_param_max_ctas_float(fold, longk, ng, xw)
+                    : contract_rowi_param_max_ctas_double(fold, longk, ng, xw);
 }
 
 cudaError_t launch_contract(int dtype, int fold, int rowi, int ng, const CArgs& a, int grid, cudaStream_t s) {

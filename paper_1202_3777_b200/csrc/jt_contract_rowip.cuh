@@ -1,0 +1,34 @@
+// Parameter-space row-per-i launchers, one translation unit per dtype
+// (jt_contract_rowip32.cu / jt_contract_rowip64.cu): the factor count per k is a
+// compile-time constant for nG <= 3, so the k loop issues exactly nG vector
+// loads per k (no per-factor predicates) — see rowi_body.
+#pragma once
+#include "jt_contract.cuh"
+
+namespace jt {
+
+template <typename T, bool FOLD, bool LONGK, bool XW>
+static auto rowi_p_fn(int ng) {
+  switch (ng) {
+    case 1: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 1>;
+    case 2: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 2>;
+    case 3: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 3>;
+    default: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 0>;
+  }
+}
+
+// ng <= 0: the generic (descriptor-driven) kernel
+template <typename T>
+static void (*rowi_p_select(int fold, int longk, int ng, bool xw))(const CArgs, const RowiParam) {
+  if (xw) {
+    if (longk) return nullptr;
+    if constexpr (sizeof(T) == 4) return fold ? rowi_p_fn<T, true, false, true>(ng) : rowi_p_fn<T, false, false, true>(ng);
+    else return rowi_p_fn<T, false, false, true>(ng);
+  }
+  if constexpr (sizeof(T) == 4) {
+    if (fold) return longk ? rowi_p_fn<T, true, true, false>(ng) : rowi_p_fn<T, true, false, false>(ng);
+  }
+  return longk ? rowi_p_fn<T, false, true, false>(ng) : rowi_p_fn<T, false, false, false>(ng);
+}
+
+}  // namespace jt
