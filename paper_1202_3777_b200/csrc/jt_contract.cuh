@@ -69,10 +69,18 @@ template <> struct CTraits<double> { static constexpr int VEC = 2; };
 #ifndef CON_RING_F
 #define CON_RING_F 2048
 #endif
+// CON_WRING: the stage also carries the k's W row (TMC entries, copied by the
+// first lanes, read by all after a warp barrier), so W loads are as far ahead
+// as the factor slices instead of one k in registers.
+#ifndef CON_WRING
+#define CON_WRING 1
+#endif
 template <typename T, int NG, bool FOLD> struct CRing {
-  static constexpr int SB = NG * 512;  // one stage: NG factor slices of 16 B per lane
+  static constexpr int SF = NG * 512;                          // NG factor slices of 16 B per lane
+  static constexpr int WB = CON_WRING ? TMC * (int)sizeof(T) : 0;  // the W row
+  static constexpr int SB = SF + WB;                           // one stage
   static constexpr int BUDGET = FOLD ? CON_RING_F : CON_RING_NF;
-  static constexpr int D = NG == 0 ? 2 : (BUDGET / SB > 8 ? 8 : (BUDGET / SB < 2 ? 2 : BUDGET / SB));
+  static constexpr int D = NG == 0 ? (CON_WRING ? 4 : 2) : (BUDGET / SF > 8 ? 8 : (BUDGET / SF < 2 ? 2 : BUDGET / SF));
   static constexpr size_t BYTES = (size_t)(NT / 32) * D * SB;
 };
 constexpr size_t CFOLD_SMEM = (size_t)TMC * 4 * NT * sizeof(double);  // fp32 fold accumulators
@@ -174,9 +182,10 @@ __device__ __forceinline__ void tile_body(const CArgs& a, const CPass* __restric
   extern __shared__ __align__(16) unsigned char csm_c[];
   double* cacc = reinterpret_cast<double*>(csm_c);  // FOLD: [TMC * VEC][NT] fp64 accumulators
   const int lane = threadIdx.x & 31;
-  // this lane's slot of stage 0, slice 0; stage q slice g at + q * SB + g * 512
-  unsigned char* const ring =
-      csm_c + (FOLD ? CFOLD_SMEM : 0) + (size_t)(threadIdx.x >> 5) * R::D * R::SB + lane * 16;
+  // this warp's stage 0; stage q: slice g of lane l at + q * SB + g * 512 + l * 16, W row at + q * SB + SF
+  unsigned char* const ring = csm_c + (FOLD ? CFOLD_SMEM : 0) + (size_t)(threadIdx.x >> 5) * R::D * R::SB;
+  constexpr bool WR = CON_WRING != 0;
+  constexpr int WL = R::WB / 16;  // lanes copying the W row (16 B each)
   const T* __restrict__ W = reinterpret_cast<const T*>(a.w);
   const T* __restrict__ aux_c = reinterpret_cast<const T*>(a.aux);
   const int n_warps = gridDim.x * (NT / 32);
@@ -228,11 +237,24 @@ __device__ __forceinline__ void tile_body(const CArgs& a, const CPass* __restric
 #pragma unroll
     for (int g = 0; g < NG; ++g) gq[g] = aux_c + P->gfac_off[g] + __ldg(ti + g);
     for (int b0 = cg * 32 * VEC + lane * VEC; b0 < a.B; b0 += bstep) {
+      // lanes of this warp with cases left (a prefix): the W row copy and the warp barrier
+      const int na = min(32, (a.B - (b0 - lane * VEC) + VEC - 1) / VEC);
+      const unsigned wm = na >= 32 ? 0xffffffffu : ((1u << na) - 1u);
       auto issue = [&](int k, unsigned char* sp) {
 #pragma unroll
-        for (int g = 0; g < NG; ++g) cp_async16(sp + g * 512, gq[g] + b0 + (PRM ? tk[k * NG + g] : __ldg(tk + k * NG + g)));
+        for (int g = 0; g < NG; ++g)
+          cp_async16(sp + g * 512 + lane * 16, gq[g] + b0 + (PRM ? tk[k * NG + g] : __ldg(tk + k * NG + g)));
+        if (WR) {
+          const T* wk = wrow + (int64_t)k * nSp;
+          if (na >= WL) {
+            if (lane < WL) cp_async16(sp + R::SF + lane * 16, wk + lane * (16 / (int)sizeof(T)));
+          } else if (lane == 0) {
+#pragma unroll
+            for (int c = 0; c < WL; ++c) cp_async16(sp + R::SF + c * 16, wk + c * (16 / (int)sizeof(T)));
+          }
+        }
       };
-      if (NG > 0) {
+      if (NG > 0 || WR) {
 #pragma unroll
         for (int q = 0; q < R::D - 1; ++q) {
           if (q < nK) issue(q, ring + q * R::SB);
@@ -247,47 +269,61 @@ __device__ __forceinline__ void tile_body(const CArgs& a, const CPass* __restric
       if (FOLD)
 #pragma unroll
         for (int q = 0; q < TMC * VEC; ++q) cacc[q * NT + threadIdx.x] = 0.0;
-      T wn[CON_WPF][TMC];  // W rows of the next CON_WPF k
+      constexpr int WPF = WR ? 1 : CON_WPF;
+      T wn[WPF][TMC];  // !WR: W rows of the next CON_WPF k
+      if (!WR) {
 #pragma unroll
-      for (int q = 0; q < CON_WPF; ++q)
+        for (int q = 0; q < WPF; ++q)
 #pragma unroll
-        for (int h = 0; h < TMC / WV; ++h) {
-          T x[WV];
-          if (q < nK) load_vec_ro<T, WV>(wrow + (int64_t)q * nSp + h * WV, x);
+          for (int h = 0; h < TMC / WV; ++h) {
+            T x[WV];
+            if (q < nK) load_vec_ro<T, WV>(wrow + (int64_t)q * nSp + h * WV, x);
 #pragma unroll
-          for (int l = 0; l < WV; ++l) wn[q][h * WV + l] = q < nK ? x[l] : (T)0;
-        }
+            for (int l = 0; l < WV; ++l) wn[q][h * WV + l] = q < nK ? x[l] : (T)0;
+          }
+      }
       unsigned char* sp = ring;                          // stage of k
       unsigned char* spn = ring + (R::D - 1) * R::SB;    // stage refilled at k (k + D - 1)
       int since = 0;
       for (int k = 0; k < nK; ++k) {
         T w[TMC];
-#pragma unroll
-        for (int r = 0; r < TMC; ++r) w[r] = wn[0][r];
-#pragma unroll
-        for (int q = 0; q + 1 < CON_WPF; ++q)
-#pragma unroll
-          for (int r = 0; r < TMC; ++r) wn[q][r] = wn[q + 1][r];
-        if (k + CON_WPF < nK) {
+        if (NG > 0 || WR) cp_async_wait<R::D - 2>();
+        if (WR) {
+          __syncwarp(wm);  // the W row of this stage was copied by the first lanes
 #pragma unroll
           for (int h = 0; h < TMC / WV; ++h) {
             T x[WV];
-            load_vec_ro<T, WV>(wrow + (int64_t)(k + CON_WPF) * nSp + h * WV, x);
+            load_vec<T, WV>(reinterpret_cast<const T*>(sp + R::SF) + h * WV, x);
 #pragma unroll
-            for (int l = 0; l < WV; ++l) wn[CON_WPF - 1][h * WV + l] = x[l];
+            for (int l = 0; l < WV; ++l) w[h * WV + l] = x[l];
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < TMC; ++r) w[r] = wn[0][r];
+#pragma unroll
+          for (int q = 0; q + 1 < WPF; ++q)
+#pragma unroll
+            for (int r = 0; r < TMC; ++r) wn[q][r] = wn[q + 1][r];
+          if (k + WPF < nK) {
+#pragma unroll
+            for (int h = 0; h < TMC / WV; ++h) {
+              T x[WV];
+              load_vec_ro<T, WV>(wrow + (int64_t)(k + WPF) * nSp + h * WV, x);
+#pragma unroll
+              for (int l = 0; l < WV; ++l) wn[WPF - 1][h * WV + l] = x[l];
+            }
           }
         }
         T pv[VEC];
 #pragma unroll
         for (int l = 0; l < VEC; ++l) pv[l] = (T)1;
-        if (NG > 0) {
-          cp_async_wait<R::D - 2>();
+        if (NG > 0 || WR) {
 #pragma unroll
           for (int g = 0; g < NG; ++g) {
             T f[VEC];
-            load_vec<T, VEC>(reinterpret_cast<const T*>(sp + g * 512), f);
+            load_vec<T, VEC>(reinterpret_cast<const T*>(sp + g * 512 + lane * 16), f);
 #pragma unroll
-            for (int l = 0; l < VEC; ++l) pv[l] *= f[l];
+            for (int l = 0; l < VEC; ++l) pv[l] = g == 0 ? f[l] : pv[l] * f[l];
           }
           // refill the stage consumed last iteration (this lane's own slot)
           if (k + R::D - 1 < nK) issue(k + R::D - 1, spn);
