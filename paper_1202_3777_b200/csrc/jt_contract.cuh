@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_p_kernel(const CArgs a,
 #ifndef ROWI_MINB_L
 #define ROWI_MINB_L 4
 #endif
-// NGC: the pass's factor count when fixed at compile time (1..3; 0 = read from
+// NGC: the pass's factor count when fixed at compile time (1..4; 0 = read from
 // the descriptor, loops bounded by CMAXG and predicated per factor)
 template <typename T, bool FOLD, bool LONGK, bool PRM, bool XW = false, int NGC = 0>
 __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restrict__ P0, const int32_t* __restrict__ tk0,

@@ -1,6 +1,6 @@
 // Parameter-space row-per-i launchers, one translation unit per dtype
 // (jt_contract_rowip32.cu / jt_contract_rowip64.cu): the factor count per k is a
-// compile-time constant for nG <= 3, so the k loop issues exactly nG vector
+// compile-time constant for nG <= 4, so the k loop issues exactly nG vector
 // loads per k (no per-factor predicates) — see rowi_body.
 #pragma once
 #include "jt_contract.cuh"
@@ -13,6 +13,7 @@ static auto rowi_p_fn(int ng) {
     case 1: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 1>;
     case 2: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 2>;
     case 3: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 3>;
+    case 4: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 4>;
     default: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 0>;
   }
 }
