@@ -149,6 +149,10 @@ struct Tensor {
   int64_t off = 0;
   std::vector<int> vars;  // ascending
   bool batch = false;     // trailing batch dim
+  // virtual separator (VDesc): the collect message of leaf clique vclique is not
+  // materialised; its readers evaluate Σ_k base · Π vfac (the leaf's evidence)
+  int vclique = -1;
+  std::vector<Tensor> vfac;
 };
 
 struct PassSpec {
@@ -181,6 +185,7 @@ struct LaunchGrp {  // one kernel launch of a wave
   int rp_idx = -1;     // >= 0: single row-per-i pass launched with its tables in the parameters
   int xw = 0;          // 1: that pass writes the clique product X (rowi_p kernel with XW)
   int tp_idx = -1;     // >= 0: single tile pass launched with its tables in the parameters
+  int vs = 0;          // 1: a pass of the launch reads virtual separators (VS kernel variant)
 };
 
 struct WaveRt {
@@ -202,6 +207,9 @@ struct Program {
   CPass* d_cpass = nullptr;
   int32_t* d_ctab = nullptr;
   void* d_w = nullptr;
+  VCodeTask* d_vtask = nullptr;  // virtual separators: mask-code tasks and their codes
+  int32_t* d_vcode = nullptr;
+  int n_vtask = 0;
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t gstream = nullptr;
   // persistent single-launch program (small single trees, jt_tiny.cu)
@@ -230,6 +238,8 @@ struct Program {
     cudaFree(d_cnt);
     cudaFree(d_cpass);
     cudaFree(d_ctab);
+    cudaFree(d_vtask);
+    cudaFree(d_vcode);
     cudaFree(d_w);
     cudaFree(d_tpass);
     cudaFree(d_unit0);
@@ -991,9 +1001,18 @@ struct HostProgram {
   std::vector<int> cpass_clique;
   std::vector<RowiParam> rparams;
   std::vector<TileParam> tparams;
+  std::map<int, VDesc> vdesc;  // virtual separators by leaf clique (Wv built once)
+  std::vector<VCodeTask> vcode;  // their evidence mask codes, computed at the start of every run
 };
 
 // ----------------------------------------------------- contraction passes --
+
+static bool has_virtual(const PassSpec& ps) {
+  if (ps.out.vclique >= 0) return true;
+  for (auto& f : ps.factors)
+    if (f.vclique >= 0) return true;
+  return false;
+}
 
 static bool contract_eligible(const jt_state* st, const PassSpec& ps) {
   return st->mode == JT_SHARED_BASE && st->B > 1 && st->B % CVEC == 0 && !st->h_base.empty() &&
@@ -1016,6 +1035,94 @@ static std::vector<int64_t> group_offsets(const jt_plan* p, const std::vector<in
   return out;
 }
 
+// Wv[j][k] (the leaf's base summed onto its separator entry j and private state
+// k; the row sum, accumulated in the arena type in k order, at [j][nK]) and the
+// mask-code task of a virtual separator; built once per program and leaf.
+// Appends to hp.w (rolled back with the pass that built it).
+static int64_t tsize_entries(const jt_plan* p, const Tensor& t) {
+  int64_t n = 1;
+  for (int v : t.vars) n *= p->cards[v];
+  return n;
+}
+
+static int virtual_sep(const jt_state* st, const Tensor& t, HostProgram& hp, VDesc& vd) {
+  auto it = hp.vdesc.find(t.vclique);
+  if (it != hp.vdesc.end()) {
+    vd = it->second;
+    return JT_OK;
+  }
+  const jt_plan* p = st->plan;
+  const int c = t.vclique;
+  const auto& C = p->cvars[c];
+  std::vector<int> K;
+  std::set_difference(C.begin(), C.end(), t.vars.begin(), t.vars.end(), std::back_inserter(K));
+  // the gather form needs the leaf's evidence to be the 0/1 mask of its one private variable
+  if (t.vfac.size() > 1 || (t.vfac.size() == 1 && t.vfac[0].vars != K)) return JT_ERR_UNSUPPORTED;
+  int64_t nK = 1, nJ = 1;
+  for (int v : K) nK *= p->cards[v];
+  for (int v : t.vars) nJ *= p->cards[v];
+  if (nJ * (nK + 1) > INT32_MAX) return JT_ERR_UNSUPPORTED;
+  Tensor te = t;
+  te.batch = false;
+  std::vector<int64_t> cj(C.size(), 0), ck(C.size(), 0);
+  for (size_t a = 0; a < C.size(); ++a) {
+    cj[a] = tensor_stride(p, te, C[a], 1);
+    int64_t st_ = 1;
+    bool in = false;
+    for (int b = (int)K.size() - 1; b >= 0; --b) {
+      if (K[b] == C[a]) {
+        in = true;
+        break;
+      }
+      st_ *= p->cards[K[b]];
+    }
+    ck[a] = in ? st_ : 0;
+  }
+  const int64_t w0 = ((int64_t)hp.w.size() + 7) & ~int64_t(7);
+  hp.w.resize(w0 + nJ * (nK + 1), 0.0);
+  double* W = hp.w.data() + w0;
+  const double* src = st->h_base.data() + st->boff[c];
+  std::vector<int> dig(C.size(), 0);
+  int64_t xj = 0, xk = 0;
+  for (int64_t e = 0; e < p->csize[c]; ++e) {
+    W[xj * (nK + 1) + xk] += src[e];
+    for (int a = (int)C.size() - 1; a >= 0; --a) {
+      xj += cj[a];
+      xk += ck[a];
+      if (++dig[a] < p->cards[C[a]]) break;
+      xj -= cj[a] * p->cards[C[a]];
+      xk -= ck[a] * p->cards[C[a]];
+      dig[a] = 0;
+    }
+  }
+  for (int64_t j = 0; j < nJ; ++j) {  // the unobserved case: Σ_k in k order, arena precision
+    double* r = W + j * (nK + 1);
+    if (st->esz == 8) {
+      double acc = 0.0;
+      for (int64_t k = 0; k < nK; ++k) acc += r[k];
+      r[nK] = acc;
+    } else {
+      float acc = 0.0f;
+      for (int64_t k = 0; k < nK; ++k) acc += (float)r[k];
+      r[nK] = (double)acc;
+    }
+  }
+  std::memset(&vd, 0, sizeof(vd));
+  vd.w_off = w0;
+  vd.nK = (int)nK;
+  vd.code_off = -1;
+  if (!t.vfac.empty()) {
+    VCodeTask tk;
+    std::memset(&tk, 0, sizeof(tk));
+    tk.mask_off = t.vfac[0].off;
+    tk.card = (int)nK;
+    vd.code_off = (int64_t)hp.vcode.size() * st->B;
+    hp.vcode.push_back(tk);
+  }
+  hp.vdesc[c] = vd;
+  return JT_OK;
+}
+
 #ifndef CON_NCG_MID
 #define CON_NCG_MID 4  // case chunks per unit group for 8 <= nK < 32
 #endif
@@ -1034,6 +1141,7 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   std::vector<const Tensor*> G, E;
   for (auto& f : ps.factors) (subset(f.vars, s) ? E : G).push_back(&f);
   if ((int)G.size() > CMAXG || (int)E.size() > MAXF) return JT_ERR_UNSUPPORTED;
+
   std::vector<int> U;
   for (auto* f : G) U.insert(U.end(), f->vars.begin(), f->vars.end());
   std::sort(U.begin(), U.end());
@@ -1055,6 +1163,26 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
     if (!std::includes(U.begin(), U.end(), s.begin(), s.end())) return JT_ERR_UNSUPPORTED;  // row-per-i only
   }
   const int nEb = (int)Eb.size();
+  // virtual separators read by this pass (E factors, old separators), distinct by leaf
+  std::vector<const Tensor*> V;
+  auto vid = [&](const Tensor* t) -> int {
+    if (t->vclique < 0) return -1;
+    for (size_t q = 0; q < V.size(); ++q)
+      if (V[q]->vclique == t->vclique) return (int)q;
+    V.push_back(t);
+    return (int)V.size() - 1;
+  };
+  for (auto* f : G)
+    if (f->vclique >= 0) return JT_ERR_UNSUPPORTED;  // (gathered in the epilogue only)
+  int8_t e_v[MAXF], e_v_b[MAXF];
+  for (int e = 0; e < nE; ++e) e_v[e] = (int8_t)vid(E[e]);
+  for (int e = 0; e < nEb; ++e) e_v_b[e] = (int8_t)vid(Eb[e]);
+  const int8_t old_v = (int8_t)vid(&ps.out);
+  const int8_t old_v_b = ps_b ? (int8_t)vid(&ps_b->out) : (int8_t)-1;
+  if ((int)V.size() > CMAXV) return JT_ERR_UNSUPPORTED;
+  if (old_v >= 0 && ps.out_kind != OUT_SEP && ps.out_kind != OUT_SEP_DFRESH) return JT_ERR_UNSUPPORTED;
+  if (old_v_b >= 0 && ps_b->out_kind != OUT_SEP && ps_b->out_kind != OUT_SEP_DFRESH) return JT_ERR_UNSUPPORTED;
+  const int nV = (int)V.size();
   // enumeration order of i (any order works: every i-dependent offset comes from
   // the per-i table): the variables that index the largest factor tensors vary
   // slowest, so consecutive i (consecutive warps) re-read the same factor rows
@@ -1079,6 +1207,13 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   }
   auto strides = [&](const std::vector<int>& vars, const Tensor& t) {
     std::vector<int64_t> o;
+    if (t.vclique >= 0) {  // virtual separator: offsets of its Wv rows ([entries][nK + 1])
+      Tensor te = t;
+      te.batch = false;
+      const int64_t row = p->csize[t.vclique] / std::max<int64_t>(1, tsize_entries(p, t)) + 1;
+      for (int v : vars) o.push_back(tensor_stride(p, te, v, 1) * row);
+      return o;
+    }
     for (int v : vars) o.push_back(tensor_stride(p, t, v, B));
     return o;
   };
@@ -1097,14 +1232,25 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
     ebI[e] = group_offsets(p, I, strides(I, *Eb[e]));
     ebS[e] = group_offsets(p, S, strides(S, *Eb[e]));
   }
+  // outputs are written in the batch layout (a virtual old separator's other
+  // outputs — ratio, final table — are stored tensors at the same offsets)
+  auto stored = [](const Tensor& t) {
+    Tensor x = t;
+    x.vclique = -1;
+    return x;
+  };
   std::vector<int64_t> obI, obS;
   if (ps_b) {
-    obI = group_offsets(p, I, strides(I, ps_b->out));
-    obS = group_offsets(p, S, strides(S, ps_b->out));
+    obI = group_offsets(p, I, strides(I, stored(ps_b->out)));
+    obS = group_offsets(p, S, strides(S, stored(ps_b->out)));
   }
-  const std::vector<int64_t> oI = group_offsets(p, I, strides(I, ps.out));
-  const std::vector<int64_t> oS = group_offsets(p, S, strides(S, ps.out));
+  const std::vector<int64_t> oI = group_offsets(p, I, strides(I, stored(ps.out)));
+  const std::vector<int64_t> oS = group_offsets(p, S, strides(S, stored(ps.out)));
   const int64_t nI = (int64_t)oI.size(), nS = (int64_t)oS.size();
+  if (nV > 0 && nS != 1) return JT_ERR_UNSUPPORTED;  // the row-per-i epilogue evaluates them
+  // per-i entry index of each virtual separator (its vars are output = i variables)
+  std::vector<std::vector<int64_t>> vI(nV);
+  for (int q = 0; q < nV; ++q) vI[q] = group_offsets(p, I, strides(I, *V[q]));
   const int64_t nK = (int64_t)group_offsets(p, K, std::vector<int64_t>(K.size(), 0)).size();
   if (nI * nK * (nS + 7) > (int64_t)1 << 31) return JT_ERR_UNSUPPORTED;
   auto fits = [](const std::vector<int64_t>& v) {
@@ -1179,6 +1325,7 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
       for (int e = 0; e < nEb; ++e) hp.ctab.push_back((int32_t)ebI[e][i]);
       hp.ctab.push_back((int32_t)obI[i]);
     }
+    for (int q = 0; q < nV; ++q) hp.ctab.push_back((int32_t)vI[q][i]);
   }
   cp.tk_off = (int64_t)hp.ctab.size();
   for (int64_t k = 0; k < nK; ++k)
@@ -1222,7 +1369,7 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   cp.igs = 1;
   // (opt-in, JT_ROWG=1: measured slower than plain row-per-i once paired passes and
   // evict-first epilogue streams cut the re-reads it was built against)
-  if (rowi && !I.empty() && env_int("JT_ROWG", 0)) {
+  if (rowi && !I.empty() && nV == 0 && env_int("JT_ROWG", 0)) {
     // i-groups: the innermost i variable's values share every factor that does not
     // index it; group them into one warp unit when those shared factors dominate
     const int v = I.back();
@@ -1306,6 +1453,24 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
     hp.w.resize(w0);
     hp.ctab.resize(cp.ti_off);
     return JT_ERR_UNSUPPORTED;  // X is written by the paired short-K row-per-i epilogue only
+  }
+  cp.nV = nV;
+  for (int e = 0; e < MAXF; ++e) {
+    cp.e_v[e] = e < nE ? e_v[e] : (int8_t)-1;
+    cp.e_v_b[e] = e < nEb ? e_v_b[e] : (int8_t)-1;
+  }
+  cp.old_v = old_v;
+  cp.old_v_b = old_v_b;
+  for (int q = 0; q < nV; ++q) {
+    int rc = virtual_sep(st, *V[q], hp, cp.vd[q]);
+    if (rc != JT_OK) {
+      for (auto it = hp.vdesc.begin(); it != hp.vdesc.end();)  // built by this call: rolled back below
+        it = it->second.w_off >= w0 ? hp.vdesc.erase(it) : std::next(it);
+      (void)0;
+      hp.w.resize(w0);
+      hp.ctab.resize(cp.ti_off);
+      return rc;
+    }
   }
   return JT_OK;
 }
@@ -1426,6 +1591,10 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
     std::vector<int> partner = pair_specs(st, w);
     for (size_t wi = 0; wi < w.size(); ++wi) {
       const PassSpec& ps = w[wi];
+      if (has_virtual(ps)) {  // virtual separators: row-per-i contraction passes only
+        bool ok = contract_eligible(st, ps) && !skipped(wi);
+        if (!ok) return JT_ERR_UNSUPPORTED;
+      }
       if (skipped(wi)) continue;  // a tiny pass (jt_tiny.cu)
       // the clique product X is written only by a paired contraction pass
       if (ps.x_off >= 0 && (!contract_eligible(st, ps) || partner[wi] < 0)) return JT_ERR_UNSUPPORTED;
@@ -1445,12 +1614,14 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
         }
         if (!paired && ps.x_off >= 0) return JT_ERR_UNSUPPORTED;
         if (paired || compile_contract(st, ps, hp, cp) == JT_OK) {
+          if (cp.nV > 0 && !(cp.rowi == 1 || cp.rowi == 4)) return JT_ERR_UNSUPPORTED;
           const int key = ((st->esz == 4 && cp.nK > CKF ? 1 : 0) + 2 * cp.rowi) * NGK + (cp.rowi ? 0 : cp.nG);
           cps[key].push_back(cp);
           cpc[key].push_back(ps.clique);
           continue;
         }
       }
+      if (has_virtual(ps)) return JT_ERR_UNSUPPORTED;  // caller rebuilds without virtual separators
       BuiltPass bp;
       const int local = (int)(passes.size() - rt.pass_base);
       const int vec = small_wave ? wave_vec : pass_max_vec(st, ps);
@@ -1568,9 +1739,10 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
             hp.tparams.push_back(tpm);
           }
           hp.cpass_clique.push_back(cpc2[key][q]);
+          cg.vs = cp.nV > 0;
           const int occ = occ_override ? occ_override
                           : cg.rp_idx >= 0
-                              ? contract_rowi_param_max_ctas(st->plan->dtype, fold, cg.m == 4, cp.nG, cg.xw != 0)
+                              ? contract_rowi_param_max_ctas(st->plan->dtype, fold, cg.m == 4, cp.nG, cg.xw != 0, cg.vs)
                               : contract_max_ctas_per_sm(st->plan->dtype, fold, cg.m, cg.vec);
           cg.grid = (int)std::min<int64_t>((cg.n_units + NT / 32 - 1) / (NT / 32), (int64_t)occ * st->num_sms);
           rt.groups.push_back(cg);
@@ -1592,6 +1764,7 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
         cp.unit0 = cg.n_units;
         cg.n_units += cp.n_units;
         cg.n_cpasses++;
+        cg.vs |= cp.nV > 0;
         hp.cpasses.push_back(cp);
         hp.cpass_clique.push_back(cpc[key][q]);
       }
@@ -1860,6 +2033,12 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
   if ((rc = up(&prog->d_rowtab, hp.rowtab))) return rc;
   if ((rc = up(&prog->d_cpass, hp.cpasses))) return rc;
   if ((rc = up(&prog->d_ctab, hp.ctab))) return rc;
+  if (!hp.vcode.empty()) {
+    if ((rc = up(&prog->d_vtask, hp.vcode))) return rc;
+    CK(cudaMalloc(&prog->d_vcode, hp.vcode.size() * st->B * sizeof(int32_t)));
+    prog->n_vtask = (int)hp.vcode.size();
+    prog->n_launches += 1;  // the mask-code launch (launch_program_waves)
+  }
   {
     const size_t n = std::max<size_t>(hp.w.size(), 1);
     CK(cudaMalloc(&prog->d_w, n * st->esz));
@@ -1887,6 +2066,7 @@ static int launch_group(jt_state* st, const Program* pr, const WaveRt& w, const 
     c.qout = st->d_qout;
     c.err = st->d_err;
     c.tab = pr->d_ctab;
+    c.codes = pr->d_vcode;
     c.passes = pr->d_cpass + g.cpass_off;
     c.n_passes = g.n_cpasses;
     c.n_units = g.n_units;
@@ -1897,11 +2077,12 @@ static int launch_group(jt_state* st, const Program* pr, const WaveRt& w, const 
     static const int stream_epi = env_int("JT_EPI_CS", 1);
     c.stream_epi = stream_epi;
     if (g.rp_idx >= 0)
-      CK(launch_contract_rowi_param(st->plan->dtype, g.lm, g.m == 4, c, pr->rparams[g.rp_idx], g.grid, s, g.xw != 0));
+      CK(launch_contract_rowi_param(st->plan->dtype, g.lm, g.m == 4, c, pr->rparams[g.rp_idx], g.grid, s, g.xw != 0,
+                                    g.vs != 0));
     else if (g.tp_idx >= 0)
       CK(launch_contract_tile_param(st->plan->dtype, g.lm, g.vec, c, pr->tparams[g.tp_idx], g.grid, s));
     else
-      CK(launch_contract(st->plan->dtype, g.lm, g.m, g.vec, c, g.grid, s));
+      CK(launch_contract(st->plan->dtype, g.lm, g.m, g.vec, c, g.grid, s, g.vs != 0));
     st->launches++;
     return JT_OK;
   }
@@ -1938,6 +2119,10 @@ static int ensure_side(jt_state* st) {
 }
 
 static int launch_program_waves(jt_state* st, Program* pr, cudaStream_t s) {
+  if (pr->n_vtask > 0) {  // virtual separators: the current evidence masks' codes
+    CK(launch_ev_code(st->d_aux, st->plan->dtype, pr->d_vtask, pr->n_vtask, (int)st->B, pr->d_vcode, s));
+    st->launches++;
+  }
   TinyArgs ta{};
   if (pr->tiny && pr->tiny_waves_launch) {
     TinyArgs& a = ta;
@@ -2133,8 +2318,9 @@ static Orient orient(const jt_plan* p, const std::vector<int>& roots) {
 // on the fly; its final table = original × Π children ratios × parent ratio is
 // written once in distribute.  Cliques with more factors than a pass carries
 // absorb their children's ratios eagerly (in-place) during collect instead.
-static int build_propagate(jt_state* st, const std::vector<int>& roots, const std::vector<int>& qvars,
-                           std::vector<std::vector<PassSpec>>& waves, bool fresh = false, bool hub_x = false) {
+static int build_propagate_waves(jt_state* st, const std::vector<int>& roots, const std::vector<int>& qvars,
+                                 std::vector<std::vector<PassSpec>>& waves, bool fresh, bool hub_x,
+                                 std::vector<char>& vleaf) {
   const jt_plan* p = st->plan;
   const bool shared = st->mode == JT_SHARED_BASE;
   const int src_arena = shared ? A_BASE : A_CLIQUE;
@@ -2145,6 +2331,39 @@ static int build_propagate(jt_state* st, const std::vector<int>& roots, const st
     for (int v = 0; v < p->n_vars; ++v)
       if (st->ev_clique[v] >= 0) evs[st->ev_clique[v]].push_back(v);
   std::vector<char> eager(n, 0);
+  for (int c = 0; c < n; ++c) {
+    const int nfac = (int)o.children[c].size() + (o.parent[c] >= 0 ? 1 : 0) + (int)evs[c].size();
+    eager[c] = nfac > MAXF;
+  }
+  // virtual separators (fresh shared-base programs): a leaf's collect message over a
+  // large separator is evaluated by its readers instead of stored (vleaf[c] requested
+  // by the caller; kept when the leaf qualifies)
+  vleaf.resize(n, 0);
+  for (int c = 0; c < n; ++c) {
+    if (!vleaf[c]) continue;
+    bool ok = shared && fresh && o.children[c].empty() && o.parent[c] >= 0 && !eager[c] && !eager[o.parent[c]] &&
+              evs[c].size() <= 1;
+    if (ok && evs[c].size() == 1) {  // the gather form: evidence on the leaf's one private variable
+      std::vector<int> K;
+      const auto& sv = p->svars[o.psep[c]];
+      std::set_difference(p->cvars[c].begin(), p->cvars[c].end(), sv.begin(), sv.end(), std::back_inserter(K));
+      ok = K == std::vector<int>{evs[c][0]};
+    }
+    vleaf[c] = ok;
+  }
+  auto ev_list = [&](int c) {
+    std::vector<Tensor> f;
+    for (int v : evs[c]) f.push_back(ev_tensor(st, v));
+    return f;
+  };
+  auto virt = [&](Tensor t, int c) {  // the collect message of leaf c (separator tensor t)
+    if (vleaf[c]) {
+      t.vclique = c;
+      t.vfac = ev_list(c);
+    }
+    return t;
+  };
+  std::fill(eager.begin(), eager.end(), 0);
   std::vector<PassSpec> hub_init;  // shared-base hubs: per-case table = base x evidence
   std::vector<std::vector<PassSpec>> hub_init_more;
   for (int c = 0; c < n; ++c) {
@@ -2178,7 +2397,7 @@ static int build_propagate(jt_state* st, const std::vector<int>& roots, const st
   const int c_kind = fresh ? OUT_SEP_FRESH : OUT_SEP;
   auto child_ratios = [&](int c) {
     std::vector<Tensor> f;
-    for (auto& ch : o.children[c]) f.push_back(sep_tensor(st, ch.second, ratC(ch.second)));
+    for (auto& ch : o.children[c]) f.push_back(virt(sep_tensor(st, ch.second, ratC(ch.second)), ch.first));
     return f;
   };
   auto ev_factors = [&](int c) {
@@ -2222,7 +2441,7 @@ static int build_propagate(jt_state* st, const std::vector<int>& roots, const st
           ps.ratio_off = sep_alt(st, o.psep[c]);
           main.push_back(ps);
         }
-      } else {
+      } else if (!vleaf[c]) {  // (a virtual separator's producer is not run)
         PassSpec ps;
         ps.clique = c;
         ps.src_arena = src_arena;
@@ -2285,6 +2504,7 @@ static int build_propagate(jt_state* st, const std::vector<int>& roots, const st
       ps.write = !shared && ch.size() == 1;
       ps.out_kind = OUT_SEP;
       ps.out = sep_tensor(st, ch[i].second, sep_cur(st, ch[i].second));
+      if (fresh) ps.out = virt(ps.out, ch[i].first);  // (ratC == sep_cur: the child's collect message)
       if (fresh) ps.out2_off = sep_alt(st, ch[i].second);
       ps.ratio_off = st->ratD_off[ch[i].second];
       if (fresh && !ps.write && !eager[c]) {
@@ -2402,6 +2622,72 @@ static int build_propagate(jt_state* st, const std::vector<int>& roots, const st
     if (!dwx[d].empty()) waves.push_back(dwx[d]);
   }
   return JT_OK;
+}
+
+// Can a pass read its virtual separators (compile_contract's classification: as
+// epilogue factors or old separators of a row-per-i contraction pass, at most CMAXV)?
+static bool vsep_readable(const jt_state* st, const PassSpec& ps) {
+  if (!has_virtual(ps)) return true;
+  if (!contract_eligible(st, ps)) return false;
+  const auto& s = ps.out.vars;
+  std::vector<int> U, vs;
+  auto subset = [](const std::vector<int>& a, const std::vector<int>& b) {
+    return std::includes(b.begin(), b.end(), a.begin(), a.end());
+  };
+  // (as K-sum factors, gathered per k, they measured slower on c5 than the factor
+  // rows they replace: epilogue reads only)
+  for (auto& f : ps.factors) {
+    if (f.vclique >= 0 && std::find(vs.begin(), vs.end(), f.vclique) == vs.end()) vs.push_back(f.vclique);
+    if (!subset(f.vars, s)) {
+      if (f.vclique >= 0) return false;
+      U.insert(U.end(), f.vars.begin(), f.vars.end());
+    }
+  }
+  std::sort(U.begin(), U.end());
+  if (ps.out.vclique >= 0) {
+    if (ps.out_kind != OUT_SEP && ps.out_kind != OUT_SEP_DFRESH) return false;
+    if (std::find(vs.begin(), vs.end(), ps.out.vclique) == vs.end()) vs.push_back(ps.out.vclique);
+  }
+  return (int)vs.size() <= CMAXV && subset(s, U);
+}
+
+// Leaves whose collect message is at least JT_VSEP_MIN_MB (default 256; 0: every
+// leaf) become virtual separators where every reader can gather them (JT_VSEP=0: off).
+static int build_propagate(jt_state* st, const std::vector<int>& roots, const std::vector<int>& qvars,
+                           std::vector<std::vector<PassSpec>>& waves, bool fresh = false, bool hub_x = false,
+                           bool vsep = false) {
+  const jt_plan* p = st->plan;
+  std::vector<char> vleaf(p->n_cliques, 0);
+  const int64_t min_mb = env_int("JT_VSEP_MIN_MB", 256);
+  if (vsep && fresh && st->mode == JT_SHARED_BASE && env_int("JT_VSEP", 1)) {
+    Orient o = orient(p, roots);
+    for (int c = 0; c < p->n_cliques; ++c)
+      if (o.parent[c] >= 0 && o.children[c].empty())
+        vleaf[c] = (double)p->ssize[o.psep[c]] * st->B * st->esz >= (double)min_mb * (1 << 20);
+  }
+  for (int it = 0; it < 16; ++it) {
+    waves.clear();
+    int rc = build_propagate_waves(st, roots, qvars, waves, fresh, hub_x, vleaf);
+    if (rc) return rc;
+    bool again = false;
+    for (auto& w : waves)
+      for (auto& ps : w)
+        if (!vsep_readable(st, ps)) {  // its leaves' messages are stored after all
+          if (getenv("JT_DEBUG_VSEP"))
+            fprintf(stderr, "vsep: pass of clique %d (out kind %d, %zu factors, eligible %d) cannot read leaf %d\n",
+                    ps.clique, ps.out_kind, ps.factors.size(), (int)contract_eligible(st, ps),
+                    ps.out.vclique >= 0 ? ps.out.vclique : [&] {
+                      for (auto& f : ps.factors)
+                        if (f.vclique >= 0) return f.vclique;
+                      return -1;
+                    }());
+          for (auto& f : ps.factors)
+            if (f.vclique >= 0) vleaf[f.vclique] = 0, again = true;
+          if (ps.out.vclique >= 0) vleaf[ps.out.vclique] = 0, again = true;
+        }
+    if (!again) return JT_OK;
+  }
+  return JT_ERR_UNSUPPORTED;
 }
 
 static std::string key_of(const char* tag, const std::vector<int>& a, const std::vector<int>& b = {}) {
@@ -3156,13 +3442,14 @@ extern "C" int jt_propagate_query(jt_state* st, int n, const int32_t* var, int n
     pr = it->second.get();
   } else {
     std::vector<std::vector<PassSpec>> waves;
-    // clique product X: fp64 default (fp64 program -3.5%; fp32 measured slower)
-    int rc = build_propagate(st, p->roots, vs, waves, fresh, env_int("JT_HUBX", st->esz == 8 ? 1 : 0) != 0);
-    if (rc) return rc;
-    rc = get_program(st, key, waves, &pr);
-    if (rc == JT_ERR_UNSUPPORTED) {  // the clique product could not be placed: plain program
-      waves.clear();
-      if ((rc = build_propagate(st, p->roots, vs, waves, fresh, false))) return rc;
+    // clique product X (with virtual separators: fp64 -7%, fp32 -11% program time);
+    // virtual separators; when a program cannot place them, the plainer ones
+    const bool hx = env_int("JT_HUBX", 1) != 0;
+    const bool attempts[3][2] = {{hx, true}, {hx, false}, {false, false}};
+    int rc = JT_ERR_UNSUPPORTED;
+    for (int a = 0; a < 3 && rc == JT_ERR_UNSUPPORTED; ++a) {
+      if (a > 0 && attempts[a][0] == attempts[a - 1][0] && attempts[a][1] == attempts[a - 1][1]) continue;
+      if ((rc = build_propagate(st, p->roots, vs, waves, fresh, attempts[a][0], attempts[a][1]))) return rc;
       rc = get_program(st, key, waves, &pr);
     }
     if (rc) return rc;
@@ -3325,15 +3612,16 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
     }
   }
   std::vector<std::vector<PassSpec>> waves;
-  int rc = build_propagate(&st, plan->roots, qv, waves, kind >= 1, env_int("JT_HUBX", st.esz == 8 ? 1 : 0) != 0);
-  if (rc) return rc;
-  rc = validate_waves(&st, waves);
-  if (rc) return rc;
+  int rc = JT_OK;
   {
-    HostProgram probe;
-    if (compile_program(&st, waves, probe, occ > 0 ? occ : 2) == JT_ERR_UNSUPPORTED) {
-      waves.clear();  // as the runtime does: the clique product could not be placed
-      if ((rc = build_propagate(&st, plan->roots, qv, waves, kind >= 1, false))) return rc;
+    // as the runtime does: clique product X and virtual separators, else plainer programs
+    const bool hx = env_int("JT_HUBX", 1) != 0;
+    const bool attempts[3][2] = {{hx, true}, {hx, false}, {false, false}};
+    for (int a = 0; a < 3; ++a) {
+      if ((rc = build_propagate(&st, plan->roots, qv, waves, kind >= 1, attempts[a][0], attempts[a][1]))) return rc;
+      if ((rc = validate_waves(&st, waves))) return rc;
+      HostProgram probe;
+      if (compile_program(&st, waves, probe, occ > 0 ? occ : 2) != JT_ERR_UNSUPPORTED) break;
     }
   }
   HostProgram hp;
@@ -3383,10 +3671,10 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
         for (auto& f : Bp.factors) {
           bool dup = same(f, A.out);
           for (auto& g : A.factors) dup = dup || same(g, f);
-          if (dup) bytes -= nbytes(f);
+          if (dup && f.vclique < 0) bytes -= nbytes(f);
         }
         for (auto& g : A.factors)
-          if (same(g, Bp.out)) bytes -= nbytes(g);
+          if (same(g, Bp.out) && g.vclique < 0) bytes -= nbytes(g);
       }
       for (auto& ps : waves[w]) {
         auto tsize = [&](const Tensor& t) {
@@ -3394,19 +3682,21 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
           for (int v : t.vars) n *= plan->cards[v];
           return n;
         };
-        for (auto& f : ps.factors) bytes += tsize(f) * st.esz;
+        for (auto& f : ps.factors) bytes += f.vclique >= 0 ? 0.0 : tsize(f) * st.esz;
         if (ps.out_kind == OUT_RAW) bytes += tsize(ps.out) * 8;
         else if (ps.out_kind == OUT_SEP_FRESH) bytes += tsize(ps.out) * st.esz;
-        else if (ps.out_kind != OUT_NONE) bytes += tsize(ps.out) * st.esz * 3;
+        else if (ps.out_kind != OUT_NONE) bytes += tsize(ps.out) * st.esz * (ps.out.vclique >= 0 ? 2 : 3);
         const double csz = (double)plan->csize[ps.clique] * (ps.src_arena == A_BASE ? 1.0 : (double)st.B);
         if (ps.scope.empty()) bytes += csz * st.esz * (ps.write ? 2 : 1);
         if (ps.x_off >= 0) bytes += tsize(ps.out) * st.esz;  // the clique product X
         if (getenv("JT_DEBUG_SPECS")) {
           double fb = 0.0;
-          for (auto& f : ps.factors) fb += tsize(f) * st.esz;
-          snprintf(line, sizeof line, "  spec w%zu clique %d src %d out %d nf %zu factors MB %.1f out MB %.1f\n", w,
+          for (auto &f : ps.factors) fb += f.vclique >= 0 ? 0.0 : tsize(f) * st.esz;
+          int nvs = ps.out.vclique >= 0;
+          for (auto& f : ps.factors) nvs += f.vclique >= 0;
+          snprintf(line, sizeof line, "  spec w%zu clique %d src %d out %d nf %zu factors MB %.1f out MB %.1f vsep %d\n", w,
                    ps.clique, ps.src_arena, ps.out_kind, ps.factors.size(), fb / 1e6,
-                   ps.out_kind != OUT_NONE ? tsize(ps.out) * st.esz / 1e6 : 0.0);
+                   ps.out_kind != OUT_NONE ? tsize(ps.out) * st.esz / 1e6 : 0.0, nvs);
           out += line;
         }
       }

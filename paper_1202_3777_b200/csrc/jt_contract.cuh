@@ -455,9 +455,49 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_p_kernel(const CArgs a,
 #ifndef ROWI_MINB_L
 #define ROWI_MINB_L 4
 #endif
+// Virtual separators (VDesc): per case lane, the column of the entry's Wv row
+// the leaf's collect pass would have summed to — the observed state, nK (the row
+// sum: unobserved / no evidence) — or -1 (conflicting evidence: zero).
+template <int VEC>
+__device__ __forceinline__ void vsep_cols(const VDesc& d, const int32_t* __restrict__ codes, int b0, int (&c)[VEC]) {
+  if (d.code_off < 0) {
+#pragma unroll
+    for (int l = 0; l < VEC; ++l) c[l] = d.nK;
+    return;
+  }
+  if constexpr (VEC == 4) {
+    const int4 x = __ldg(reinterpret_cast<const int4*>(codes + d.code_off + b0));
+    c[0] = x.x, c[1] = x.y, c[2] = x.z, c[3] = x.w;
+  } else if constexpr (VEC == 2) {
+    const int2 x = __ldg(reinterpret_cast<const int2*>(codes + d.code_off + b0));
+    c[0] = x.x, c[1] = x.y;
+  } else {
+#pragma unroll
+    for (int l = 0; l < VEC; ++l) c[l] = __ldg(codes + d.code_off + b0 + l);
+  }
+#pragma unroll
+  for (int l = 0; l < VEC; ++l) c[l] = c[l] >= 0 ? c[l] : c[l] == -1 ? d.nK : -1;
+}
+// the value at a Wv row (pointer to its first column) for the lanes' columns
+template <typename T, int VEC>
+__device__ __forceinline__ void vsep_gather(const T* __restrict__ row, const int (&c)[VEC], T (&f)[VEC]) {
+#pragma unroll
+  for (int l = 0; l < VEC; ++l) f[l] = c[l] >= 0 ? __ldg(row + c[l]) : (T)0;
+}
+template <typename T, int VEC>
+__device__ __forceinline__ void vsep_pick(int v, const T (&vv)[CMAXV][VEC], T (&f)[VEC]) {
+#pragma unroll
+  for (int l = 0; l < VEC; ++l) f[l] = v == 0 ? vv[0][l] : vv[1][l];
+}
+
 // NGC: the pass's factor count when fixed at compile time (1..4; 0 = read from
 // the descriptor, loops bounded by CMAXG and predicated per factor)
-template <typename T, bool FOLD, bool LONGK, bool PRM, bool XW = false, int NGC = 0>
+// VS: the pass reads virtual separators (the epilogue evaluates them; a separate
+// instantiation at a larger register budget, so plain passes keep theirs)
+#ifndef ROWI_MINB_V
+#define ROWI_MINB_V 4
+#endif
+template <typename T, bool FOLD, bool LONGK, bool PRM, bool XW = false, int NGC = 0, bool VS = false>
 __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restrict__ P0, const int32_t* __restrict__ tk0,
                                           const int32_t* __restrict__ ts0) {
   // one i per warp unit (few registers: three or four CTAs per SM), KU values
@@ -490,7 +530,8 @@ __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restric
     constexpr int GM = NGC ? NGC : CMAXG;
     const int nK = P->nK, nG = NGC ? NGC : P->nG, nE = P->nE;
     const bool two = P->out_kind_b != OUT_NONE;  // paired sibling output (same K-sum)
-    const int tw = nG + nE + 1 + (two ? P->nE_b + 1 : 0);
+    const int nV = VS ? P->nV : 0;  // virtual separators (entry indices at the end of the ti row)
+    const int tw = nG + nE + 1 + (two ? P->nE_b + 1 : 0) + nV;
     const int32_t* __restrict__ tir = a.tab + P->ti_off + i * tw;
     const int32_t* __restrict__ tk = PRM ? tk0 : a.tab + P->tk_off;
     const int32_t* __restrict__ ts = PRM ? ts0 : a.tab + P->ts_off;
@@ -545,12 +586,25 @@ __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restric
 #pragma unroll
       for (int l = 0; l < VEC; ++l) v[l] = vsum[l] = acc[l] + (double)part[l];
       const bool cs = a.stream_epi != 0;
+      T vv[CMAXV][VEC];  // the virtual separators at this i (epilogue factors / old separators)
+      if (VS && nV > 0) {
+#pragma unroll
+        for (int q = 0; q < CMAXV; ++q)
+          if (q < nV) {
+            int vc[VEC];  // the lanes' Wv columns
+            vsep_cols<VEC>(P->vd[q], a.codes, b0, vc);
+            vsep_gather<T, VEC>(W + P->vd[q].w_off + __ldg(tir + tw - nV + q), vc, vv[q]);
+          }
+      }
       double xp[XW ? VEC : 1];  // XW: product of the E factors (times old below) -> X
 #pragma unroll
       for (int l = 0; l < (XW ? VEC : 1); ++l) xp[l] = 1.0;
       for (int e = 0; e < nE; ++e) {
         T f[VEC];
-        {
+        const int ev = nV > 0 ? P->e_v[e] : -1;
+        if (ev >= 0) {
+          vsep_pick<T, VEC>(ev, vv, f);
+        } else {
           const T* ep = aux_c + P->efac_off[e] + __ldg(tir + nG + e) + TSV(e) + b0;
           if (cs) load_vec_cs<T, VEC>(ep, f);
           else load_vec_ro<T, VEC>(ep, f);
@@ -564,7 +618,8 @@ __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restric
       const int64_t j = (int64_t)__ldg(tir + nG + nE) + TSV(nE) + b0;
       T old[VEC] = {};
       if (P->out_kind == OUT_SEP || P->out_kind == OUT_SEP_DFRESH) {
-        if (cs) load_vec_cs<T, VEC>(aux_c + P->out_off + j, old);
+        if (nV > 0 && P->old_v >= 0) vsep_pick<T, VEC>(P->old_v, vv, old);
+        else if (cs) load_vec_cs<T, VEC>(aux_c + P->out_off + j, old);
         else load_vec<T, VEC>(aux_c + P->out_off + j, old);
       }
       if (XW) {  // X = old * Π E (the product of every factor over the output scope)
@@ -584,16 +639,22 @@ __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restric
         for (int l = 0; l < VEC; ++l) v[l] = vsum[l];
         for (int e = 0; e < nEb; ++e) {
           T f[VEC];
-          const T* ep = aux_c + P->efac_off_b[e] + __ldg(tb + e) + SBV(e) + b0;
-          if (cs) load_vec_cs<T, VEC>(ep, f);
-          else load_vec_ro<T, VEC>(ep, f);
+          const int ev = nV > 0 ? P->e_v_b[e] : -1;
+          if (ev >= 0) {
+            vsep_pick<T, VEC>(ev, vv, f);
+          } else {
+            const T* ep = aux_c + P->efac_off_b[e] + __ldg(tb + e) + SBV(e) + b0;
+            if (cs) load_vec_cs<T, VEC>(ep, f);
+            else load_vec_ro<T, VEC>(ep, f);
+          }
 #pragma unroll
           for (int l = 0; l < VEC; ++l) v[l] *= (double)f[l];
         }
         const int64_t jb = (int64_t)__ldg(tb + nEb) + SBV(nEb) + b0;
         T oldb[VEC] = {};
         if (P->out_kind_b == OUT_SEP || P->out_kind_b == OUT_SEP_DFRESH) {
-          if (cs) load_vec_cs<T, VEC>(aux_c + P->out_off_b + jb, oldb);
+          if (nV > 0 && P->old_v_b >= 0) vsep_pick<T, VEC>(P->old_v_b, vv, oldb);
+          else if (cs) load_vec_cs<T, VEC>(aux_c + P->out_off_b + jb, oldb);
           else load_vec<T, VEC>(aux_c + P->out_off_b + jb, oldb);
         }
         bad |= finalize_lanes<T, double, VEC>(P->out_kind_b, P->out_off_b, P->ratio_off_b, P->out2_off_b, jb, v, oldb,
@@ -606,18 +667,19 @@ __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restric
   }
 }
 
-template <typename T, bool FOLD, bool LONGK = false>
-__global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F : sizeof(T) == 8 ? ROWI_MINB_D : ROWI_MINB_NF)
-    contract_rowi_kernel(const CArgs a) {
+#define ROWI_MINB(T, FOLD, LONGK, VS) \
+  (LONGK ? ROWI_MINB_L : VS ? ROWI_MINB_V : FOLD ? ROWI_MINB_F : sizeof(T) == 8 ? ROWI_MINB_D : ROWI_MINB_NF)
+template <typename T, bool FOLD, bool LONGK = false, bool VS = false>
+__global__ void __launch_bounds__(NT, ROWI_MINB(T, FOLD, LONGK, VS)) contract_rowi_kernel(const CArgs a) {
   pdl_enter();
-  rowi_body<T, FOLD, LONGK, false>(a, nullptr, nullptr, nullptr);
+  rowi_body<T, FOLD, LONGK, false, false, 0, VS>(a, nullptr, nullptr, nullptr);
 }
 
-template <typename T, bool FOLD, bool LONGK, bool XW = false, int NGC = 0>
-__global__ void __launch_bounds__(NT, LONGK ? ROWI_MINB_L : FOLD ? ROWI_MINB_F : sizeof(T) == 8 ? ROWI_MINB_D : ROWI_MINB_NF)
+template <typename T, bool FOLD, bool LONGK, bool XW = false, int NGC = 0, bool VS = false>
+__global__ void __launch_bounds__(NT, ROWI_MINB(T, FOLD, LONGK, VS))
     contract_rowi_p_kernel(const CArgs a, const __grid_constant__ RowiParam rp) {
   pdl_enter();
-  rowi_body<T, FOLD, LONGK, true, XW, NGC>(a, &rp.cp, rp.tk, rp.ts);
+  rowi_body<T, FOLD, LONGK, true, XW, NGC, VS>(a, &rp.cp, rp.tk, rp.ts);
 }
 
 

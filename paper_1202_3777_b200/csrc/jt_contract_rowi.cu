@@ -9,12 +9,15 @@ namespace jt {
 cudaError_t launch_contract_tile(int dtype, int fold, int ng, const CArgs& a, int grid, cudaStream_t s);
 int contract_tile_max_ctas_per_sm(int dtype, int fold, int ng);
 
-cudaError_t launch_contract_rowi_param_float(int fold, int longk, int ng, const CArgs& a, const RowiParam& rp, int grid,
-                                            cudaStream_t s, bool xw);
-cudaError_t launch_contract_rowi_param_double(int fold, int longk, int ng, const CArgs& a, const RowiParam& rp, int grid,
-                                             cudaStream_t s, bool xw);
-int contract_rowi_param_max_ctas_float(int fold, int longk, int ng, bool xw);
-int contract_rowi_param_max_ctas_double(int fold, int longk, int ng, bool xw);
+#define ROWIP_DECL(T)                                                                                          \
+  cudaError_t launch_contract_rowi_param_##T(int fold, int longk, int ng, const CArgs& a, const RowiParam& rp,    \
+                                             int grid, cudaStream_t s, bool xw);                                 \
+  int contract_rowi_param_max_ctas_##T(int fold, int longk, int ng, bool xw);
+ROWIP_DECL(float)
+ROWIP_DECL(double)
+ROWIP_DECL(floatv)
+ROWIP_DECL(doublev)
+#undef ROWIP_DECL
 
 // JT_ROWI_NGC=0: the descriptor-driven kernel for every factor count (A/B switch)
 static int rowi_ngc(int ng) {
@@ -22,23 +25,37 @@ static int rowi_ngc(int ng) {
   return on ? ng : 0;
 }
 
-// xw: paired short-K passes that also write the clique's product X
+// xw: paired short-K passes that also write the clique's product X; vs: the pass
+// reads virtual separators
 cudaError_t launch_contract_rowi_param(int dtype, int fold, int longk, const CArgs& a, const RowiParam& rp, int grid,
-                                       cudaStream_t s, bool xw) {
+                                       cudaStream_t s, bool xw, bool vs) {
   if (grid <= 0 || a.n_units <= 0) return cudaSuccess;
   const int ng = rowi_ngc(rp.cp.nG);
+  if (vs)
+    return dtype == 0 ? launch_contract_rowi_param_floatv(fold, longk, ng, a, rp, grid, s, xw)
+                      : launch_contract_rowi_param_doublev(fold, longk, ng, a, rp, grid, s, xw);
   return dtype == 0 ? launch_contract_rowi_param_float(fold, longk, ng, a, rp, grid, s, xw)
                     : launch_contract_rowi_param_double(fold, longk, ng, a, rp, grid, s, xw);
 }
 
-int contract_rowi_param_max_ctas(int dtype, int fold, int longk, int ng, bool xw) {
+int contract_rowi_param_max_ctas(int dtype, int fold, int longk, int ng, bool xw, bool vs) {
   ng = rowi_ngc(ng);
+  if (vs)
+    return dtype == 0 ? contract_rowi_param_max_ctas_floatv(fold, longk, ng, xw)
+                      : contract_rowi_param_max_ctas_doublev(fold, longk, ng, xw);
   return dtype == 0 ? contract_rowi_param_max_ctas_float(fold, longk, ng, xw)
                     : contract_rowi_param_max_ctas_double(fold, longk, ng, xw);
 }
 
-cudaError_t launch_contract(int dtype, int fold, int rowi, int ng, const CArgs& a, int grid, cudaStream_t s) {
+template <typename T, bool FOLD, bool LONGK>
+static cudaError_t launch_rowi_t(bool vs, const CArgs& a, int grid, cudaStream_t s) {
+  return vs ? launch_pdl(contract_rowi_kernel<T, FOLD, LONGK, true>, grid, NT, 0, s, a)
+            : launch_pdl(contract_rowi_kernel<T, FOLD, LONGK, false>, grid, NT, 0, s, a);
+}
+
+cudaError_t launch_contract(int dtype, int fold, int rowi, int ng, const CArgs& a, int grid, cudaStream_t s, bool vs) {
   if (grid <= 0 || a.n_units <= 0) return cudaSuccess;
+  if (vs && rowi != 1 && rowi != 4) return cudaErrorInvalidValue;
   if (rowi == 2 || rowi == 3) {  // i-groups: IGM 4 (rowi 2) or 8 (rowi 3)
     if (dtype == 0) {
       if (fold)
@@ -52,12 +69,12 @@ cudaError_t launch_contract(int dtype, int fold, int rowi, int ng, const CArgs& 
   }
   if (rowi) {
     if (dtype == 0)
-      return rowi == 4 ? (fold ? launch_pdl(contract_rowi_kernel<float, true, true>, grid, NT, 0, s, a)
-                               : launch_pdl(contract_rowi_kernel<float, false, true>, grid, NT, 0, s, a))
-             : fold ? launch_pdl(contract_rowi_kernel<float, true>, grid, NT, 0, s, a)
-                    : launch_pdl(contract_rowi_kernel<float, false>, grid, NT, 0, s, a);
-    return rowi == 4 ? launch_pdl(contract_rowi_kernel<double, false, true>, grid, NT, 0, s, a)
-                     : launch_pdl(contract_rowi_kernel<double, false>, grid, NT, 0, s, a);
+      return rowi == 4 ? (fold ? launch_rowi_t<float, true, true>(vs, a, grid, s)
+                               : launch_rowi_t<float, false, true>(vs, a, grid, s))
+             : fold ? launch_rowi_t<float, true, false>(vs, a, grid, s)
+                    : launch_rowi_t<float, false, false>(vs, a, grid, s);
+    return rowi == 4 ? launch_rowi_t<double, false, true>(vs, a, grid, s)
+                     : launch_rowi_t<double, false, false>(vs, a, grid, s);
   }
   return launch_contract_tile(dtype, fold, ng, a, grid, s);
 }

@@ -7,29 +7,30 @@
 
 namespace jt {
 
-template <typename T, bool FOLD, bool LONGK, bool XW>
+template <typename T, bool FOLD, bool LONGK, bool XW, bool VS>
 static auto rowi_p_fn(int ng) {
   switch (ng) {
-    case 1: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 1>;
-    case 2: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 2>;
-    case 3: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 3>;
-    case 4: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 4>;
-    default: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 0>;
+    case 1: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 1, VS>;
+    case 2: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 2, VS>;
+    case 3: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 3, VS>;
+    case 4: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 4, VS>;
+    default: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 0, VS>;
   }
 }
 
 // ng <= 0: the generic (descriptor-driven) kernel
-template <typename T>
+template <typename T, bool VS>
 static void (*rowi_p_select(int fold, int longk, int ng, bool xw))(const CArgs, const RowiParam) {
   if (xw) {
     if (longk) return nullptr;
-    if constexpr (sizeof(T) == 4) return fold ? rowi_p_fn<T, true, false, true>(ng) : rowi_p_fn<T, false, false, true>(ng);
-    else return rowi_p_fn<T, false, false, true>(ng);
+    if constexpr (sizeof(T) == 4)
+      return fold ? rowi_p_fn<T, true, false, true, VS>(ng) : rowi_p_fn<T, false, false, true, VS>(ng);
+    else return rowi_p_fn<T, false, false, true, VS>(ng);
   }
   if constexpr (sizeof(T) == 4) {
-    if (fold) return longk ? rowi_p_fn<T, true, true, false>(ng) : rowi_p_fn<T, true, false, false>(ng);
+    if (fold) return longk ? rowi_p_fn<T, true, true, false, VS>(ng) : rowi_p_fn<T, true, false, false, VS>(ng);
   }
-  return longk ? rowi_p_fn<T, false, true, false>(ng) : rowi_p_fn<T, false, false, false>(ng);
+  return longk ? rowi_p_fn<T, false, true, false, VS>(ng) : rowi_p_fn<T, false, false, false, VS>(ng);
 }
 
 }  // namespace jt

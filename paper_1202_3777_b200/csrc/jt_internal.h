@@ -104,6 +104,23 @@ struct WaveArgs {
 constexpr int TMC = 8;     // W rows per warp unit
 constexpr int CVEC = 4;    // B must be a multiple of this (fp32 lanes per vector; fp64 uses 2)
 constexpr int CMAXG = 4;   // factors multiplied per k (more: the pass takes the general kernels)
+// Virtual separator (shared-base fresh programs): a leaf clique's collect message
+// phi*(j, b) = Σ_k Wv[j][k] · mask_v[k][b] (the leaf's one private variable v and
+// its 0/1 evidence mask) is not materialised.  The row-per-i passes that read it
+// (as an epilogue factor or as the old separator of a distribute output) gather
+// it: with the mask's per-case code c (a one-hot state, -1 all ones, -2 all
+// zeros) the sum is Wv[j][c], the precomputed row sum Wv[j][nK], or 0.
+struct VDesc {
+  int64_t w_off;            // W arena offset of Wv, layout [entries][nK + 1] (row sum last)
+  int64_t code_off;         // int32 offset of the leaf's mask codes [B] in CArgs::codes; -1: no evidence
+  int nK, pad;
+};
+struct VCodeTask {          // per-program mask code of one evidence variable
+  int64_t mask_off;         // aux offset of its mask [card][B]
+  int card, pad;
+};
+constexpr int CMAXV = 2;    // virtual separators per pass
+
 struct CPass {
   int64_t w_off;            // W arena offset, layout [nI][nK][nS]
   int64_t ti_off;           // int32 [nI][nG + nE + 1]: G i-offsets, E i-offsets, out i-offset
@@ -136,6 +153,13 @@ struct CPass {
   int out_kind_b, nE_b;
   int64_t out_off_b, ratio_off_b, out2_off_b;
   int64_t efac_off_b[MAXF];
+  // virtual separators read by this (row-per-i) pass: ti rows end with their nV Wv
+  // row offsets; E slot e (E_b slot) is virtual separator e_v[e] (e_v_b[e]) when >= 0, the
+  // old separator of the output (second output) when old_v (old_v_b) >= 0
+  int nV;
+  int8_t e_v[MAXF], e_v_b[MAXF];
+  int8_t old_v, old_v_b;
+  VDesc vd[CMAXV];
 };
 struct CArgs {
   const void* w;
@@ -149,6 +173,7 @@ struct CArgs {
   int B;
   double* partials;         // K-split partial sums
   int* counters;            // K-split arrival counters (reset by the last warp)
+  const int32_t* codes;     // virtual separators: per-case evidence mask codes (VDesc::code_off)
   int stream_epi;           // 1: epilogue inputs (E factors, old separators) load and outputs store
                             //    with evict-first hints: the streams do not flush reused factor rows
   int interleave;           // 1: every pass has n_units / n_passes units and unit u belongs to
@@ -156,7 +181,7 @@ struct CArgs {
 };
 constexpr int CKF = 16;     // fp32 contraction sums longer than this fold into fp64
 // ng: factors per k (0..CMAXG) of every pass of the launch (compile-time in the kernel; ignored for rowi)
-cudaError_t launch_contract(int dtype, int fold, int rowi, int ng, const CArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_contract(int dtype, int fold, int rowi, int ng, const CArgs& a, int grid, cudaStream_t s, bool vs = false);
 // A single row-per-i pass with its descriptor and k-table carried in the kernel
 // parameters (__grid_constant__): the per-k, warp-uniform table lookups come from
 // the constant bank instead of competing with the factor streams for L1.
@@ -168,7 +193,7 @@ struct RowiParam {
   int32_t ts[RP_TS];
 };
 cudaError_t launch_contract_rowi_param(int dtype, int fold, int longk, const CArgs& a, const RowiParam& rp, int grid,
-                                       cudaStream_t s, bool xw = false);
+                                       cudaStream_t s, bool xw = false, bool vs = false);
 constexpr int TP_TS = 1024;  // ints of the s'-row table of a tile pass (nS x (nE + 1))
 struct TileParam {
   CPass cp;
@@ -179,7 +204,7 @@ cudaError_t launch_contract_tile_param(int dtype, int fold, int ng, const CArgs&
                                        cudaStream_t s);
 int contract_max_ctas_per_sm(int dtype, int fold, int rowi, int ng);
 // occupancy of the parameter-space row-per-i kernel a pass launches (nG specialised)
-int contract_rowi_param_max_ctas(int dtype, int fold, int longk, int ng, bool xw);
+int contract_rowi_param_max_ctas(int dtype, int fold, int longk, int ng, bool xw, bool vs = false);
 
 // device initialize: one entry per clique, one term per CPT, 3 int64 per CPT variable
 // (clique stride, card, CPT stride)
@@ -265,6 +290,8 @@ cudaError_t launch_scale_pow2(int dtype, void* p, int64_t n, int exp2, cudaStrea
 cudaError_t launch_fill(int dtype, void* dst, int64_t n, double v, cudaStream_t s);
 cudaError_t launch_ev_fill(void* aux, int dtype, const int32_t* vars, int nv, const int64_t* var_off,
                            const int32_t* cards, int B, cudaStream_t s);
+cudaError_t launch_ev_code(const void* aux, int dtype, const VCodeTask* tasks, int nt, int B, int32_t* codes,
+                           cudaStream_t s);
 cudaError_t launch_ev_zero(void* aux, int dtype, const int32_t* obs, int n, const int64_t* var_off,
                            const int32_t* cards, int B, cudaStream_t s);
 cudaError_t launch_mapping_table(int64_t* out, int64_t n_sep, int64_t n_rest,

@@ -1171,6 +1171,31 @@ cudaError_t launch_ev_fill(void* aux, int dtype, const int32_t* vars, int nv, co
   return cudaGetLastError();
 }
 
+// Per-case code of an evidence mask (virtual separators, VDesc): -1 all ones
+// (unobserved), -2 all zeros (conflicting observations), else the one state
+// left (ev_zero leaves at most one).
+__global__ void ev_code_kernel(const void* aux, int dtype, const VCodeTask* __restrict__ tasks, int B,
+                               int32_t* __restrict__ codes) {
+  const VCodeTask t = tasks[blockIdx.y];
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) {
+    int ones = 0, first = -1;
+    for (int d = 0; d < t.card; ++d) {
+      const int64_t i = t.mask_off + (int64_t)d * B + b;
+      const bool one = dtype == 0 ? ((const float*)aux)[i] != 0.0f : ((const double*)aux)[i] != 0.0;
+      ones += one;
+      if (one && first < 0) first = d;
+    }
+    codes[(int64_t)blockIdx.y * B + b] = ones == t.card ? -1 : ones == 0 ? -2 : first;
+  }
+}
+
+cudaError_t launch_ev_code(const void* aux, int dtype, const VCodeTask* tasks, int nt, int B, int32_t* codes,
+                           cudaStream_t s) {
+  if (nt == 0) return cudaSuccess;
+  ev_code_kernel<<<dim3((B + 255) / 256, nt), 256, 0, s>>>(aux, dtype, tasks, B, codes);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_ev_zero(void* aux, int dtype, const int32_t* obs, int n, const int64_t* var_off,
                            const int32_t* cards, int B, cudaStream_t s) {
   if (n == 0) return cudaSuccess;

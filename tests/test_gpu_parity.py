@@ -660,3 +660,32 @@ def test_shared_base_batches_with_hub_cliques(dtype, batch):
         assert rel_err(out[i], golden[i % len(golden)][1]) < TOL[dtype], (dtype, batch, i)
     for k, want in enumerate(want_extra):
         assert rel_err(out[n - len(extra) + k], want) < TOL[dtype], (dtype, batch, "extra", k)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_virtual_separators_c5(dtype, monkeypatch):
+    """c5's two 140000-entry leaf messages are gathered by their readers instead
+    of stored (virtual separators): the batch program at a
+    contraction-path batch size matches the reference goldens and the oracle,
+    with the threshold at 0 (every qualifying leaf) and with them off."""
+    from paper_1202_3777_b200.batch import BatchPropagator
+
+    tree, data = load_golden("c5")
+    tables = synth.scaled_potentials(tree, 0)
+    golden = golden_cases(data)
+    extra = synth.evidence_cases(tree, 4, seed=31)
+    template = jtref.from_potentials(tree, tables)
+    want_extra = [jtref.case_posteriors(template, ev, range(len(tree.cards))) for ev in extra]
+    cases = [golden[i % len(golden)][0] for i in range(124)] + extra
+    outs = []
+    for on in ("1", "0"):
+        monkeypatch.setenv("JT_VSEP_MIN_MB", "0")
+        monkeypatch.setenv("JT_VSEP", on)
+        bp = BatchPropagator(tree, tables, batch=128, dtype=dtype, mode="shared")
+        out = bp.run(cases, to_host=True)
+        for i in range(124):
+            assert rel_err(out[i], golden[i % len(golden)][1]) < TOL[dtype], (dtype, on, i)
+        for k, want in enumerate(want_extra):
+            assert rel_err(out[124 + k], want) < TOL[dtype], (dtype, on, "extra", k)
+        outs.append(out)
+    assert rel_err(outs[0], outs[1]) < (1e-12 if dtype == "f64" else 1e-5)

@@ -64,7 +64,7 @@ def test_batch_program_uses_contraction_passes():
     text = report("c5", batch=2048, mode="shared", kind=1, dtype="f32")
     assert "contract clique" in text
     total = float(next(l for l in text.splitlines() if l.startswith("compulsory total MB")).split()[-1])
-    assert 30000 < total < 60000  # ~46.6 GB per 2048-case micro-batch
+    assert 20000 < total < 60000  # ~29 GB per 2048-case micro-batch (46.6 before X / virtual separators)
 
 
 @pytest.mark.parametrize("batch", [128, 4096])
@@ -95,6 +95,7 @@ def test_batch_program_pairs_siblings_and_shares_the_hub_product(monkeypatch):
     two epilogues; in fp64 that pass also writes the clique product X and the
     hub's two other distribute passes read it (one sub-wave later), which the
     compulsory-bytes accounting reflects."""
+    monkeypatch.setenv("JT_VSEP", "0")  # (virtual separators: the next test)
     f64 = report("c5", batch=4096, mode="shared", kind=1, dtype="f64")
     paired = [l for l in f64.splitlines() if l.startswith("  contract clique 2 out 4 nI 140000")]
     assert len(paired) == 1, paired  # two DFRESH passes -> one paired pass
@@ -102,3 +103,28 @@ def test_batch_program_pairs_siblings_and_shares_the_hub_product(monkeypatch):
     monkeypatch.setenv("JT_HUBX", "0")
     f64_nox = report("c5", batch=4096, mode="shared", kind=1, dtype="f64")
     assert total(f64) < total(f64_nox) - 10000  # ~13.8 GB fewer per 4096-case micro-batch
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_batch_program_gathers_virtual_separators(dtype, monkeypatch):
+    """c5's leaves 3 and 12 send 140000-entry collect messages that only hub
+    clique 2 reads: the planner drops their producer passes and the hub's
+    row-per-i passes (its collect pass and the paired distribute pass) gather the
+    messages from the leaves' summed tables by each case's evidence code, which
+    removes 4.59 GB (fp64) of writes plus their re-reads per message from the
+    compulsory bytes."""
+    monkeypatch.setenv("JT_DEBUG_SPECS", "1")
+    total = lambda t: float(next(l for l in t.splitlines() if l.startswith("compulsory total MB")).split()[-1])
+    on = report("c5", batch=4096, mode="shared", kind=1, dtype=dtype)
+    readers = [l for l in on.splitlines() if l.startswith("  spec") and not l.endswith("vsep 0")]
+    hub = [l for l in readers if " clique 2 " in l]
+    assert len(hub) == 3, readers  # the collect pass and the two (paired) distribute passes
+    assert all(l.endswith("vsep 2") for l in hub)
+    assert len(readers) == 3, readers  # (leaf 14's message is a K-sum factor of clique 13: stored)
+    monkeypatch.setenv("JT_VSEP_MIN_MB", "0")
+    assert total(report("c5", batch=4096, mode="shared", kind=1, dtype=dtype)) <= total(on)
+    monkeypatch.setenv("JT_VSEP", "0")
+    off = report("c5", batch=4096, mode="shared", kind=1, dtype=dtype)
+    assert "vsep 2" not in off
+    saved = total(off) - total(on)
+    assert saved > (25000 if dtype == "f64" else 12500), saved
