@@ -220,6 +220,7 @@ struct Program {
   int tiny_waves_launch = 0;           // 1: per-wave launches (PDL), tiny kernel on the waves flagged below
   std::vector<char> tiny_w;            // per (non-empty) wave: run as a tiny-pass launch
   std::vector<int> tiny_wave_grid;     // per-wave grids of the per-wave launches
+  std::vector<int> vsep_leaves;        // leaves whose collect message this program does not store
   TPass* d_tpass = nullptr;
   int64_t* d_unit0 = nullptr;
   TinyWave* d_twaves = nullptr;
@@ -313,6 +314,9 @@ struct jt_state {
   // propagation writes the collect messages into the current table and the
   // distribute results into the other one, then the roles swap.
   bool sep_in_y = false;
+  // leaves whose collect message the last propagation did not store (virtual
+  // separators): materialised before a later query reads it (materialize_vsep)
+  std::vector<int> vsep_pending;
   // host copy of the base replica (shared-base states): contraction passes
   // precompute W = base summed over the variables no factor or output sees
   std::vector<double> h_base;
@@ -1954,6 +1958,16 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
   rc0 = compile_program(st, waves, hp, 0, tiny ? &tmask : nullptr);
   if (rc0) return rc0;
   auto prog = std::make_unique<Program>();
+  for (auto& w : waves)
+    for (auto& ps : w) {
+      auto note = [&](const Tensor& t) {
+        if (t.vclique >= 0 && std::find(prog->vsep_leaves.begin(), prog->vsep_leaves.end(), t.vclique) ==
+                                  prog->vsep_leaves.end())
+          prog->vsep_leaves.push_back(t.vclique);
+      };
+      note(ps.out);
+      for (auto& f : ps.factors) note(f);
+    }
   prog->waves = hp.waves;
   prog->rparams = hp.rparams;
   prog->tparams = hp.tparams;
@@ -2965,6 +2979,7 @@ extern "C" int jt_state_clone(jt_state* src, jt_state** out) {
   dst->fresh = src->fresh;
   dst->seps_stale = src->seps_stale;
   dst->sep_in_y = src->sep_in_y;
+  dst->vsep_pending = src->vsep_pending;
   dst->ev_clique = src->ev_clique;
   dst->h_base = src->h_base;
   dst->pre_e = src->pre_e;
@@ -3205,6 +3220,7 @@ static int resolve_roots(const jt_state* st, const int32_t* roots_or_null, std::
 // accumulates as masks until reset): calibrated tables are P(C, e) whatever the
 // message history, so this equals the reference's repeated belief_propagation.
 static void shared_restart(jt_state* st) {
+  st->vsep_pending.clear();
   if (st->mode != JT_SHARED_BASE || st->fresh) return;
   st->fresh = true;
   st->seps_stale = st->plan->n_seps > 0;
@@ -3305,6 +3321,33 @@ static int finish_query(jt_state* st, int n, const int32_t* var, int normalize, 
   return JT_OK;
 }
 
+// The collect messages of the leaves the last (fused) propagation gathered
+// instead of storing (virtual separators), written where a stored one would be
+// now (sep_alt after the run's swap), for the queries that read them.
+static int materialize_vsep(jt_state* st, cudaStream_t s) {
+  const jt_plan* p = st->plan;
+  Orient o = orient(p, p->roots);
+  std::vector<PassSpec> w;
+  for (int c : st->vsep_pending) {
+    PassSpec ps;
+    ps.clique = c;
+    ps.src_arena = A_BASE;
+    for (int v = 0; v < p->n_vars; ++v)
+      if (st->ev_clique[v] == c) ps.factors.push_back(ev_tensor(st, v));
+    ps.out_kind = OUT_SEP_FRESH;
+    ps.out = sep_tensor(st, o.psep[c], sep_alt(st, o.psep[c]));
+    w.push_back(ps);
+  }
+  std::vector<int> kv = active_ev(st);
+  kv.push_back((int)st->sep_in_y);
+  Program* pr;
+  int rc = get_program(st, key_of("vm", st->vsep_pending, kv), {w}, &pr);
+  if (rc) return rc;
+  if ((rc = run_program(st, pr, s))) return rc;
+  st->vsep_pending.clear();
+  return JT_OK;
+}
+
 static int query_program(jt_state* st, int n, const int32_t* var, const int32_t* clique, cudaStream_t s,
                          std::vector<int>& exps) {
   const jt_plan* p = st->plan;
@@ -3325,6 +3368,12 @@ static int query_program(jt_state* st, int n, const int32_t* var, const int32_t*
   const bool shared = st->mode == JT_SHARED_BASE;
   // shared-base state not propagated since reset/load: its tables are base × evidence
   const bool unprop = shared && st->fresh;
+#ifndef JT_NO_VSEP_MATERIALIZE  // (test-sensitivity variant only)
+  if (shared && !unprop && !st->vsep_pending.empty()) {
+    int rc = materialize_vsep(st, s);
+    if (rc) return rc;
+  }
+#endif
   std::vector<int> kv = active_ev(st);
   kv.push_back((int)st->sep_in_y);
   kv.push_back((int)unprop);
@@ -3456,6 +3505,7 @@ extern "C" int jt_propagate_query(jt_state* st, int n, const int32_t* var, int n
   }
   int rc = run_program(st, pr, s);
   if (rc) return rc;
+  st->vsep_pending = pr->vsep_leaves;
   set_all_exp(st, joint_exp(st));
   if (fresh) st->sep_in_y = !st->sep_in_y;
   st->fresh = false;

@@ -689,3 +689,30 @@ def test_virtual_separators_c5(dtype, monkeypatch):
             assert rel_err(out[124 + k], want) < TOL[dtype], (dtype, on, "extra", k)
         outs.append(out)
     assert rel_err(outs[0], outs[1]) < (1e-12 if dtype == "f64" else 1e-5)
+
+
+def test_virtual_separators_materialised_for_later_queries(monkeypatch):
+    """After a fused propagation that gathered leaf messages instead of storing
+    them, a later query on the hub clique (which reads its children's collect
+    messages) first materialises them: its marginals equal the fused ones."""
+    import ctypes as C
+
+    from paper_1202_3777_b200 import _lib
+    from paper_1202_3777_b200._lib import i32, ptr
+    from paper_1202_3777_b200.batch import BatchPropagator
+
+    monkeypatch.setenv("JT_VSEP_MIN_MB", "0")
+    tree, data = load_golden("c5")
+    tables = synth.scaled_potentials(tree, 0)
+    cases = [ev for ev, _ in golden_cases(data)]
+    cases = [cases[i % len(cases)] for i in range(128)]
+    bp = BatchPropagator(tree, tables, batch=128, dtype="f64", mode="shared")
+    fused = bp.run(cases, to_host=True)
+    cols = np.cumsum([0] + [int(tree.cards[v]) for v in bp.query_vars])
+    hub = 2
+    for v in tree.cliques[hub].scope.ids:
+        k = list(bp.query_vars).index(v)
+        got = np.zeros((128, int(tree.cards[v])))
+        _lib.check(_lib.lib().jt_query(bp.handle, 1, ptr(i32([v]), C.c_int32), ptr(i32([hub]), C.c_int32), 1,
+                                       got.ctypes.data_as(C.POINTER(C.c_double)), None), "jt_query")
+        assert rel_err(got, fused[:, cols[k]:cols[k + 1]]) < 1e-10, v
