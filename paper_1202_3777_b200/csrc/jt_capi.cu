@@ -167,6 +167,8 @@ struct PassSpec {
   int64_t ratio_off = -1;
   int64_t out2_off = -1;
   int64_t x_off = -1;       // >= 0: this (paired) pass also writes its clique's product X here
+  int sep = -1;             // distribute passes: the separator of the output
+  bool skip_out2 = false;   // fused propagation: the final table of `sep` is rebuilt on demand
 };
 
 struct LaunchGrp {  // one kernel launch of a wave
@@ -221,6 +223,7 @@ struct Program {
   std::vector<char> tiny_w;            // per (non-empty) wave: run as a tiny-pass launch
   std::vector<int> tiny_wave_grid;     // per-wave grids of the per-wave launches
   std::vector<int> vsep_leaves;        // leaves whose collect message this program does not store
+  std::vector<int> final_skip;         // separators whose final table it does not store
   TPass* d_tpass = nullptr;
   int64_t* d_unit0 = nullptr;
   TinyWave* d_twaves = nullptr;
@@ -317,6 +320,9 @@ struct jt_state {
   // leaves whose collect message the last propagation did not store (virtual
   // separators): materialised before a later query reads it (materialize_vsep)
   std::vector<int> vsep_pending;
+  // separators whose final table the last propagation did not store (rebuilt as
+  // collect message x distribute ratio before it is read: materialize_final)
+  std::vector<int> final_pending;
   // host copy of the base replica (shared-base states): contraction passes
   // precompute W = base summed over the variables no factor or output sees
   std::vector<double> h_base;
@@ -1432,7 +1438,7 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   cp.out_kind = ps.out_kind;
   cp.out_off = ps.out.off;
   cp.ratio_off = ps.ratio_off;
-  cp.out2_off = ps.out2_off;
+  cp.out2_off = ps.skip_out2 && ps.out_kind == OUT_SEP_DFRESH ? OUT2_SKIP : ps.out2_off;
   for (int g = 0; g < nG; ++g) cp.gfac_off[g] = G[g]->off;
   for (int e = 0; e < nE; ++e) cp.efac_off[e] = E[e]->off;
   cp.out_kind_b = OUT_NONE;
@@ -1449,7 +1455,7 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
     cp.nE_b = nEb;
     cp.out_off_b = ps_b->out.off;
     cp.ratio_off_b = ps_b->ratio_off;
-    cp.out2_off_b = ps_b->out2_off;
+    cp.out2_off_b = ps_b->skip_out2 && ps_b->out_kind == OUT_SEP_DFRESH ? OUT2_SKIP : ps_b->out2_off;
     for (int e = 0; e < nEb; ++e) cp.efac_off_b[e] = Eb[e]->off;
     cp.x_off = ps.x_off;
   }
@@ -1967,6 +1973,7 @@ static int build_program(jt_state* st, const std::vector<std::vector<PassSpec>>&
       };
       note(ps.out);
       for (auto& f : ps.factors) note(f);
+      if (ps.skip_out2 && ps.sep >= 0) prog->final_skip.push_back(ps.sep);
     }
   prog->waves = hp.waves;
   prog->rparams = hp.rparams;
@@ -2334,7 +2341,7 @@ static Orient orient(const jt_plan* p, const std::vector<int>& roots) {
 // absorb their children's ratios eagerly (in-place) during collect instead.
 static int build_propagate_waves(jt_state* st, const std::vector<int>& roots, const std::vector<int>& qvars,
                                  std::vector<std::vector<PassSpec>>& waves, bool fresh, bool hub_x,
-                                 std::vector<char>& vleaf) {
+                                 std::vector<char>& vleaf, bool lazy_final) {
   const jt_plan* p = st->plan;
   const bool shared = st->mode == JT_SHARED_BASE;
   const int src_arena = shared ? A_BASE : A_CLIQUE;
@@ -2520,6 +2527,9 @@ static int build_propagate_waves(jt_state* st, const std::vector<int>& roots, co
       ps.out = sep_tensor(st, ch[i].second, sep_cur(st, ch[i].second));
       if (fresh) ps.out = virt(ps.out, ch[i].first);  // (ratC == sep_cur: the child's collect message)
       if (fresh) ps.out2_off = sep_alt(st, ch[i].second);
+      ps.sep = ch[i].second;
+      // (fused queries of this separator read its final table in this program)
+      ps.skip_out2 = lazy_final && fresh && shared && qsep[ch[i].second].empty();
       ps.ratio_off = st->ratD_off[ch[i].second];
       if (fresh && !ps.write && !eager[c]) {
         // message to child k: product of the OTHER messages, marginalised
@@ -2681,7 +2691,7 @@ static int build_propagate(jt_state* st, const std::vector<int>& roots, const st
   }
   for (int it = 0; it < 16; ++it) {
     waves.clear();
-    int rc = build_propagate_waves(st, roots, qvars, waves, fresh, hub_x, vleaf);
+    int rc = build_propagate_waves(st, roots, qvars, waves, fresh, hub_x, vleaf, vsep && env_int("JT_LAZY_FINAL", 1));
     if (rc) return rc;
     bool again = false;
     for (auto& w : waves)
@@ -2926,6 +2936,8 @@ extern "C" int jt_state_initialize(jt_state* st, int n_cpts, const int32_t* cpt_
   return JT_OK;
 }
 
+static int materialize_final(jt_state* st, cudaStream_t s);
+
 extern "C" int jt_state_store(jt_state* st, int case_idx, double* clique_concat, double* sep_concat) {
   if (!st || case_idx < 0 || case_idx >= st->B_user) return JT_ERR_BAD_ARG;
   const jt_plan* p = st->plan;
@@ -2949,6 +2961,7 @@ extern "C" int jt_state_store(jt_state* st, int case_idx, double* clique_concat,
     CK(cudaStreamSynchronize(s));
   }
   if (sep_concat) {
+    if (!st->final_pending.empty() && (rc = materialize_final(st, s))) return rc;
     int64_t o = 0;
     for (int sp = 0; sp < p->n_seps; ++sp) {
       const char* src = (const char*)st->d_aux + (sep_cur(st, sp) + case_idx) * st->esz;
@@ -2980,6 +2993,7 @@ extern "C" int jt_state_clone(jt_state* src, jt_state** out) {
   dst->seps_stale = src->seps_stale;
   dst->sep_in_y = src->sep_in_y;
   dst->vsep_pending = src->vsep_pending;
+  dst->final_pending = src->final_pending;
   dst->ev_clique = src->ev_clique;
   dst->h_base = src->h_base;
   dst->pre_e = src->pre_e;
@@ -3221,6 +3235,7 @@ static int resolve_roots(const jt_state* st, const int32_t* roots_or_null, std::
 // message history, so this equals the reference's repeated belief_propagation.
 static void shared_restart(jt_state* st) {
   st->vsep_pending.clear();
+  st->final_pending.clear();
   if (st->mode != JT_SHARED_BASE || st->fresh) return;
   st->fresh = true;
   st->seps_stale = st->plan->n_seps > 0;
@@ -3345,6 +3360,23 @@ static int materialize_vsep(jt_state* st, cudaStream_t s) {
   if (rc) return rc;
   if ((rc = run_program(st, pr, s))) return rc;
   st->vsep_pending.clear();
+  return JT_OK;
+}
+
+// Final separator tables the last fused propagation did not store: collect
+// message (sep_alt after the run's swap) x distribute ratio, as its distribute
+// pass would have written them (OUT_SEP_DFRESH: new = old * Σ, ratio = Σ or 0).
+static int materialize_final(jt_state* st, cudaStream_t s) {
+  int rc;
+  if (!st->vsep_pending.empty() && (rc = materialize_vsep(st, s))) return rc;
+  for (int sp : st->final_pending) {
+    char* aux = (char*)st->d_aux;
+    const int64_t n = st->plan->ssize[sp] * st->B;
+    CK(launch_mul(st->plan->dtype, aux + sep_cur(st, sp) * st->esz, aux + sep_alt(st, sp) * st->esz,
+                  aux + st->ratD_off[sp] * st->esz, n, s));
+    st->launches++;
+  }
+  st->final_pending.clear();
   return JT_OK;
 }
 
@@ -3506,6 +3538,7 @@ extern "C" int jt_propagate_query(jt_state* st, int n, const int32_t* var, int n
   int rc = run_program(st, pr, s);
   if (rc) return rc;
   st->vsep_pending = pr->vsep_leaves;
+  st->final_pending = pr->final_skip;
   set_all_exp(st, joint_exp(st));
   if (fresh) st->sep_in_y = !st->sep_in_y;
   st->fresh = false;
@@ -3735,7 +3768,8 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
         for (auto& f : ps.factors) bytes += f.vclique >= 0 ? 0.0 : tsize(f) * st.esz;
         if (ps.out_kind == OUT_RAW) bytes += tsize(ps.out) * 8;
         else if (ps.out_kind == OUT_SEP_FRESH) bytes += tsize(ps.out) * st.esz;
-        else if (ps.out_kind != OUT_NONE) bytes += tsize(ps.out) * st.esz * (ps.out.vclique >= 0 ? 2 : 3);
+        else if (ps.out_kind != OUT_NONE)
+          bytes += tsize(ps.out) * st.esz * (3 - (ps.out.vclique >= 0) - (ps.skip_out2 && ps.out_kind == OUT_SEP_DFRESH));
         const double csz = (double)plan->csize[ps.clique] * (ps.src_arena == A_BASE ? 1.0 : (double)st.B);
         if (ps.scope.empty()) bytes += csz * st.esz * (ps.write ? 2 : 1);
         if (ps.x_off >= 0) bytes += tsize(ps.out) * st.esz;  // the clique product X

@@ -46,12 +46,13 @@ __device__ __forceinline__ bool finalize_lanes(int kind, int64_t out_off, int64_
       nw[l] = (T)star[l];
     }
   }
+  const bool keep = out2_off != OUT2_SKIP;
   if (cs) {
     store_vec_cs<T, VEC>(aux + ratio_off + j, rt);
-    store_vec_cs<T, VEC>(aux + (out2_off >= 0 ? out2_off : out_off) + j, nw);
+    if (keep) store_vec_cs<T, VEC>(aux + (out2_off >= 0 ? out2_off : out_off) + j, nw);
   } else {
     store_vec<T, VEC>(aux + ratio_off + j, rt);
-    store_vec<T, VEC>(aux + (out2_off >= 0 ? out2_off : out_off) + j, nw);
+    if (keep) store_vec<T, VEC>(aux + (out2_off >= 0 ? out2_off : out_off) + j, nw);
   }
   return bad;
 }

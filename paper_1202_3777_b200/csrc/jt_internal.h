@@ -13,6 +13,9 @@ constexpr int MAXDI = 8;    // merged inner dimensions per pass
 
 enum ArenaId : int { A_CLIQUE = 0, A_BASE = 1, A_AUX = 2 };
 enum OutKind : int { OUT_NONE = 0, OUT_SEP = 1, OUT_RAW = 2, OUT_SEP_FRESH = 3, OUT_SEP_DFRESH = 4 };
+// out2_off == OUT2_SKIP: a distribute pass of a fused propagation does not store the
+// separator's final table (old x ratio, rebuilt on demand: materialize_final)
+constexpr int64_t OUT2_SKIP = -2;
 // OUT_SEP_DFRESH: distribute output of a fresh propagation; the pass sums
 // WITHOUT the target separator's own collect message c (= old value), so
 // new = c*S and ratio = new/old = S (0 where c == 0): the Hugin division cancels.
@@ -288,6 +291,7 @@ cudaError_t launch_convert_t2d(int dtype, const void* src, int64_t src_stride,
                                double* dst, int64_t n, cudaStream_t s, int exp2 = 0);
 cudaError_t launch_scale_pow2(int dtype, void* p, int64_t n, int exp2, cudaStream_t s);
 cudaError_t launch_fill(int dtype, void* dst, int64_t n, double v, cudaStream_t s);
+cudaError_t launch_mul(int dtype, void* dst, const void* a, const void* b, int64_t n, cudaStream_t s);
 cudaError_t launch_ev_fill(void* aux, int dtype, const int32_t* vars, int nv, const int64_t* var_off,
                            const int32_t* cards, int B, cudaStream_t s);
 cudaError_t launch_ev_code(const void* aux, int dtype, const VCodeTask* tasks, int nt, int B, int32_t* codes,

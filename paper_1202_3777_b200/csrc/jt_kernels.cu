@@ -1125,6 +1125,22 @@ cudaError_t launch_scale_pow2(int dtype, void* p, int64_t n, int exp2, cudaStrea
   return cudaGetLastError();
 }
 
+template <typename T>
+__global__ void mul_kernel(T* __restrict__ dst, const T* __restrict__ a, const T* __restrict__ b, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = a[i] * b[i];
+}
+
+// dst = a * b elementwise (a separator's final table from its collect message and
+// distribute ratio)
+cudaError_t launch_mul(int dtype, void* dst, const void* a, const void* b, int64_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  if (dtype == 0) mul_kernel<float><<<g, 256, 0, s>>>((float*)dst, (const float*)a, (const float*)b, n);
+  else mul_kernel<double><<<g, 256, 0, s>>>((double*)dst, (const double*)a, (const double*)b, n);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fill(int dtype, void* dst, int64_t n, double v, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   const unsigned g = (unsigned)((n + 255) / 256);

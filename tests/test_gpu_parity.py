@@ -716,3 +716,38 @@ def test_virtual_separators_materialised_for_later_queries(monkeypatch):
         _lib.check(_lib.lib().jt_query(bp.handle, 1, ptr(i32([v]), C.c_int32), ptr(i32([hub]), C.c_int32), 1,
                                        got.ctypes.data_as(C.POINTER(C.c_double)), None), "jt_query")
         assert rel_err(got, fused[:, cols[k]:cols[k + 1]]) < 1e-10, v
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_lazy_final_separator_tables(dtype, monkeypatch):
+    """A fused batch propagation does not store the final separator tables its
+    queries do not read (collect message x distribute ratio); reading them back
+    afterwards rebuilds them: equal to a program that stores them, for a case
+    with evidence and one without (c5's 140000-entry hub separators included,
+    virtual separators on)."""
+    import ctypes as C
+
+    from paper_1202_3777_b200 import _lib
+    from paper_1202_3777_b200.batch import BatchPropagator
+
+    monkeypatch.setenv("JT_VSEP_MIN_MB", "0")
+    tree, data = load_golden("c5")
+    tables = synth.scaled_potentials(tree, 0)
+    cases = [ev for ev, _ in golden_cases(data)]
+    cases = [cases[i % len(cases)] for i in range(127)] + [{}]
+    seps = {}
+    for lazy in ("1", "0"):
+        monkeypatch.setenv("JT_LAZY_FINAL", lazy)
+        bp = BatchPropagator(tree, tables, batch=128, dtype=dtype, mode="shared")
+        bp.run(cases, to_host=True)
+        n = sum(int(np.prod([tree.cards[v] for v in s.scope.ids])) for s in tree.separators)
+        got = []
+        for case in (0, 127):
+            buf = np.zeros(n)
+            _lib.check(_lib.lib().jt_state_store(bp.handle, case, None, buf.ctypes.data_as(C.POINTER(C.c_double))),
+                       "jt_state_store")
+            got.append(buf)
+        seps[lazy] = np.stack(got)
+        bp.close()
+    assert np.all(np.isfinite(seps["1"])) and seps["1"].max() > 0
+    assert rel_err(seps["1"], seps["0"]) < (1e-13 if dtype == "f64" else 1e-6)
