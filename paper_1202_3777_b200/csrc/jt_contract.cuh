@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_p_kernel(const CArgs a,
 #define ROWI_MINB_F 4
 #endif
 #ifndef ROWI_MINB_D
-#define ROWI_MINB_D 8
+#define ROWI_MINB_D 6
 #endif
 // LONGK: passes with long K sums (nK >= 16) keep ROWI_KU_L values of k in flight
 // per lane (their loads would otherwise chain one memory latency per k) at a
@@ -542,6 +542,18 @@ __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restric
     const T* __restrict__ wrow = W + P->w_off + i * (int64_t)nK;
     const int bstep = 32 * VEC * nCG;
     for (int b0 = cg * 32 * VEC + lane * VEC; b0 < a.B; b0 += bstep) {
+      // VS: the virtual separators at this i (epilogue factors / old separators),
+      // gathered before the K-sum so their latency hides behind it
+      T vv[CMAXV][VEC];
+      if (VS && nV > 0) {
+#pragma unroll
+        for (int q = 0; q < CMAXV; ++q)
+          if (q < nV) {
+            int vc[VEC];  // the lanes' Wv columns
+            vsep_cols<VEC>(P->vd[q], a.codes, b0, vc);
+            vsep_gather<T, VEC>(W + P->vd[q].w_off + __ldg(tir + tw - nV + q), vc, vv[q]);
+          }
+      }
       double acc[VEC];
 #pragma unroll
       for (int l = 0; l < VEC; ++l) acc[l] = 0.0;
@@ -587,16 +599,6 @@ __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restric
 #pragma unroll
       for (int l = 0; l < VEC; ++l) v[l] = vsum[l] = acc[l] + (double)part[l];
       const bool cs = a.stream_epi != 0;
-      T vv[CMAXV][VEC];  // the virtual separators at this i (epilogue factors / old separators)
-      if (VS && nV > 0) {
-#pragma unroll
-        for (int q = 0; q < CMAXV; ++q)
-          if (q < nV) {
-            int vc[VEC];  // the lanes' Wv columns
-            vsep_cols<VEC>(P->vd[q], a.codes, b0, vc);
-            vsep_gather<T, VEC>(W + P->vd[q].w_off + __ldg(tir + tw - nV + q), vc, vv[q]);
-          }
-      }
       double xp[XW ? VEC : 1];  // XW: product of the E factors (times old below) -> X
 #pragma unroll
       for (int l = 0; l < (XW ? VEC : 1); ++l) xp[l] = 1.0;
