@@ -478,8 +478,9 @@ def roofline_block(args, tree, dtype, r, alg_elems):
                       "contraction, thread-owned and general wave kernels)",
             "alg_bytes_per_launch": comp if comp else alg_bytes_launch,
             "alg_bytes_def": "compulsory bytes of the shared-base program: factor tensors read once, "
-                             "outputs written once, separator updates read old + write ratio "
-                             "(planner, DESIGN.md 5)" if comp else "B_alg1 x cases",
+                             "outputs written once, separator updates read old + write ratio (+ final table "
+                             "unless rebuilt on demand); virtual separators (gathered leaf messages) move no "
+                             "bytes (planner, DESIGN.md 3b/5)" if comp else "B_alg1 x cases",
             "b_alg1_bytes_per_launch": alg_bytes_launch,
             "frac_b_alg1": round(achieved / pk["hbm_gbs"], 3),
             "physical_frac": round(traffic["bytes_per_launch"] / (prog_ms * 1e-3) / 1e9 / pk["hbm_gbs"], 3)

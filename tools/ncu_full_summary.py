@@ -1,40 +1,24 @@
-"""Key metrics of an `ncu --set full` report (one line per captured launch).
-usage: python tools/ncu_full_summary.py gpurun_out/prof.ncu-rep"""
+"""Key metrics of an ncu --set full report (one launch): section / metric / value, for profiles/.
+usage: python tools/ncu_full_summary.py report.ncu-rep "header line" [launch_skip]"""
 import csv
 import io
 import subprocess
 import sys
 
-WANT = [
-    ("gpu__time_duration.sum", "time"),
-    ("dram__bytes_read.sum", "dram_rd"),
-    ("dram__bytes_write.sum", "dram_wr"),
-    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram%"),
-    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm%"),
-    ("lts__t_sector_hit_rate.pct", "L2hit%"),
-    ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps_active%"),
-    ("launch__registers_per_thread", "regs"),
-    ("launch__shared_mem_per_block_dynamic", "dyn_smem"),
-    ("launch__grid_size", "grid"),
-    ("launch__occupancy_limit_registers", "occ_lim_regs"),
-    ("launch__occupancy_limit_shared_mem", "occ_lim_smem"),
-    ("smsp__inst_executed.sum", "inst"),
-]
-
-
-def main(path):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(raw)))
-    hdr, units = rows[0], rows[1]
-    for r in rows[2:]:
-        name = r[hdr.index("Kernel Name")]
-        parts = [name[:44]]
-        for key, short in WANT:
-            if key in hdr:
-                i = hdr.index(key)
-                parts.append(f"{short}={r[i]}{units[i]}")
-        print(" | ".join(parts))
-
-
-if __name__ == "__main__":
-    main(sys.argv[1])
+KEEP = ("Memory Throughput", "DRAM Throughput", "Duration", "L1/TEX Cache Throughput", "L2 Cache Throughput",
+        "Compute (SM) Throughput", "Mem Busy", "Max Bandwidth", "L1/TEX Hit Rate", "L2 Hit Rate",
+        "Issued Warp Per Scheduler", "Warp Cycles Per Issued Instruction", "Issue Slots Busy", "Executed Instructions",
+        "Grid Size", "Registers Per Thread", "Achieved Occupancy", "Theoretical Occupancy")
+rep, head = sys.argv[1], sys.argv[2]
+skip = sys.argv[3] if len(sys.argv) > 3 else "0"
+out = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv", "--launch-skip", skip, "--launch-count", "1"],
+                     capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+hdr = rows[0]
+ix = {h: i for i, h in enumerate(hdr)}
+print(head)
+print("kernel:", rows[1][ix["Kernel Name"]])
+for r in rows[1:]:
+    name = r[ix["Metric Name"]]
+    if name in KEEP:
+        print(f"{r[ix['Section Name']]:30} {name:45} {r[ix['Metric Value']]:>14} {r[ix['Metric Unit']]}")
