@@ -241,12 +241,15 @@ __device__ __forceinline__ void tile_body(const CArgs& a, const CPass* __restric
       // lanes of this warp with cases left (a prefix): the W row copy and the warp barrier
       const int na = min(32, (a.B - (b0 - lane * VEC) + VEC - 1) / VEC);
       const unsigned wm = na >= 32 ? 0xffffffffu : ((1u << na) - 1u);
+      const T* gb[NG > 0 ? NG : 1];  // this lane's case vector of each factor (per k: + the k-offset)
+#pragma unroll
+      for (int g = 0; g < NG; ++g) gb[g] = gq[g] + b0;
       auto issue = [&](int k, unsigned char* sp) {
 #pragma unroll
         for (int g = 0; g < NG; ++g)
-          cp_async16(sp + g * 512 + lane * 16, gq[g] + b0 + (PRM ? tk[k * NG + g] : __ldg(tk + k * NG + g)));
+          cp_async16(sp + g * 512 + lane * 16, gb[g] + (PRM ? tk[k * NG + g] : __ldg(tk + k * NG + g)));
         if (WR) {
-          const T* wk = wrow + (int64_t)k * nSp;
+          const T* wk = wrow + k * nSp;
           if (na >= WL) {
             if (lane < WL) cp_async16(sp + R::SF + lane * 16, wk + lane * (16 / (int)sizeof(T)));
           } else if (lane == 0) {
@@ -561,6 +564,9 @@ __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restric
 #pragma unroll
       for (int l = 0; l < VEC; ++l) part[l] = (T)0;
       int since = 0;
+      const T* gb[GM];  // this lane's case vector of each factor (per k: + the k-offset, one IMAD.WIDE)
+#pragma unroll
+      for (int g = 0; g < GM; ++g) gb[g] = gq[g] + b0;
       for (int k = 0; k < nK; k += KU) {
         T pv[KU][VEC];
         T w[KU];
@@ -573,7 +579,7 @@ __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restric
           for (int g = 0; g < GM; ++g) {
             if (NGC || g < nG) {
               T f[VEC];
-              load_vec_ro<T, VEC>(gq[g] + b0 + (PRM ? tk[kq * nG + g] : __ldg(tk + kq * nG + g)), f);
+              load_vec_ro<T, VEC>(gb[g] + (PRM ? tk[kq * nG + g] : __ldg(tk + kq * nG + g)), f);
 #pragma unroll
               for (int l = 0; l < VEC; ++l) pv[q][l] *= f[l];
             }
