@@ -501,13 +501,16 @@ __device__ __forceinline__ void vsep_pick(int v, const T (&vv)[CMAXV][VEC], T (&
 #ifndef ROWI_MINB_V
 #define ROWI_MINB_V 4
 #endif
+#ifndef ROWI_KU_V
+#define ROWI_KU_V 1  // k per step of the VS variant (2 and 4 measured slower)
+#endif
 template <typename T, bool FOLD, bool LONGK, bool PRM, bool XW = false, int NGC = 0, bool VS = false>
 __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restrict__ P0, const int32_t* __restrict__ tk0,
                                           const int32_t* __restrict__ ts0) {
   // one i per warp unit (few registers: three or four CTAs per SM), KU values
   // of k in flight, each with its nG factor-row vectors
   constexpr int VEC = CTraits<T>::VEC;
-  constexpr int KU = LONGK ? ROWI_KU_L : FOLD ? ROWI_KU_F : ROWI_KU_NF;
+  constexpr int KU = LONGK ? ROWI_KU_L : VS ? ROWI_KU_V : FOLD ? ROWI_KU_F : ROWI_KU_NF;
   constexpr int KF = 16;
   T* __restrict__ aux = reinterpret_cast<T*>(a.aux);
   const T* __restrict__ aux_c = aux;
