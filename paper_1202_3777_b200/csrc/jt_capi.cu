@@ -1187,8 +1187,14 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
   int8_t e_v[MAXF], e_v_b[MAXF];
   for (int e = 0; e < nE; ++e) e_v[e] = (int8_t)vid(E[e]);
   for (int e = 0; e < nEb; ++e) e_v_b[e] = (int8_t)vid(Eb[e]);
-  const int8_t old_v = (int8_t)vid(&ps.out);
-  const int8_t old_v_b = ps_b ? (int8_t)vid(&ps_b->out) : (int8_t)-1;
+  // a fresh distribute output whose final table is rebuilt on demand needs no old
+  // separator (unless it feeds the clique product X): ratio only
+  auto kind_of = [](const PassSpec& q) {
+    return q.out_kind == OUT_SEP_DFRESH && q.skip_out2 && q.x_off < 0 && env_int("JT_DRATIO", 1) ? OUT_SEP_DRATIO
+                                                                                                 : q.out_kind;
+  };
+  const int8_t old_v = kind_of(ps) == OUT_SEP_DRATIO ? (int8_t)-1 : (int8_t)vid(&ps.out);
+  const int8_t old_v_b = ps_b && kind_of(*ps_b) != OUT_SEP_DRATIO ? (int8_t)vid(&ps_b->out) : (int8_t)-1;
   if ((int)V.size() > CMAXV) return JT_ERR_UNSUPPORTED;
   if (old_v >= 0 && ps.out_kind != OUT_SEP && ps.out_kind != OUT_SEP_DFRESH) return JT_ERR_UNSUPPORTED;
   if (old_v_b >= 0 && ps_b->out_kind != OUT_SEP && ps_b->out_kind != OUT_SEP_DFRESH) return JT_ERR_UNSUPPORTED;
@@ -1435,7 +1441,7 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
     hp.ctab.resize(cp.ti_off);
     return JT_ERR_UNSUPPORTED;
   }
-  cp.out_kind = ps.out_kind;
+  cp.out_kind = kind_of(ps);
   cp.out_off = ps.out.off;
   cp.ratio_off = ps.ratio_off;
   cp.out2_off = ps.skip_out2 && ps.out_kind == OUT_SEP_DFRESH ? OUT2_SKIP : ps.out2_off;
@@ -1451,7 +1457,7 @@ static int compile_contract(const jt_state* st, const PassSpec& ps, HostProgram&
     cp.igs = 1;  // the paired epilogue lives in the plain row-per-i kernel
     cp.rowi = cp.rowi == 4 ? 4 : 1;
     cp.n_units = cp.nT * cp.nCG;
-    cp.out_kind_b = ps_b->out_kind;
+    cp.out_kind_b = kind_of(*ps_b);
     cp.nE_b = nEb;
     cp.out_off_b = ps_b->out.off;
     cp.ratio_off_b = ps_b->ratio_off;
@@ -3768,6 +3774,8 @@ extern "C" int jt_debug_plan(const jt_plan* plan, int batch, int mode, int kind,
         for (auto& f : ps.factors) bytes += f.vclique >= 0 ? 0.0 : tsize(f) * st.esz;
         if (ps.out_kind == OUT_RAW) bytes += tsize(ps.out) * 8;
         else if (ps.out_kind == OUT_SEP_FRESH) bytes += tsize(ps.out) * st.esz;
+        else if (ps.out_kind == OUT_SEP_DFRESH && ps.skip_out2 && ps.x_off < 0 && env_int("JT_DRATIO", 1))
+          bytes += tsize(ps.out) * st.esz;  // ratio only (OUT_SEP_DRATIO)
         else if (ps.out_kind != OUT_NONE)
           bytes += tsize(ps.out) * st.esz * (3 - (ps.out.vclique >= 0) - (ps.skip_out2 && ps.out_kind == OUT_SEP_DFRESH));
         const double csz = (double)plan->csize[ps.clique] * (ps.src_arena == A_BASE ? 1.0 : (double)st.B);

@@ -25,11 +25,12 @@ __device__ __forceinline__ bool finalize_lanes(int kind, int64_t out_off, int64_
     return false;
   }
   T nw[VEC];
-  if (kind == OUT_SEP_FRESH) {
+  if (kind == OUT_SEP_FRESH || kind == OUT_SEP_DRATIO) {
 #pragma unroll
     for (int l = 0; l < VEC; ++l) nw[l] = (T)star[l];
-    if (cs) store_vec_cs<T, VEC>(aux + out_off + j, nw);
-    else store_vec<T, VEC>(aux + out_off + j, nw);
+    T* dst = aux + (kind == OUT_SEP_FRESH ? out_off : ratio_off) + j;
+    if (cs) store_vec_cs<T, VEC>(dst, nw);
+    else store_vec<T, VEC>(dst, nw);
     return false;
   }
   T rt[VEC];
@@ -403,6 +404,11 @@ __device__ __forceinline__ void tile_body(const CArgs& a, const CPass* __restric
 #pragma unroll
           for (int h = 0; h < TMC; h += TMC / 2)
             contract_epilogue_half<T, A, VEC, OUT_SEP_DFRESH, FOLD, NG, PRM>(P, a, h, rows, s0, ti, ts, b0, part, cacc);
+          break;
+        case OUT_SEP_DRATIO:
+#pragma unroll
+          for (int h = 0; h < TMC; h += TMC / 2)
+            contract_epilogue_half<T, A, VEC, OUT_SEP_DRATIO, FOLD, NG, PRM>(P, a, h, rows, s0, ti, ts, b0, part, cacc);
           break;
         default:
 #pragma unroll

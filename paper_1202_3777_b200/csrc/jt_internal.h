@@ -12,7 +12,12 @@ constexpr int MAXF = 8;     // factors (ratio / evidence tensors) multiplied in 
 constexpr int MAXDI = 8;    // merged inner dimensions per pass
 
 enum ArenaId : int { A_CLIQUE = 0, A_BASE = 1, A_AUX = 2 };
-enum OutKind : int { OUT_NONE = 0, OUT_SEP = 1, OUT_RAW = 2, OUT_SEP_FRESH = 3, OUT_SEP_DFRESH = 4 };
+enum OutKind : int { OUT_NONE = 0, OUT_SEP = 1, OUT_RAW = 2, OUT_SEP_FRESH = 3, OUT_SEP_DFRESH = 4, OUT_SEP_DRATIO = 5 };
+// OUT_SEP_DRATIO (contraction passes of fused propagations): a fresh distribute output
+// whose final table is rebuilt on demand writes only the ratio Σ (no old read).  Where
+// the old separator is 0 the reference's ratio is 0 and this one is Σ; every consumer
+// multiplies it into clique entries that sum to that 0 — nonnegative, hence all 0 —
+// so every table, posterior and rebuilt final separator is the same.
 // out2_off == OUT2_SKIP: a distribute pass of a fused propagation does not store the
 // separator's final table (old x ratio, rebuilt on demand: materialize_final)
 constexpr int64_t OUT2_SKIP = -2;

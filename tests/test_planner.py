@@ -102,7 +102,7 @@ def test_batch_program_pairs_siblings_and_shares_the_hub_product(monkeypatch):
     total = lambda t: float(next(l for l in t.splitlines() if l.startswith("compulsory total MB")).split()[-1])
     monkeypatch.setenv("JT_HUBX", "0")
     f64_nox = report("c5", batch=4096, mode="shared", kind=1, dtype="f64")
-    assert total(f64) < total(f64_nox) - 10000  # ~13.8 GB fewer per 4096-case micro-batch
+    assert total(f64) < total(f64_nox) - 5000  # ~9 GB fewer per 4096-case micro-batch (13.8 before ratio-only outputs)
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
@@ -127,4 +127,4 @@ def test_batch_program_gathers_virtual_separators(dtype, monkeypatch):
     off = report("c5", batch=4096, mode="shared", kind=1, dtype=dtype)
     assert "vsep 2" not in off
     saved = total(off) - total(on)
-    assert saved > (25000 if dtype == "f64" else 12500), saved
+    assert saved > (20000 if dtype == "f64" else 10000), saved
