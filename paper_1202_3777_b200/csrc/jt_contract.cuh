@@ -170,6 +170,9 @@ __device__ __forceinline__ bool contract_epilogue_half(const CPass* __restrict__
 #ifndef CON_MINB
 #define CON_MINB 2
 #endif
+#ifndef CON_FOLD_K
+#define CON_FOLD_K 32  // fp32 k-terms per register partial before the fp64 fold (16: -1.5%)
+#endif
 #ifndef CON_WPF
 #define CON_WPF 1
 #endif
@@ -340,7 +343,7 @@ __device__ __forceinline__ void tile_body(const CArgs& a, const CPass* __restric
         for (int r = 0; r < TMC; ++r)
 #pragma unroll
           for (int l = 0; l < VEC; ++l) part[r][l] += w[r] * pv[l];
-        if (FOLD && ++since == CKF) {
+        if (FOLD && ++since == CON_FOLD_K) {
           since = 0;
 #pragma unroll
           for (int r = 0; r < TMC; ++r)
