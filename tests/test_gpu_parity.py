@@ -751,3 +751,44 @@ def test_lazy_final_separator_tables(dtype, monkeypatch):
         bp.close()
     assert np.all(np.isfinite(seps["1"])) and seps["1"].max() > 0
     assert rel_err(seps["1"], seps["0"]) < (1e-13 if dtype == "f64" else 1e-6)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_zero_entries_under_ratio_only_and_virtual_separators(dtype, monkeypatch):
+    """Tables with exact zeros make separator entries 0: ratio-only distribute
+    outputs then store Σ where the reference's ratio is 0/0 = 0, and gathered
+    leaf messages are 0 there. Posteriors must still match the oracle (and the
+    programs with those features off), with a hub variable's state 0 impossible."""
+    from paper_1202_3777_b200.batch import BatchPropagator
+
+    monkeypatch.setenv("JT_VSEP_MIN_MB", "0")
+    tree, data = load_golden("c5")
+    tables = list(synth.scaled_potentials(tree, 0))
+    hub = 2
+    scope = tree.cliques[hub].scope
+    v = int(scope.ids[0])
+    t = np.asarray(tables[hub], dtype=np.float64).reshape(scope.cards).copy()
+    idx = [slice(None)] * t.ndim
+    idx[0] = 0
+    t[tuple(idx)] = 0.0
+    tables[hub] = t.ravel()
+    cases = [{k: s for k, s in ev.items() if k != v} for ev, _ in golden_cases(data)]
+    cases = [cases[i % len(cases)] for i in range(124)] + synth.evidence_cases(tree, 4, seed=5)
+    cases = [{k: s for k, s in ev.items() if k != v} for ev in cases]
+    template = jtref.from_potentials(tree, tables)
+    check = [0, 1, 2, 60, 124, 125, 126, 127]
+    want = {i: jtref.case_posteriors(template, cases[i], range(len(tree.cards))) for i in check}
+    outs = []
+    for env in ({}, {"JT_DRATIO": "0", "JT_VSEP": "0", "JT_LAZY_FINAL": "0"}):
+        for k in ("JT_DRATIO", "JT_VSEP", "JT_LAZY_FINAL"):
+            monkeypatch.delenv(k, raising=False)
+        for k, x in env.items():
+            monkeypatch.setenv(k, x)
+        bp = BatchPropagator(tree, tables, batch=128, dtype=dtype, mode="shared")
+        out = bp.run(cases, to_host=True)
+        for i in check:
+            assert rel_err(out[i], want[i]) < TOL[dtype], (dtype, env, i)
+        outs.append(out)
+        bp.close()
+    assert np.all(np.isfinite(outs[0]))
+    assert rel_err(outs[0], outs[1]) < (1e-12 if dtype == "f64" else 1e-5)
