@@ -23,6 +23,8 @@ gathered with one NCCL all-gather (`gather_posteriors`).
 from __future__ import annotations
 
 import ctypes as C
+from itertools import chain
+from operator import methodcaller
 
 import numpy as np
 
@@ -30,6 +32,8 @@ from . import _lib
 from ._lib import JT_MATERIALIZED, JT_SHARED_BASE, check, f64, i32, ptr
 from .errors import StateOutOfRangeError, UnknownVariableError, ZeroMassError
 from .propagate import _scope_size, plan_for
+
+_values = methodcaller("values")
 
 MODES = {"shared": JT_SHARED_BASE, "materialized": JT_MATERIALIZED}
 MAX_FACTORS = 8  # jt::MAXF
@@ -167,14 +171,15 @@ class BatchPropagator:
         unknown variables raise UnknownVariableError, states outside [0, card)
         raise StateOutOfRangeError."""
         evs = [ev.assignments if hasattr(ev, "assignments") else ev for ev in cases]
-        counts = [len(ev) for ev in evs]
+        counts = list(map(len, evs))
         n = sum(counts)
         if not n:
             return np.zeros((0, 3), np.int32)
         obs = np.empty((n, 3), dtype=np.int64)
         obs[:, 0] = np.repeat(np.arange(len(evs), dtype=np.int64), counts)
-        obs[:, 1] = np.fromiter((v for ev in evs for v in ev), dtype=np.int64, count=n)
-        obs[:, 2] = np.fromiter((x for ev in evs for x in ev.values()), dtype=np.int64, count=n)
+        # (C-level iteration: the e2e path encodes every micro-batch's dicts here)
+        obs[:, 1] = np.fromiter(chain.from_iterable(evs), dtype=np.int64, count=n)
+        obs[:, 2] = np.fromiter(chain.from_iterable(map(_values, evs)), dtype=np.int64, count=n)
         own = self._owner_arr
         v, x = obs[:, 1], obs[:, 2]
         bad_v = (v < 0) | (v >= len(own))
