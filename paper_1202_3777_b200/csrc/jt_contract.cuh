@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_p_kernel(const CArgs a,
 #define ROWI_KU_NF 1
 #endif
 #ifndef ROWI_MINB_NF
-#define ROWI_MINB_NF 8
+#define ROWI_MINB_NF 6
 #endif
 #ifndef ROWI_KU_F
 #define ROWI_KU_F 2
