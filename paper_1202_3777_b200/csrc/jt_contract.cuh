@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(NT, CON_MINB) contract_p_kernel(const CArgs a,
 #define ROWI_KU_F 2
 #endif
 #ifndef ROWI_MINB_F
-#define ROWI_MINB_F 4
+#define ROWI_MINB_F 5
 #endif
 #ifndef ROWI_MINB_D
 #define ROWI_MINB_D 6
