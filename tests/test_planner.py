@@ -92,7 +92,7 @@ def test_small_single_trees_use_tiny_passes():
 def test_batch_program_pairs_siblings_and_shares_the_hub_product(monkeypatch):
     """c5's hub clique 2 sends distribute messages to two children over the same
     140000-entry separator: the planner pairs them into ONE row-per-i pass with
-    two epilogues; in fp64 that pass also writes the clique product X and the
+    two epilogues; that pass also writes the clique product X and the
     hub's two other distribute passes read it (one sub-wave later), which the
     compulsory-bytes accounting reflects."""
     monkeypatch.setenv("JT_VSEP", "0")  # (virtual separators: the next test)
