@@ -1758,7 +1758,8 @@ static int compile_program(const jt_state* st, const std::vector<std::vector<Pas
           cg.vs = cp.nV > 0;
           const int occ = occ_override ? occ_override
                           : cg.rp_idx >= 0
-                              ? contract_rowi_param_max_ctas(st->plan->dtype, fold, cg.m == 4, cp.nG, cg.xw != 0, cg.vs)
+                              ? contract_rowi_param_max_ctas(st->plan->dtype, fold, cg.m == 4, cp.nG, cg.xw != 0, cg.vs,
+                                                             cp.out_kind, cp.out_kind_b)
                               : contract_max_ctas_per_sm(st->plan->dtype, fold, cg.m, cg.vec);
           cg.grid = (int)std::min<int64_t>((cg.n_units + NT / 32 - 1) / (NT / 32), (int64_t)occ * st->num_sms);
           rt.groups.push_back(cg);

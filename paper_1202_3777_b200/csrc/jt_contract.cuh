@@ -513,7 +513,9 @@ __device__ __forceinline__ void vsep_pick(int v, const T (&vv)[CMAXV][VEC], T (&
 #ifndef ROWI_KU_V
 #define ROWI_KU_V 1  // k per step of the VS variant (2 and 4 measured slower)
 #endif
-template <typename T, bool FOLD, bool LONGK, bool PRM, bool XW = false, int NGC = 0, bool VS = false>
+// KP (VS kernels): output kinds fixed at compile time — 1: (collect FRESH, no second
+// output), 2: (DFRESH, ratio-only second output); 0: read from the descriptor
+template <typename T, bool FOLD, bool LONGK, bool PRM, bool XW = false, int NGC = 0, bool VS = false, int KP = 0>
 __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restrict__ P0, const int32_t* __restrict__ tk0,
                                           const int32_t* __restrict__ ts0) {
   // one i per warp unit (few registers: three or four CTAs per SM), KU values
@@ -545,7 +547,10 @@ __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restric
     const int64_t i = P->cmaj ? ul % P->nI : ul / nCG;
     constexpr int GM = NGC ? NGC : CMAXG;
     const int nK = P->nK, nG = NGC ? NGC : P->nG, nE = P->nE;
-    const bool two = P->out_kind_b != OUT_NONE;  // paired sibling output (same K-sum)
+    constexpr int KA = KP == 1 ? OUT_SEP_FRESH : KP == 2 ? OUT_SEP_DFRESH : -1;
+    constexpr int KB = KP == 1 ? OUT_NONE : KP == 2 ? OUT_SEP_DRATIO : -1;
+    const int ka = KA >= 0 ? KA : P->out_kind, kb = KB >= 0 ? KB : P->out_kind_b;
+    const bool two = kb != OUT_NONE;  // paired sibling output (same K-sum)
     const int nV = VS ? P->nV : 0;  // virtual separators (entry indices at the end of the ti row)
     const int tw = nG + nE + 1 + (two ? P->nE_b + 1 : 0) + nV;
     const int32_t* __restrict__ tir = a.tab + P->ti_off + i * tw;
@@ -638,7 +643,7 @@ __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restric
       }
       const int64_t j = (int64_t)__ldg(tir + nG + nE) + TSV(nE) + b0;
       T old[VEC] = {};
-      if (P->out_kind == OUT_SEP || P->out_kind == OUT_SEP_DFRESH) {
+      if (ka == OUT_SEP || ka == OUT_SEP_DFRESH) {
         if (nV > 0 && P->old_v >= 0) vsep_pick<T, VEC>(P->old_v, vv, old);
         else if (cs) load_vec_cs<T, VEC>(aux_c + P->out_off + j, old);
         else load_vec<T, VEC>(aux_c + P->out_off + j, old);
@@ -650,7 +655,7 @@ __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restric
         if (cs) store_vec_cs<T, VEC>(aux + P->x_off + j, xv);
         else store_vec<T, VEC>(aux + P->x_off + j, xv);
       }
-      bool bad = finalize_lanes<T, double, VEC>(P->out_kind, P->out_off, P->ratio_off, P->out2_off, j, v, old, aux,
+      bool bad = finalize_lanes<T, double, VEC>(ka, P->out_off, P->ratio_off, P->out2_off, j, v, old, aux,
                                                 a.qout, cs);
       if (two) {
         const int32_t* tb = tir + nG + nE + 1;  // [E_b..., out_b] of this i
@@ -673,12 +678,12 @@ __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restric
         }
         const int64_t jb = (int64_t)__ldg(tb + nEb) + SBV(nEb) + b0;
         T oldb[VEC] = {};
-        if (P->out_kind_b == OUT_SEP || P->out_kind_b == OUT_SEP_DFRESH) {
+        if (kb == OUT_SEP || kb == OUT_SEP_DFRESH) {
           if (nV > 0 && P->old_v_b >= 0) vsep_pick<T, VEC>(P->old_v_b, vv, oldb);
           else if (cs) load_vec_cs<T, VEC>(aux_c + P->out_off_b + jb, oldb);
           else load_vec<T, VEC>(aux_c + P->out_off_b + jb, oldb);
         }
-        bad |= finalize_lanes<T, double, VEC>(P->out_kind_b, P->out_off_b, P->ratio_off_b, P->out2_off_b, jb, v, oldb,
+        bad |= finalize_lanes<T, double, VEC>(kb, P->out_off_b, P->ratio_off_b, P->out2_off_b, jb, v, oldb,
                                               aux, a.qout, cs);
       }
       if (bad) atomicOr(a.err, EB_INCONSISTENT);
@@ -696,11 +701,11 @@ __global__ void __launch_bounds__(NT, ROWI_MINB(T, FOLD, LONGK, VS)) contract_ro
   rowi_body<T, FOLD, LONGK, false, false, 0, VS>(a, nullptr, nullptr, nullptr);
 }
 
-template <typename T, bool FOLD, bool LONGK, bool XW = false, int NGC = 0, bool VS = false>
+template <typename T, bool FOLD, bool LONGK, bool XW = false, int NGC = 0, bool VS = false, int KP = 0>
 __global__ void __launch_bounds__(NT, ROWI_MINB(T, FOLD, LONGK, VS))
     contract_rowi_p_kernel(const CArgs a, const __grid_constant__ RowiParam rp) {
   pdl_enter();
-  rowi_body<T, FOLD, LONGK, true, XW, NGC, VS>(a, &rp.cp, rp.tk, rp.ts);
+  rowi_body<T, FOLD, LONGK, true, XW, NGC, VS, KP>(a, &rp.cp, rp.tk, rp.ts);
 }
 
 

@@ -7,20 +7,27 @@
 
 namespace jt {
 
-template <typename T, bool FOLD, bool LONGK, bool XW, bool VS>
+template <typename T, bool FOLD, bool LONGK, bool XW, bool VS, int KP = 0>
 static auto rowi_p_fn(int ng) {
   switch (ng) {
-    case 1: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 1, VS>;
-    case 2: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 2, VS>;
-    case 3: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 3, VS>;
-    case 4: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 4, VS>;
-    default: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 0, VS>;
+    case 1: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 1, VS, KP>;
+    case 2: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 2, VS, KP>;
+    case 3: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 3, VS, KP>;
+    case 4: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 4, VS, KP>;
+    default: return contract_rowi_p_kernel<T, FOLD, LONGK, XW, 0, VS, KP>;
   }
 }
 
-// ng <= 0: the generic (descriptor-driven) kernel
+// ng <= 0: the generic (descriptor-driven) kernel; kp (VS only, short K, unfolded):
+// the output-kind pattern fixed at compile time (rowi_body KP)
 template <typename T, bool VS>
-static void (*rowi_p_select(int fold, int longk, int ng, bool xw))(const CArgs, const RowiParam) {
+static void (*rowi_p_select(int fold, int longk, int ng, bool xw, int kp = 0))(const CArgs, const RowiParam) {
+  if constexpr (VS) {
+    if (kp && !fold && !longk) {
+      if (kp == 1 && !xw) return rowi_p_fn<T, false, false, false, VS, 1>(ng);
+      if (kp == 2) return xw ? rowi_p_fn<T, false, false, true, VS, 2>(ng) : rowi_p_fn<T, false, false, false, VS, 2>(ng);
+    }
+  }
   if (xw) {
     if (longk) return nullptr;
     if constexpr (sizeof(T) == 4)

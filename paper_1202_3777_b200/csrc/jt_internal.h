@@ -212,7 +212,8 @@ cudaError_t launch_contract_tile_param(int dtype, int fold, int ng, const CArgs&
                                        cudaStream_t s);
 int contract_max_ctas_per_sm(int dtype, int fold, int rowi, int ng);
 // occupancy of the parameter-space row-per-i kernel a pass launches (nG specialised)
-int contract_rowi_param_max_ctas(int dtype, int fold, int longk, int ng, bool xw, bool vs = false);
+int contract_rowi_param_max_ctas(int dtype, int fold, int longk, int ng, bool xw, bool vs = false, int ka = 0,
+                                 int kb = 0);
 
 // device initialize: one entry per clique, one term per CPT, 3 int64 per CPT variable
 // (clique stride, card, CPT stride)
