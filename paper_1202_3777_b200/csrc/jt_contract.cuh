@@ -513,8 +513,8 @@ __device__ __forceinline__ void vsep_pick(int v, const T (&vv)[CMAXV][VEC], T (&
 #ifndef ROWI_KU_V
 #define ROWI_KU_V 1  // k per step of the VS variant (2 and 4 measured slower)
 #endif
-// KP (VS kernels): output kinds fixed at compile time — 1: (collect FRESH, no second
-// output), 2: (DFRESH, ratio-only second output); 0: read from the descriptor
+// KP: output kinds fixed at compile time — 1: (collect FRESH, no second output),
+// 2: (DFRESH, ratio-only second output), 3: (ratio-only, none); 0: read from the descriptor
 template <typename T, bool FOLD, bool LONGK, bool PRM, bool XW = false, int NGC = 0, bool VS = false, int KP = 0>
 __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restrict__ P0, const int32_t* __restrict__ tk0,
                                           const int32_t* __restrict__ ts0) {
@@ -547,8 +547,8 @@ __device__ __forceinline__ void rowi_body(const CArgs& a, const CPass* __restric
     const int64_t i = P->cmaj ? ul % P->nI : ul / nCG;
     constexpr int GM = NGC ? NGC : CMAXG;
     const int nK = P->nK, nG = NGC ? NGC : P->nG, nE = P->nE;
-    constexpr int KA = KP == 1 ? OUT_SEP_FRESH : KP == 2 ? OUT_SEP_DFRESH : -1;
-    constexpr int KB = KP == 1 ? OUT_NONE : KP == 2 ? OUT_SEP_DRATIO : -1;
+    constexpr int KA = KP == 1 ? OUT_SEP_FRESH : KP == 2 ? OUT_SEP_DFRESH : KP == 3 ? OUT_SEP_DRATIO : -1;
+    constexpr int KB = KP == 1 || KP == 3 ? OUT_NONE : KP == 2 ? OUT_SEP_DRATIO : -1;
     const int ka = KA >= 0 ? KA : P->out_kind, kb = KB >= 0 ? KB : P->out_kind_b;
     const bool two = kb != OUT_NONE;  // paired sibling output (same K-sum)
     const int nV = VS ? P->nV : 0;  // virtual separators (entry indices at the end of the ti row)

@@ -19,12 +19,13 @@ ROWIP_DECL(floatv)
 ROWIP_DECL(doublev)
 #undef ROWIP_DECL
 
-// VS kernels with the output kinds fixed at compile time (JT_ROWI_KP=0: off)
+// row-per-i kernels with the output kinds fixed at compile time (JT_ROWI_KP=0: off)
 static int rowi_kind_pattern(int ka, int kb) {
   static const int on = getenv("JT_ROWI_KP") ? atoi(getenv("JT_ROWI_KP")) : 1;
   if (!on) return 0;
   if (ka == OUT_SEP_FRESH && kb == OUT_NONE) return 1;
   if (ka == OUT_SEP_DFRESH && kb == OUT_SEP_DRATIO) return 2;
+  if (ka == OUT_SEP_DRATIO && kb == OUT_NONE) return 3;
   return 0;
 }
 
@@ -40,22 +41,22 @@ cudaError_t launch_contract_rowi_param(int dtype, int fold, int longk, const CAr
                                        cudaStream_t s, bool xw, bool vs) {
   if (grid <= 0 || a.n_units <= 0) return cudaSuccess;
   const int ng = rowi_ngc(rp.cp.nG);
-  const int kp = vs ? rowi_kind_pattern(rp.cp.out_kind, rp.cp.out_kind_b) : 0;
+  const int kp = rowi_kind_pattern(rp.cp.out_kind, rp.cp.out_kind_b);
   if (vs)
     return dtype == 0 ? launch_contract_rowi_param_floatv(fold, longk, ng, a, rp, grid, s, xw, kp)
                       : launch_contract_rowi_param_doublev(fold, longk, ng, a, rp, grid, s, xw, kp);
-  return dtype == 0 ? launch_contract_rowi_param_float(fold, longk, ng, a, rp, grid, s, xw, 0)
-                    : launch_contract_rowi_param_double(fold, longk, ng, a, rp, grid, s, xw, 0);
+  return dtype == 0 ? launch_contract_rowi_param_float(fold, longk, ng, a, rp, grid, s, xw, kp)
+                    : launch_contract_rowi_param_double(fold, longk, ng, a, rp, grid, s, xw, kp);
 }
 
 int contract_rowi_param_max_ctas(int dtype, int fold, int longk, int ng, bool xw, bool vs, int ka, int kb) {
   ng = rowi_ngc(ng);
-  const int kp = vs ? rowi_kind_pattern(ka, kb) : 0;
+  const int kp = rowi_kind_pattern(ka, kb);
   if (vs)
     return dtype == 0 ? contract_rowi_param_max_ctas_floatv(fold, longk, ng, xw, kp)
                       : contract_rowi_param_max_ctas_doublev(fold, longk, ng, xw, kp);
-  return dtype == 0 ? contract_rowi_param_max_ctas_float(fold, longk, ng, xw, 0)
-                    : contract_rowi_param_max_ctas_double(fold, longk, ng, xw, 0);
+  return dtype == 0 ? contract_rowi_param_max_ctas_float(fold, longk, ng, xw, kp)
+                    : contract_rowi_param_max_ctas_double(fold, longk, ng, xw, kp);
 }
 
 template <typename T, bool FOLD, bool LONGK>

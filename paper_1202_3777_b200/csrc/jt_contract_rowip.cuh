@@ -18,15 +18,15 @@ static auto rowi_p_fn(int ng) {
   }
 }
 
-// ng <= 0: the generic (descriptor-driven) kernel; kp (VS only, short K, unfolded):
-// the output-kind pattern fixed at compile time (rowi_body KP)
+// ng <= 0: the generic (descriptor-driven) kernel; kp (short K, unfolded): the
+// output-kind pattern fixed at compile time (rowi_body KP; 2 for VS kernels only)
 template <typename T, bool VS>
 static void (*rowi_p_select(int fold, int longk, int ng, bool xw, int kp = 0))(const CArgs, const RowiParam) {
-  if constexpr (VS) {
-    if (kp && !fold && !longk) {
-      if (kp == 1 && !xw) return rowi_p_fn<T, false, false, false, VS, 1>(ng);
+  if (kp && !fold && !longk) {
+    if (kp == 1 && !xw) return rowi_p_fn<T, false, false, false, VS, 1>(ng);
+    if (kp == 3 && !xw) return rowi_p_fn<T, false, false, false, VS, 3>(ng);
+    if constexpr (VS)
       if (kp == 2) return xw ? rowi_p_fn<T, false, false, true, VS, 2>(ng) : rowi_p_fn<T, false, false, false, VS, 2>(ng);
-    }
   }
   if (xw) {
     if (longk) return nullptr;
